@@ -1,0 +1,144 @@
+/*
+ * cqr.h -- C ABI of the B200-native shifted Cholesky QR hot path (libcqr.so).
+ *
+ * The reference (arXiv 2507.07788 `cholqr` package, Python/NumPy) reaches the
+ * tall-side arithmetic through the VectorArray interface
+ * (/root/reference/pkg/src/cholqr/varray.py:47-100) and the k x k stage through
+ * kernels.py:61-194.  Each entry point below replaces one of those calls; the
+ * citation is given per function.  INTEGRATION.md shows the ctypes binding the
+ * reference would add (and the one paper_2507_07788_b200/_lib.py uses).
+ *
+ * Conventions
+ *  - All matrices are fp64, column-major.  A tall array of m rows and k columns
+ *    is stored with leading dimension ld (column j starts at X + j*ld).
+ *  - Tall operands: ld is even, ld >= round_up(m, 16), base 16-byte aligned,
+ *    and rows [m, round_up(m,16)) of every column are zero.  Kernels process
+ *    round_up(m,16) rows; outputs keep the padding rows zero.
+ *  - Small (k x n) coefficient operands C / Rinv: leading dimension ldc even,
+ *    ldc >= round_up(k, 32), rows [k, round_up(k,32)) zero.
+ *  - All pointers except `cfg` are DEVICE pointers; `stream` is a cudaStream_t
+ *    (NULL = legacy default stream).  Every call is asynchronous on `stream`;
+ *    results are valid once the stream reaches that point.
+ *  - Return value: 0 = launched, CQR_EINVAL = bad arguments, CQR_ECUDA = CUDA
+ *    error; cqr_last_error() describes the last failure of the calling thread.
+ *  - Not thread-safe per workspace buffer.  Gram outputs are LOCAL partial sums
+ *    over the rows passed in; under row sharding the caller sums them across
+ *    ranks (NCCL allreduce of the lower triangle) before cqr_factor.
+ */
+#ifndef CQR_H
+#define CQR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CQR_ABI_VERSION 1
+
+#define CQR_OK 0
+#define CQR_EINVAL (-1)
+#define CQR_ECUDA (-2)
+
+/* cqr_factor_status.code */
+#define CQR_FACTORED 0     /* Rk, Rinv written; Racc (and B) updated                  */
+#define CQR_CONVERGED 1    /* ||X - I||_F < tol on entry: nothing factored            */
+#define CQR_CAPPED 2       /* cfg.stop set: only ||X - I||_F measured                 */
+#define CQR_BREAKDOWN 3    /* CholeskyBreakdown (kernels.py:25-39, :76-77)            */
+#define CQR_SHIFT_LIMIT 4  /* ShiftAttemptLimitError (algorithms.py:47-56,309-310,384) */
+#define CQR_TRI_SINGULAR 5 /* TriangularSingularError (kernels.py:42-47,94-99)        */
+#define CQR_ASYMMETRIC 6   /* ValueError of spectral_norm_estimate (kernels.py:148-153) */
+
+/* cqr_factor_config.policy: which reference factorization rule runs */
+#define CQR_POLICY_PLAIN 0      /* cholesky(x)                       algorithms.py:209-210 */
+#define CQR_POLICY_SHIFT_ONCE 1 /* cholesky(x + sigma I), sigma from the norm estimate
+                                                                     algorithms.py:233-237 */
+#define CQR_POLICY_RECOMPUTE 2  /* plain, then recomputed + escalated shifts
+                                                                     algorithms.py:344-349, 295-317 */
+#define CQR_POLICY_UPDATE 3     /* deflated x = G - Bt^T Bt; sigma = 0, recomputed, escalated
+                                                                     algorithms.py:358-397 */
+
+typedef struct cqr_factor_config {
+  int32_t policy;
+  int32_t shift_width;        /* width entering compute_shift (n, or q/p for updates) */
+  int64_t m_global;           /* GLOBAL row count (compute_shift, kernels.py:181-194) */
+  double unit_roundoff;       /* AlgoConfig.unit_roundoff (1.11e-16)                 */
+  double shift_escalation;    /* AlgoConfig.shift_escalation (10)                    */
+  int32_t max_shift_attempts; /* AlgoConfig.max_shift_attempts (60)                  */
+  int32_t check_tol;          /* 1: report CONVERGED when ||X - I||_F < tol         */
+  double tol;                 /* AlgoConfig.effective_tol(width)                     */
+  int32_t stop;               /* 1: iteration cap reached, measure only              */
+  int32_t accumulate;         /* 1: Racc <- triu(Rk Racc)  (kernels.py:103-114)      */
+  int32_t update_b;           /* 1: B <- B + Bt Racc_old   (algorithms.py:445)       */
+  int32_t est_max_iter;       /* power-iteration cap (100, kernels.py:126)           */
+  double est_tol;             /* power-iteration settling tolerance (1e-2)           */
+} cqr_factor_config;
+
+typedef struct cqr_factor_status {
+  int32_t code;          /* CQR_FACTORED ... CQR_ASYMMETRIC                            */
+  int32_t retries;       /* shifted retries this pass (QRResult.shift_attempts entry)  */
+  int32_t n_shifts;      /* shifts appended to `shifts` this pass                      */
+  int32_t pivot_index;   /* last breakdown: pivot index                                */
+  double pivot_value;    /* last breakdown: Schur diagonal (<= 0 or NaN)              */
+  double err;            /* ||X - I||_F on entry (X deflated for updates)             */
+  double norm_est;       /* spectral norm estimate used for the shift (if any)        */
+  double last_shift;     /* ShiftAttemptLimitError.last_shift                          */
+  double min_pivot_rel;  /* min diag(Rk)^2 / max diag(X + sigma I): decision margin    */
+  int32_t est_calls;     /* spectral estimates run (ledger eig_est)                    */
+  int32_t est_flag;      /* 0 converged, 1 stalled, 2 not converged (UserWarning)      */
+  int32_t escalations;   /* escalation steps charged one flop each (ledger eig_est)    */
+  int32_t singular_index;/* TriangularSingularError.index                             */
+} cqr_factor_status;
+
+int cqr_abi_version(void);
+const char* cqr_last_error(void);
+
+/* Gram G = X^T X over the local rows, written full and bit-symmetric (lower
+ * triangle computed, mirrored) into G (k x k, ldg >= k).  Replaces
+ * DenseVectorArray.gramian() (varray.py:150-153, _charged_gramian
+ * algorithms.py:159-165). */
+size_t cqr_gram_workspace_bytes(int64_t m, int ka, int kb, int self);
+int cqr_gram(const double* X, int64_t ldx, int64_t m, int k, double* G, int ldg, void* ws, size_t ws_bytes,
+             void* stream);
+
+/* Cross Gram G = A^T B (ka x kb).  Replaces gramian(other) (varray.py:154-155). */
+int cqr_cross_gram(const double* A, int64_t lda, int ka, const double* B, int64_t ldb, int kb, int64_t m, double* G,
+                   int ldg, void* ws, size_t ws_bytes, void* stream);
+
+/* Y = X C (m x n).  upper=1 declares C upper triangular (TRMM by R^-1; zero
+ * blocks are skipped).  Y may alias X only when n <= 64.  Replaces
+ * DenseVectorArray.lincomb (varray.py:157-163, algorithms.py:168-174). */
+int cqr_lincomb(const double* X, int64_t ldx, int64_t m, int k, const double* C, int ldc, int n, int upper,
+                double* Y, int64_t ldy, void* stream);
+
+/* Y += alpha X, in place.  Replaces DenseVectorArray.axpy (varray.py:165-171). */
+int cqr_axpy(double* Y, int64_t ldy, double alpha, const double* X, int64_t ldx, int64_t m, int n, void* stream);
+
+/* Fused pass: Q = X Rinv (Rinv upper triangular) and G = Q^T Q in one stream
+ * over X (Q may alias X).  Replaces the lincomb + gramian pair of one
+ * iteration (algorithms.py:350,352 / :238,:240 / :211 + :209). */
+size_t cqr_apply_gram_workspace_bytes(int64_t m, int k);
+/* 1 when cqr_apply_gram may run in place (Q == X) for width k. */
+int cqr_apply_gram_inplace_ok(int k);
+int cqr_apply_gram(const double* X, int64_t ldx, int64_t m, int k, const double* Rinv, int ldr, double* Q,
+                   int64_t ldq, double* G, int ldg, void* ws, size_t ws_bytes, void* stream);
+
+/* The k x k stage of one pass, one launch: forms X (G, or the deflated
+ * G - Bt^T Bt for updates), measures ||X - I||_F, runs the policy's
+ * factorization attempts with breakdown detection, power-iteration norm
+ * estimate and shift rule (kernels.py:61-194, algorithms.py:187-198,295-317,
+ * 369-397), inverts the factor (kernels.py:85-100) and accumulates
+ * Racc <- triu(Rk Racc) and B <- B + Bt Racc.  Rk, Rinv, Racc: ldr >=
+ * round_up(k, 32), zero-padded.  `shifts` receives the shift values tried
+ * (capacity max_shift_attempts + 1).  `status` is device memory. */
+size_t cqr_factor_workspace_bytes(int k);
+int cqr_factor(const cqr_factor_config* cfg, int k, const double* G, int ldg, const double* Bt, int ldbt, int q,
+               double* Rk, double* Rinv, int ldr, double* Racc, double* B, int ldb, double* shifts,
+               cqr_factor_status* status, void* ws, size_t ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CQR_H */

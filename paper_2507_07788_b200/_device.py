@@ -1,0 +1,99 @@
+"""Per-process device context: CUDA device, stream, workspaces, row sharding.
+
+PyTorch is plumbing here: device allocations (caching allocator), the
+stream handle passed to libcqr, pinned host staging and torch.distributed
+(NCCL) for the one collective of a pass.  One process drives one GPU; under
+torch.distributed each rank owns a contiguous block of rows of every tall
+array.
+"""
+
+from __future__ import annotations
+
+import os
+
+import torch
+
+from . import _lib
+
+_ctx = None
+
+
+def round_up(a, b):
+    return (a + b - 1) // b * b
+
+
+class DeviceContext:
+    def __init__(self):
+        if not torch.cuda.is_available():
+            raise RuntimeError(
+                "paper_2507_07788_b200 needs a CUDA device (B200, sm_100a); there is no CPU fallback")
+        self.lib = _lib.load()
+        if torch.distributed.is_available() and torch.distributed.is_initialized():
+            self.rank = torch.distributed.get_rank()
+            self.world = torch.distributed.get_world_size()
+            local = int(os.environ.get("LOCAL_RANK", self.rank % max(torch.cuda.device_count(), 1)))
+        else:
+            self.rank, self.world, local = 0, 1, torch.cuda.current_device()
+        self.device = torch.device("cuda", local)
+        torch.cuda.set_device(self.device)
+        self._ws = torch.empty(0, dtype=torch.uint8, device=self.device)
+        self._ws2 = torch.empty(0, dtype=torch.uint8, device=self.device)
+        self.launches = 0   # libcqr kernel launches issued (bench bookkeeping)
+
+    # ---------------------------------------------------------------- plumbing
+    @property
+    def stream(self):
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def workspace(self, nbytes, which=0):
+        """Reusable device scratch (grown on demand)."""
+        buf = self._ws if which == 0 else self._ws2
+        if buf.numel() < nbytes:
+            buf = torch.empty(round_up(max(nbytes, 1 << 20), 1 << 20), dtype=torch.uint8, device=self.device)
+            if which == 0:
+                self._ws = buf
+            else:
+                self._ws2 = buf
+        return buf
+
+    def row_range(self, m):
+        """Rows [lo, hi) of a global row count m owned by this rank."""
+        lo = m * self.rank // self.world
+        hi = m * (self.rank + 1) // self.world
+        return lo, hi
+
+    def allreduce_(self, t):
+        """Sum a small device tensor over ranks (NCCL); no-op on one rank."""
+        if self.world > 1:
+            torch.distributed.all_reduce(t)
+        return t
+
+    def allgather_rows(self, local, m):
+        """Concatenate per-rank row blocks (host numpy, m_local x k) to m x k."""
+        if self.world == 1:
+            return local
+        import numpy as np
+
+        t = torch.from_numpy(np.ascontiguousarray(local)).to(self.device)
+        sizes = [self_hi - self_lo for (self_lo, self_hi) in
+                 (((m * r) // self.world, (m * (r + 1)) // self.world) for r in range(self.world))]
+        mx = max(sizes)
+        pad = torch.zeros((mx, t.shape[1]), dtype=t.dtype, device=self.device)
+        pad[: t.shape[0]] = t
+        out = [torch.empty_like(pad) for _ in range(self.world)]
+        torch.distributed.all_gather(out, pad)
+        return np.concatenate([o[:s].cpu().numpy() for o, s in zip(out, sizes)], axis=0)
+
+
+def ctx():
+    """The process-wide device context (created on first use)."""
+    global _ctx
+    if _ctx is None:
+        _ctx = DeviceContext()
+    return _ctx
+
+
+def reset():
+    """Forget the context (after torch.distributed is (re)initialized)."""
+    global _ctx
+    _ctx = None

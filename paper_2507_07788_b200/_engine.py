@@ -1,0 +1,173 @@
+"""Device pass engine: the tall passes and the k x k stage of one algorithm
+run, with the one collective (Gram allreduce) and the one status read per
+pass.  `algorithms.py` drives it with the reference's control flow.
+
+Per run the engine owns, on the device:
+  G      k x k Gram of the current pass (allreduced over ranks)
+  Rk/Rinv/Racc  ldr x k (ldr = round_up(k, 32), zero padded) factors
+  B, Bt  q x p blocks of the update path
+  stat   status record + shift list (one D2H copy per pass)
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._device import ctx, round_up
+
+STATUS_BYTES = 80   # sizeof(cqr_factor_status) rounded to 16
+
+
+def _gram_ws(m_local, ka, kb, self_):
+    cx = ctx()
+    return cx.workspace(cx.lib.cqr_gram_workspace_bytes(m_local, ka, kb, 1 if self_ else 0))
+
+
+def _symmetrize_(g):
+    """Mirror the lower triangle (exact), keeping the Gram bit-symmetric after
+    a cross-rank reduction whose per-element order may differ."""
+    low = torch.tril(g)
+    g.copy_(low + torch.tril(g, -1).T)
+    return g
+
+
+def gram_device(arr, out=None):
+    """G = X^T X (allreduced, bit-symmetric) as a k x k device tensor."""
+    cx = ctx()
+    k = arr.ncols
+    g = out if out is not None else torch.empty((k, k), dtype=torch.float64, device=cx.device)
+    ws = _gram_ws(arr.m_local, k, k, True)
+    # G is column-major k x k: torch (k, k) row-major of G^T == G (symmetric)
+    _lib.check(cx.lib.cqr_gram(arr.ptr(), arr.ld, arr.m_local, k, g.data_ptr(), k, ws.data_ptr(), ws.numel(),
+                               cx.stream), "gram")
+    cx.launches += 2
+    if cx.world > 1:
+        cx.allreduce_(g)
+        _symmetrize_(g)
+    return g
+
+
+def gram_host(arr):
+    if arr.ncols == 0:
+        return np.zeros((0, 0))
+    return gram_device(arr).cpu().numpy()
+
+
+def cross_gram_device(left, right, out=None):
+    """G = L^T R (ka x kb) as a column-major device buffer: torch (kb, ka)."""
+    cx = ctx()
+    ka, kb = left.ncols, right.ncols
+    g = out if out is not None else torch.empty((kb, ka), dtype=torch.float64, device=cx.device)
+    if ka and kb:
+        ws = _gram_ws(left.m_local, ka, kb, False)
+        _lib.check(cx.lib.cqr_cross_gram(left.ptr(), left.ld, ka, right.ptr(), right.ld, kb, left.m_local,
+                                         g.data_ptr(), ka, ws.data_ptr(), ws.numel(), cx.stream), "cross_gram")
+        cx.launches += 2
+        cx.allreduce_(g)
+    else:
+        g.zero_()
+    return g
+
+
+def cross_gram_host(left, right):
+    g = cross_gram_device(left, right)
+    return g.cpu().numpy().T.copy()
+
+
+class PassStatus:
+    """Host copy of one cqr_factor_status plus the shifts it appended."""
+
+    def __init__(self, raw, shifts):
+        st = _lib.FactorStatus.from_buffer_copy(raw[: ctypes.sizeof(_lib.FactorStatus)])
+        for name, _ in _lib.FactorStatus._fields_:
+            setattr(self, name, getattr(st, name))
+        self.shifts = [float(s) for s in shifts[: max(st.n_shifts, 0)]]
+
+
+class Engine:
+    """Buffers and launches for one algorithm run on width-k blocks."""
+
+    def __init__(self, k, cfg, q=0):
+        cx = ctx()
+        self.cx = cx
+        self.k = k
+        self.q = q
+        self.cfg = cfg
+        dev = cx.device
+        self.ldr = max(round_up(k, 32), 32)
+        self.G = torch.empty((k, k), dtype=torch.float64, device=dev)
+        self.Rk = torch.zeros((k, self.ldr), dtype=torch.float64, device=dev)
+        self.Rinv = torch.zeros((k, self.ldr), dtype=torch.float64, device=dev)
+        self.Racc = torch.zeros((k, self.ldr), dtype=torch.float64, device=dev)
+        self.Racc[:, :k] = torch.eye(k, dtype=torch.float64, device=dev)
+        self.cap = cfg.max_shift_attempts + 1
+        nbytes = STATUS_BYTES + 8 * self.cap
+        self.stat = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+        self.stat_host = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+        self.fws = torch.empty(cx.lib.cqr_factor_workspace_bytes(k), dtype=torch.uint8, device=dev)
+        if q:
+            self.B = torch.zeros((k, q), dtype=torch.float64, device=dev)     # (p, q): column-major q x p
+            self.Bt = torch.zeros((k, q), dtype=torch.float64, device=dev)
+        else:
+            self.B = self.Bt = None
+
+    # ------------------------------------------------------------ k x k stage
+    def factor(self, policy, m_global, width, *, tol=0.0, check_tol=False, stop=False, update_b=False):
+        cx = self.cx
+        cfg = self.cfg
+        fc = _lib.FactorConfig(
+            policy=policy, shift_width=width, m_global=m_global, unit_roundoff=cfg.unit_roundoff,
+            shift_escalation=cfg.shift_escalation, max_shift_attempts=cfg.max_shift_attempts,
+            check_tol=1 if check_tol else 0, tol=tol, stop=1 if stop else 0, accumulate=1,
+            update_b=1 if update_b else 0, est_max_iter=100, est_tol=1e-2)
+        bt = self.Bt.data_ptr() if self.Bt is not None else None
+        b = self.B.data_ptr() if self.B is not None else None
+        base = self.stat.data_ptr()
+        _lib.check(cx.lib.cqr_factor(ctypes.byref(fc), self.k, self.G.data_ptr(), self.k, bt, max(self.q, 1),
+                                     self.q, self.Rk.data_ptr(), self.Rinv.data_ptr(), self.ldr,
+                                     self.Racc.data_ptr(), b, max(self.q, 1), base + STATUS_BYTES, base,
+                                     self.fws.data_ptr(), self.fws.numel(), cx.stream), "factor")
+        cx.launches += 1
+        self.stat_host.copy_(self.stat, non_blocking=True)
+        torch.cuda.current_stream(cx.device).synchronize()
+        raw = self.stat_host.numpy()
+        shifts = raw[STATUS_BYTES:].view(np.float64)
+        return PassStatus(raw.tobytes(), shifts)
+
+    # ------------------------------------------------------------ tall passes
+    def gram(self, arr):
+        gram_device(arr, self.G)
+
+    def apply(self, src, dst, with_gram=True):
+        """dst = src R^-1 (TRMM); with_gram also forms G = dst^T dst."""
+        cx = self.cx
+        if with_gram:
+            ws = cx.workspace(cx.lib.cqr_apply_gram_workspace_bytes(src.m_local, self.k))
+            _lib.check(cx.lib.cqr_apply_gram(src.ptr(), src.ld, src.m_local, self.k, self.Rinv.data_ptr(),
+                                             self.ldr, dst.ptr(), dst.ld, self.G.data_ptr(), self.k,
+                                             ws.data_ptr(), ws.numel(), cx.stream), "apply_gram")
+            cx.launches += 3
+            if cx.world > 1:
+                cx.allreduce_(self.G)
+        else:
+            _lib.check(cx.lib.cqr_lincomb(src.ptr(), src.ld, src.m_local, self.k, self.Rinv.data_ptr(), self.ldr,
+                                          self.k, 1, dst.ptr(), dst.ld, cx.stream), "apply")
+            cx.launches += 1
+
+    def in_place_ok(self):
+        """TRMM may overwrite its input (one 64-wide column tile per row tile)."""
+        return self.k <= 64
+
+    def in_place_gram_ok(self):
+        """apply_gram may overwrite its input (fused kernel, or k <= 64)."""
+        return self.k <= 64 or self.cx.lib.cqr_apply_gram_inplace_ok(self.k) == 1
+
+    def r_host(self):
+        return self.Racc[:, : self.k].cpu().numpy().T.copy()
+
+    def b_host(self):
+        return self.B.cpu().numpy().T.copy()

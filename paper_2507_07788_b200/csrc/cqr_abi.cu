@@ -1,0 +1,189 @@
+// C ABI of libcqr.so (declared in include/cqr.h).  Argument validation,
+// workspace accounting and dispatch to the kernel files; every entry point
+// is asynchronous on the caller's stream.
+#include <cstdio>
+#include <string>
+
+#include "cqr_common.cuh"
+#include "cqr_kernels.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return CQR_OK;
+  return fail(CQR_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int check_tall(const double* X, int64_t ld, int64_t m, int k, const char* who) {
+  if (m < 0 || k < 0) return fail(CQR_EINVAL, std::string(who) + ": negative shape");
+  if (k == 0 || m == 0) return CQR_OK;
+  if (X == nullptr) return fail(CQR_EINVAL, std::string(who) + ": null pointer");
+  if (!aligned16(X)) return fail(CQR_EINVAL, std::string(who) + ": base pointer not 16-byte aligned");
+  if (ld % 2 != 0) return fail(CQR_EINVAL, std::string(who) + ": leading dimension must be even");
+  if (ld < cqr::round_up(m, 16)) return fail(CQR_EINVAL, std::string(who) + ": leading dimension < round_up(m, 16)");
+  return CQR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cqr_abi_version(void) { return CQR_ABI_VERSION; }
+
+const char* cqr_last_error(void) { return g_last_error.c_str(); }
+
+size_t cqr_gram_workspace_bytes(int64_t m, int ka, int kb, int self) {
+  if (ka <= 0 || kb <= 0) return 256;
+  cqr::GramArgs a = cqr::gram_plan(nullptr, 0, ka, nullptr, 0, kb, cqr::round_up(m, 16), self != 0);
+  return cqr::gram_workspace_bytes(a) + 256;
+}
+
+static int gram_common(const double* A, int64_t lda, int ka, const double* B, int64_t ldb, int kb, int64_t m,
+                       bool self, double* G, int ldg, void* ws, size_t ws_bytes, void* stream, const char* who) {
+  int rc = check_tall(A, lda, m, ka, who);
+  if (rc) return rc;
+  if (!self) {
+    rc = check_tall(B, ldb, m, kb, who);
+    if (rc) return rc;
+  }
+  if (ka == 0 || kb == 0) return CQR_OK;
+  if (G == nullptr || ldg < ka) return fail(CQR_EINVAL, std::string(who) + ": bad output G / ldg");
+  cqr::GramArgs a = cqr::gram_plan(A, lda, ka, B, ldb, kb, cqr::round_up(m, 16), self);
+  if (ws_bytes < cqr::gram_workspace_bytes(a) || ws == nullptr)
+    return fail(CQR_EINVAL, std::string(who) + ": workspace too small");
+  a.ws = static_cast<double*>(ws);
+  return cuda_check(cqr::gram_launch(a, G, ldg, static_cast<cudaStream_t>(stream)), who);
+}
+
+int cqr_gram(const double* X, int64_t ldx, int64_t m, int k, double* G, int ldg, void* ws, size_t ws_bytes,
+             void* stream) {
+  return gram_common(X, ldx, k, X, ldx, k, m, true, G, ldg, ws, ws_bytes, stream, "cqr_gram");
+}
+
+int cqr_cross_gram(const double* A, int64_t lda, int ka, const double* B, int64_t ldb, int kb, int64_t m, double* G,
+                   int ldg, void* ws, size_t ws_bytes, void* stream) {
+  return gram_common(A, lda, ka, B, ldb, kb, m, false, G, ldg, ws, ws_bytes, stream, "cqr_cross_gram");
+}
+
+int cqr_lincomb(const double* X, int64_t ldx, int64_t m, int k, const double* C, int ldc, int n, int upper,
+                double* Y, int64_t ldy, void* stream) {
+  int rc = check_tall(X, ldx, m, k, "cqr_lincomb(X)");
+  if (rc) return rc;
+  rc = check_tall(Y, ldy, m, n, "cqr_lincomb(Y)");
+  if (rc) return rc;
+  if (n == 0 || m == 0) return CQR_OK;
+  if (k == 0) return fail(CQR_EINVAL, "cqr_lincomb: k == 0 with n > 0 (zero-fill the output instead)");
+  if (C == nullptr || !aligned16(C) || ldc % 2 != 0 || ldc < cqr::round_up(k, 32))
+    return fail(CQR_EINVAL, "cqr_lincomb: C needs ldc even and >= round_up(k, 32), 16-byte aligned");
+  if (upper && n != k) return fail(CQR_EINVAL, "cqr_lincomb: upper-triangular C must be square");
+  if (X == Y && (n > 64 || ldx != ldy)) return fail(CQR_EINVAL, "cqr_lincomb: in place only for n <= 64");
+  cqr::GemmArgs a{};
+  a.X = X; a.ldx = ldx; a.kx = k;
+  a.C = C; a.ldc = ldc;
+  a.Y = Y; a.ldy = ldy; a.n = n;
+  a.rows = cqr::round_up(m, 16);
+  a.upper = upper ? 1 : 0;
+  return cuda_check(cqr::gemm_launch(a, static_cast<cudaStream_t>(stream)), "cqr_lincomb");
+}
+
+int cqr_axpy(double* Y, int64_t ldy, double alpha, const double* X, int64_t ldx, int64_t m, int n, void* stream) {
+  int rc = check_tall(Y, ldy, m, n, "cqr_axpy(Y)");
+  if (rc) return rc;
+  rc = check_tall(X, ldx, m, n, "cqr_axpy(X)");
+  if (rc) return rc;
+  if (n == 0 || m == 0) return CQR_OK;
+  return cuda_check(cqr::axpy_launch(Y, ldy, alpha, X, ldx, cqr::round_up(m, 16), n, static_cast<cudaStream_t>(stream)),
+                    "cqr_axpy");
+}
+
+size_t cqr_apply_gram_workspace_bytes(int64_t m, int k) {
+  size_t a = cqr_gram_workspace_bytes(m, k, k, 1);
+  if (cqr::apply_gram_fused_supported(k)) {
+    size_t b = cqr::apply_gram_fused_ws_bytes(cqr::round_up(m, 16), k);
+    if (b > a) a = b;
+  }
+  return a;
+}
+
+int cqr_apply_gram_inplace_ok(int k) { return (k <= 64 || cqr::apply_gram_fused_supported(k)) ? 1 : 0; }
+
+int cqr_apply_gram(const double* X, int64_t ldx, int64_t m, int k, const double* Rinv, int ldr, double* Q,
+                   int64_t ldq, double* G, int ldg, void* ws, size_t ws_bytes, void* stream) {
+  int rc = check_tall(X, ldx, m, k, "cqr_apply_gram(X)");
+  if (rc) return rc;
+  rc = check_tall(Q, ldq, m, k, "cqr_apply_gram(Q)");
+  if (rc) return rc;
+  if (k == 0 || m == 0) return CQR_OK;
+  if (Rinv == nullptr || !aligned16(Rinv) || ldr % 2 != 0 || ldr < cqr::round_up(k, 32))
+    return fail(CQR_EINVAL, "cqr_apply_gram: Rinv needs ldr even and >= round_up(k, 32)");
+  if (G == nullptr || ldg < k) return fail(CQR_EINVAL, "cqr_apply_gram: bad G / ldg");
+  if (ws == nullptr || ws_bytes < cqr_apply_gram_workspace_bytes(m, k))
+    return fail(CQR_EINVAL, "cqr_apply_gram: workspace too small");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (cqr::apply_gram_fused_supported(k))
+    return cuda_check(cqr::apply_gram_fused_launch(X, ldx, k, Rinv, ldr, Q, ldq, cqr::round_up(m, 16), G, ldg,
+                                                   static_cast<double*>(ws), ws_bytes, s),
+                      "cqr_apply_gram(fused)");
+  if (X == Q && k > 64) return fail(CQR_EINVAL, "cqr_apply_gram: in place needs the fused kernel (k <= 128)");
+  rc = cqr_lincomb(X, ldx, m, k, Rinv, ldr, k, 1, Q, ldq, stream);
+  if (rc) return rc;
+  return cqr_gram(Q, ldq, m, k, G, ldg, ws, ws_bytes, stream);
+}
+
+size_t cqr_factor_workspace_bytes(int k) { return k > 0 ? cqr::factor_workspace_bytes(k) : 256; }
+
+int cqr_factor(const cqr_factor_config* cfg, int k, const double* G, int ldg, const double* Bt, int ldbt, int q,
+               double* Rk, double* Rinv, int ldr, double* Racc, double* B, int ldb, double* shifts,
+               cqr_factor_status* status, void* ws, size_t ws_bytes, void* stream) {
+  if (cfg == nullptr || status == nullptr) return fail(CQR_EINVAL, "cqr_factor: null cfg/status");
+  if (k < 1 || k > 2048) return fail(CQR_EINVAL, "cqr_factor: k must be in [1, 2048]");
+  if (G == nullptr || ldg < k) return fail(CQR_EINVAL, "cqr_factor: bad G / ldg");
+  if (Rk == nullptr || Rinv == nullptr || Racc == nullptr || ldr < cqr::round_up(k, 32))
+    return fail(CQR_EINVAL, "cqr_factor: bad R buffers / ldr");
+  if (cfg->policy < CQR_POLICY_PLAIN || cfg->policy > CQR_POLICY_UPDATE)
+    return fail(CQR_EINVAL, "cqr_factor: unknown policy");
+  if (cfg->policy == CQR_POLICY_UPDATE && q > 0 && (Bt == nullptr || ldbt < q))
+    return fail(CQR_EINVAL, "cqr_factor: update policy needs Bt (q x k)");
+  if (cfg->update_b && q > 0 && (B == nullptr || ldb < q)) return fail(CQR_EINVAL, "cqr_factor: bad B / ldb");
+  if (shifts == nullptr) return fail(CQR_EINVAL, "cqr_factor: null shifts buffer");
+  if (cfg->max_shift_attempts < 1) return fail(CQR_EINVAL, "cqr_factor: max_shift_attempts must be >= 1");
+  if (ws == nullptr || ws_bytes < cqr::factor_workspace_bytes(k)) return fail(CQR_EINVAL, "cqr_factor: workspace too small");
+  cqr::FactorArgs a{};
+  a.G = G; a.ldg = ldg;
+  a.Bt = Bt; a.ldbt = ldbt; a.q = (cfg->policy == CQR_POLICY_UPDATE || cfg->update_b) ? q : 0;
+  a.k = k;
+  a.policy = cfg->policy;
+  a.m_global = cfg->m_global;
+  a.shift_width = cfg->shift_width;
+  a.u = cfg->unit_roundoff;
+  a.esc = cfg->shift_escalation;
+  a.max_shift_attempts = cfg->max_shift_attempts;
+  a.tol = cfg->tol;
+  a.check_tol = cfg->check_tol;
+  a.stop = cfg->stop;
+  a.est_tol = cfg->est_tol;
+  a.est_max_iter = cfg->est_max_iter;
+  a.accumulate = cfg->accumulate;
+  a.update_b = cfg->update_b;
+  double* w = static_cast<double*>(ws);
+  a.X = w;
+  a.W = w + (size_t)k * k;
+  a.Ri = a.W + (size_t)k * (k + 1) / 2;
+  a.Rk = Rk; a.Rinv = Rinv; a.ldr = ldr;
+  a.Racc = Racc;
+  a.B = B; a.ldb = ldb;
+  a.shifts = shifts;
+  a.st = status;
+  return cuda_check(cqr::factor_launch(a, static_cast<cudaStream_t>(stream)), "cqr_factor");
+}
+
+}  // extern "C"

@@ -1,0 +1,74 @@
+// Internal (C++) interfaces between the C-ABI layer and the kernel files.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/cqr.h"
+
+namespace cqr {
+
+int num_sms();
+
+// ------------------------------------------------------------- Gram (K1)
+struct GramArgs {
+  const double* A; int64_t lda; int ka;
+  const double* B; int64_t ldb; int kb;
+  int64_t rows;       // padded local row count (multiple of 16)
+  int self;           // lower-triangular tiles only, mirrored output
+  int ntile_i, ntile_j, ntiles;
+  int nsplit;
+  int64_t npanels;
+  double* ws;         // [nsplit][ntiles][64*64]
+};
+GramArgs gram_plan(const double* A, int64_t lda, int ka, const double* B, int64_t ldb, int kb, int64_t rows,
+                   bool self);
+size_t gram_workspace_bytes(const GramArgs& a);
+cudaError_t gram_launch(GramArgs& a, double* G, int ldg, cudaStream_t stream);
+
+// ------------------------------------------------------------- row-panel GEMM (K2 building block)
+struct GemmArgs {
+  const double* X; int64_t ldx; int kx;   // m x kx
+  const double* C; int ldc;               // kx x n, rows zero-padded to round_up(kx, 32)
+  double* Y; int64_t ldy; int n;          // m x n
+  int64_t rows;                           // padded local row count
+  int upper;                              // C upper triangular: skip zero blocks
+  int ntile_n;
+  int64_t nrow_tiles;
+};
+cudaError_t gemm_launch(GemmArgs& a, cudaStream_t stream);
+
+cudaError_t axpy_launch(double* Y, int64_t ldy, double alpha, const double* X, int64_t ldx, int64_t rows, int n,
+                        cudaStream_t stream);
+
+// ------------------------------------------------------------- fused TRMM + Gram (K2, k <= 128)
+cudaError_t apply_gram_fused_launch(const double* X, int64_t ldx, int k, const double* Rinv, int ldr, double* Q,
+                                    int64_t ldq, int64_t rows, double* G, int ldg, double* ws, size_t ws_bytes,
+                                    cudaStream_t stream);
+size_t apply_gram_fused_ws_bytes(int64_t rows, int k);
+bool apply_gram_fused_supported(int k);
+
+// ------------------------------------------------------------- k x k stage (K4)
+struct FactorArgs {
+  const double* G; int ldg;
+  const double* Bt; int ldbt; int q;
+  int k;
+  int policy;
+  int64_t m_global; int shift_width;
+  double u, esc; int max_shift_attempts;
+  double tol; int check_tol; int stop;
+  double est_tol; int est_max_iter;
+  int accumulate; int update_b;
+  double* X;       // k*k workspace
+  double* W;       // packed-upper workspace (k > smem limit)
+  double* Ri;      // packed-upper workspace (k > smem limit)
+  double* Rk; double* Rinv; int ldr;
+  double* Racc;
+  double* B; int ldb;
+  double* shifts;
+  cqr_factor_status* st;
+};
+cudaError_t factor_launch(FactorArgs& a, cudaStream_t stream);
+size_t factor_workspace_bytes(int k);
+
+}  // namespace cqr

@@ -1,0 +1,134 @@
+"""BASELINE.json configurations, full size where the CPU oracle finishes in
+seconds (config 1) and row-scaled otherwise, CUDA path vs the oracle on the
+same seeded bits.  GPU only.
+
+Decision rule: shift_attempts must match exactly whenever
+both implementations accepted their factorizations with a pivot margin above
+100 k u; below that the branch is rounding-determined, and either branch is
+accepted provided the final LOO_F and RRR_F are within 10x of the oracle's.
+"""
+
+from __future__ import annotations
+
+import math
+import warnings
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+U = 1.11e-16
+
+
+def _cq():
+    import paper_2507_07788_b200 as cq
+
+    return cq
+
+
+def _quality(cq, a_dev, res):
+    return (cq.loss_of_orthogonality(res.q, norm="frobenius"),
+            cq.reconstruction_residual(a_dev, res.q, res.r, norm="frobenius"))
+
+
+def _check_quality(mine, ref, k):
+    floor = 10 * U * math.sqrt(k)
+    assert mine[0] <= 10 * max(ref[0], floor), (mine, ref)
+    assert mine[1] <= 10 * max(ref[1], floor), (mine, ref)
+
+
+def _decisions_match(res, ref, k):
+    robust = all(mg > 100 * k * U for mg in ref.pivot_margins) and \
+        all(mg > 100 * k * U for mg in res.pivot_margins)
+    if robust:
+        assert res.shift_attempts == ref.shift_attempts
+        assert len(res.shifts_applied) == len(ref.shifts_applied)
+        np.testing.assert_allclose(res.shifts_applied, ref.shifts_applied, rtol=1e-6)
+    return robust
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2025])
+def test_config1_scholqr3_full_size(seed):
+    cq = _cq()
+    from oracle import cholqr_oracle as co
+    from paper_2507_07788_b200.workloads import host_config
+
+    x = host_config(1, seed=seed)
+    ref = co.s_chol_qr3(x)
+    a = cq.CudaVectorArray.from_numpy(x)
+    res = cq.s_chol_qr3(a)
+    assert res.shifts_applied[0] == pytest.approx(ref.shifts_applied[0], rel=1e-6)
+    _check_quality(_quality(cq, a, res), (co.loo_fro(ref.q), co.rrr_fro(x, ref.q, ref.r)), 64)
+
+
+def test_config1_rscholqr_full_size():
+    cq = _cq()
+    from oracle import cholqr_oracle as co
+    from paper_2507_07788_b200.workloads import host_config
+
+    x = host_config(1, seed=2025)
+    ref = co.rs_chol_qr(x)
+    a = cq.CudaVectorArray.from_numpy(x)
+    res = cq.rs_chol_qr(a)
+    assert res.success
+    _decisions_match(res, ref, 64)
+    _check_quality(_quality(cq, a, res), (co.loo_fro(ref.q), co.rrr_fro(x, ref.q, ref.r)), 64)
+
+
+@pytest.mark.parametrize("cfg_id,m", [(2, 400_000), (5, 2_000_000)])
+def test_config2_5_cholqr2_scaled(cfg_id, m):
+    cq = _cq()
+    from oracle import cholqr_oracle as co
+    from paper_2507_07788_b200.workloads import host_config
+
+    x = host_config(cfg_id, m=m, seed=7)
+    ref = co.chol_qr2(x)
+    a = cq.CudaVectorArray.from_numpy(x)
+    res = cq.chol_qr2(a)
+    assert np.max(np.abs(res.r - ref.r)) <= 1e-10 * np.max(np.abs(ref.r))
+    k = x.shape[1]
+    _check_quality(_quality(cq, a, res), (co.loo_fro(ref.q), co.rrr_fro(x, ref.q, ref.r)), k)
+
+
+def test_config3_rscholqr_scaled():
+    cq = _cq()
+    from oracle import cholqr_oracle as co
+    from paper_2507_07788_b200.workloads import host_config
+
+    x = host_config(3, m=200_000, seed=2025)
+    ref = co.rs_chol_qr(x)
+    a = cq.CudaVectorArray.from_numpy(x)
+    res = cq.rs_chol_qr(a)
+    assert res.success and ref.success
+    _decisions_match(res, ref, 256)
+    _check_quality(_quality(cq, a, res), (co.loo_fro(ref.q), co.rrr_fro(x, ref.q, ref.r)), 256)
+
+
+def test_config4_update_chain_scaled():
+    cq = _cq()
+    from oracle import cholqr_oracle as co
+    from paper_2507_07788_b200.workloads import next_block
+
+    m, p, blocks = 60_000, 16, 6
+    rng = np.random.default_rng(4)
+    q0 = np.linalg.qr(rng.standard_normal((m, p)))[0]
+    ref = co.rs_chol_qr(q0)
+    q_ref, r_ref = ref.q, ref.r
+    res0 = cq.rs_chol_qr(cq.CudaVectorArray.from_numpy(q0))
+    q_dev, r_dev = res0.q, res0.r
+    q_dev.reserve(p * (blocks + 1))
+    for j in range(blocks):
+        a_new = next_block(q_ref, rng, p)
+        r_o = co.chol_qr_update(q_ref, r_ref, a_new)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            r_d = cq.chol_qr_update(q_dev, r_dev, cq.CudaVectorArray.from_numpy(a_new))
+        assert r_d.success and r_o.success
+        _decisions_match(r_d, r_o, p)
+        k = r_d.q.ncols
+        np.testing.assert_array_equal(r_d.r[k - p:, : k - p], 0.0)
+        q_ref, r_ref = r_o.q, r_o.r
+        q_dev, r_dev = r_d.q, r_d.r
+    loo = cq.loss_of_orthogonality(q_dev, norm="frobenius")
+    assert loo <= 10 * max(co.loo_fro(q_ref), 10 * U * math.sqrt(q_dev.ncols))

