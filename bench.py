@@ -1,0 +1,327 @@
+"""Benchmark of the shifted Cholesky QR hot path (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+Default workload: BASELINE.json config 3 (the metric is quoted on shifted
+CholeskyQR3; config 3 is the largest shifted-CholQR3 configuration that fits
+one GPU): `rs_chol_qr` ("shifted CholeskyQR3 with the paper's improved
+shift") on X = U diag(sigma) V^T, 2,000,000 x 256, sigma 1 -> 1e-15.  One
+step = one full `rs_chol_qr` call on the input resident in HBM (all passes,
+k x k stages, status reads).  Rows are sharded evenly over ranks (strong
+scaling: the global matrix is fixed).  value = global rows*cols / step time.
+
+e2e: the same call through the public API from pinned HOST memory (H2D of the
+rank's rows, the run, D2H of Q and R inside the timed region).
+roofline: the dominant kernel (fused TRMM + Gram pass) timed with CUDA events
+on the launching stream inside the timed region; achieved = algorithmic fp64
+flops per launch (k(k+1) per row for the TRMM by the triangular R^-1 plus
+k(k+1) per row for the symmetric Gram) / mean launch time, against the FP64
+peak measured on this pool's B200s (profiles/r01_fp64_peak.json, DMMA).
+cpu_baseline: the CPU oracle (NumPy restatement of the reference, `oracle/`)
+on a bounded row sample of the same construction, all host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+FP64_PEAK_TFS = 37.2          # measured DMMA peak, profiles/r01_fp64_peak.json
+FP64_PEAK_SRC = "measured DMMA.8x8x4 microbenchmark (profiles/r01_fp64_peak.json)"
+
+
+def _args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 5])
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--rows", type=int, default=None, help="override global rows (testing)")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    return p.parse_args()
+
+
+ARGS = _args()
+if ARGS.impl == "reference":
+    # reference CLI pins BLAS threads before NumPy loads (cli.py:179-199)
+    n = str(os.cpu_count() or 1)
+    for v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS", "CHOLQR_THREADS"):
+        os.environ.setdefault(v, n)
+
+import numpy as np  # noqa: E402
+
+sys.path.insert(0, ROOT)
+
+CFG = {
+    1: dict(workload="s_chol_qr3 200000x64 kappa=1e12 (BASELINE config 1)", m=200_000, k=64, algo="s_chol_qr3",
+            cond=12.0, cpu_rows=200_000),
+    2: dict(workload="chol_qr2 4000000x128 N(0,1) (BASELINE config 2)", m=4_000_000, k=128, algo="chol_qr2",
+            cond=None, cpu_rows=1_000_000),
+    3: dict(workload="rs_chol_qr 2000000x256 kappa=1e15 (BASELINE config 3)", m=2_000_000, k=256,
+            algo="rs_chol_qr", cond=15.0, cpu_rows=200_000),
+    5: dict(workload="chol_qr2 128000000x64 N(0,1) (BASELINE config 5)", m=128_000_000, k=64, algo="chol_qr2",
+            cond=None, cpu_rows=4_000_000),
+}
+SEED = 2025
+
+
+def _metric():
+    return "shifted CholQR3 rows*cols/s" if ARGS.config in (1, 3) else "CholQR2 rows*cols/s"
+
+
+# ---------------------------------------------------------------------------- CPU legs
+def _cpu_run(cfg, rows, reps):
+    """Time the oracle (reference restatement) on `rows` rows of the config's
+    construction; returns (seconds per call, sample description)."""
+    from oracle import cholqr_oracle as co
+    from paper_2507_07788_b200.workloads import host_config
+
+    x = host_config(ARGS.config, m=rows, seed=SEED)
+    fn = {"s_chol_qr3": co.s_chol_qr3, "chol_qr2": co.chol_qr2, "rs_chol_qr": co.rs_chol_qr}[cfg["algo"]]
+    fn(x)  # warm-up (cli.py:463)
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        res = fn(x)
+        times.append(time.perf_counter() - t0)
+    passes = res.iterations
+    return float(np.median(times)), f"{cfg['algo']} on {rows}x{cfg['k']} rows of the same construction " \
+                                    f"({passes} passes), median of {reps}"
+
+
+def run_reference():
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = CFG[ARGS.config]
+    rows = ARGS.rows or cfg["cpu_rows"]
+    from oracle import cholqr_oracle as co  # noqa: F401
+    from paper_2507_07788_b200.workloads import host_config
+
+    x = host_config(ARGS.config, m=rows, seed=SEED)
+    fn = {"s_chol_qr3": co.s_chol_qr3, "chol_qr2": co.chol_qr2, "rs_chol_qr": co.rs_chol_qr}[cfg["algo"]]
+    for _ in range(ARGS.warmup):
+        fn(x)
+    t0 = time.perf_counter()
+    for _ in range(ARGS.steps):
+        fn(x)
+    dt = (time.perf_counter() - t0) / ARGS.steps
+    value = rows * cfg["k"] / dt
+    cores = os.cpu_count()
+    line = {
+        "impl": "reference", "metric": _metric(), "value": value, "unit": "rows*cols/s",
+        "n_gpus": ARGS.gpus, "steps": ARGS.steps, "warmup": ARGS.warmup, "ms_per_step": dt * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded)",
+        "config": {"workload": cfg["workload"], "rows_sampled": rows, "cols": cfg["k"]},
+        "cpu_baseline": {"value": value, "unit": "rows*cols/s", "cores": cores, "kind": "port",
+                         "sample": f"oracle {cfg['algo']} on {rows}x{cfg['k']} (bounded row sample of the "
+                                   f"workload), {cores} BLAS threads"},
+        "e2e": {"value": value, "unit": "rows*cols/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, idx):
+        self.idx = idx
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        def run():
+            q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap")
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([s.strip() for s in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = sorted(float(r[1]) for r in self.rows)
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for n, v in zip(names, r[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(self.rows[0][2]), "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------- GPU arm
+def run_ours():
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2507_07788_b200 as cq
+    from paper_2507_07788_b200 import _device
+    from paper_2507_07788_b200.workloads import device_gaussian, device_svd_matrix
+
+    cx = _device.ctx()
+    cfg = CFG[ARGS.config]
+    m, k = (ARGS.rows or cfg["m"]), cfg["k"]
+    space = cq.VectorSpace(m)
+    algo = getattr(cq, cfg["algo"])
+
+    # ---- input resident in HBM (each rank builds the global matrix's own rows)
+    def from_global(x_full):
+        lo, hi = cx.row_range(m)
+        arr = cq.CudaVectorArray.zeros(space, k)
+        arr.device_view().copy_(x_full[lo:hi].T)
+        return arr
+
+    if cfg["cond"] is not None:
+        u_from = "householder" if ARGS.config == 1 else "cholqr2"
+        a = device_svd_matrix(from_global, m, k, cfg["cond"], SEED, u_from=u_from)
+    else:
+        a = device_gaussian(lambda mm, kk: cq.CudaVectorArray.zeros(space, kk), m, k, SEED + rank)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=cx.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- warm-up
+    res = None
+    for _ in range(ARGS.warmup):
+        res = algo(a)
+    barrier()
+
+    # ---- timed region (device-resident input)
+    cx.timer = _device.KernelTimer()
+    launches0 = cx.launches
+    with ClockSampler(local) as clocks:
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(ARGS.steps):
+            res = algo(a)
+        e1.record()
+        barrier()
+    launches = (cx.launches - launches0) // ARGS.steps
+    ktimes = cx.timer.summary()
+    cx.timer = None
+    ms = max_over_ranks(e0.elapsed_time(e1) / ARGS.steps)
+    value = m * k / (ms * 1e-3)
+
+    # ---- dominant kernel roofline
+    dom = "apply_gram" if "apply_gram" in ktimes else "gram"
+    lm = [w[0] for w in ktimes[dom]["work"]]
+    kms = ktimes[dom]["ms"]
+    flops = [2.0 * rows * k * (k + 1) if dom == "apply_gram" else 1.0 * rows * k * (k + 1) for rows in lm]
+    tfs = sum(flops) / (sum(kms) * 1e-3) / 1e12
+    step_share = sum(kms) / ARGS.steps / ms
+    kernel_summary = {n: {"launches_per_step": len(v["ms"]) / ARGS.steps, "mean_ms": float(np.mean(v["ms"]))}
+                      for n, v in ktimes.items()}
+
+    # ---- e2e through the public API from pinned host memory
+    e2e = None
+    if not ARGS.no_e2e:
+        lo, hi = cx.row_range(m)
+        host = torch.empty((k, hi - lo), dtype=torch.float64, pin_memory=True)
+        host.copy_(a.device_view())
+        qhost = torch.empty((k, hi - lo), dtype=torch.float64, pin_memory=True)
+        torch.cuda.synchronize()
+
+        def e2e_step():
+            arr = cq.CudaVectorArray.zeros(space, k)
+            arr.device_view().copy_(host, non_blocking=True)
+            r = algo(arr)
+            qhost.copy_(r.q.device_view(), non_blocking=True)
+            torch.cuda.synchronize()
+            return r.r
+
+        e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(max(1, min(ARGS.steps, 3))):
+            e2e_step()
+        barrier()
+        e2e_ms = max_over_ranks((time.perf_counter() - t0) / max(1, min(ARGS.steps, 3)) * 1e3)
+        h2d = (hi - lo) * k * 8
+        e2e = {"value": m * k / (e2e_ms * 1e-3), "unit": "rows*cols/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": (h2d + k * k * 8) * world,
+               "api": f"CudaVectorArray (H2D from pinned host) -> {cfg['algo']} -> Q, R to host"}
+
+    # ---- CPU baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not ARGS.no_cpu:
+        try:
+            sec, sample = _cpu_run(cfg, cfg["cpu_rows"], 1)
+            cpu = {"value": cfg["cpu_rows"] * k / sec, "unit": "rows*cols/s", "cores": os.cpu_count(),
+                   "kind": "port", "sample": sample + f", {os.cpu_count()} BLAS threads"}
+        except Exception as exc:  # pragma: no cover
+            cpu = {"value": None, "unit": "rows*cols/s", "cores": os.cpu_count(), "kind": "port",
+                   "sample": f"failed: {exc!r}"}
+
+    if rank == 0:
+        line = {
+            "metric": _metric(), "value": value, "unit": "rows*cols/s", "n_gpus": world,
+            "steps": ARGS.steps, "warmup": ARGS.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, built in HBM)",
+            "config": {"workload": cfg["workload"], "rows": m, "cols": k, "algo": cfg["algo"],
+                       "passes": res.iterations, "shift_attempts": res.shift_attempts,
+                       "parallelism": f"row-sharded dp{world}",
+                       "l2": "inputs larger than L2 (%.1f GB)" % (m * k * 8 / 1e9)},
+            "roofline": {"bound": "fp64", "kernel": dom, "achieved": tfs, "peak": FP64_PEAK_TFS,
+                         "unit": "TFLOP/s", "frac": tfs / FP64_PEAK_TFS, "traffic": None,
+                         "peak_source": FP64_PEAK_SRC, "kernel_share_of_step": step_share,
+                         "flops_model": "TRMM k(k+1) + SYRK k(k+1) flops per row"},
+            "kernels": kernel_summary,
+            "gpu_launches": launches,
+            "clocks": clocks.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    if ARGS.impl == "reference":
+        run_reference()
+    else:
+        run_ours()

@@ -119,6 +119,8 @@ int cqr_axpy(double* Y, int64_t ldy, double alpha, const double* X, int64_t ldx,
  * over X (Q may alias X).  Replaces the lincomb + gramian pair of one
  * iteration (algorithms.py:350,352 / :238,:240 / :211 + :209). */
 size_t cqr_apply_gram_workspace_bytes(int64_t m, int k);
+/* Number of kernel launches one cqr_apply_gram call issues for width k. */
+int cqr_apply_gram_launches(int k);
 /* 1 when cqr_apply_gram may run in place (Q == X) for width k. */
 int cqr_apply_gram_inplace_ok(int k);
 int cqr_apply_gram(const double* X, int64_t ldx, int64_t m, int k, const double* Rinv, int ldr, double* Q,

@@ -177,6 +177,9 @@ class Result:
         # relative min pivot min(diag(R)^2)/max(diag(X)) of each accepted
         # factorization: tells how rounding-determined a decision was
         self.pivot_margins = list(margins)
+        # ||X - I||_F measured at the top of each outer iteration (iterated
+        # schemes): tells how rounding-determined the convergence test was
+        self.err_history = []
 
 
 def _margin(x, r):
@@ -268,9 +271,12 @@ def rs_chol_qr(a, cfg=None):
     shifts, attempts, margins = [], [], []
     its = 0
     err = identity_distance(x)
+    hist = [err]
     while not err < tol:
         if its == cfg["max_iter"]:
-            return Result(q, r, its, shifts, attempts, False, err, margins)
+            out = Result(q, r, its, shifts, attempts, False, err, margins)
+            out.err_history = hist
+            return out
         try:
             rk = cholesky_upper(x)
             attempts.append(0)
@@ -284,7 +290,10 @@ def rs_chol_qr(a, cfg=None):
         x = gram(q)
         its += 1
         err = identity_distance(x)
-    return Result(q, r, its, shifts, attempts, True, err, margins)
+        hist.append(err)
+    out = Result(q, r, its, shifts, attempts, True, err, margins)
+    out.err_history = hist
+    return out
 
 
 def _deflated(q, bt):
@@ -335,6 +344,7 @@ def chol_qr_update(q_in, r_in, a_new, cfg=None):
     its = 0
     ok = True
     err = identity_distance(x)
+    hist = [err]
     while not err < tol:
         if its == cfg["max_iter"]:
             ok = False
@@ -350,9 +360,12 @@ def chol_qr_update(q_in, r_in, a_new, cfg=None):
         x = _deflated(q, bt)
         its += 1
         err = identity_distance(x)
+        hist.append(err)
     q_out = np.asfortranarray(np.concatenate([q_in, q], axis=1))
     r_out = np.block([[r_in, b], [np.zeros((p, k)), r]])
-    return Result(q_out, r_out, its, shifts, attempts, ok, err, margins)
+    out = Result(q_out, r_out, its, shifts, attempts, ok, err, margins)
+    out.err_history = hist
+    return out
 
 
 # ----------------------------------------------------------------------------

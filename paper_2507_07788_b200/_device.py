@@ -39,6 +39,7 @@ class DeviceContext:
         self._ws = torch.empty(0, dtype=torch.uint8, device=self.device)
         self._ws2 = torch.empty(0, dtype=torch.uint8, device=self.device)
         self.launches = 0   # libcqr kernel launches issued (bench bookkeeping)
+        self.timer = None   # optional KernelTimer (bench): CUDA events per libcqr call
 
     # ---------------------------------------------------------------- plumbing
     @property
@@ -83,6 +84,33 @@ class DeviceContext:
         out = [torch.empty_like(pad) for _ in range(self.world)]
         torch.distributed.all_gather(out, pad)
         return np.concatenate([o[:s].cpu().numpy() for o, s in zip(out, sizes)], axis=0)
+
+
+class KernelTimer:
+    """CUDA events around each libcqr call on the launching stream, by name.
+    Used by bench.py to time the dominant kernel inside the timed region."""
+
+    def __init__(self):
+        self.events = []   # (name, start, end, work)
+
+    def start(self):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        return e
+
+    def stop(self, name, start, work=None):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.events.append((name, start, e, work))
+
+    def summary(self):
+        torch.cuda.synchronize()
+        out = {}
+        for name, s, e, work in self.events:
+            d = out.setdefault(name, {"ms": [], "work": []})
+            d["ms"].append(s.elapsed_time(e))
+            d["work"].append(work)
+        return out
 
 
 def ctx():

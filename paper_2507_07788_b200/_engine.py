@@ -41,9 +41,12 @@ def gram_device(arr, out=None):
     k = arr.ncols
     g = out if out is not None else torch.empty((k, k), dtype=torch.float64, device=cx.device)
     ws = _gram_ws(arr.m_local, k, k, True)
+    t0 = cx.timer.start() if cx.timer else None
     # G is column-major k x k: torch (k, k) row-major of G^T == G (symmetric)
     _lib.check(cx.lib.cqr_gram(arr.ptr(), arr.ld, arr.m_local, k, g.data_ptr(), k, ws.data_ptr(), ws.numel(),
                                cx.stream), "gram")
+    if t0 is not None:
+        cx.timer.stop("gram", t0, (arr.m_local, k))
     cx.launches += 2
     if cx.world > 1:
         cx.allreduce_(g)
@@ -127,10 +130,13 @@ class Engine:
         bt = self.Bt.data_ptr() if self.Bt is not None else None
         b = self.B.data_ptr() if self.B is not None else None
         base = self.stat.data_ptr()
+        t0 = cx.timer.start() if cx.timer else None
         _lib.check(cx.lib.cqr_factor(ctypes.byref(fc), self.k, self.G.data_ptr(), self.k, bt, max(self.q, 1),
                                      self.q, self.Rk.data_ptr(), self.Rinv.data_ptr(), self.ldr,
                                      self.Racc.data_ptr(), b, max(self.q, 1), base + STATUS_BYTES, base,
                                      self.fws.data_ptr(), self.fws.numel(), cx.stream), "factor")
+        if t0 is not None:
+            cx.timer.stop("factor", t0, (self.k,))
         cx.launches += 1
         self.stat_host.copy_(self.stat, non_blocking=True)
         torch.cuda.current_stream(cx.device).synchronize()
@@ -145,17 +151,22 @@ class Engine:
     def apply(self, src, dst, with_gram=True):
         """dst = src R^-1 (TRMM); with_gram also forms G = dst^T dst."""
         cx = self.cx
+        t0 = cx.timer.start() if cx.timer else None
         if with_gram:
             ws = cx.workspace(cx.lib.cqr_apply_gram_workspace_bytes(src.m_local, self.k))
             _lib.check(cx.lib.cqr_apply_gram(src.ptr(), src.ld, src.m_local, self.k, self.Rinv.data_ptr(),
                                              self.ldr, dst.ptr(), dst.ld, self.G.data_ptr(), self.k,
                                              ws.data_ptr(), ws.numel(), cx.stream), "apply_gram")
-            cx.launches += 3
+            cx.launches += cx.lib.cqr_apply_gram_launches(self.k)
+            if t0 is not None:
+                cx.timer.stop("apply_gram", t0, (src.m_local, self.k))
             if cx.world > 1:
                 cx.allreduce_(self.G)
         else:
             _lib.check(cx.lib.cqr_lincomb(src.ptr(), src.ld, src.m_local, self.k, self.Rinv.data_ptr(), self.ldr,
                                           self.k, 1, dst.ptr(), dst.ld, cx.stream), "apply")
+            if t0 is not None:
+                cx.timer.stop("apply", t0, (src.m_local, self.k))
             cx.launches += 1
 
     def in_place_ok(self):

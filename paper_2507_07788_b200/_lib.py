@@ -78,6 +78,7 @@ SIGNATURES = {
     "cqr_lincomb": (_I, [_P, _I64, _I64, _I, _P, _I, _I, _I, _P, _I64, _P]),
     "cqr_axpy": (_I, [_P, _I64, ctypes.c_double, _P, _I64, _I64, _I, _P]),
     "cqr_apply_gram_workspace_bytes": (_SZ, [_I64, _I]),
+    "cqr_apply_gram_launches": (_I, [_I]),
     "cqr_apply_gram_inplace_ok": (_I, [_I]),
     "cqr_apply_gram": (_I, [_P, _I64, _I64, _I, _P, _I, _P, _I64, _P, _I, _P, _SZ, _P]),
     "cqr_factor_workspace_bytes": (_SZ, [_I]),

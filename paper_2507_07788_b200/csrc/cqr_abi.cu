@@ -114,6 +114,8 @@ size_t cqr_apply_gram_workspace_bytes(int64_t m, int k) {
   return a;
 }
 
+int cqr_apply_gram_launches(int k) { return cqr::apply_gram_fused_supported(k) ? 2 : 3; }
+
 int cqr_apply_gram_inplace_ok(int k) { return (k <= 64 || cqr::apply_gram_fused_supported(k)) ? 1 : 0; }
 
 int cqr_apply_gram(const double* X, int64_t ldx, int64_t m, int k, const double* Rinv, int ldr, double* Q,
