@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define CQR_ABI_VERSION 1
+#define CQR_ABI_VERSION 2
 
 #define CQR_OK 0
 #define CQR_EINVAL (-1)
@@ -89,6 +89,10 @@ typedef struct cqr_factor_status {
   int32_t est_flag;      /* 0 converged, 1 stalled, 2 not converged (UserWarning)      */
   int32_t escalations;   /* escalation steps charged one flop each (ledger eig_est)    */
   int32_t singular_index;/* TriangularSingularError.index                             */
+  double plain_margin;   /* signed min Schur pivot / max diag(X) of the pass's first
+                            attempt (< 0: it broke down): how far the breakdown
+                            decision was from rounding noise                        */
+  double diag_max;       /* max diag(X)                                              */
 } cqr_factor_status;
 
 int cqr_abi_version(void);

@@ -81,7 +81,10 @@ def cholesky_upper(x):
         col = r[:j, j]
         s = x[j, j] - col @ col
         if not s > 0.0:
-            raise OracleBreakdown(j, float(s))
+            exc = OracleBreakdown(j, float(s))
+            top = float(np.max(np.diag(x)))
+            exc.margin = float(s) / top if top > 0 else float("nan")
+            raise exc
         d = math.sqrt(s)
         r[j, j] = d
         if j + 1 < n:
@@ -180,6 +183,19 @@ class Result:
         # ||X - I||_F measured at the top of each outer iteration (iterated
         # schemes): tells how rounding-determined the convergence test was
         self.err_history = []
+        # signed relative pivot of each pass's first factorization attempt
+        # (min Schur diagonal / max diag(X); negative when it broke down)
+        self.decision_margins = []
+
+
+def _attempt(x):
+    """One factorization attempt: (r, signed margin) or (None, margin)."""
+    top = float(np.max(np.diag(x))) if x.size else 1.0
+    try:
+        r = cholesky_upper(x)
+    except OracleBreakdown as exc:
+        return None, exc.pivot_value / top, exc
+    return r, _margin(x, r), None
 
 
 def _margin(x, r):
@@ -272,16 +288,19 @@ def rs_chol_qr(a, cfg=None):
     its = 0
     err = identity_distance(x)
     hist = [err]
+    dms = []
     while not err < tol:
         if its == cfg["max_iter"]:
             out = Result(q, r, its, shifts, attempts, False, err, margins)
             out.err_history = hist
+            out.decision_margins = dms
             return out
-        try:
-            rk = cholesky_upper(x)
+        rk, dm, _ = _attempt(x)
+        dms.append(dm)
+        if rk is not None:
             attempts.append(0)
             xs = x
-        except OracleBreakdown:
+        else:
             rk, tries, xs = _recomputed_shift_attempts(x, m, n, cfg, shifts)
             attempts.append(tries)
         margins.append(_margin(xs, rk))
@@ -293,6 +312,7 @@ def rs_chol_qr(a, cfg=None):
         hist.append(err)
     out = Result(q, r, its, shifts, attempts, True, err, margins)
     out.err_history = hist
+    out.decision_margins = dms
     return out
 
 
@@ -345,10 +365,12 @@ def chol_qr_update(q_in, r_in, a_new, cfg=None):
     ok = True
     err = identity_distance(x)
     hist = [err]
+    dms = []
     while not err < tol:
         if its == cfg["max_iter"]:
             ok = False
             break
+        dms.append(_attempt(_with_shift(x, 0.0))[1])
         rk, tries, xs = _update_attempts(x, m, width, cfg, shifts)
         attempts.append(tries)
         margins.append(_margin(xs, rk))
@@ -365,6 +387,7 @@ def chol_qr_update(q_in, r_in, a_new, cfg=None):
     r_out = np.block([[r_in, b], [np.zeros((p, k)), r]])
     out = Result(q_out, r_out, its, shifts, attempts, ok, err, margins)
     out.err_history = hist
+    out.decision_margins = dms
     return out
 
 

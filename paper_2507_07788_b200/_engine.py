@@ -19,7 +19,7 @@ import torch
 from . import _lib
 from ._device import ctx, round_up
 
-STATUS_BYTES = 80   # sizeof(cqr_factor_status) rounded to 16
+STATUS_BYTES = 96   # sizeof(cqr_factor_status) rounded to 16
 
 
 def _gram_ws(m_local, ka, kb, self_):
@@ -137,7 +137,7 @@ class Engine:
                                      self.fws.data_ptr(), self.fws.numel(), cx.stream), "factor")
         if t0 is not None:
             cx.timer.stop("factor", t0, (self.k,))
-        cx.launches += 1
+        cx.launches += 2
         self.stat_host.copy_(self.stat, non_blocking=True)
         torch.cuda.current_stream(cx.device).synchronize()
         raw = self.stat_host.numpy()

@@ -61,6 +61,8 @@ class FactorStatus(ctypes.Structure):
         ("est_flag", ctypes.c_int32),
         ("escalations", ctypes.c_int32),
         ("singular_index", ctypes.c_int32),
+        ("plain_margin", ctypes.c_double),
+        ("diag_max", ctypes.c_double),
     ]
 
 

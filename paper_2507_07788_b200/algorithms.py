@@ -73,9 +73,11 @@ class AlgoConfig:
 class QRResult:
     """Factors plus run diagnostics (reference algorithms.py:99-156).
 
-    `pivot_margins` is an addition: min diag(R_k)^2 / max diag(X + sigma I)
-    of every accepted factorization, i.e. how far each decision was from the
-    rounding boundary."""
+    `pivot_margins` / `decision_margins` are additions: min diag(R_k)^2 /
+    max diag(X + sigma I) of every accepted factorization, and the signed
+    relative Schur pivot of each pass's first attempt (negative: it broke
+    down), i.e. how far each decision was from the rounding boundary
+    (SURVEY.md §8(c))."""
 
     q: "CudaVectorArray"
     r: np.ndarray
@@ -87,6 +89,7 @@ class QRResult:
     dropped: list = field(default_factory=list)
     panel_profiles: list | None = None
     pivot_margins: list = field(default_factory=list)
+    decision_margins: list = field(default_factory=list)
 
     @property
     def profile(self):
@@ -135,7 +138,9 @@ def _emit_estimate_warning(st):
 
 def _raise_for(st):
     if st.code == _lib.BREAKDOWN:
-        raise CholeskyBreakdown(int(st.pivot_index), float(st.pivot_value))
+        exc = CholeskyBreakdown(int(st.pivot_index), float(st.pivot_value))
+        exc.margin = float(st.plain_margin)   # pivot / max diag: how decisive the breakdown was
+        raise exc
     if st.code == _lib.SHIFT_LIMIT:
         raise ShiftAttemptLimitError(int(st.retries), float(st.last_shift))
     if st.code == _lib.TRI_SINGULAR:
@@ -191,7 +196,8 @@ def chol_qr(a, cfg=None, ledger=None):
     q = _fresh_like(a, n)
     eng.apply(a, q, with_gram=False)
     _charge(ledger, "gemm", _flops.gemm_flops(m, n, n))
-    return QRResult(q=q, r=eng.r_host(), iterations=1, pivot_margins=[st.min_pivot_rel])
+    return QRResult(q=q, r=eng.r_host(), iterations=1, pivot_margins=[st.min_pivot_rel],
+                    decision_margins=[st.plain_margin])
 
 
 def _fresh_like(a, n):
@@ -313,7 +319,7 @@ def rs_chol_qr(a, cfg=None, ledger=None):
     eng.gram(a)
     _charge(ledger, "gemm", _flops.gemm_flops(m, n, n))
     q = None                       # the reference's q = a.copy(), taken lazily
-    shifts, attempts, margins = [], [], []
+    shifts, attempts, margins, dms = [], [], [], []
     its = 0
     while True:
         st = eng.factor(_lib.POLICY_RECOMPUTE, m, n, tol=tol, check_tol=True, stop=(its == cfg.max_iter))
@@ -322,10 +328,11 @@ def rs_chol_qr(a, cfg=None, ledger=None):
             break
         if st.code == _lib.CAPPED:
             return QRResult(q if q is not None else a.copy(), eng.r_host(), its, shifts, attempts,
-                            success=False, orth_error=st.err, pivot_margins=margins)
+                            success=False, orth_error=st.err, pivot_margins=margins, decision_margins=dms)
         _emit_estimate_warning(st)
         _charge_recompute(ledger, n, st)
         _raise_for(st)
+        dms.append(st.plain_margin)
         attempts.append(st.retries)
         shifts.extend(st.shifts)
         margins.append(st.min_pivot_rel)
@@ -336,7 +343,7 @@ def rs_chol_qr(a, cfg=None, ledger=None):
         _charge(ledger, "gemm", _flops.gemm_flops(m, n, n))
         its += 1
     return QRResult(q if q is not None else a.copy(), eng.r_host(), its, shifts, attempts,
-                    success=True, orth_error=st.err, pivot_margins=margins)
+                    success=True, orth_error=st.err, pivot_margins=margins, decision_margins=dms)
 
 
 # ----------------------------------------------------------------------------
@@ -377,7 +384,7 @@ def chol_qr_update(q_in, r_in, a_new, cfg=None, ledger=None):
 
     q = None
     deflated_gram(a_new)
-    shifts, attempts, margins = [], [], []
+    shifts, attempts, margins, dms = [], [], [], []
     its = 0
     success = True
     while True:
@@ -392,6 +399,7 @@ def chol_qr_update(q_in, r_in, a_new, cfg=None, ledger=None):
         _emit_estimate_warning(st)
         _charge_update(ledger, p, st)
         _raise_for(st)
+        dms.append(st.plain_margin)
         attempts.append(st.retries)
         shifts.extend(st.shifts)
         margins.append(st.min_pivot_rel)
@@ -433,7 +441,7 @@ def chol_qr_update(q_in, r_in, a_new, cfg=None, ledger=None):
     b = eng.b_host() if k else np.zeros((0, p))
     r_out = np.block([[r_in, b], [np.zeros((p, k)), eng.r_host()]])
     return QRResult(q_out, r_out, its, shifts, attempts, success=success, orth_error=st.err,
-                    pivot_margins=margins)
+                    pivot_margins=margins, decision_margins=dms)
 
 
 def _lincomb_device(arr, coeff_dev, k, p):
@@ -471,7 +479,7 @@ def pn_chol_qr(a, r_panels, cfg=None, ledger=None):
     widths = panel_widths(a.ncols, r_panels)
     q = CudaVectorArray.zeros(a.space, 0, capacity=a.ncols)
     r = np.zeros((0, 0))
-    shifts, attempts, profiles, margins = [], [], [], []
+    shifts, attempts, profiles, margins, dms = [], [], [], [], []
     its = 0
     success = True
     err = None
@@ -490,7 +498,8 @@ def pn_chol_qr(a, r_panels, cfg=None, ledger=None):
         attempts.extend(res.shift_attempts)
         profiles.append(res.profile)
         margins.extend(res.pivot_margins)
+        dms.extend(res.decision_margins)
         err = res.orth_error
         success = success and res.success
     return QRResult(q, r, its, shifts, attempts, success=success, orth_error=err,
-                    panel_profiles=profiles, pivot_margins=margins)
+                    panel_profiles=profiles, pivot_margins=margins, decision_margins=dms)

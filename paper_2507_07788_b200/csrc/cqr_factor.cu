@@ -15,14 +15,25 @@
 // The loop control that stays on the host (iteration count, QRResult) only
 // reads the status record this kernel writes.
 //
+// Two launches per pass.  `factor_kernel` (one CTA, 512 threads) forms X,
+// measures it, runs the policy's factorization attempts and writes Rk;
+// `factor_finish_kernel` (one warp per column, k/8 CTAs) does the column-
+// independent rest: B += Bt Racc, Racc <- triu(Rk Racc) and the inverse by
+// column back substitution (R Rinv = I), reading Rk from L2.
+//
 // Storage: X (the symmetric input) is kept in a k x k global workspace (L2
-// resident) so shifted retries can restart from it; the Cholesky factor W and
-// the inverse accumulator Ri are packed upper triangles, in shared memory for
-// k <= 128 (2 x 66 KB) and in global workspace otherwise.  The Cholesky is
-// right-looking (row j scaled, rank-1 trailing update), the inverse is the
-// row-by-row back substitution R Rinv = I with rank-1 updates; both need two
-// block barriers per step.  All reductions use a fixed order, so results are
-// bitwise reproducible run to run.
+// resident) so shifted retries restart from it.  The Cholesky is
+// right-looking (pivot check, row scaled, rank-1 trailing update, two block
+// barriers per step) on a packed upper triangle in shared memory:
+//   k <= 128      : the whole packed triangle (66 KB);
+//   128 < k <= 256: the first 32 rows are factored as a panel in shared
+//                   memory and written to Rk, the trailing (k-32) matrix
+//                   S = X22 - R12^T R12 is formed with DMMA from the panel in
+//                   L2 straight into shared memory (202 KB at k = 256), and
+//                   the unblocked loop continues there;
+//   k > 256       : packed triangle in global memory (slow generic path).
+// All reductions use a fixed order: bitwise reproducible run to run.
+#include <algorithm>
 #include <cmath>
 
 #include "cqr_common.cuh"
@@ -32,7 +43,8 @@ namespace cqr {
 
 constexpr int FK_THREADS = 512;
 constexpr int FK_NW = FK_THREADS / 32;
-constexpr int FK_SMEM_K = 128;
+constexpr int FK_SMEM_K = 128;   // whole packed triangle in shared memory
+constexpr int FK_BIG_K = 256;    // panel + shared trailing matrix
 constexpr int FK_MAX_K = 2048;
 
 __host__ __device__ __forceinline__ int64_t pk(int i, int c) { return (int64_t)c * (c + 1) / 2 + i; }
@@ -64,38 +76,32 @@ __device__ __forceinline__ double shift_value(int64_t m, int64_t w, double norm,
 }
 
 struct FState {
-  int code, retries, n_shifts, pivot_index, est_calls, est_flag, escalations, singular_index;
-  double pivot_value, err, norm_est, last_shift, min_pivot_rel, sigma;
+  int code, retries, n_shifts, pivot_index, est_calls, est_flag, escalations, singular_index, attempts;
+  double pivot_value, err, norm_est, last_shift, min_pivot_rel, sigma, plain_margin, diag_max, min_pivot;
 };
 
-// One factorization attempt of X + sigma I into the packed upper factor W.
-// Returns true on success; on breakdown records the pivot in fs (thread 0).
-__device__ bool chol_attempt(const double* __restrict__ X, int k, double sigma, double* W, double* rowbuf,
-                             FState& fs) {
+// Unblocked right-looking Cholesky of the packed upper n x n matrix W (already
+// loaded).  Pivot indices are reported offset by `off`; `smin` carries the
+// smallest pivot seen so far.  Returns false (pivot recorded) on breakdown.
+__device__ bool chol_packed(double* W, int n, int off, double* rowbuf, double& smin, FState& fs) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int c = warp; c < k; c += FK_NW)
-    for (int i = lane; i <= c; i += 32) {
-      double x = X[(int64_t)c * k + i];
-      if (i == c) x = __dadd_rn(x, sigma);
-      W[pk(i, c)] = x;
-    }
-  __syncthreads();
-  for (int j = 0; j < k; ++j) {
+  for (int j = 0; j < n; ++j) {
     const double s = W[pk(j, j)];
     if (!(s > 0.0)) {
-      if (tid == 0) { fs.pivot_index = j; fs.pivot_value = s; }
+      if (tid == 0) { fs.pivot_index = j + off; fs.pivot_value = s; }
       __syncthreads();
       return false;
     }
+    smin = fmin(smin, s);
     const double d = sqrt(s);
-    for (int c = j + 1 + tid; c < k; c += FK_THREADS) {
+    for (int c = j + 1 + tid; c < n; c += FK_THREADS) {
       const double v = W[pk(j, c)] / d;
       W[pk(j, c)] = v;
       rowbuf[c] = v;
     }
     __syncthreads();
     if (tid == 0) W[pk(j, j)] = d;
-    for (int c = j + 1 + warp; c < k; c += FK_NW) {
+    for (int c = j + 1 + warp; c < n; c += FK_NW) {
       const double rc = rowbuf[c];
       double* col = W + pk(0, c);
       for (int i = j + 1 + lane; i <= c; i += 32) col[i] -= rowbuf[i] * rc;
@@ -103,6 +109,115 @@ __device__ bool chol_attempt(const double* __restrict__ X, int k, double sigma, 
     __syncthreads();
   }
   return true;
+}
+
+// Packed n x n upper W (rows/cols offset by `off` in R) -> Rk columns.
+__device__ void store_packed(const double* W, int n, int off, double* Rk, int ldr) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int c = warp; c < n; c += FK_NW)
+    for (int i = lane; i <= c; i += 32) Rk[(int64_t)(c + off) * ldr + off + i] = W[pk(i, c)];
+}
+
+constexpr int FK_PANEL = 32;
+
+// One factorization attempt of X + sigma I; on success the factor is in Rk
+// (upper triangle; the caller zeroes the rest).  `smem_w` is the shared work
+// area, `gW` the global fallback for k > FK_BIG_K.
+__device__ bool chol_attempt(const double* __restrict__ X, int k, double sigma, double* smem_w, double* gW,
+                             double* Rk, int ldr, double* rowbuf, FState& fs) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  double smin = INFINITY;
+  bool ok;
+  if (k <= FK_SMEM_K || k > FK_BIG_K) {
+    double* W = (k <= FK_SMEM_K) ? smem_w : gW;
+    for (int c = warp; c < k; c += FK_NW)
+      for (int i = lane; i <= c; i += 32) {
+        double x = X[(int64_t)c * k + i];
+        if (i == c) x = __dadd_rn(x, sigma);
+        W[pk(i, c)] = x;
+      }
+    __syncthreads();
+    ok = chol_packed(W, k, 0, rowbuf, smin, fs);
+    if (ok) store_packed(W, k, 0, Rk, ldr);
+  } else {
+    // ---- stage 1: rows 0..31 as a row-major panel P[r][c] (c >= r) in shared memory
+    const int b = FK_PANEL;
+    double* P = smem_w;
+    for (int r = warp; r < b; r += FK_NW)
+      for (int c = r + lane; c < k; c += 32) {
+        double x = X[(int64_t)c * k + r];
+        if (c == r) x = __dadd_rn(x, sigma);
+        P[r * k + c] = x;
+      }
+    __syncthreads();
+    ok = true;
+    for (int j = 0; j < b; ++j) {
+      const double s = P[j * k + j];
+      if (!(s > 0.0)) {
+        if (tid == 0) { fs.pivot_index = j; fs.pivot_value = s; }
+        __syncthreads();
+        ok = false;
+        break;
+      }
+      smin = fmin(smin, s);
+      const double d = sqrt(s);
+      for (int c = j + 1 + tid; c < k; c += FK_THREADS) P[j * k + c] = P[j * k + c] / d;
+      __syncthreads();
+      if (tid == 0) P[j * k + j] = d;
+      // rows j+1..b-1 of the panel: P[i][c] -= P[j][i] P[j][c], c >= i
+      for (int i = j + 1 + warp; i < b; i += FK_NW) {
+        const double ri = P[j * k + i];
+        for (int c = i + lane; c < k; c += 32) P[i * k + c] -= ri * P[j * k + c];
+      }
+      __syncthreads();
+    }
+    if (ok) {
+      // panel rows are final rows of R
+      for (int r = warp; r < b; r += FK_NW)
+        for (int c = r + lane; c < k; c += 32) Rk[(int64_t)c * ldr + r] = P[r * k + c];
+      __syncthreads();
+      // ---- stage 2: S = X22 - R12^T R12 (packed upper, n = k - 32) with DMMA,
+      // fragments of R12 read from Rk (L2); S overwrites the panel area
+      const int n = k - b;
+      double* S = smem_w;
+      const int nb = (n + 7) / 8;
+      const int nblk = nb * (nb + 1) / 2;
+      const int g = lane >> 2, t = lane & 3;
+      for (int blk = warp; blk < nblk; blk += FK_NW) {
+        int J = 0, rem = blk;
+        while (rem > J) { rem -= J + 1; ++J; }
+        const int I = rem;  // I <= J
+        const int ci = b + 8 * I + g, cj = b + 8 * J + g;
+        double acc[2] = {0.0, 0.0};
+#pragma unroll
+        for (int l0 = 0; l0 < FK_PANEL; l0 += 4) {
+          const double av = (ci < k) ? Rk[(int64_t)ci * ldr + l0 + t] : 0.0;
+          const double bv = (cj < k) ? Rk[(int64_t)cj * ldr + l0 + t] : 0.0;
+          dmma(acc, av, bv);
+        }
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int i = 8 * I + g, c = 8 * J + 2 * t + e;  // trailing coordinates
+          if (i <= c && c < n) {
+            double x = X[(int64_t)(b + c) * k + b + i];
+            if (i == c) x = __dadd_rn(x, sigma);
+            S[pk(i, c)] = x - acc[e];
+          }
+        }
+      }
+      __syncthreads();
+      ok = chol_packed(S, n, b, rowbuf, smin, fs);
+      if (ok) store_packed(S, n, b, Rk, ldr);
+    }
+  }
+  if (tid == 0) {
+    const double margin = (ok ? smin : fs.pivot_value) / fs.diag_max;
+    if (fs.attempts == 0) fs.plain_margin = margin;
+    fs.attempts += 1;
+    if (ok) fs.min_pivot = smin;
+  }
+  __syncthreads();
+  return ok;
 }
 
 // spectral_norm_estimate (kernels.py:126-178) on the full symmetric X.
@@ -164,20 +279,18 @@ __global__ void __launch_bounds__(FK_THREADS) factor_kernel(FactorArgs a) {
   const int k = a.k;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int kpad = (int)round_up(k, 2);
-  const int64_t npk = pk(0, k);  // k (k+1) / 2
   double* red = fsm;
   double* rowbuf = fsm + 32;
   double* vec = rowbuf + kpad;
   double* wv = vec + kpad;
-  double* W = (k <= FK_SMEM_K) ? wv + kpad : a.W;
-  double* Ri = (k <= FK_SMEM_K) ? W + npk : a.Ri;
+  double* Wsm = wv + kpad;   // shared work area (packed triangle / panel / trailing matrix)
   double* X = a.X;
 
   if (tid == 0) {
     fs.code = CQR_FACTORED; fs.retries = 0; fs.n_shifts = 0; fs.pivot_index = -1; fs.est_calls = 0;
     fs.est_flag = 0; fs.escalations = 0; fs.singular_index = -1;
     fs.pivot_value = 0.0; fs.err = 0.0; fs.norm_est = 0.0; fs.last_shift = 0.0; fs.min_pivot_rel = 0.0;
-    fs.sigma = 0.0;
+    fs.sigma = 0.0; fs.attempts = 0; fs.plain_margin = 0.0; fs.diag_max = 0.0; fs.min_pivot = 0.0;
   }
 
   // ---- 1. X = G (or G - Bt^T Bt), symmetric by construction from the lower triangle
@@ -204,7 +317,13 @@ __global__ void __launch_bounds__(FK_THREADS) factor_kernel(FactorArgs a) {
     loc += d * d;
   }
   const double err = sqrt(block_sum(loc, red));
-  if (tid == 0) fs.err = err;
+  if (tid == 0) {
+    fs.err = err;
+    double dm = -INFINITY;
+    for (int j = 0; j < k; ++j) dm = fmax(dm, X[(int64_t)j * k + j]);
+    fs.diag_max = dm;
+  }
+  __syncthreads();
 
   // `while not err < tol: if its == max_iter: ...` (algorithms.py:341-343):
   // convergence is tested before the iteration cap.
@@ -224,7 +343,7 @@ __global__ void __launch_bounds__(FK_THREADS) factor_kernel(FactorArgs a) {
     const double u2 = 2.0 * a.u;
     switch (a.policy) {
       case CQR_POLICY_PLAIN:
-        ok = chol_attempt(X, k, 0.0, W, rowbuf, fs);
+        ok = chol_attempt(X, k, 0.0, Wsm, a.W, a.Rk, a.ldr, rowbuf, fs);
         break;
       case CQR_POLICY_SHIFT_ONCE: {
         const double est = norm_estimate(X, k, a.est_tol, a.est_max_iter, vec, wv, red, fs);
@@ -232,11 +351,11 @@ __global__ void __launch_bounds__(FK_THREADS) factor_kernel(FactorArgs a) {
         if (fs.code == CQR_ASYMMETRIC) { done = true; break; }
         sigma = shift_value(a.m_global, a.shift_width, est, a.u);
         if (tid == 0) { fs.est_calls = 1; fs.norm_est = est; a.shifts[0] = sigma; fs.n_shifts = 1; }
-        ok = chol_attempt(X, k, sigma, W, rowbuf, fs);
+        ok = chol_attempt(X, k, sigma, Wsm, a.W, a.Rk, a.ldr, rowbuf, fs);
         break;
       }
       case CQR_POLICY_RECOMPUTE: {
-        ok = chol_attempt(X, k, 0.0, W, rowbuf, fs);
+        ok = chol_attempt(X, k, 0.0, Wsm, a.W, a.Rk, a.ldr, rowbuf, fs);
         if (ok) break;
         const double est = norm_estimate(X, k, a.est_tol, a.est_max_iter, vec, wv, red, fs);
         __syncthreads();
@@ -253,7 +372,7 @@ __global__ void __launch_bounds__(FK_THREADS) factor_kernel(FactorArgs a) {
           }
           if (tid == 0) a.shifts[nsh] = sigma;
           ++nsh;
-          ok = chol_attempt(X, k, sigma, W, rowbuf, fs);
+          ok = chol_attempt(X, k, sigma, Wsm, a.W, a.Rk, a.ldr, rowbuf, fs);
           if (ok) break;
           if (tid == 0) fs.escalations += 1;
           sigma = py_max(a.esc * sigma, u2);
@@ -265,7 +384,7 @@ __global__ void __launch_bounds__(FK_THREADS) factor_kernel(FactorArgs a) {
         int retries = 0, nsh = 0;
         sigma = 0.0;
         while (true) {
-          ok = chol_attempt(X, k, sigma, W, rowbuf, fs);
+          ok = chol_attempt(X, k, sigma, Wsm, a.W, a.Rk, a.ldr, rowbuf, fs);
           if (ok) break;
           ++retries;
           if (retries > a.max_shift_attempts) {
@@ -301,81 +420,17 @@ __global__ void __launch_bounds__(FK_THREADS) factor_kernel(FactorArgs a) {
   }
 
   if (!done) {
-    // ---- 4. triangular inverse (zero diagonal -> TriangularSingularError)
+    // ---- 4. TriangularSingularError check, decision margin, zero lower part + padding of Rk
     if (tid == 0) {
       for (int j = 0; j < k; ++j)
-        if (W[pk(j, j)] == 0.0) { fs.code = CQR_TRI_SINGULAR; fs.singular_index = j; break; }
-      double top = -INFINITY, mn = INFINITY;
-      for (int j = 0; j < k; ++j) {
-        const double xd = __dadd_rn(X[(int64_t)j * k + j], sigma);
-        top = fmax(top, xd);
-        const double d = W[pk(j, j)];
-        mn = fmin(mn, d * d);
-      }
-      fs.min_pivot_rel = mn / top;
+        if (a.Rk[(int64_t)j * a.ldr + j] == 0.0) { fs.code = CQR_TRI_SINGULAR; fs.singular_index = j; break; }
+      double top = -INFINITY;
+      for (int j = 0; j < k; ++j) top = fmax(top, __dadd_rn(X[(int64_t)j * k + j], sigma));
+      fs.min_pivot_rel = fs.min_pivot / top;
     }
-    __syncthreads();
-    if (fs.code == CQR_TRI_SINGULAR) done = true;
-  }
-
-  if (!done) {
-    for (int64_t e = tid; e < npk; e += FK_THREADS) Ri[e] = 0.0;
-    __syncthreads();
-    for (int l = k - 1; l >= 0; --l) {
-      const double rll = W[pk(l, l)];
-      for (int c = l + tid; c < k; c += FK_THREADS) {
-        const double v = (((c == l) ? 1.0 : 0.0) - Ri[pk(l, c)]) / rll;
-        Ri[pk(l, c)] = v;
-        rowbuf[c] = v;
-      }
-      __syncthreads();
-      const double* rcol = W + pk(0, l);  // column l of R: rows 0..l
-      for (int c = l + warp; c < k; c += FK_NW) {
-        const double rc = rowbuf[c];
-        double* col = Ri + pk(0, c);
-        for (int i = lane; i < l; i += 32) col[i] += rcol[i] * rc;
-      }
-      __syncthreads();
-    }
-    // with R Rinv = I solved as Rinv(i,c) = (delta - sum_{l>i} R(i,l) Rinv(l,c)) / R(i,i),
-    // the accumulator above holds +sum; rows were finalized as (delta - acc) / R(i,i).
-
-    // ---- 5. write Rk and Rinv (ldr rows, zero below the diagonal and in the padding)
     const int KP = (int)round_up(k, 32);
-    for (int64_t e = tid; e < (int64_t)KP * k; e += FK_THREADS) {
-      const int i = (int)(e % KP), c = (int)(e / KP);
-      const bool up = (i <= c);
-      a.Rk[(int64_t)c * a.ldr + i] = up ? W[pk(i, c)] : 0.0;
-      a.Rinv[(int64_t)c * a.ldr + i] = up ? Ri[pk(i, c)] : 0.0;
-    }
-    __syncthreads();
-
-    // ---- 6. B <- B + Bt Racc_old  (q x k), before Racc changes
-    if (a.update_b && a.q > 0) {
-      for (int64_t e = tid; e < (int64_t)a.q * k; e += FK_THREADS) {
-        const int i = (int)(e % a.q), j = (int)(e / a.q);
-        double s = 0.0;
-        for (int l = 0; l <= j; ++l) s += a.Bt[(int64_t)l * a.ldbt + i] * a.Racc[(int64_t)j * a.ldr + l];
-        a.B[(int64_t)j * a.ldb + i] = a.B[(int64_t)j * a.ldb + i] + s;
-      }
-      __syncthreads();
-    }
-
-    // ---- 7. Racc <- triu(Rk Racc); staged through X (no longer needed)
-    if (a.accumulate) {
-      for (int64_t e = tid; e < kk; e += FK_THREADS) {
-        const int i = (int)(e % k), c = (int)(e / k);
-        double s = 0.0;
-        if (i <= c)
-          for (int l = i; l <= c; ++l) s += W[pk(i, l)] * a.Racc[(int64_t)c * a.ldr + l];
-        X[e] = s;
-      }
-      __syncthreads();
-      for (int64_t e = tid; e < kk; e += FK_THREADS) {
-        const int i = (int)(e % k), c = (int)(e / k);
-        a.Racc[(int64_t)c * a.ldr + i] = X[e];
-      }
-    }
+    for (int c = warp; c < k; c += FK_NW)
+      for (int i = c + 1 + lane; i < KP; i += 32) a.Rk[(int64_t)c * a.ldr + i] = 0.0;
   }
 
   __syncthreads();
@@ -394,7 +449,66 @@ __global__ void __launch_bounds__(FK_THREADS) factor_kernel(FactorArgs a) {
     st->est_flag = fs.est_flag;
     st->escalations = fs.escalations;
     st->singular_index = fs.singular_index;
+    st->plain_margin = fs.plain_margin;
+    st->diag_max = fs.diag_max;
   }
+}
+
+// ---------------------------------------------------------------------------
+// finish: one warp per column c (column-independent work, Rk read from L2)
+//   B(:, c)    += Bt Racc_old(:, c)                    (algorithms.py:445)
+//   Racc(:, c)  = triu(Rk Racc_old)(:, c)               (kernels.py:103-114)
+//   Rinv(:, c)  = R^-1 e_c by back substitution         (kernels.py:85-100)
+constexpr int FF_WARPS = 8;
+
+__global__ void __launch_bounds__(FF_WARPS * 32) factor_finish_kernel(FactorArgs a) {
+  extern __shared__ __align__(16) double ffs[];
+  if (a.st->code != CQR_FACTORED) return;
+  const int k = a.k;
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int c = blockIdx.x * FF_WARPS + wl;
+  if (c >= k) return;
+  double* col = ffs + (size_t)wl * k;   // per-warp column scratch
+  const int ldr = a.ldr;
+  const int KP = (int)round_up(k, 32);
+  const double* R = a.Rk;
+  // old Racc column c
+  for (int l = lane; l <= c; l += 32) col[l] = a.Racc[(int64_t)c * ldr + l];
+  __syncwarp();
+  if (a.update_b && a.q > 0) {
+    for (int i = lane; i < a.q; i += 32) {
+      double s = 0.0;
+      for (int l = 0; l <= c; ++l) s += a.Bt[(int64_t)l * a.ldbt + i] * col[l];
+      a.B[(int64_t)c * a.ldb + i] = a.B[(int64_t)c * a.ldb + i] + s;
+    }
+  }
+  if (a.accumulate) {
+    // new(i) = sum_{l=i..c} R(i,l) old(l): lanes own rows i, loop over l (coalesced R columns)
+    for (int i0 = 0; i0 <= c; i0 += 32) {
+      const int i = i0 + lane;
+      double s = 0.0;
+      for (int l = i0; l <= c; ++l) {
+        const double r = (i <= l) ? R[(int64_t)l * ldr + i] : 0.0;
+        s += r * col[l];
+      }
+      if (i <= c) a.Racc[(int64_t)c * ldr + i] = s;
+    }
+    for (int i = c + 1 + lane; i < KP; i += 32) a.Racc[(int64_t)c * ldr + i] = 0.0;
+  }
+  __syncwarp();
+  // inverse column: acc = e_c; for i = c..0: x_i = acc_i / R_ii; acc_l -= R_li x_i (l < i)
+  for (int l = lane; l <= c; l += 32) col[l] = (l == c) ? 1.0 : 0.0;
+  __syncwarp();
+  double* out = a.Rinv + (int64_t)c * ldr;
+  for (int i = c; i >= 0; --i) {
+    const double x = col[i] / R[(int64_t)i * ldr + i];
+    __syncwarp();
+    if (lane == 0) out[i] = x;
+    const double* ri = R + (int64_t)i * ldr;   // column i of R: R(l, i), l < i
+    for (int l = lane; l < i; l += 32) col[l] -= ri[l] * x;
+    __syncwarp();
+  }
+  for (int i = c + 1 + lane; i < KP; i += 32) out[i] = 0.0;
 }
 
 size_t factor_workspace_bytes(int k) {
@@ -407,15 +521,26 @@ cudaError_t factor_launch(FactorArgs& a, cudaStream_t stream) {
   if (a.k < 1 || a.k > FK_MAX_K) return cudaErrorInvalidValue;
   const int kpad = (int)round_up(a.k, 2);
   size_t smem = (32 + 3 * (size_t)kpad) * sizeof(double);
-  if (a.k <= FK_SMEM_K) smem += 2 * (size_t)pk(0, a.k) * sizeof(double);
+  if (a.k <= FK_SMEM_K) {
+    smem += (size_t)pk(0, a.k) * sizeof(double);
+  } else if (a.k <= FK_BIG_K) {
+    const int64_t n = a.k - FK_PANEL;
+    smem += (size_t)std::max<int64_t>((int64_t)FK_PANEL * a.k, pk(0, (int)n)) * sizeof(double);
+  }
   static bool attr_set = false;
   if (!attr_set) {
-    const int mx = (int)((32 + 3 * FK_MAX_K) * sizeof(double) + 2 * pk(0, FK_SMEM_K) * sizeof(double));
+    const int mx = 227 * 1024;
     cudaError_t e = cudaFuncSetAttribute(factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(factor_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   factor_kernel<<<1, FK_THREADS, smem, stream>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const int blocks = (a.k + FF_WARPS - 1) / FF_WARPS;
+  factor_finish_kernel<<<blocks, FF_WARPS * 32, (size_t)FF_WARPS * a.k * sizeof(double), stream>>>(a);
   return cudaGetLastError();
 }
 

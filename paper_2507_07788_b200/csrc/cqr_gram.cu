@@ -30,30 +30,90 @@ constexpr int GR_THREADS = 160;     // 4 consumer warps + 1 producer warp
 
 size_t gram_smem_bytes() { return GR_STAGES * GR_STAGE_DOUBLES * sizeof(double) + 2 * GR_STAGES * 8 + 64; }
 
-__device__ __forceinline__ void tile_coords(int tile, bool self, int ntj, int& ti, int& tj) {
-  if (self) {
-    int t = tile, r = 0;
-    while (t > r) { t -= r + 1; ++r; }
-    ti = r; tj = t;
-  } else {
-    ti = tile / ntj; tj = tile % ntj;
+// Work items.  Non-self: one item per 64x64 tile.  Self (lower triangle of
+// T x T tiles): items 0 .. T/2-1 pair diagonal tiles (p, T-1-p) -- two
+// half-full tiles make one full CTA load -- item T/2 is the middle diagonal
+// tile when T is odd, then the off-diagonal tiles (ti > tj) in row order.
+// Every item reads two 64-column blocks (or one) and stores two 64x64 slots.
+__host__ __device__ __forceinline__ int self_items(int T) { return (T + 1) / 2 + T * (T - 1) / 2; }
+
+// item -> (column block of operand A, of operand B, kind); kind 0 = off, 1 = diag pair, 2 = single diag
+__device__ __forceinline__ void item_blocks(int item, bool self, int T, int ntj, int& ba, int& bb, int& kind) {
+  if (!self) { ba = item / ntj; bb = item % ntj; kind = 0; return; }
+  const int nd = (T + 1) / 2;
+  if (item < T / 2) { ba = item; bb = T - 1 - item; kind = 1; return; }
+  if (item < nd) { ba = bb = item; kind = 2; return; }
+  int t = item - nd, r = 1;
+  while (t >= r) { t -= r; ++r; }
+  ba = r; bb = t; kind = 0;
+}
+
+// tile (ti, tj) -> (item, slot) of the partial storage
+__device__ __forceinline__ void tile_item(int ti, int tj, bool self, int T, int ntj, int& item, int& slot) {
+  if (!self) { item = ti * ntj + tj; slot = 0; return; }
+  if (ti == tj) {
+    if (2 * ti + 1 == T) { item = ti; slot = 0; return; }      // middle single
+    if (ti < T / 2) { item = ti; slot = 0; } else { item = T - 1 - ti; slot = 1; }
+    return;
+  }
+  item = (T + 1) / 2 + ti * (ti - 1) / 2 + tj;
+  slot = 0;
+}
+
+// 8 k4-steps of one 32x32 register sub-tile; DIAG skips blocks above the diagonal
+template <bool DIAG>
+__device__ __forceinline__ void subtile(double (&acc)[4][4][2], const double* ap, const double* bp, int ks0,
+                                        int ks1, int kstep) {
+  for (int ks = ks0; ks < ks1; ks += kstep) {
+    double a[4], b[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = ap[8 * i * GR_LDP + 4 * ks];
+    if (DIAG) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j <= i; ++j) dmma(acc[i][j], a[i], a[j]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = bp[8 * j * GR_LDP + 4 * ks];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j], a[i], b[j]);
+    }
   }
 }
 
-__global__ void __launch_bounds__(GR_THREADS) gram_kernel(GramArgs args) {
+__device__ __forceinline__ void zero_acc(double (&acc)[4][4][2]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) { acc[i][j][0] = 0.0; acc[i][j][1] = 0.0; }
+}
+
+__device__ __forceinline__ void store_acc(const double (&acc)[4][4][2], double* out, int r0, int c0, int g, int t) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) out[(c0 + 8 * j + 2 * t + e) * GR_CT + r0 + 8 * i + g] = acc[i][j][e];
+}
+
+__global__ void __launch_bounds__(GR_THREADS, 2) gram_kernel(GramArgs args) {
   extern __shared__ __align__(128) double smem[];
   double* stage_base = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + GR_STAGES * GR_STAGE_DOUBLES);
   uint64_t* empty = full + GR_STAGES;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x, split = blockIdx.y;
-  int ti, tj;
-  tile_coords(tile, args.self, args.ntile_j, ti, tj);
-  const bool diag = args.self && ti == tj;
-  const int ia0 = ti * GR_CT, jb0 = tj * GR_CT;
+  const int item = blockIdx.x, split = blockIdx.y;
+  const bool self = args.self != 0;
+  int ba, bb, kind;
+  item_blocks(item, self, args.ntile_i, args.ntile_j, ba, bb, kind);
+  const int ia0 = ba * GR_CT, jb0 = bb * GR_CT;
   const int ncolA = min(GR_CT, args.ka - ia0);
-  const int ncolB = diag ? 0 : min(GR_CT, args.kb - jb0);
+  const int ncolB = (kind == 2) ? 0 : min(GR_CT, args.kb - jb0);
 
   const int64_t npan = args.npanels;
   const int64_t p_begin = npan * split / args.nsplit;
@@ -87,16 +147,14 @@ __global__ void __launch_bounds__(GR_THREADS) gram_kernel(GramArgs args) {
     return;
   }
 
-  // ---------------- consumer warps
-  const int wi = warp >> 1, wj = warp & 1;
-  const bool idle = diag && wi < wj;            // sub-tile wholly above the diagonal
-  const bool wdiag = diag && wi == wj;          // sub-tile on the diagonal
+  // ---------------- consumer warps.  Roles (sub-tile = 32x32 of a 64x64 tile):
+  //  off tile   : warp w -> sub-tile (w>>1, w&1) of tile (A, B)
+  //  diag pair  : w0 -> A(0,0)+A(1,1), w1 -> A(1,0), w2 -> B(0,0)+B(1,1), w3 -> B(1,0)
+  //  single diag: w0 -> (0,0), w2 -> (1,1), w1 / w3 -> (1,0) on even / odd k4 steps
   const int g = lane >> 2, t = lane & 3;
-  double acc[4][4][2];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) { acc[i][j][0] = 0.0; acc[i][j][1] = 0.0; }
+  double acc0[4][4][2], acc1[4][4][2];
+  zero_acc(acc0);
+  zero_acc(acc1);
 
   int it = 0;
   for (int64_t p = p_begin; p < p_end; ++p, ++it) {
@@ -105,49 +163,59 @@ __global__ void __launch_bounds__(GR_THREADS) gram_kernel(GramArgs args) {
     const int64_t r0 = p * GR_BR;
     const int nk4 = (int)imin64(GR_BR, args.rows - r0) >> 2;
     const double* As = stage_base + s * GR_STAGE_DOUBLES;
-    const double* Bs = diag ? As : As + GR_CT * GR_LDP;
-    if (!idle) {
-      const double* ap = As + (32 * wi + g) * GR_LDP + t;
-      const double* bp = Bs + (32 * wj + g) * GR_LDP + t;
-      if (wdiag) {
-        for (int ks = 0; ks < nk4; ++ks) {
-          double a[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) a[i] = ap[8 * i * GR_LDP + 4 * ks];
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j <= i; ++j) dmma(acc[i][j], a[i], a[j]);
-        }
+    const double* Bs = As + GR_CT * GR_LDP;
+    if (kind == 0) {
+      const int wi = warp >> 1, wj = warp & 1;
+      subtile<false>(acc0, As + (32 * wi + g) * GR_LDP + t, Bs + (32 * wj + g) * GR_LDP + t, 0, nk4, 1);
+    } else if (kind == 1) {
+      const double* T = (warp < 2) ? As : Bs;
+      if ((warp & 1) == 0) {
+        subtile<true>(acc0, T + g * GR_LDP + t, nullptr, 0, nk4, 1);
+        subtile<true>(acc1, T + (32 + g) * GR_LDP + t, nullptr, 0, nk4, 1);
       } else {
-        for (int ks = 0; ks < nk4; ++ks) {
-          double a[4], b[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) a[i] = ap[8 * i * GR_LDP + 4 * ks];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) b[j] = bp[8 * j * GR_LDP + 4 * ks];
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) dmma(acc[i][j], a[i], b[j]);
-        }
+        subtile<false>(acc0, T + (32 + g) * GR_LDP + t, T + g * GR_LDP + t, 0, nk4, 1);
       }
+    } else {
+      if (warp == 0) subtile<true>(acc0, As + g * GR_LDP + t, nullptr, 0, nk4, 1);
+      else if (warp == 2) subtile<true>(acc0, As + (32 + g) * GR_LDP + t, nullptr, 0, nk4, 1);
+      else subtile<false>(acc0, As + (32 + g) * GR_LDP + t, As + g * GR_LDP + t, warp == 1 ? 0 : 1, nk4, 2);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
 
-  // ---------------- partial tile -> workspace (tile-local column-major 64x64)
-  double* out = args.ws + ((int64_t)split * args.ntiles + tile) * (GR_CT * GR_CT);
+  // ---------------- partials -> workspace: item slots of 64x64 (tile-local column-major)
+  double* out = args.ws + ((int64_t)split * args.nitems + item) * (2 * GR_CT * GR_CT);
+  if (kind == 0) {
+    store_acc(acc0, out, 32 * (warp >> 1), 32 * (warp & 1), g, t);
+  } else if (kind == 1) {
+    double* o = out + ((warp < 2) ? 0 : GR_CT * GR_CT);
+    if ((warp & 1) == 0) {
+      store_acc(acc0, o, 0, 0, g, t);
+      store_acc(acc1, o, 32, 32, g, t);
+    } else {
+      store_acc(acc0, o, 32, 0, g, t);
+    }
+  } else {
+    // (1,0) is split over warps 1 and 3: warp 3 parks its half in the second slot,
+    // warp 1 adds it after the barrier (fixed order: deterministic)
+    if (warp == 0) store_acc(acc0, out, 0, 0, g, t);
+    if (warp == 2) store_acc(acc0, out, 32, 32, g, t);
+    if (warp == 3) store_acc(acc0, out + GR_CT * GR_CT, 32, 0, g, t);
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (warp == 1) {
+      const double* o3 = out + GR_CT * GR_CT;
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < 4; ++j)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int row = 32 * wi + 8 * i + g, col = 32 * wj + 8 * j + 2 * t + e;
-        out[col * GR_CT + row] = acc[i][j][e];
-      }
+          for (int e = 0; e < 2; ++e) {
+            const int idx = (8 * j + 2 * t + e) * GR_CT + 32 + 8 * i + g;
+            out[idx] = acc0[i][j][e] + o3[idx];
+          }
+    }
+  }
 }
 
 // Fixed-order sum of the split partials.  One thread per output element of
@@ -158,9 +226,10 @@ __global__ void gram_reduce_kernel(GramArgs args, double* G, int ldg) {
     const int gi = (int)(e % args.ka), gj = (int)(e / args.ka);
     if (args.self && gi < gj) continue;
     const int ti = gi / GR_CT, tj = gj / GR_CT;
-    const int tile = args.self ? (ti * (ti + 1) / 2 + tj) : (ti * args.ntile_j + tj);
-    const double* p = args.ws + (int64_t)tile * (GR_CT * GR_CT) + (gj % GR_CT) * GR_CT + (gi % GR_CT);
-    const int64_t stride = (int64_t)args.ntiles * GR_CT * GR_CT;
+    int item, slot;
+    tile_item(ti, tj, args.self != 0, args.ntile_i, args.ntile_j, item, slot);
+    const double* p = args.ws + ((int64_t)item * 2 + slot) * (GR_CT * GR_CT) + (gj % GR_CT) * GR_CT + (gi % GR_CT);
+    const int64_t stride = (int64_t)args.nitems * 2 * GR_CT * GR_CT;
     double s = 0.0;
     for (int sp = 0; sp < args.nsplit; ++sp) s += p[sp * stride];
     G[(int64_t)gj * ldg + gi] = s;
@@ -189,9 +258,11 @@ GramArgs gram_plan(const double* A, int64_t lda, int ka, const double* B, int64_
   a.ntile_i = (int)ceil_div(ka, GR_CT);
   a.ntile_j = (int)ceil_div(a.kb, GR_CT);
   a.ntiles = self ? a.ntile_i * (a.ntile_i + 1) / 2 : a.ntile_i * a.ntile_j;
+  a.nitems = self ? self_items(a.ntile_i) : a.ntiles;
   a.npanels = ceil_div(rows, GR_BR);
-  const int64_t target = 2 * (int64_t)num_sms();  // 2 CTAs per SM
-  int64_t ns = ceil_div(target, a.ntiles);
+  // one full wave: 2 resident CTAs per SM, nsplit * nitems <= 2 * SMs
+  const int64_t target = 2 * (int64_t)num_sms();
+  int64_t ns = target / a.nitems;
   if (ns > a.npanels) ns = a.npanels;
   if (ns < 1) ns = 1;
   a.nsplit = (int)ns;
@@ -199,7 +270,7 @@ GramArgs gram_plan(const double* A, int64_t lda, int ka, const double* B, int64_
 }
 
 size_t gram_workspace_bytes(const GramArgs& a) {
-  return (size_t)a.nsplit * a.ntiles * GR_CT * GR_CT * sizeof(double);
+  return (size_t)a.nsplit * a.nitems * 2 * GR_CT * GR_CT * sizeof(double);
 }
 
 cudaError_t gram_launch(GramArgs& a, double* G, int ldg, cudaStream_t stream) {
@@ -211,7 +282,7 @@ cudaError_t gram_launch(GramArgs& a, double* G, int ldg, cudaStream_t stream) {
     attr_set = true;
   }
   if (a.rows > 0) {
-    dim3 grid(a.ntiles, a.nsplit);
+    dim3 grid(a.nitems, a.nsplit);
     gram_kernel<<<grid, GR_THREADS, smem, stream>>>(a);
   } else {
     a.nsplit = 0;

@@ -16,10 +16,10 @@ struct GramArgs {
   const double* B; int64_t ldb; int kb;
   int64_t rows;       // padded local row count (multiple of 16)
   int self;           // lower-triangular tiles only, mirrored output
-  int ntile_i, ntile_j, ntiles;
+  int ntile_i, ntile_j, ntiles, nitems;
   int nsplit;
   int64_t npanels;
-  double* ws;         // [nsplit][ntiles][64*64]
+  double* ws;         // [nsplit][nitems][2][64*64]
 };
 GramArgs gram_plan(const double* A, int64_t lda, int ka, const double* B, int64_t ldb, int kb, int64_t rows,
                    bool self);
