@@ -529,7 +529,7 @@ cudaError_t factor_launch(FactorArgs& a, cudaStream_t stream) {
   }
   static bool attr_set = false;
   if (!attr_set) {
-    const int mx = 227 * 1024;
+    const int mx = 220 * 1024;  // <= 227 KB minus the static shared state
     cudaError_t e = cudaFuncSetAttribute(factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(factor_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
