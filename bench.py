@@ -199,15 +199,13 @@ def run_ours():
     # ---- input resident in HBM (each rank builds the global matrix's own rows)
     def from_global(x_full):
         lo, hi = cx.row_range(m)
-        arr = cq.CudaVectorArray.zeros(space, k)
-        arr.device_view().copy_(x_full[lo:hi].T)
-        return arr
+        return cq.CudaVectorArray.from_device_colmajor(space, x_full[lo:hi].T)
 
     if cfg["cond"] is not None:
         u_from = "householder" if ARGS.config == 1 else "cholqr2"
         a = device_svd_matrix(from_global, m, k, cfg["cond"], SEED, u_from=u_from)
     else:
-        a = device_gaussian(lambda mm, kk: cq.CudaVectorArray.zeros(space, kk), m, k, SEED + rank)
+        a = device_gaussian(cq.CudaVectorArray.zeros(space, k), SEED + rank)
     torch.cuda.synchronize()
 
     def barrier():
@@ -261,15 +259,15 @@ def run_ours():
     if not ARGS.no_e2e:
         lo, hi = cx.row_range(m)
         host = torch.empty((k, hi - lo), dtype=torch.float64, pin_memory=True)
-        host.copy_(a.device_view())
+        host.copy_(a.to_device_colmajor())
         qhost = torch.empty((k, hi - lo), dtype=torch.float64, pin_memory=True)
         torch.cuda.synchronize()
 
         def e2e_step():
-            arr = cq.CudaVectorArray.zeros(space, k)
-            arr.device_view().copy_(host, non_blocking=True)
+            # host (pinned, column-major) -> HBM -> rs_chol_qr -> Q, R back to host
+            arr = cq.CudaVectorArray.from_device_colmajor(space, host.to(cx.device, non_blocking=True))
             r = algo(arr)
-            qhost.copy_(r.q.device_view(), non_blocking=True)
+            qhost.copy_(r.q.to_device_colmajor(), non_blocking=True)
             torch.cuda.synchronize()
             return r.r
 

@@ -9,13 +9,22 @@
  * reference would add (and the one paper_2507_07788_b200/_lib.py uses).
  *
  * Conventions
- *  - All matrices are fp64, column-major.  A tall array of m rows and k columns
- *    is stored with leading dimension ld (column j starts at X + j*ld).
- *  - Tall operands: ld is even, ld >= round_up(m, 16), base 16-byte aligned,
- *    and rows [m, round_up(m,16)) of every column are zero.  Kernels process
- *    round_up(m,16) rows; outputs keep the padding rows zero.
- *  - Small (k x n) coefficient operands C / Rinv: leading dimension ldc even,
- *    ldc >= round_up(k, 32), rows [k, round_up(k,32)) zero.
+ *  - All matrices are fp64.  TALL arrays (m rows, k columns, column capacity
+ *    ldk >= k) use the row-quad interleaved ("QI") layout:
+ *        element (r, c)  at  X[(r/4)*4*ldk + 4*c + r%4]
+ *    i.e. blocks of 4 consecutive rows, each block holding its k columns as
+ *    contiguous 4-row runs.  A panel of 32 rows is one contiguous 32*ldk run,
+ *    so a single bulk (TMA) copy stages it, and the DMMA fragment loads from
+ *    the staged copy are bank-conflict free without padding.  Storage covers
+ *    m_pad = round_up(m, 16) rows; rows [m, m_pad) must be zero (kernels
+ *    process m_pad rows and keep the padding zero).  Base pointers are 16-byte
+ *    aligned.  cqr_pack_tall / cqr_unpack_tall convert from / to column-major.
+ *  - SMALL outputs (Gram G, Rk, Racc, B) are column-major with a leading
+ *    dimension.  Coefficient operands of a tall product (C of lincomb, R^-1)
+ *    use the tiled layout written by cqr_pack_coeffs and by cqr_factor:
+ *        32 x 64 tiles, tile (kt, nt) at (nt*ceil(k/32) + kt) * 2304,
+ *        element (i, j) at +(j%64)*36 + i%32, zero padded
+ *    (cqr_coeff_doubles(k, n) doubles).
  *  - All pointers except `cfg` are DEVICE pointers; `stream` is a cudaStream_t
  *    (NULL = legacy default stream).  Every call is asynchronous on `stream`;
  *    results are valid once the stream reaches that point.
@@ -23,7 +32,7 @@
  *    error; cqr_last_error() describes the last failure of the calling thread.
  *  - Not thread-safe per workspace buffer.  Gram outputs are LOCAL partial sums
  *    over the rows passed in; under row sharding the caller sums them across
- *    ranks (NCCL allreduce of the lower triangle) before cqr_factor.
+ *    ranks (NCCL allreduce) before cqr_factor, which reads the lower triangle.
  */
 #ifndef CQR_H
 #define CQR_H
@@ -35,7 +44,7 @@
 extern "C" {
 #endif
 
-#define CQR_ABI_VERSION 2
+#define CQR_ABI_VERSION 3
 
 #define CQR_OK 0
 #define CQR_EINVAL (-1)
@@ -110,14 +119,25 @@ int cqr_gram(const double* X, int64_t ldx, int64_t m, int k, double* G, int ldg,
 int cqr_cross_gram(const double* A, int64_t lda, int ka, const double* B, int64_t ldb, int kb, int64_t m, double* G,
                    int ldg, void* ws, size_t ws_bytes, void* stream);
 
-/* Y = X C (m x n).  upper=1 declares C upper triangular (TRMM by R^-1; zero
- * blocks are skipped).  Y may alias X only when n <= 64.  Replaces
- * DenseVectorArray.lincomb (varray.py:157-163, algorithms.py:168-174). */
-int cqr_lincomb(const double* X, int64_t ldx, int64_t m, int k, const double* C, int ldc, int n, int upper,
-                double* Y, int64_t ldy, void* stream);
+/* Y = X C (m x n), C in coefficient tiles (k x n).  upper=1 declares C upper
+ * triangular (TRMM by R^-1; zero blocks are skipped).  Y may alias X only
+ * when n <= 64.  Replaces DenseVectorArray.lincomb (varray.py:157-163,
+ * algorithms.py:168-174). */
+int cqr_lincomb(const double* X, int64_t ldx, int64_t m, int k, const double* C, int n, int upper, double* Y,
+                int64_t ldy, void* stream);
 
 /* Y += alpha X, in place.  Replaces DenseVectorArray.axpy (varray.py:165-171). */
 int cqr_axpy(double* Y, int64_t ldy, double alpha, const double* X, int64_t ldx, int64_t m, int n, void* stream);
+
+/* Layout conversions and column moves (the copy / append / from_numpy /
+ * _iter_columns plumbing of varray.py:139-148,291-319). */
+int cqr_pack_tall(const double* src, int64_t lds, int64_t m, int k, double* dst, int64_t ldk, void* stream);
+int cqr_unpack_tall(const double* src, int64_t ldk, int64_t m, int k, double* dst, int64_t ldd, void* stream);
+/* dst(:, dcol0 + j) = src(:, idx ? idx[j] : j0 + j), j < n (idx: device int array) */
+int cqr_gather_cols(const double* src, int64_t lds, const int* idx, int j0, double* dst, int64_t ldd, int dcol0,
+                    int n, int64_t m, void* stream);
+size_t cqr_coeff_doubles(int k, int n);
+int cqr_pack_coeffs(const double* src, int ld, int k, int n, double* dst, void* stream);
 
 /* Fused pass: Q = X Rinv (Rinv upper triangular) and G = Q^T Q in one stream
  * over X (Q may alias X).  Replaces the lincomb + gramian pair of one
@@ -127,7 +147,7 @@ size_t cqr_apply_gram_workspace_bytes(int64_t m, int k);
 int cqr_apply_gram_launches(int k);
 /* 1 when cqr_apply_gram may run in place (Q == X) for width k. */
 int cqr_apply_gram_inplace_ok(int k);
-int cqr_apply_gram(const double* X, int64_t ldx, int64_t m, int k, const double* Rinv, int ldr, double* Q,
+int cqr_apply_gram(const double* X, int64_t ldx, int64_t m, int k, const double* Rinv_tiles, double* Q,
                    int64_t ldq, double* G, int ldg, void* ws, size_t ws_bytes, void* stream);
 
 /* The k x k stage of one pass, one launch: forms X (G, or the deflated
@@ -135,8 +155,10 @@ int cqr_apply_gram(const double* X, int64_t ldx, int64_t m, int k, const double*
  * factorization attempts with breakdown detection, power-iteration norm
  * estimate and shift rule (kernels.py:61-194, algorithms.py:187-198,295-317,
  * 369-397), inverts the factor (kernels.py:85-100) and accumulates
- * Racc <- triu(Rk Racc) and B <- B + Bt Racc.  Rk, Rinv, Racc: ldr >=
- * round_up(k, 32), zero-padded.  `shifts` receives the shift values tried
+ * Racc <- triu(Rk Racc) and B <- B + Bt Racc (two launches: a single-CTA
+ * factorization and a one-warp-per-column finish).  Rk, Racc: column-major,
+ * ldr >= round_up(k, 32), zero-padded; Rinv: coefficient tiles
+ * (cqr_coeff_doubles(k, k), zero-initialised once).  `shifts` receives the shift values tried
  * (capacity max_shift_attempts + 1).  `status` is device memory. */
 size_t cqr_factor_workspace_bytes(int k);
 int cqr_factor(const cqr_factor_config* cfg, int k, const double* G, int ldg, const double* Bt, int ldbt, int q,

@@ -104,7 +104,7 @@ class Engine:
         self.ldr = max(round_up(k, 32), 32)
         self.G = torch.empty((k, k), dtype=torch.float64, device=dev)
         self.Rk = torch.zeros((k, self.ldr), dtype=torch.float64, device=dev)
-        self.Rinv = torch.zeros((k, self.ldr), dtype=torch.float64, device=dev)
+        self.Rinv = torch.zeros(max(cx.lib.cqr_coeff_doubles(k, k), 1), dtype=torch.float64, device=dev)  # tiles
         self.Racc = torch.zeros((k, self.ldr), dtype=torch.float64, device=dev)
         self.Racc[:, :k] = torch.eye(k, dtype=torch.float64, device=dev)
         self.cap = cfg.max_shift_attempts + 1
@@ -155,7 +155,7 @@ class Engine:
         if with_gram:
             ws = cx.workspace(cx.lib.cqr_apply_gram_workspace_bytes(src.m_local, self.k))
             _lib.check(cx.lib.cqr_apply_gram(src.ptr(), src.ld, src.m_local, self.k, self.Rinv.data_ptr(),
-                                             self.ldr, dst.ptr(), dst.ld, self.G.data_ptr(), self.k,
+                                             dst.ptr(), dst.ld, self.G.data_ptr(), self.k,
                                              ws.data_ptr(), ws.numel(), cx.stream), "apply_gram")
             cx.launches += cx.lib.cqr_apply_gram_launches(self.k)
             if t0 is not None:
@@ -163,7 +163,7 @@ class Engine:
             if cx.world > 1:
                 cx.allreduce_(self.G)
         else:
-            _lib.check(cx.lib.cqr_lincomb(src.ptr(), src.ld, src.m_local, self.k, self.Rinv.data_ptr(), self.ldr,
+            _lib.check(cx.lib.cqr_lincomb(src.ptr(), src.ld, src.m_local, self.k, self.Rinv.data_ptr(),
                                           self.k, 1, dst.ptr(), dst.ld, cx.stream), "apply")
             if t0 is not None:
                 cx.timer.stop("apply", t0, (src.m_local, self.k))

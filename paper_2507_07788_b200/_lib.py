@@ -77,12 +77,17 @@ SIGNATURES = {
     "cqr_gram_workspace_bytes": (_SZ, [_I64, _I, _I, _I]),
     "cqr_gram": (_I, [_P, _I64, _I64, _I, _P, _I, _P, _SZ, _P]),
     "cqr_cross_gram": (_I, [_P, _I64, _I, _P, _I64, _I, _I64, _P, _I, _P, _SZ, _P]),
-    "cqr_lincomb": (_I, [_P, _I64, _I64, _I, _P, _I, _I, _I, _P, _I64, _P]),
+    "cqr_lincomb": (_I, [_P, _I64, _I64, _I, _P, _I, _I, _P, _I64, _P]),
     "cqr_axpy": (_I, [_P, _I64, ctypes.c_double, _P, _I64, _I64, _I, _P]),
+    "cqr_pack_tall": (_I, [_P, _I64, _I64, _I, _P, _I64, _P]),
+    "cqr_unpack_tall": (_I, [_P, _I64, _I64, _I, _P, _I64, _P]),
+    "cqr_gather_cols": (_I, [_P, _I64, _P, _I, _P, _I64, _I, _I, _I64, _P]),
+    "cqr_coeff_doubles": (_SZ, [_I, _I]),
+    "cqr_pack_coeffs": (_I, [_P, _I, _I, _I, _P, _P]),
     "cqr_apply_gram_workspace_bytes": (_SZ, [_I64, _I]),
     "cqr_apply_gram_launches": (_I, [_I]),
     "cqr_apply_gram_inplace_ok": (_I, [_I]),
-    "cqr_apply_gram": (_I, [_P, _I64, _I64, _I, _P, _I, _P, _I64, _P, _I, _P, _SZ, _P]),
+    "cqr_apply_gram": (_I, [_P, _I64, _I64, _I, _P, _P, _I64, _P, _I, _P, _SZ, _P]),
     "cqr_factor_workspace_bytes": (_SZ, [_I]),
     "cqr_factor": (_I, [ctypes.POINTER(FactorConfig), _I, _P, _I, _P, _I, _I, _P, _P, _I, _P, _P, _I, _P, _P,
                         _P, _SZ, _P]),

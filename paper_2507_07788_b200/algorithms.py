@@ -446,17 +446,14 @@ def chol_qr_update(q_in, r_in, a_new, cfg=None, ledger=None):
 
 def _lincomb_device(arr, coeff_dev, k, p):
     """arr (m x k) @ C with C = Bt already on the device as column-major k x p
-    (torch (p, k)): padded to ld = round_up(k, 32) for libcqr."""
-    import torch
-
-    from ._device import ctx, round_up
+    (torch (p, k)), packed into coefficient tiles for libcqr."""
+    from ._device import ctx
+    from .varray import coeff_tiles
 
     cx = ctx()
-    ldc = max(round_up(k, 32), 32)
-    c = torch.zeros((p, ldc), dtype=torch.float64, device=cx.device)
-    c[:, :k] = coeff_dev
+    c = coeff_tiles(coeff_dev, k, p, k)
     out = _fresh_like(arr, p)
-    _lib.check(cx.lib.cqr_lincomb(arr.ptr(), arr.ld, arr.m_local, k, c.data_ptr(), ldc, p, 0, out.ptr(), out.ld,
+    _lib.check(cx.lib.cqr_lincomb(arr.ptr(), arr.ld, arr.m_local, k, c.data_ptr(), p, 0, out.ptr(), out.ld,
                                   cx.stream), "projection")
     cx.launches += 1
     return out

@@ -23,13 +23,13 @@ int cuda_check(cudaError_t e, const char* what) {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-int check_tall(const double* X, int64_t ld, int64_t m, int k, const char* who) {
+// QI tall operand: ldk is the column capacity (>= k)
+int check_tall(const double* X, int64_t ldk, int64_t m, int k, const char* who) {
   if (m < 0 || k < 0) return fail(CQR_EINVAL, std::string(who) + ": negative shape");
   if (k == 0 || m == 0) return CQR_OK;
   if (X == nullptr) return fail(CQR_EINVAL, std::string(who) + ": null pointer");
   if (!aligned16(X)) return fail(CQR_EINVAL, std::string(who) + ": base pointer not 16-byte aligned");
-  if (ld % 2 != 0) return fail(CQR_EINVAL, std::string(who) + ": leading dimension must be even");
-  if (ld < cqr::round_up(m, 16)) return fail(CQR_EINVAL, std::string(who) + ": leading dimension < round_up(m, 16)");
+  if (ldk < k) return fail(CQR_EINVAL, std::string(who) + ": column capacity ldk < k");
   return CQR_OK;
 }
 
@@ -74,21 +74,20 @@ int cqr_cross_gram(const double* A, int64_t lda, int ka, const double* B, int64_
   return gram_common(A, lda, ka, B, ldb, kb, m, false, G, ldg, ws, ws_bytes, stream, "cqr_cross_gram");
 }
 
-int cqr_lincomb(const double* X, int64_t ldx, int64_t m, int k, const double* C, int ldc, int n, int upper,
-                double* Y, int64_t ldy, void* stream) {
+int cqr_lincomb(const double* X, int64_t ldx, int64_t m, int k, const double* C, int n, int upper, double* Y,
+                int64_t ldy, void* stream) {
   int rc = check_tall(X, ldx, m, k, "cqr_lincomb(X)");
   if (rc) return rc;
   rc = check_tall(Y, ldy, m, n, "cqr_lincomb(Y)");
   if (rc) return rc;
   if (n == 0 || m == 0) return CQR_OK;
   if (k == 0) return fail(CQR_EINVAL, "cqr_lincomb: k == 0 with n > 0 (zero-fill the output instead)");
-  if (C == nullptr || !aligned16(C) || ldc % 2 != 0 || ldc < cqr::round_up(k, 32))
-    return fail(CQR_EINVAL, "cqr_lincomb: C needs ldc even and >= round_up(k, 32), 16-byte aligned");
+  if (C == nullptr || !aligned16(C)) return fail(CQR_EINVAL, "cqr_lincomb: C (coefficient tiles) null / unaligned");
   if (upper && n != k) return fail(CQR_EINVAL, "cqr_lincomb: upper-triangular C must be square");
   if (X == Y && (n > 64 || ldx != ldy)) return fail(CQR_EINVAL, "cqr_lincomb: in place only for n <= 64");
   cqr::GemmArgs a{};
   a.X = X; a.ldx = ldx; a.kx = k;
-  a.C = C; a.ldc = ldc;
+  a.C = C;
   a.Y = Y; a.ldy = ldy; a.n = n;
   a.rows = cqr::round_up(m, 16);
   a.upper = upper ? 1 : 0;
@@ -101,8 +100,40 @@ int cqr_axpy(double* Y, int64_t ldy, double alpha, const double* X, int64_t ldx,
   rc = check_tall(X, ldx, m, n, "cqr_axpy(X)");
   if (rc) return rc;
   if (n == 0 || m == 0) return CQR_OK;
-  return cuda_check(cqr::axpy_launch(Y, ldy, alpha, X, ldx, cqr::round_up(m, 16), n, static_cast<cudaStream_t>(stream)),
-                    "cqr_axpy");
+  return cuda_check(cqr::axpy_launch(Y, ldy, alpha, X, ldx, m, n, static_cast<cudaStream_t>(stream)), "cqr_axpy");
+}
+
+int cqr_pack_tall(const double* src, int64_t lds, int64_t m, int k, double* dst, int64_t ldk, void* stream) {
+  int rc = check_tall(dst, ldk, m, k, "cqr_pack_tall(dst)");
+  if (rc) return rc;
+  if (m && k && (src == nullptr || lds < m)) return fail(CQR_EINVAL, "cqr_pack_tall: bad source / lds");
+  return cuda_check(cqr::pack_tall_launch(src, lds, m, k, dst, ldk, static_cast<cudaStream_t>(stream)),
+                    "cqr_pack_tall");
+}
+
+int cqr_unpack_tall(const double* src, int64_t ldk, int64_t m, int k, double* dst, int64_t ldd, void* stream) {
+  int rc = check_tall(src, ldk, m, k, "cqr_unpack_tall(src)");
+  if (rc) return rc;
+  if (m && k && (dst == nullptr || ldd < m)) return fail(CQR_EINVAL, "cqr_unpack_tall: bad destination / ldd");
+  return cuda_check(cqr::unpack_tall_launch(src, ldk, m, k, dst, ldd, static_cast<cudaStream_t>(stream)),
+                    "cqr_unpack_tall");
+}
+
+int cqr_gather_cols(const double* src, int64_t lds, const int* idx, int j0, double* dst, int64_t ldd, int dcol0,
+                    int n, int64_t m, void* stream) {
+  if (n < 0 || dcol0 < 0 || dcol0 + n > ldd) return fail(CQR_EINVAL, "cqr_gather_cols: bad destination columns");
+  if (!idx && (j0 < 0 || j0 + n > lds)) return fail(CQR_EINVAL, "cqr_gather_cols: bad source range");
+  return cuda_check(cqr::gather_cols_launch(src, lds, idx, j0, dst, ldd, dcol0, n, m,
+                                            static_cast<cudaStream_t>(stream)),
+                    "cqr_gather_cols");
+}
+
+size_t cqr_coeff_doubles(int k, int n) { return (size_t)cqr::coeff_tiles_doubles(k, n); }
+
+int cqr_pack_coeffs(const double* src, int ld, int k, int n, double* dst, void* stream) {
+  if (k < 0 || n < 0 || (k && ld < k)) return fail(CQR_EINVAL, "cqr_pack_coeffs: bad shape / ld");
+  return cuda_check(cqr::pack_coeff_launch(src, ld, k, n, dst, static_cast<cudaStream_t>(stream)),
+                    "cqr_pack_coeffs");
 }
 
 size_t cqr_apply_gram_workspace_bytes(int64_t m, int k) {
@@ -118,25 +149,24 @@ int cqr_apply_gram_launches(int k) { return cqr::apply_gram_fused_supported(k) ?
 
 int cqr_apply_gram_inplace_ok(int k) { return (k <= 64 || cqr::apply_gram_fused_supported(k)) ? 1 : 0; }
 
-int cqr_apply_gram(const double* X, int64_t ldx, int64_t m, int k, const double* Rinv, int ldr, double* Q,
-                   int64_t ldq, double* G, int ldg, void* ws, size_t ws_bytes, void* stream) {
+int cqr_apply_gram(const double* X, int64_t ldx, int64_t m, int k, const double* Rinv, double* Q, int64_t ldq,
+                   double* G, int ldg, void* ws, size_t ws_bytes, void* stream) {
   int rc = check_tall(X, ldx, m, k, "cqr_apply_gram(X)");
   if (rc) return rc;
   rc = check_tall(Q, ldq, m, k, "cqr_apply_gram(Q)");
   if (rc) return rc;
   if (k == 0 || m == 0) return CQR_OK;
-  if (Rinv == nullptr || !aligned16(Rinv) || ldr % 2 != 0 || ldr < cqr::round_up(k, 32))
-    return fail(CQR_EINVAL, "cqr_apply_gram: Rinv needs ldr even and >= round_up(k, 32)");
+  if (Rinv == nullptr || !aligned16(Rinv)) return fail(CQR_EINVAL, "cqr_apply_gram: Rinv tiles null / unaligned");
   if (G == nullptr || ldg < k) return fail(CQR_EINVAL, "cqr_apply_gram: bad G / ldg");
   if (ws == nullptr || ws_bytes < cqr_apply_gram_workspace_bytes(m, k))
     return fail(CQR_EINVAL, "cqr_apply_gram: workspace too small");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (cqr::apply_gram_fused_supported(k))
-    return cuda_check(cqr::apply_gram_fused_launch(X, ldx, k, Rinv, ldr, Q, ldq, cqr::round_up(m, 16), G, ldg,
+    return cuda_check(cqr::apply_gram_fused_launch(X, ldx, k, Rinv, Q, ldq, cqr::round_up(m, 16), G, ldg,
                                                    static_cast<double*>(ws), ws_bytes, s),
                       "cqr_apply_gram(fused)");
   if (X == Q && k > 64) return fail(CQR_EINVAL, "cqr_apply_gram: in place needs the fused kernel (k <= 128)");
-  rc = cqr_lincomb(X, ldx, m, k, Rinv, ldr, k, 1, Q, ldq, stream);
+  rc = cqr_lincomb(X, ldx, m, k, Rinv, k, 1, Q, ldq, stream);
   if (rc) return rc;
   return cqr_gram(Q, ldq, m, k, G, ldg, ws, ws_bytes, stream);
 }

@@ -90,6 +90,22 @@ __host__ __device__ constexpr int64_t ceil_div(int64_t a, int64_t b) { return (a
 __host__ __device__ constexpr int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
 __host__ __device__ constexpr int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 
+// ---------------------------------------------------------------- layouts (include/cqr.h)
+// QI tall layout: element (r, c) of an array with column capacity ldk
+__host__ __device__ __forceinline__ int64_t qi_off(int64_t r, int64_t c, int64_t ldk) {
+  return (r >> 2) * 4 * ldk + 4 * c + (r & 3);
+}
+// coefficient tiles: 32 (k) x 64 (n) tiles, each [64][36] (4 padding doubles per
+// column keep the DMMA B-fragment loads bank-conflict free)
+constexpr int CT_K = 32, CT_N = 64, CT_LD = 36, CT_TILE = CT_N * CT_LD;
+__host__ __device__ constexpr int64_t coeff_tiles_doubles(int k, int n) {
+  return ceil_div(k, CT_K) * ceil_div(n, CT_N) * CT_TILE;
+}
+__host__ __device__ __forceinline__ int64_t coeff_off(int kk, int nn, int k) {
+  const int64_t nkt = ceil_div(k, CT_K);
+  return ((nn / CT_N) * nkt + kk / CT_K) * CT_TILE + (nn % CT_N) * CT_LD + kk % CT_K;
+}
+
 // Python's max(a, b): returns b only when b > a, so a NaN first argument wins
 // (kernels.py:194, algorithms.py:317,396 rely on this for NaN propagation).
 __device__ __forceinline__ double py_max(double a, double b) { return (b > a) ? b : a; }

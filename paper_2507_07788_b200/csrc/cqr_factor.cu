@@ -499,16 +499,19 @@ __global__ void __launch_bounds__(FF_WARPS * 32) factor_finish_kernel(FactorArgs
   // inverse column: acc = e_c; for i = c..0: x_i = acc_i / R_ii; acc_l -= R_li x_i (l < i)
   for (int l = lane; l <= c; l += 32) col[l] = (l == c) ? 1.0 : 0.0;
   __syncwarp();
-  double* out = a.Rinv + (int64_t)c * ldr;
+  // Rinv is written straight into the coefficient-tile layout the TRMM reads
+  double* out = a.Rinv + coeff_off(0, c, k);   // column c of its tile column; rows at +i%32 per 32-row tile
+  const int64_t nkt = ceil_div(k, CT_K);
   for (int i = c; i >= 0; --i) {
     const double x = col[i] / R[(int64_t)i * ldr + i];
     __syncwarp();
-    if (lane == 0) out[i] = x;
+    if (lane == 0) out[(i / CT_K) * CT_TILE + i % CT_K] = x;
     const double* ri = R + (int64_t)i * ldr;   // column i of R: R(l, i), l < i
     for (int l = lane; l < i; l += 32) col[l] -= ri[l] * x;
     __syncwarp();
   }
-  for (int i = c + 1 + lane; i < KP; i += 32) out[i] = 0.0;
+  for (int i = c + 1 + lane; i < KP; i += 32) out[(i / CT_K) * CT_TILE + i % CT_K] = 0.0;
+  (void)nkt;
 }
 
 size_t factor_workspace_bytes(int k) {

@@ -1,45 +1,36 @@
-// K2 building blocks: row-panel GEMM Y = X C (TRMM when C = R^-1 is upper
-// triangular) and the in-place axpy.
+// K2 building block: row-panel GEMM Y = X C on QI tall arrays (TRMM when
+// C = R^-1 is upper triangular).
 //
 // Replaces `DenseVectorArray.lincomb` (reference varray.py:157-163: X @ C plus
-// a Fortran re-layout copy) and `DenseVectorArray.axpy` (varray.py:165-171).
-//
-// GEMM layout: CTA tile = 64 rows x 64 output columns, 4 consumer warps in a
-// 2x2 grid of 32x32 register tiles, 1 producer warp.  The K dimension (columns
-// of X) is streamed in chunks of 32: per chunk one stage holds X[64 rows, 32
-// cols] (bulk copy per column, row stride 68 doubles) and C[32, 64 cols]
-// (bulk copy per column, stride 36) -- both strides are 4 (mod 16) doubles so
-// every DMMA fragment load is bank-conflict free.  CTAs are persistent over
-// row tiles (grid.y) so the pipeline runs across tiles.  For upper-triangular
-// C the K chunks and 8x8 blocks that only meet zeros are skipped, so a TRMM
-// costs m k (k+1) flops instead of 2 m k^2.
+// a Fortran re-layout copy).  CTA tile = 64 rows x 64 output columns, four
+// consumer warps in a 2x2 grid of 32x32 register tiles, one producer warp.
+// The K dimension is streamed in chunks of 32 columns: per chunk one stage
+// holds X[64 rows, 32 cols] (16 bulk copies of one 1 KB quad run each) and
+// the 32 x 64 coefficient tile (one 18 KB bulk copy of the pre-tiled C,
+// columns padded to 36 doubles).  Both fragment loads are bank-conflict free:
+// A at quad offset 4*col + row%4, B at 36*col + k.  For a triangular C the K
+// chunks and 8x8 blocks that only meet zeros are skipped (a TRMM costs
+// m k (k+1) flops), and column tiles j and T-1-j share a CTA so every CTA
+// gets the same work.  CTAs are persistent over row tiles in one wave of two
+// CTAs per SM.
 #include "cqr_common.cuh"
 #include "cqr_kernels.h"
 
 namespace cqr {
 
-constexpr int GM_BR = 64;            // rows per tile
-constexpr int GM_KC = 32;            // K chunk
-constexpr int GM_BN = 64;            // output columns per tile
-constexpr int GM_LDX = GM_BR + 4;    // 68
-constexpr int GM_LDC = GM_KC + 4;    // 36
+constexpr int GM_BR = 64;                 // rows per tile (16 quads)
+constexpr int GM_KC = CT_K;               // K chunk (32)
+constexpr int GM_BN = CT_N;               // output columns per tile (64)
+constexpr int GM_XS = (GM_BR / 4) * GM_KC * 4;   // 2048 doubles
 constexpr int GM_STAGES = 3;
-constexpr int GM_XS = GM_KC * GM_LDX;
-constexpr int GM_CS = GM_BN * GM_LDC;
-constexpr int GM_STAGE_DOUBLES = GM_XS + GM_CS;
+constexpr int GM_STAGE_DOUBLES = GM_XS + CT_TILE;
 constexpr int GM_THREADS = 160;
 
 static size_t gemm_smem_bytes() { return GM_STAGES * GM_STAGE_DOUBLES * sizeof(double) + 2 * GM_STAGES * 8 + 64; }
 
-// Column groups: for a triangular C the work of column tile j grows with j,
-// so tiles j and T-1-j share a CTA (equal work per CTA); otherwise one tile
-// per group.  CTAs are persistent over row tiles and run their group's
-// column tiles back to back on each row tile (the second pass over the X
-// row tile hits L2).
 __device__ __forceinline__ int group_tiles(int grp, int T, int upper, int (&tiles)[2]) {
-  if (!upper) { tiles[0] = grp; return 1; }
   tiles[0] = grp;
-  if (T - 1 - grp != grp) { tiles[1] = T - 1 - grp; return 2; }
+  if (upper && T - 1 - grp != grp) { tiles[1] = T - 1 - grp; return 2; }
   return 1;
 }
 
@@ -50,6 +41,7 @@ __global__ void __launch_bounds__(GM_THREADS, 2) gemm_kernel(GemmArgs args) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int tiles[2];
   const int ntl = group_tiles(blockIdx.x, args.ntile_n, args.upper, tiles);
+  const int nkt = (int)ceil_div(args.kx, GM_KC);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < GM_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 4); }
@@ -61,12 +53,10 @@ __global__ void __launch_bounds__(GM_THREADS, 2) gemm_kernel(GemmArgs args) {
     int it = 0;
     for (int64_t rt = blockIdx.y; rt < args.nrow_tiles; rt += gridDim.y) {
       const int64_t r0 = rt * GM_BR;
-      const int nrows = (int)imin64(GM_BR, args.rows - r0);
-      const uint32_t xbytes = nrows * 8;
+      const int nq = (int)imin64(GM_BR, args.rows - r0) >> 2;
       for (int tl = 0; tl < ntl; ++tl) {
-        const int n0 = tiles[tl] * GM_BN;
-        const int ncols = min(GM_BN, args.n - n0);
-        const int kend = args.upper ? min(args.kx, n0 + GM_BN) : args.kx;
+        const int nt = tiles[tl];
+        const int kend = args.upper ? min(args.kx, (nt + 1) * GM_BN) : args.kx;
         const int nchunks = (int)ceil_div(kend, GM_KC);
         for (int ch = 0; ch < nchunks; ++ch, ++it) {
           const int s = it % GM_STAGES;
@@ -76,12 +66,13 @@ __global__ void __launch_bounds__(GM_THREADS, 2) gemm_kernel(GemmArgs args) {
           const int nxc = min(GM_KC, args.kx - kc);
           double* Xs = smem + s * GM_STAGE_DOUBLES;
           double* Cs = Xs + GM_XS;
-          if (lane == 0) mbar_arrive_expect_tx(&full[s], nxc * xbytes + ncols * (GM_KC * 8));
+          if (lane == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)nq * nxc * 32 + CT_TILE * 8);
           __syncwarp();
-          for (int c = lane; c < nxc; c += 32)
-            bulk_g2s(Xs + c * GM_LDX, args.X + (int64_t)(kc + c) * args.ldx + r0, xbytes, &full[s]);
-          for (int c = lane; c < ncols; c += 32)
-            bulk_g2s(Cs + c * GM_LDC, args.C + (int64_t)(n0 + c) * args.ldc + kc, GM_KC * 8, &full[s]);
+          const double* xb = args.X + (r0 >> 2) * 4 * args.ldx + 4 * (int64_t)kc;
+          for (int q = lane; q < nq; q += 32)
+            bulk_g2s(Xs + q * (GM_KC * 4), xb + q * 4 * args.ldx, (uint32_t)nxc * 32, &full[s]);
+          if (lane == 0)
+            bulk_g2s(Cs, args.C + ((int64_t)nt * nkt + ch) * CT_TILE, CT_TILE * 8, &full[s]);
         }
       }
     }
@@ -109,8 +100,9 @@ __global__ void __launch_bounds__(GM_THREADS, 2) gemm_kernel(GemmArgs args) {
         const int kc = ch * GM_KC;
         const double* Xs = smem + s * GM_STAGE_DOUBLES;
         const double* Cs = Xs + GM_XS;
-        const double* xp = Xs + t * GM_LDX + 32 * wi + g;
-        const double* cp = Cs + (32 * wj + g) * GM_LDC + t;
+        // A fragment (row 32wi+8i+g, col kc+4ks+t): quad 8wi+2i+g/4, offset 4(4ks+t) + g%4
+        const double* xp = Xs + (8 * wi + (g >> 2)) * (GM_KC * 4) + 4 * t + (g & 3);
+        const double* cp = Cs + (32 * wj + g) * CT_LD + t;
         const bool tail = kc + GM_KC > args.kx;   // X columns past kx hold stale data
         const int colmax = n0 + 32 * wj + 31;     // last output column of this warp
 #pragma unroll 2
@@ -121,9 +113,9 @@ __global__ void __launch_bounds__(GM_THREADS, 2) gemm_kernel(GemmArgs args) {
           double a[4], b[4];
           const bool kval = !tail || (k4 + t < args.kx);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) a[i] = kval ? xp[4 * ks * GM_LDX + 8 * i] : 0.0;
+          for (int i = 0; i < 4; ++i) a[i] = kval ? xp[2 * i * (GM_KC * 4) + 16 * ks] : 0.0;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) b[j] = cp[8 * j * GM_LDC + 4 * ks];
+          for (int j = 0; j < 4; ++j) b[j] = cp[8 * j * CT_LD + 4 * ks];
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             if (args.upper && k4 > n0 + 32 * wj + 8 * j + 7) continue;  // block of zeros
@@ -134,17 +126,18 @@ __global__ void __launch_bounds__(GM_THREADS, 2) gemm_kernel(GemmArgs args) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
       }
-      // ---- store this tile (rows < rows, cols < n)
+      // ---- store this tile (rows < nrows, cols < n) in the QI layout
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int row = 32 * wi + 8 * i + g;
         if (row >= nrows) continue;
+        double* yq = args.Y + ((r0 + row) >> 2) * 4 * args.ldy + (row & 3);
 #pragma unroll
         for (int j = 0; j < 4; ++j)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int col = n0 + 32 * wj + 8 * j + 2 * t + e;
-            if (col < args.n) args.Y[(int64_t)col * args.ldy + r0 + row] = acc[i][j][e];
+            if (col < args.n) yq[4 * (int64_t)col] = acc[i][j][e];
           }
       }
     }
@@ -170,32 +163,6 @@ cudaError_t gemm_launch(GemmArgs& a, cudaStream_t stream) {
   if (gy > 65535) gy = 65535;
   dim3 grid(ngroups, (unsigned)gy);
   gemm_kernel<<<grid, GM_THREADS, smem, stream>>>(a);
-  return cudaGetLastError();
-}
-
-// ------------------------------------------------------------------ axpy
-__global__ void axpy_kernel(double* __restrict__ Y, int64_t ldy, double alpha, const double* __restrict__ X,
-                            int64_t ldx, int64_t rows2, int n) {
-  const int64_t total = rows2 * n;  // in double2 units
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = e / rows2, r = e % rows2;
-    double2* y = reinterpret_cast<double2*>(Y + j * ldy) + r;
-    const double2 x = reinterpret_cast<const double2*>(X + j * ldx)[r];
-    double2 v = *y;
-    // y + (alpha x) with two roundings, as NumPy's `data += alpha * other`
-    v.x = __dadd_rn(v.x, __dmul_rn(alpha, x.x));
-    v.y = __dadd_rn(v.y, __dmul_rn(alpha, x.y));
-    *y = v;
-  }
-}
-
-cudaError_t axpy_launch(double* Y, int64_t ldy, double alpha, const double* X, int64_t ldx, int64_t rows, int n,
-                        cudaStream_t stream) {
-  const int64_t rows2 = rows / 2;
-  const int64_t total = rows2 * n;
-  if (total == 0) return cudaSuccess;
-  int blocks = (int)imin64(ceil_div(total, 256), 16 * num_sms());
-  axpy_kernel<<<blocks, 256, 0, stream>>>(Y, ldy, alpha, X, ldx, rows2, n);
   return cudaGetLastError();
 }
 

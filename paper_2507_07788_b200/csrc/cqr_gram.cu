@@ -4,37 +4,36 @@
 // Gram X^T X (bit-symmetric by construction: only the lower triangle is
 // computed and mirrored) and the cross Gram Q_in^T Q of the update path.
 //
-// Layout: A, B column-major fp64 (column j at A + j*lda), `rows` = m padded to
-// 16 with zero rows.  The k x k output is cut into 64x64 CTA tiles (self: the
-// lower-triangular tiles only); the rows are cut into `nsplit` contiguous
-// ranges.  Grid = (tile, split): CTAs of one split run side by side and share
-// the row panels through L2.  Each CTA streams 32-row panels of its column
-// blocks into padded shared memory with cp.async.bulk (one bulk copy per
-// column, row stride 36 doubles so the DMMA fragment loads are bank-conflict
-// free), a 3-stage full/empty mbarrier ring fed by one producer warp, and 4
-// consumer warps each own a 32x32 sub-tile held in registers (16 DMMA.8x8x4
-// per 8 LDS.64).  On diagonal tiles blocks above the diagonal are skipped.
-// Per-(split, tile) partials go to a workspace; `reduce` sums them in a fixed
-// split order (deterministic, bitwise run-to-run) and writes G (+ mirror).
+// Layout: tall arrays are row-quad interleaved (cqr.h): element (r, c) at
+// (r/4)*4*ldk + 4c + r%4, so a 32-row panel of a 64-column block is eight
+// contiguous 2 KB runs (one run when the block spans the whole row) and the
+// DMMA fragment loads from the staged copy are bank-conflict free without
+// padding (lane (g, t) of a half-warp hits offset 4g + t (mod 16)).
+//
+// Work split: the k x k output is cut into 64x64 tiles; the self Gram pairs
+// diagonal tiles (p, T-1-p) into one work item (two half tiles = one full
+// load) and gives each off-diagonal tile its own item.  Rows are cut into
+// `nsplit` contiguous ranges with nitems * nsplit <= 2 * SMs (one wave of two
+// resident CTAs per SM).  Each CTA: one producer warp feeding a 3-stage
+// full/empty mbarrier ring with cp.async.bulk (TMA bulk engine), four
+// consumer warps each holding 32x32 register sub-tiles (16 DMMA.8x8x4 per 8
+// LDS.64).  Per-(split, item) partials go to a workspace; `reduce` sums them
+// in a fixed split order (deterministic, bitwise run-to-run).
 #include "cqr_common.cuh"
 #include "cqr_kernels.h"
 
 namespace cqr {
 
-constexpr int GR_BR = 32;           // rows per panel stage
-constexpr int GR_LDP = GR_BR + 4;   // 36 == 4 (mod 16): conflict-free fragments
-constexpr int GR_CT = 64;           // CTA tile edge
+constexpr int GR_BR = 32;                       // rows per stage (8 quads)
+constexpr int GR_CT = 64;                       // tile edge
+constexpr int GR_QD = GR_CT * 4;                // doubles per quad of a 64-column block
+constexpr int GR_BLK = (GR_BR / 4) * GR_QD;     // doubles per staged block (2048)
 constexpr int GR_STAGES = 3;
-constexpr int GR_STAGE_DOUBLES = 2 * GR_CT * GR_LDP;
-constexpr int GR_THREADS = 160;     // 4 consumer warps + 1 producer warp
+constexpr int GR_STAGE_DOUBLES = 2 * GR_BLK;
+constexpr int GR_THREADS = 160;                 // 4 consumer warps + 1 producer warp
 
 size_t gram_smem_bytes() { return GR_STAGES * GR_STAGE_DOUBLES * sizeof(double) + 2 * GR_STAGES * 8 + 64; }
 
-// Work items.  Non-self: one item per 64x64 tile.  Self (lower triangle of
-// T x T tiles): items 0 .. T/2-1 pair diagonal tiles (p, T-1-p) -- two
-// half-full tiles make one full CTA load -- item T/2 is the middle diagonal
-// tile when T is odd, then the off-diagonal tiles (ti > tj) in row order.
-// Every item reads two 64-column blocks (or one) and stores two 64x64 slots.
 __host__ __device__ __forceinline__ int self_items(int T) { return (T + 1) / 2 + T * (T - 1) / 2; }
 
 // item -> (column block of operand A, of operand B, kind); kind 0 = off, 1 = diag pair, 2 = single diag
@@ -60,14 +59,16 @@ __device__ __forceinline__ void tile_item(int ti, int tj, bool self, int T, int 
   slot = 0;
 }
 
-// 8 k4-steps of one 32x32 register sub-tile; DIAG skips blocks above the diagonal
+// k4-steps [ks0, ks1) (stride kstep) of one 32x32 register sub-tile.  ap / bp
+// point at (column g, row t) of the sub-tile's A / B column range in a staged
+// block; quad ks sits at +ks*GR_QD, the 8-column block i at +32*i.
 template <bool DIAG>
 __device__ __forceinline__ void subtile(double (&acc)[4][4][2], const double* ap, const double* bp, int ks0,
                                         int ks1, int kstep) {
   for (int ks = ks0; ks < ks1; ks += kstep) {
     double a[4], b[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) a[i] = ap[8 * i * GR_LDP + 4 * ks];
+    for (int i = 0; i < 4; ++i) a[i] = ap[ks * GR_QD + 32 * i];
     if (DIAG) {
 #pragma unroll
       for (int i = 0; i < 4; ++i)
@@ -75,7 +76,7 @@ __device__ __forceinline__ void subtile(double (&acc)[4][4][2], const double* ap
         for (int j = 0; j <= i; ++j) dmma(acc[i][j], a[i], a[j]);
     } else {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = bp[8 * j * GR_LDP + 4 * ks];
+      for (int j = 0; j < 4; ++j) b[j] = bp[ks * GR_QD + 32 * j];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -98,6 +99,20 @@ __device__ __forceinline__ void store_acc(const double (&acc)[4][4][2], double* 
     for (int j = 0; j < 4; ++j)
 #pragma unroll
       for (int e = 0; e < 2; ++e) out[(c0 + 8 * j + 2 * t + e) * GR_CT + r0 + 8 * i + g] = acc[i][j][e];
+}
+
+// stage rows [r0, r0 + nrows) of columns [c0, c0 + ncol) of a QI array into a
+// dense [quad][64][4] block: one bulk copy per quad, or one in total when the
+// block spans whole rows of the array
+__device__ __forceinline__ void stage_block(double* dst, const double* src, int64_t ldk, int64_t r0, int nrows,
+                                            int c0, int ncol, uint64_t* bar, int lane) {
+  const int nq = nrows >> 2;
+  const double* base = src + (r0 >> 2) * 4 * ldk + 4 * (int64_t)c0;
+  if (ncol == GR_CT && ldk == GR_CT) {
+    if (lane == 0) bulk_g2s(dst, base, (uint32_t)nq * GR_QD * 8, bar);
+  } else {
+    for (int q = lane; q < nq; q += 32) bulk_g2s(dst + q * GR_QD, base + q * 4 * ldk, (uint32_t)ncol * 32, bar);
+  }
 }
 
 __global__ void __launch_bounds__(GR_THREADS, 2) gram_kernel(GramArgs args) {
@@ -126,7 +141,7 @@ __global__ void __launch_bounds__(GR_THREADS, 2) gram_kernel(GramArgs args) {
   __syncthreads();
 
   if (warp == 4) {
-    // ---------------- producer warp: bulk copies of the row panels
+    // ---------------- producer warp
     int it = 0;
     for (int64_t p = p_begin; p < p_end; ++p, ++it) {
       const int s = it % GR_STAGES;
@@ -134,15 +149,12 @@ __global__ void __launch_bounds__(GR_THREADS, 2) gram_kernel(GramArgs args) {
       if (use > 0) mbar_wait(&empty[s], (use - 1) & 1);
       const int64_t r0 = p * GR_BR;
       const int nrows = (int)imin64(GR_BR, args.rows - r0);
-      const uint32_t bytes = nrows * 8;
       double* As = stage_base + s * GR_STAGE_DOUBLES;
-      double* Bs = As + GR_CT * GR_LDP;
-      if (lane == 0) mbar_arrive_expect_tx(&full[s], (ncolA + ncolB) * bytes);
+      double* Bs = As + GR_BLK;
+      if (lane == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)(ncolA + ncolB) * nrows * 8);
       __syncwarp();
-      for (int c = lane; c < ncolA; c += 32)
-        bulk_g2s(As + c * GR_LDP, args.A + (int64_t)(ia0 + c) * args.lda + r0, bytes, &full[s]);
-      for (int c = lane; c < ncolB; c += 32)
-        bulk_g2s(Bs + c * GR_LDP, args.B + (int64_t)(jb0 + c) * args.ldb + r0, bytes, &full[s]);
+      stage_block(As, args.A, args.lda, r0, nrows, ia0, ncolA, &full[s], lane);
+      if (ncolB) stage_block(Bs, args.B, args.ldb, r0, nrows, jb0, ncolB, &full[s], lane);
     }
     return;
   }
@@ -152,6 +164,7 @@ __global__ void __launch_bounds__(GR_THREADS, 2) gram_kernel(GramArgs args) {
   //  diag pair  : w0 -> A(0,0)+A(1,1), w1 -> A(1,0), w2 -> B(0,0)+B(1,1), w3 -> B(1,0)
   //  single diag: w0 -> (0,0), w2 -> (1,1), w1 / w3 -> (1,0) on even / odd k4 steps
   const int g = lane >> 2, t = lane & 3;
+  const int fo = 4 * g + t;   // fragment offset inside a quad
   double acc0[4][4][2], acc1[4][4][2];
   zero_acc(acc0);
   zero_acc(acc1);
@@ -162,23 +175,23 @@ __global__ void __launch_bounds__(GR_THREADS, 2) gram_kernel(GramArgs args) {
     mbar_wait(&full[s], (it / GR_STAGES) & 1);
     const int64_t r0 = p * GR_BR;
     const int nk4 = (int)imin64(GR_BR, args.rows - r0) >> 2;
-    const double* As = stage_base + s * GR_STAGE_DOUBLES;
-    const double* Bs = As + GR_CT * GR_LDP;
+    const double* As = stage_base + s * GR_STAGE_DOUBLES + fo;
+    const double* Bs = As + GR_BLK;
     if (kind == 0) {
       const int wi = warp >> 1, wj = warp & 1;
-      subtile<false>(acc0, As + (32 * wi + g) * GR_LDP + t, Bs + (32 * wj + g) * GR_LDP + t, 0, nk4, 1);
+      subtile<false>(acc0, As + 128 * wi, Bs + 128 * wj, 0, nk4, 1);
     } else if (kind == 1) {
       const double* T = (warp < 2) ? As : Bs;
       if ((warp & 1) == 0) {
-        subtile<true>(acc0, T + g * GR_LDP + t, nullptr, 0, nk4, 1);
-        subtile<true>(acc1, T + (32 + g) * GR_LDP + t, nullptr, 0, nk4, 1);
+        subtile<true>(acc0, T, nullptr, 0, nk4, 1);
+        subtile<true>(acc1, T + 128, nullptr, 0, nk4, 1);
       } else {
-        subtile<false>(acc0, T + (32 + g) * GR_LDP + t, T + g * GR_LDP + t, 0, nk4, 1);
+        subtile<false>(acc0, T + 128, T, 0, nk4, 1);
       }
     } else {
-      if (warp == 0) subtile<true>(acc0, As + g * GR_LDP + t, nullptr, 0, nk4, 1);
-      else if (warp == 2) subtile<true>(acc0, As + (32 + g) * GR_LDP + t, nullptr, 0, nk4, 1);
-      else subtile<false>(acc0, As + (32 + g) * GR_LDP + t, As + g * GR_LDP + t, warp == 1 ? 0 : 1, nk4, 2);
+      if (warp == 0) subtile<true>(acc0, As, nullptr, 0, nk4, 1);
+      else if (warp == 2) subtile<true>(acc0, As + 128, nullptr, 0, nk4, 1);
+      else subtile<false>(acc0, As + 128, As, warp == 1 ? 0 : 1, nk4, 2);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);

@@ -28,9 +28,9 @@ cudaError_t gram_launch(GramArgs& a, double* G, int ldg, cudaStream_t stream);
 
 // ------------------------------------------------------------- row-panel GEMM (K2 building block)
 struct GemmArgs {
-  const double* X; int64_t ldx; int kx;   // m x kx
-  const double* C; int ldc;               // kx x n, rows zero-padded to round_up(kx, 32)
-  double* Y; int64_t ldy; int n;          // m x n
+  const double* X; int64_t ldx; int kx;   // QI m x kx (ldx = column capacity)
+  const double* C;                        // kx x n coefficient tiles
+  double* Y; int64_t ldy; int n;          // QI m x n
   int64_t rows;                           // padded local row count
   int upper;                              // C upper triangular: skip zero blocks
   int ntile_n;
@@ -38,11 +38,18 @@ struct GemmArgs {
 };
 cudaError_t gemm_launch(GemmArgs& a, cudaStream_t stream);
 
-cudaError_t axpy_launch(double* Y, int64_t ldy, double alpha, const double* X, int64_t ldx, int64_t rows, int n,
+cudaError_t axpy_launch(double* Y, int64_t ldy, double alpha, const double* X, int64_t ldx, int64_t m, int n,
                         cudaStream_t stream);
+cudaError_t pack_tall_launch(const double* src, int64_t lds, int64_t m, int k, double* dst, int64_t ldk,
+                             cudaStream_t s);
+cudaError_t unpack_tall_launch(const double* src, int64_t ldk, int64_t m, int k, double* dst, int64_t ldd,
+                               cudaStream_t s);
+cudaError_t gather_cols_launch(const double* src, int64_t lds, const int* idx, int j0, double* dst, int64_t ldd,
+                               int dcol0, int n, int64_t m, cudaStream_t s);
+cudaError_t pack_coeff_launch(const double* src, int ld, int k, int n, double* dst, cudaStream_t s);
 
 // ------------------------------------------------------------- fused TRMM + Gram (K2, k <= 128)
-cudaError_t apply_gram_fused_launch(const double* X, int64_t ldx, int k, const double* Rinv, int ldr, double* Q,
+cudaError_t apply_gram_fused_launch(const double* X, int64_t ldx, int k, const double* Rinv_tiles, double* Q,
                                     int64_t ldq, int64_t rows, double* G, int ldg, double* ws, size_t ws_bytes,
                                     cudaStream_t stream);
 size_t apply_gram_fused_ws_bytes(int64_t rows, int k);
@@ -62,7 +69,7 @@ struct FactorArgs {
   double* X;       // k*k workspace
   double* W;       // packed-upper workspace (k > smem limit)
   double* Ri;      // packed-upper workspace (k > smem limit)
-  double* Rk; double* Rinv; int ldr;
+  double* Rk; double* Rinv; int ldr;   // Rk column-major (ldr); Rinv coefficient tiles
   double* Racc;
   double* B; int ldb;
   double* shifts;

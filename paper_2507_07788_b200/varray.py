@@ -9,13 +9,17 @@ source, axpy mutates in place, gramian returns a host ndarray) and the same
 exceptions (ValueError on space/shape, TypeError on backend mixing,
 IndexError on bad column indices).
 
-HBM layout: one fp64 buffer per array, column-major like the reference's
-Fortran block (reference varray.py:107): column j of the local row shard is
-contiguous, leading dimension ld = round_up(m_local, 16) with zero padding
-rows, so every column starts 128-byte aligned for the bulk-copy engine.
-Column capacity may exceed ncols, so appends (the update path) do not
-reallocate.  Under torch.distributed each rank holds rows
-[r m / P, (r+1) m / P) of every array; `space.dim` is always the GLOBAL m.
+HBM layout (include/cqr.h): the local row shard is stored row-quad
+interleaved -- a (m_pad/4, capacity, 4) fp64 tensor, element (r, c) at
+[r // 4, c, r % 4] -- instead of the reference's Fortran block
+(varray.py:107).  The interface never exposes rows, so the layout is free:
+a 32-row panel is one contiguous run (one bulk copy per pipeline stage) and
+the DMMA fragment loads are bank-conflict free.  m_pad = round_up(m, 16),
+padding rows are zero.  Column capacity may exceed ncols, so appends (the
+update path) do not reallocate.  Under torch.distributed each rank holds
+rows [r m / P, (r+1) m / P) of every array; `space.dim` is the GLOBAL m.
+Host <-> device transfers go through column-major staging converted by the
+libcqr pack / unpack kernels, in row chunks.
 """
 
 from __future__ import annotations
@@ -27,6 +31,8 @@ import torch
 
 from . import _lib
 from ._device import ctx, round_up
+
+_CHUNK_ROWS = 1 << 22   # rows per host-transfer chunk (multiple of 16)
 
 
 @dataclass(frozen=True)
@@ -52,15 +58,23 @@ def _as_index_list(indices, ncols, who):
     return idx
 
 
-def upload_coeffs(c, rows_pad=None):
-    """Host k x n coefficients -> device buffer with zero-padded rows
-    (ld = round_up(k, 32)), the layout libcqr expects for C / R^-1."""
+def coeff_tiles(c_dev, k, n, ld):
+    """Column-major k x n device coefficients (leading dimension ld) -> the
+    tiled operand layout of libcqr (cqr_pack_coeffs)."""
+    cx = ctx()
+    out = torch.empty(max(cx.lib.cqr_coeff_doubles(k, n), 1), dtype=torch.float64, device=cx.device)
+    if k and n:
+        _lib.check(cx.lib.cqr_pack_coeffs(c_dev.data_ptr(), ld, k, n, out.data_ptr(), cx.stream), "pack_coeffs")
+        cx.launches += 1
+    return out
+
+
+def upload_coeffs(c):
+    """Host k x n coefficients -> device coefficient tiles."""
     c = np.asarray(c, dtype=float)
     k, n = c.shape
-    ld = rows_pad or max(round_up(k, 32), 32)
-    host = np.zeros((n, ld))
-    host[:, :k] = c.T
-    return torch.from_numpy(host).to(ctx().device, non_blocking=False), ld
+    dev = torch.from_numpy(np.ascontiguousarray(c.T)).to(ctx().device)   # (n, k): column-major k x n
+    return coeff_tiles(dev, k, n, max(k, 1))
 
 
 class CudaVectorArray:
@@ -68,21 +82,20 @@ class CudaVectorArray:
 
     def __init__(self, space, buf, ncols):
         self.space = space
-        self._buf = buf          # (capacity, ld) float64, row j = column j
+        self._buf = buf          # (m_pad/4, capacity, 4) float64
         self._k = int(ncols)
 
     # ------------------------------------------------------------ construction
     @staticmethod
     def _local_rows(space):
-        lo, hi = ctx().row_range(space.dim)
-        return lo, hi
+        return ctx().row_range(space.dim)
 
     @classmethod
     def _alloc(cls, space, cap, zero=True):
         lo, hi = cls._local_rows(space)
-        ld = max(round_up(hi - lo, 16), 16)
+        nq = max(round_up(hi - lo, 16), 16) // 4
         fn = torch.zeros if zero else torch.empty
-        return fn((max(cap, 0), ld), dtype=torch.float64, device=ctx().device)
+        return fn((nq, max(cap, 0), 4), dtype=torch.float64, device=ctx().device)
 
     @classmethod
     def zeros(cls, space, k, capacity=None):
@@ -102,7 +115,19 @@ class CudaVectorArray:
         if k:
             lo, hi = cls._local_rows(space)
             local = block[lo:hi]
-            out._buf[:k, : hi - lo].copy_(torch.from_numpy(np.ascontiguousarray(local.T)))
+            for r0 in range(0, hi - lo, _CHUNK_ROWS):
+                r1 = min(hi - lo, r0 + _CHUNK_ROWS)
+                stage = torch.from_numpy(np.ascontiguousarray(local[r0:r1].T)).to(out._buf.device, non_blocking=True)
+                out._load_rows(stage, r0)
+        return out
+
+    @classmethod
+    def from_device_colmajor(cls, space, t, capacity=None):
+        """Build from a device (k, m_local) tensor (column-major local shard)."""
+        k = t.shape[0]
+        out = cls.zeros(space, k, capacity)
+        if k:
+            out._load_rows(t.contiguous(), 0)
         return out
 
     @classmethod
@@ -117,6 +142,14 @@ class CudaVectorArray:
         block = np.column_stack(cols) if cols else np.zeros((a.space.dim, 0))
         return cls.from_numpy(block)
 
+    def _load_rows(self, stage, r0):
+        """Pack a device column-major (k, rows) block into local rows r0.."""
+        cx = ctx()
+        k, rows = stage.shape
+        dst = self._buf.data_ptr() + 8 * (r0 // 4) * 4 * self.capacity
+        _lib.check(cx.lib.cqr_pack_tall(stage.data_ptr(), rows, rows, k, dst, self.capacity, cx.stream), "pack")
+        cx.launches += 1
+
     # ------------------------------------------------------------ views
     @property
     def ncols(self):
@@ -124,23 +157,29 @@ class CudaVectorArray:
 
     @property
     def ld(self):
+        """Column capacity (the QI layout's ldk)."""
         return self._buf.shape[1]
+
+    capacity = ld
 
     @property
     def m_local(self):
         lo, hi = self._local_rows(self.space)
         return hi - lo
 
-    @property
-    def capacity(self):
-        return self._buf.shape[0]
+    def ptr(self):
+        return self._buf.data_ptr()
 
-    def ptr(self, col=0):
-        return self._buf.data_ptr() + 8 * col * self.ld
-
-    def device_view(self):
-        """(ncols, m_local) torch view of the local shard (row j = column j)."""
-        return self._buf[: self._k, : self.m_local]
+    def to_device_colmajor(self):
+        """Device (k, m_local) column-major copy of the local shard."""
+        cx = ctx()
+        m = self.m_local
+        out = torch.empty((self._k, m), dtype=torch.float64, device=cx.device)
+        if self._k and m:
+            _lib.check(cx.lib.cqr_unpack_tall(self.ptr(), self.ld, m, self._k, out.data_ptr(), m, cx.stream),
+                       "unpack")
+            cx.launches += 1
+        return out
 
     def __len__(self):
         return self._k
@@ -154,32 +193,41 @@ class CudaVectorArray:
         if type(self) is not type(other):
             raise TypeError(f"backend mismatch: {type(self).__name__} vs {type(other).__name__}")
 
+    def _gather(self, src, idx=None, j0=0, n=None, dcol0=0):
+        cx = ctx()
+        n = len(idx) if idx is not None else n
+        if not n:
+            return
+        idx_dev = torch.tensor(idx, dtype=torch.int32, device=cx.device) if idx is not None else None
+        _lib.check(cx.lib.cqr_gather_cols(src.ptr(), src.ld, idx_dev.data_ptr() if idx_dev is not None else None,
+                                          j0, self.ptr(), self.ld, dcol0, n, self.m_local, cx.stream), "gather")
+        cx.launches += 1
+
     # ------------------------------------------------------------ interface
     def copy(self, indices=None):
         if indices is None:
             out = CudaVectorArray(self.space, self._alloc(self.space, self._k, zero=False), self._k)
-            out._buf.copy_(self._buf[: self._k])
+            out._gather(self, j0=0, n=self._k)
             return out
         idx = _as_index_list(indices, self._k, "copy")
         out = CudaVectorArray(self.space, self._alloc(self.space, len(idx), zero=False), len(idx))
-        if idx:
-            out._buf.copy_(self._buf[torch.tensor(idx, device=self._buf.device)])
+        out._gather(self, idx=idx)
         return out
 
     def reserve(self, capacity):
         """Grow the column capacity (keeps contents)."""
         if capacity <= self.capacity:
             return
-        buf = self._alloc(self.space, capacity)
-        buf[: self._k].copy_(self._buf[: self._k])
-        self._buf = buf
+        old = CudaVectorArray(self.space, self._buf, self._k)
+        self._buf = self._alloc(self.space, capacity)
+        self._gather(old, j0=0, n=self._k)
 
     def append(self, other):
         self._check_space(other)
         need = self._k + other._k
         if need > self.capacity:
             self.reserve(max(need, 2 * self.capacity))
-        self._buf[self._k: need].copy_(other._buf[: other._k])
+        self._gather(other, j0=0, n=other._k, dcol0=self._k)
         self._k = need
 
     def gramian(self, other=None):
@@ -199,9 +247,9 @@ class CudaVectorArray:
         n = coeffs.shape[1]
         out = CudaVectorArray(self.space, self._alloc(self.space, n, zero=self._k == 0), n)
         if n and self._k:
-            c, ldc = upload_coeffs(coeffs)
+            c = upload_coeffs(coeffs)
             cx = ctx()
-            _lib.check(cx.lib.cqr_lincomb(self.ptr(), self.ld, self.m_local, self._k, c.data_ptr(), ldc, n, 0,
+            _lib.check(cx.lib.cqr_lincomb(self.ptr(), self.ld, self.m_local, self._k, c.data_ptr(), n, 0,
                                           out.ptr(), out.ld, cx.stream), "lincomb")
             cx.launches += 1
         return out
@@ -219,15 +267,13 @@ class CudaVectorArray:
     def remove_columns(self, indices):
         idx = set(_as_index_list(indices, self._k, "remove_columns"))
         keep = [j for j in range(self._k) if j not in idx]
-        buf = self._alloc(self.space, max(len(keep), 0), zero=False)
-        if keep:
-            buf.copy_(self._buf[torch.tensor(keep, device=self._buf.device)])
-        self._buf = buf
-        self._k = len(keep)
+        out = CudaVectorArray(self.space, self._alloc(self.space, len(keep), zero=False), len(keep))
+        out._gather(self, idx=keep)
+        self._buf, self._k = out._buf, out._k
 
     def to_numpy(self):
         """Copy of the full m x k block (Fortran order), gathered over ranks."""
-        local = self.device_view().cpu().numpy().T
+        local = self.to_device_colmajor().cpu().numpy().T
         full = ctx().allgather_rows(local, self.space.dim)
         return np.asfortranarray(full)
 

@@ -91,14 +91,20 @@ def device_svd_matrix(arr_factory, m, k, log10_cond, seed, u_from="householder")
     return arr_factory(x)
 
 
-def device_gaussian(arr_factory_empty, m, k, seed, chunk_rows=1 << 24):
-    """N(0,1) m x k written column-block-wise straight into device storage."""
+def device_gaussian(arr, seed, chunk_quads=1 << 22):
+    """Fill a device array (QI storage) with N(0,1), padding rows kept zero.
+    The values are a function of the seed and the local shard only."""
     import torch
 
     gen = torch.Generator(device="cuda").manual_seed(seed)
-    arr = arr_factory_empty(m, k)
-    view = arr.device_view()         # (k, m_local)
-    for r0 in range(0, view.shape[1], chunk_rows):
-        r1 = min(view.shape[1], r0 + chunk_rows)
-        view[:, r0:r1].normal_(generator=gen)
+    buf = arr._buf[:, : arr.ncols, :]
+    nq = buf.shape[0]
+    for q0 in range(0, nq, chunk_quads):
+        buf[q0: q0 + chunk_quads].normal_(generator=gen)
+    m = arr.m_local
+    qa = m // 4
+    if m % 4:
+        buf[qa, :, m % 4:] = 0.0
+        qa += 1
+    buf[qa:] = 0.0
     return arr

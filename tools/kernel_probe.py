@@ -30,8 +30,9 @@ def main():
     from paper_2507_07788_b200._engine import Engine
 
     m, k = a.m, a.k
-    x = cq.CudaVectorArray.zeros(cq.VectorSpace(m), k)
-    x.device_view().normal_(generator=torch.Generator(device="cuda").manual_seed(1))
+    from paper_2507_07788_b200.workloads import device_gaussian
+
+    x = device_gaussian(cq.CudaVectorArray.zeros(cq.VectorSpace(m), k), 1)
     q = cq.CudaVectorArray.zeros(cq.VectorSpace(m), k)
     eng = Engine(k, cq.AlgoConfig())
     eng.gram(x)
