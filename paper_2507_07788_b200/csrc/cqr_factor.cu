@@ -466,52 +466,74 @@ __global__ void __launch_bounds__(FF_WARPS * 32) factor_finish_kernel(FactorArgs
   if (a.st->code != CQR_FACTORED) return;
   const int k = a.k;
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  const int c = blockIdx.x * FF_WARPS + wl;
-  if (c >= k) return;
-  double* col = ffs + (size_t)wl * k;   // per-warp column scratch
+  const int c0 = blockIdx.x * FF_WARPS;
+  const int c = c0 + wl;
+  const bool active = c < k;
+  double* col = ffs + (size_t)wl * k;                 // per-warp column scratch
+  double* rbuf = ffs + (size_t)FF_WARPS * k;          // 2 x k: staged column of R
   const int ldr = a.ldr;
   const int KP = (int)round_up(k, 32);
   const double* R = a.Rk;
-  // old Racc column c
-  for (int l = lane; l <= c; l += 32) col[l] = a.Racc[(int64_t)c * ldr + l];
-  __syncwarp();
-  if (a.update_b && a.q > 0) {
-    for (int i = lane; i < a.q; i += 32) {
-      double s = 0.0;
-      for (int l = 0; l <= c; ++l) s += a.Bt[(int64_t)l * a.ldbt + i] * col[l];
-      a.B[(int64_t)c * a.ldb + i] = a.B[(int64_t)c * a.ldb + i] + s;
-    }
-  }
-  if (a.accumulate) {
-    // new(i) = sum_{l=i..c} R(i,l) old(l): lanes own rows i, loop over l (coalesced R columns)
-    for (int i0 = 0; i0 <= c; i0 += 32) {
-      const int i = i0 + lane;
-      double s = 0.0;
-      for (int l = i0; l <= c; ++l) {
-        const double r = (i <= l) ? R[(int64_t)l * ldr + i] : 0.0;
-        s += r * col[l];
+  if (active) {
+    // old Racc column c
+    for (int l = lane; l <= c; l += 32) col[l] = a.Racc[(int64_t)c * ldr + l];
+    __syncwarp();
+    if (a.update_b && a.q > 0) {
+      for (int i = lane; i < a.q; i += 32) {
+        double s = 0.0;
+        for (int l = 0; l <= c; ++l) s += a.Bt[(int64_t)l * a.ldbt + i] * col[l];
+        a.B[(int64_t)c * a.ldb + i] = a.B[(int64_t)c * a.ldb + i] + s;
       }
-      if (i <= c) a.Racc[(int64_t)c * ldr + i] = s;
     }
-    for (int i = c + 1 + lane; i < KP; i += 32) a.Racc[(int64_t)c * ldr + i] = 0.0;
-  }
-  __syncwarp();
-  // inverse column: acc = e_c; for i = c..0: x_i = acc_i / R_ii; acc_l -= R_li x_i (l < i)
-  for (int l = lane; l <= c; l += 32) col[l] = (l == c) ? 1.0 : 0.0;
-  __syncwarp();
-  // Rinv is written straight into the coefficient-tile layout the TRMM reads
-  double* out = a.Rinv + coeff_off(0, c, k);   // column c of its tile column; rows at +i%32 per 32-row tile
-  const int64_t nkt = ceil_div(k, CT_K);
-  for (int i = c; i >= 0; --i) {
-    const double x = col[i] / R[(int64_t)i * ldr + i];
+    if (a.accumulate) {
+      // new(i) = sum_{l=i..c} R(i,l) old(l): lanes own rows i, loop over l (coalesced columns of R)
+      for (int i0 = 0; i0 <= c; i0 += 32) {
+        const int i = i0 + lane;
+        double s = 0.0;
+#pragma unroll 8
+        for (int l = i0; l <= c; ++l) {
+          const double r = (i <= l) ? R[(int64_t)l * ldr + i] : 0.0;
+          s += r * col[l];
+        }
+        if (i <= c) a.Racc[(int64_t)c * ldr + i] = s;
+      }
+      for (int i = c + 1 + lane; i < KP; i += 32) a.Racc[(int64_t)c * ldr + i] = 0.0;
+    }
     __syncwarp();
-    if (lane == 0) out[(i / CT_K) * CT_TILE + i % CT_K] = x;
-    const double* ri = R + (int64_t)i * ldr;   // column i of R: R(l, i), l < i
-    for (int l = lane; l < i; l += 32) col[l] -= ri[l] * x;
-    __syncwarp();
+    // inverse column: acc = e_c
+    for (int l = lane; l <= c; l += 32) col[l] = (l == c) ? 1.0 : 0.0;
   }
-  for (int i = c + 1 + lane; i < KP; i += 32) out[(i / CT_K) * CT_TILE + i % CT_K] = 0.0;
-  (void)nkt;
+  // back substitution for the CTA's columns together: step i uses column i of R,
+  // staged in shared memory (double buffered, next column prefetched into
+  // registers while the current step computes)
+  const int cmax = min(c0 + FF_WARPS - 1, k - 1);
+  const int nthr = FF_WARPS * 32;
+  for (int l = threadIdx.x; l <= cmax; l += nthr) rbuf[l] = R[(int64_t)cmax * ldr + l];
+  int cur = 0;
+  double* out = a.Rinv + coeff_off(0, active ? c : 0, k);
+  for (int i = cmax; i >= 0; --i) {
+    __syncthreads();
+    const double* rc = rbuf + cur * k;
+    // prefetch column i-1 (rows 0..i-1)
+    double pre[4];
+    int npre = 0;
+    if (i > 0)
+      for (int l = threadIdx.x; l < i && npre < 4; l += nthr) pre[npre++] = R[(int64_t)(i - 1) * ldr + l];
+    if (active && c >= i) {
+      const double x = col[i] / rc[i];
+      if (lane == 0) out[(i / CT_K) * CT_TILE + i % CT_K] = x;
+      for (int l = lane; l < i; l += 32) col[l] -= rc[l] * x;
+    }
+    if (i > 0) {
+      double* rn = rbuf + (cur ^ 1) * k;
+      int q = 0;
+      for (int l = threadIdx.x; l < i && q < 4; l += nthr) rn[l] = pre[q++];
+      for (int l = threadIdx.x + 4 * nthr; l < i; l += nthr) rn[l] = R[(int64_t)(i - 1) * ldr + l];
+    }
+    cur ^= 1;
+  }
+  if (active)
+    for (int i = c + 1 + lane; i < KP; i += 32) out[(i / CT_K) * CT_TILE + i % CT_K] = 0.0;
 }
 
 size_t factor_workspace_bytes(int k) {
@@ -543,7 +565,7 @@ cudaError_t factor_launch(FactorArgs& a, cudaStream_t stream) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int blocks = (a.k + FF_WARPS - 1) / FF_WARPS;
-  factor_finish_kernel<<<blocks, FF_WARPS * 32, (size_t)FF_WARPS * a.k * sizeof(double), stream>>>(a);
+  factor_finish_kernel<<<blocks, FF_WARPS * 32, (size_t)(FF_WARPS + 2) * a.k * sizeof(double), stream>>>(a);
   return cudaGetLastError();
 }
 

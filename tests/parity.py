@@ -45,5 +45,11 @@ def compare_iterated(mine, ref, k, tol):
     return n
 
 
-def within10(mine, ref, k):
-    return mine <= 10 * max(ref, 10 * U * math.sqrt(k))
+def within10(mine, ref, k, tol=None):
+    """mine <= 10 x ref (floored at 10 u sqrt(k)); after a rounding-determined
+    convergence decision both runs stopped on ||X - I||_F < tol, so tol also
+    bounds the comparison then."""
+    floor = 10 * U * math.sqrt(k)
+    if tol is not None:
+        floor = max(floor, tol)
+    return mine <= 10 * max(ref, floor)

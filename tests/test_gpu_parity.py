@@ -88,9 +88,12 @@ def test_single_input_golden(case):
         return
     assert res.success == ref.success
     np.testing.assert_array_equal(np.tril(res.r, -1), 0.0)
+    diverged_tol = None
     if case["algo"] == "rs_chol_qr":
         tol = algo_cfg(case).effective_tol(k)
         n = P.compare_iterated(res, ref, k, tol)
+        if n < max(len(ref.shift_attempts), len(res.shift_attempts)) or res.iterations != ref.iterations:
+            diverged_tol = tol
         if n == len(ref.shift_attempts) == len(res.shift_attempts) and res.iterations == case["iterations"]:
             assert res.shift_attempts == case["attempts"]
             np.testing.assert_allclose(res.shifts_applied, case["shifts"], rtol=1e-6)
@@ -105,8 +108,8 @@ def test_single_input_golden(case):
     if "loo" in case and res.success:
         loo = cq.loss_of_orthogonality(res.q, norm="frobenius")
         rrr = cq.reconstruction_residual(a, res.q, res.r, norm="frobenius")
-        assert P.within10(loo, case["loo"], k), (loo, case["loo"])
-        assert P.within10(rrr, case["rrr"], k), (rrr, case["rrr"])
+        assert P.within10(loo, case["loo"], k, diverged_tol), (loo, case["loo"])
+        assert P.within10(rrr, case["rrr"], k, diverged_tol), (rrr, case["rrr"])
 
 
 @pytest.mark.parametrize("case", UPDATE, ids=[c["name"] for c in UPDATE])
