@@ -188,9 +188,11 @@ class Result:
         self.decision_margins = []
 
 
-def _attempt(x):
-    """One factorization attempt: (r, signed margin) or (None, margin)."""
-    top = float(np.max(np.diag(x))) if x.size else 1.0
+def _attempt(x, top=None):
+    """One factorization attempt: (r, signed margin) or (None, margin); the
+    margin is the smallest Schur pivot over `top` (default max diag(x))."""
+    if top is None:
+        top = float(np.max(np.diag(x))) if x.size else 1.0
     try:
         r = cholesky_upper(x)
     except OracleBreakdown as exc:
@@ -370,7 +372,8 @@ def chol_qr_update(q_in, r_in, a_new, cfg=None):
         if its == cfg["max_iter"]:
             ok = False
             break
-        dms.append(_attempt(_with_shift(x, 0.0))[1])
+        top = float(np.max(np.diag(x) + np.sum(bt * bt, axis=0))) if bt.size else None
+        dms.append(_attempt(_with_shift(x, 0.0), top)[1])
         rk, tries, xs = _update_attempts(x, m, width, cfg, shifts)
         attempts.append(tries)
         margins.append(_margin(xs, rk))

@@ -319,8 +319,10 @@ __global__ void __launch_bounds__(FK_THREADS) factor_kernel(FactorArgs a) {
   const double err = sqrt(block_sum(loc, red));
   if (tid == 0) {
     fs.err = err;
+    // decision-margin scale: max diag of the undeflated Gram (for updates the
+    // deflated X is itself at rounding level when the block is dependent)
     double dm = -INFINITY;
-    for (int j = 0; j < k; ++j) dm = fmax(dm, X[(int64_t)j * k + j]);
+    for (int j = 0; j < k; ++j) dm = fmax(dm, a.G[(int64_t)j * a.ldg + j]);
     fs.diag_max = dm;
   }
   __syncthreads();
