@@ -111,6 +111,96 @@ __device__ bool chol_packed(double* W, int n, int off, double* rowbuf, double& s
   return true;
 }
 
+// ---------------------------------------------------------------------------
+// Blocked right-looking Cholesky on a block-packed upper triangle in shared
+// memory: 8x8 blocks (I <= J) stored full (64 doubles, column-major inside),
+// block (I, J) at ((J (J+1))/2 + I) * 64.  Each block step factors an 8-pivot
+// panel (block row P) with scalar updates restricted to the panel, then
+// applies the rank-8 update to every trailing block with two DMMA.8x8x4.
+// Rows/columns >= n are identity padding (pivots 1, no coupling).
+__device__ __forceinline__ int boff(int I, int J) { return (J * (J + 1) / 2 + I) * 64; }
+__device__ __forceinline__ int belem(int i, int c) { return boff(i >> 3, c >> 3) + (c & 7) * 8 + (i & 7); }
+
+__device__ bool chol_blocked(double* Wb, int n, int off, double* rowbuf, double& smin, FState& fs) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int nb = (n + 7) >> 3;
+  for (int P = 0; P < nb; ++P) {
+    const int ncb = nb - 1 - P;   // blocks right of the diagonal block in row P
+    for (int jj = 0; jj < 8; ++jj) {
+      const int j = 8 * P + jj;
+      const double s = Wb[boff(P, P) + jj * 8 + jj];
+      if (j < n) {
+        if (!(s > 0.0)) {
+          if (tid == 0) { fs.pivot_index = j + off; fs.pivot_value = s; }
+          __syncthreads();
+          return false;
+        }
+        smin = fmin(smin, s);
+      }
+      const double d = sqrt(s);
+      // scale row j: columns c > j (diagonal block: cl > jj; blocks (P, J > P): all 8)
+      const int nd = 7 - jj, T = nd + 8 * ncb;
+      for (int e = tid; e < T; e += FK_THREADS) {
+        int c, idx;
+        if (e < nd) { c = 8 * P + jj + 1 + e; idx = boff(P, P) + (jj + 1 + e) * 8 + jj; }
+        else { const int q = e - nd; c = 8 * (P + 1) + q; idx = boff(P, P + 1 + (q >> 3)) + (q & 7) * 8 + jj; }
+        const double v = Wb[idx] / d;
+        Wb[idx] = v;
+        rowbuf[c] = v;
+      }
+      __syncthreads();
+      if (tid == 0) Wb[boff(P, P) + jj * 8 + jj] = d;
+      // rows ii = jj+1..7 of the panel: (j+? , c) -= R(j, 8P+ii) R(j, c), c >= 8P+ii
+      for (int ii = jj + 1; ii < 8; ++ii) {
+        const double ri = rowbuf[8 * P + ii];
+        const int nd2 = 8 - ii, T2 = nd2 + 8 * ncb;
+        for (int e = tid; e < T2; e += FK_THREADS) {
+          int c, idx;
+          if (e < nd2) { c = 8 * P + ii + e; idx = boff(P, P) + (ii + e) * 8 + ii; }
+          else { const int q = e - nd2; c = 8 * (P + 1) + q; idx = boff(P, P + 1 + (q >> 3)) + (q & 7) * 8 + ii; }
+          Wb[idx] -= ri * rowbuf[c];
+        }
+      }
+      __syncthreads();
+    }
+    // trailing rank-8 update: blocks (I, J), P < I <= J < nb
+    const int nblk = ncb * (ncb + 1) / 2;
+    for (int blk = warp; blk < nblk; blk += FK_NW) {
+      int J = 0, rem = blk;
+      while (rem > J) { rem -= J + 1; ++J; }
+      const int I = P + 1 + rem, Jb = P + 1 + J;
+      const double* pa = Wb + boff(P, I) + g * 8 + t;
+      const double* pb = Wb + boff(P, Jb) + g * 8 + t;
+      double* pc = Wb + boff(I, Jb) + 2 * t * 8 + g;
+      double c2[2] = {pc[0], pc[8]};
+      dmma(c2, -pa[0], pb[0]);
+      dmma(c2, -pa[4], pb[4]);
+      pc[0] = c2[0];
+      pc[8] = c2[1];
+    }
+    __syncthreads();
+  }
+  return true;
+}
+
+__device__ void store_blocked(const double* Wb, int n, int off, double* Rk, int ldr) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int c = warp; c < n; c += FK_NW)
+    for (int i = lane; i <= c; i += 32) Rk[(int64_t)(c + off) * ldr + off + i] = Wb[belem(i, c)];
+}
+
+// identity padding for rows / columns [n, 8 ceil(n/8)) of a block-packed matrix
+__device__ void pad_blocked(double* Wb, int n) {
+  const int np = (n + 7) & ~7;
+  if (np == n) return;
+  for (int e = threadIdx.x; e < (np - n) * np; e += FK_THREADS) {
+    const int c = e % np, i = n + e / np;    // row i >= n
+    if (c >= i) Wb[belem(i, c)] = (i == c) ? 1.0 : 0.0;
+    else Wb[belem(c, i)] = 0.0;              // column i >= n, row c < i
+  }
+}
+
 // Packed n x n upper W (rows/cols offset by `off` in R) -> Rk columns.
 __device__ void store_packed(const double* W, int n, int off, double* Rk, int ldr) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -128,8 +218,20 @@ __device__ bool chol_attempt(const double* __restrict__ X, int k, double sigma, 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   double smin = INFINITY;
   bool ok;
-  if (k <= FK_SMEM_K || k > FK_BIG_K) {
-    double* W = (k <= FK_SMEM_K) ? smem_w : gW;
+  if (k <= FK_SMEM_K) {
+    double* Wb = smem_w;
+    for (int c = warp; c < k; c += FK_NW)
+      for (int i = lane; i <= c; i += 32) {
+        double x = X[(int64_t)c * k + i];
+        if (i == c) x = __dadd_rn(x, sigma);
+        Wb[belem(i, c)] = x;
+      }
+    pad_blocked(Wb, k);
+    __syncthreads();
+    ok = chol_blocked(Wb, k, 0, rowbuf, smin, fs);
+    if (ok) store_blocked(Wb, k, 0, Rk, ldr);
+  } else if (k > FK_BIG_K) {
+    double* W = gW;
     for (int c = warp; c < k; c += FK_NW)
       for (int i = lane; i <= c; i += 32) {
         double x = X[(int64_t)c * k + i];
@@ -201,13 +303,14 @@ __device__ bool chol_attempt(const double* __restrict__ X, int k, double sigma, 
           if (i <= c && c < n) {
             double x = X[(int64_t)(b + c) * k + b + i];
             if (i == c) x = __dadd_rn(x, sigma);
-            S[pk(i, c)] = x - acc[e];
+            S[belem(i, c)] = x - acc[e];
           }
         }
       }
+      pad_blocked(S, n);
       __syncthreads();
-      ok = chol_packed(S, n, b, rowbuf, smin, fs);
-      if (ok) store_packed(S, n, b, Rk, ldr);
+      ok = chol_blocked(S, n, b, rowbuf, smin, fs);
+      if (ok) store_blocked(S, n, b, Rk, ldr);
     }
   }
   if (tid == 0) {
@@ -548,11 +651,12 @@ cudaError_t factor_launch(FactorArgs& a, cudaStream_t stream) {
   if (a.k < 1 || a.k > FK_MAX_K) return cudaErrorInvalidValue;
   const int kpad = (int)round_up(a.k, 2);
   size_t smem = (32 + 3 * (size_t)kpad) * sizeof(double);
+  auto blocked = [](int n) { const int nb = (n + 7) / 8; return (int64_t)nb * (nb + 1) / 2 * 64; };
   if (a.k <= FK_SMEM_K) {
-    smem += (size_t)pk(0, a.k) * sizeof(double);
+    smem += (size_t)blocked(a.k) * sizeof(double);
   } else if (a.k <= FK_BIG_K) {
-    const int64_t n = a.k - FK_PANEL;
-    smem += (size_t)std::max<int64_t>((int64_t)FK_PANEL * a.k, pk(0, (int)n)) * sizeof(double);
+    const int n = a.k - FK_PANEL;
+    smem += (size_t)std::max<int64_t>((int64_t)FK_PANEL * a.k, blocked(n)) * sizeof(double);
   }
   static bool attr_set = false;
   if (!attr_set) {
