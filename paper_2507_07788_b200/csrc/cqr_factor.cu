@@ -68,6 +68,23 @@ __device__ double block_sum(double v, double* red) {
   return s;
 }
 
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ double block_max(double v, double* red) {
+  v = warp_max(v);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double s = -INFINITY;
+#pragma unroll
+  for (int w = 0; w < FK_NW; ++w) s = fmax(s, red[w]);
+  return s;
+}
+
 // compute_shift (kernels.py:194): ((11 * N) * u) * norm, then Python max with 2u.
 __device__ __forceinline__ double shift_value(int64_t m, int64_t w, double norm, double u) {
   const double N = (double)(m * w + w * (w + 1));
@@ -381,7 +398,7 @@ __global__ void __launch_bounds__(FK_THREADS) factor_kernel(FactorArgs a) {
   __shared__ FState fs;
   const int k = a.k;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int kpad = (int)round_up(k, 2);
+  const int kpad = (int)round_up(k, 8);
   double* red = fsm;
   double* rowbuf = fsm + 32;
   double* vec = rowbuf + kpad;
@@ -420,12 +437,13 @@ __global__ void __launch_bounds__(FK_THREADS) factor_kernel(FactorArgs a) {
     loc += d * d;
   }
   const double err = sqrt(block_sum(loc, red));
+  // decision-margin scale: max diag of the undeflated Gram (for updates the
+  // deflated X is itself at rounding level when the block is dependent)
+  double dml = -INFINITY;
+  for (int j = tid; j < k; j += FK_THREADS) dml = fmax(dml, a.G[(int64_t)j * a.ldg + j]);
+  const double dm = block_max(dml, red);
   if (tid == 0) {
     fs.err = err;
-    // decision-margin scale: max diag of the undeflated Gram (for updates the
-    // deflated X is itself at rounding level when the block is dependent)
-    double dm = -INFINITY;
-    for (int j = 0; j < k; ++j) dm = fmax(dm, a.G[(int64_t)j * a.ldg + j]);
     fs.diag_max = dm;
   }
   __syncthreads();
@@ -526,11 +544,15 @@ __global__ void __launch_bounds__(FK_THREADS) factor_kernel(FactorArgs a) {
 
   if (!done) {
     // ---- 4. TriangularSingularError check, decision margin, zero lower part + padding of Rk
+    double tl = -INFINITY, zl = INFINITY;
+    for (int j = tid; j < k; j += FK_THREADS) {
+      tl = fmax(tl, __dadd_rn(X[(int64_t)j * k + j], sigma));
+      if (a.Rk[(int64_t)j * a.ldr + j] == 0.0) zl = fmin(zl, (double)j);
+    }
+    const double top = block_max(tl, red);
+    const double zfirst = -block_max(-zl, red);
     if (tid == 0) {
-      for (int j = 0; j < k; ++j)
-        if (a.Rk[(int64_t)j * a.ldr + j] == 0.0) { fs.code = CQR_TRI_SINGULAR; fs.singular_index = j; break; }
-      double top = -INFINITY;
-      for (int j = 0; j < k; ++j) top = fmax(top, __dadd_rn(X[(int64_t)j * k + j], sigma));
+      if (zfirst < INFINITY) { fs.code = CQR_TRI_SINGULAR; fs.singular_index = (int)zfirst; }
       fs.min_pivot_rel = fs.min_pivot / top;
     }
     const int KP = (int)round_up(k, 32);
@@ -649,7 +671,7 @@ size_t factor_workspace_bytes(int k) {
 
 cudaError_t factor_launch(FactorArgs& a, cudaStream_t stream) {
   if (a.k < 1 || a.k > FK_MAX_K) return cudaErrorInvalidValue;
-  const int kpad = (int)round_up(a.k, 2);
+  const int kpad = (int)round_up(a.k, 8);
   size_t smem = (32 + 3 * (size_t)kpad) * sizeof(double);
   auto blocked = [](int n) { const int nb = (n + 7) / 8; return (int64_t)nb * (nb + 1) / 2 * 64; };
   if (a.k <= FK_SMEM_K) {
