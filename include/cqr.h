@@ -161,6 +161,9 @@ int cqr_apply_gram(const double* X, int64_t ldx, int64_t m, int k, const double*
  * (cqr_coeff_doubles(k, k), zero-initialised once).  `shifts` receives the shift values tried
  * (capacity max_shift_attempts + 1).  `status` is device memory. */
 size_t cqr_factor_workspace_bytes(int k);
+/* Diagnostics: globaltimer stamps (ns) of the phases of the last cqr_factor
+ * launch (HOST array of 16; synchronous). */
+int cqr_debug_factor_profile(unsigned long long* out16);
 int cqr_factor(const cqr_factor_config* cfg, int k, const double* G, int ldg, const double* Bt, int ldbt, int q,
                double* Rk, double* Rinv, int ldr, double* Racc, double* B, int ldb, double* shifts,
                cqr_factor_status* status, void* ws, size_t ws_bytes, void* stream);

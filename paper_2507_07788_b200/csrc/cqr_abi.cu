@@ -171,6 +171,8 @@ int cqr_apply_gram(const double* X, int64_t ldx, int64_t m, int k, const double*
   return cqr_gram(Q, ldq, m, k, G, ldg, ws, ws_bytes, stream);
 }
 
+int cqr_debug_factor_profile(unsigned long long* out16) { return cqr::factor_profile(out16); }
+
 size_t cqr_factor_workspace_bytes(int k) { return k > 0 ? cqr::factor_workspace_bytes(k) : 256; }
 
 int cqr_factor(const cqr_factor_config* cfg, int k, const double* G, int ldg, const double* Bt, int ldbt, int q,

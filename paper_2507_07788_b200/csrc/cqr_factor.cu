@@ -144,9 +144,11 @@ __device__ bool chol_blocked(double* Wb, int n, int off, double* rowbuf, double&
   const int nb = (n + 7) >> 3;
   for (int P = 0; P < nb; ++P) {
     const int ncb = nb - 1 - P;   // blocks right of the diagonal block in row P
+    const int w8 = 8 * ncb;
     for (int jj = 0; jj < 8; ++jj) {
       const int j = 8 * P + jj;
-      const double s = Wb[boff(P, P) + jj * 8 + jj];
+      const int dgi = boff(P, P) + jj * 8 + jj;
+      const double s = Wb[dgi];
       if (j < n) {
         if (!(s > 0.0)) {
           if (tid == 0) { fs.pivot_index = j + off; fs.pivot_value = s; }
@@ -157,7 +159,7 @@ __device__ bool chol_blocked(double* Wb, int n, int off, double* rowbuf, double&
       }
       const double d = sqrt(s);
       // scale row j: columns c > j (diagonal block: cl > jj; blocks (P, J > P): all 8)
-      const int nd = 7 - jj, T = nd + 8 * ncb;
+      const int nd = 7 - jj, T = nd + w8;
       for (int e = tid; e < T; e += FK_THREADS) {
         int c, idx;
         if (e < nd) { c = 8 * P + jj + 1 + e; idx = boff(P, P) + (jj + 1 + e) * 8 + jj; }
@@ -166,27 +168,38 @@ __device__ bool chol_blocked(double* Wb, int n, int off, double* rowbuf, double&
         Wb[idx] = v;
         rowbuf[c] = v;
       }
+      if (tid == 0) Wb[dgi] = d;   // nobody reads the pivot element before the next step
       __syncthreads();
-      if (tid == 0) Wb[boff(P, P) + jj * 8 + jj] = d;
-      // rows ii = jj+1..7 of the panel: (j+? , c) -= R(j, 8P+ii) R(j, c), c >= 8P+ii
-      for (int ii = jj + 1; ii < 8; ++ii) {
-        const double ri = rowbuf[8 * P + ii];
-        const int nd2 = 8 - ii, T2 = nd2 + 8 * ncb;
-        for (int e = tid; e < T2; e += FK_THREADS) {
-          int c, idx;
-          if (e < nd2) { c = 8 * P + ii + e; idx = boff(P, P) + (ii + e) * 8 + ii; }
-          else { const int q = e - nd2; c = 8 * (P + 1) + q; idx = boff(P, P + 1 + (q >> 3)) + (q & 7) * 8 + ii; }
-          Wb[idx] -= ri * rowbuf[c];
+      // rows ii = jj+1..7 of the panel, flattened over (ii, c):
+      //   off-diagonal blocks: (7 - jj) * 8 ncb elements; diagonal block: pairs ii <= cl
+      const int noff = (7 - jj) * w8;
+      const int ndg = (7 - jj) * (8 - jj) / 2;
+      for (int e = tid; e < noff + ndg; e += FK_THREADS) {
+        int ii, c, idx;
+        if (e < noff) {
+          ii = jj + 1 + e / w8;
+          const int q = e % w8;
+          c = 8 * (P + 1) + q;
+          idx = boff(P, P + 1 + (q >> 3)) + (q & 7) * 8 + ii;
+        } else {
+          int r = e - noff;
+          ii = jj + 1;
+          while (r >= 8 - ii) { r -= 8 - ii; ++ii; }
+          const int cl = ii + r;
+          c = 8 * P + cl;
+          idx = boff(P, P) + cl * 8 + ii;
         }
+        Wb[idx] -= rowbuf[8 * P + ii] * rowbuf[c];
       }
       __syncthreads();
     }
     // trailing rank-8 update: blocks (I, J), P < I <= J < nb
     const int nblk = ncb * (ncb + 1) / 2;
     for (int blk = warp; blk < nblk; blk += FK_NW) {
-      int J = 0, rem = blk;
-      while (rem > J) { rem -= J + 1; ++J; }
-      const int I = P + 1 + rem, Jb = P + 1 + J;
+      int J = (int)((sqrtf(8.0f * blk + 1.0f) - 1.0f) * 0.5f);
+      while ((J + 1) * (J + 2) / 2 <= blk) ++J;
+      while (J * (J + 1) / 2 > blk) --J;
+      const int I = P + 1 + (blk - J * (J + 1) / 2), Jb = P + 1 + J;
       const double* pa = Wb + boff(P, I) + g * 8 + t;
       const double* pb = Wb + boff(P, Jb) + g * 8 + t;
       double* pc = Wb + boff(I, Jb) + 2 * t * 8 + g;
@@ -227,6 +240,16 @@ __device__ void store_packed(const double* W, int n, int off, double* Rk, int ld
 
 constexpr int FK_PANEL = 32;
 
+// phase timestamps of the last factor launch (globaltimer ns), for profiling
+__device__ unsigned long long g_fprof[16];
+__device__ __forceinline__ void fmark(int slot) {
+  if (threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_fprof[slot] = t;
+  }
+}
+
 // One factorization attempt of X + sigma I; on success the factor is in Rk
 // (upper triangle; the caller zeroes the rest).  `smem_w` is the shared work
 // area, `gW` the global fallback for k > FK_BIG_K.
@@ -259,12 +282,13 @@ __device__ bool chol_attempt(const double* __restrict__ X, int k, double sigma, 
     ok = chol_packed(W, k, 0, rowbuf, smin, fs);
     if (ok) store_packed(W, k, 0, Rk, ldr);
   } else {
+    fmark(2);
     // ---- stage 1: rows 0..31 as a row-major panel P[r][c] (c >= r) in shared memory
     const int b = FK_PANEL;
     double* P = smem_w;
     for (int r = warp; r < b; r += FK_NW)
       for (int c = r + lane; c < k; c += 32) {
-        double x = X[(int64_t)c * k + r];
+        double x = X[(int64_t)r * k + c];   // = X(r, c) by symmetry; contiguous in c
         if (c == r) x = __dadd_rn(x, sigma);
         P[r * k + c] = x;
       }
@@ -295,6 +319,7 @@ __device__ bool chol_attempt(const double* __restrict__ X, int k, double sigma, 
       for (int r = warp; r < b; r += FK_NW)
         for (int c = r + lane; c < k; c += 32) Rk[(int64_t)c * ldr + r] = P[r * k + c];
       __syncthreads();
+      fmark(3);
       // ---- stage 2: S = X22 - R12^T R12 (packed upper, n = k - 32) with DMMA,
       // fragments of R12 read from Rk (L2); S overwrites the panel area
       const int n = k - b;
@@ -326,7 +351,9 @@ __device__ bool chol_attempt(const double* __restrict__ X, int k, double sigma, 
       }
       pad_blocked(S, n);
       __syncthreads();
+      fmark(4);
       ok = chol_blocked(S, n, b, rowbuf, smin, fs);
+      fmark(5);
       if (ok) store_blocked(S, n, b, Rk, ldr);
     }
   }
@@ -371,6 +398,7 @@ __device__ double norm_estimate(const double* __restrict__ X, int k, double tol,
     double nw_loc = 0.0;
     for (int i = tid; i < k; i += FK_THREADS) {
       double s = 0.0;
+#pragma unroll 8
       for (int c = 0; c < k; ++c) s += X[(int64_t)c * k + i] * vec[c];
       wv[i] = s;
       nw_loc += s * s;
@@ -403,8 +431,10 @@ __global__ void __launch_bounds__(FK_THREADS) factor_kernel(FactorArgs a) {
   double* rowbuf = fsm + 32;
   double* vec = rowbuf + kpad;
   double* wv = vec + kpad;
-  double* Wsm = wv + kpad;   // shared work area (packed triangle / panel / trailing matrix)
-  double* X = a.X;
+  // k <= 128: X itself lives in shared memory (k^2 doubles) before the work area
+  const bool xs = (k <= FK_SMEM_K);
+  double* X = xs ? wv + kpad : a.X;
+  double* Wsm = xs ? X + (int64_t)k * k : wv + kpad;   // shared work area
 
   if (tid == 0) {
     fs.code = CQR_FACTORED; fs.retries = 0; fs.n_shifts = 0; fs.pivot_index = -1; fs.est_calls = 0;
@@ -413,11 +443,14 @@ __global__ void __launch_bounds__(FK_THREADS) factor_kernel(FactorArgs a) {
     fs.sigma = 0.0; fs.attempts = 0; fs.plain_margin = 0.0; fs.diag_max = 0.0; fs.min_pivot = 0.0;
   }
 
+  fmark(0);
   // ---- 1. X = G (or G - Bt^T Bt), symmetric by construction from the lower triangle
+  //         (lower triangle read column by column: coalesced)
   const int64_t kk = (int64_t)k * k;
+#pragma unroll 4
   for (int64_t e = tid; e < kk; e += FK_THREADS) {
-    const int i = (int)(e % k), c = (int)(e / k);
-    const int r = max(i, c), cc = min(i, c);
+    const int r = (int)(e % k), cc = (int)(e / k);
+    if (r < cc) continue;
     double x = a.G[(int64_t)cc * a.ldg + r];
     if (a.policy == CQR_POLICY_UPDATE && a.q > 0) {
       const double* br = a.Bt + (int64_t)r * a.ldbt;
@@ -426,12 +459,14 @@ __global__ void __launch_bounds__(FK_THREADS) factor_kernel(FactorArgs a) {
       for (int l = 0; l < a.q; ++l) d += br[l] * bc[l];
       x = x - d;
     }
-    X[e] = x;
+    X[(int64_t)cc * k + r] = x;
+    X[(int64_t)r * k + cc] = x;
   }
   __syncthreads();
 
   // ---- 2. err = ||X - I||_F
   double loc = 0.0;
+#pragma unroll 8
   for (int64_t e = tid; e < kk; e += FK_THREADS) {
     const double d = X[e] - (((e % k) == (e / k)) ? 1.0 : 0.0);
     loc += d * d;
@@ -448,6 +483,7 @@ __global__ void __launch_bounds__(FK_THREADS) factor_kernel(FactorArgs a) {
   }
   __syncthreads();
 
+  fmark(1);
   // `while not err < tol: if its == max_iter: ...` (algorithms.py:341-343):
   // convergence is tested before the iteration cap.
   bool done = false;
@@ -561,6 +597,7 @@ __global__ void __launch_bounds__(FK_THREADS) factor_kernel(FactorArgs a) {
   }
 
   __syncthreads();
+  fmark(6);
   if (tid == 0) {
     cqr_factor_status* st = a.st;
     st->code = fs.code;
@@ -582,22 +619,172 @@ __global__ void __launch_bounds__(FK_THREADS) factor_kernel(FactorArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// finish: one warp per column c (column-independent work, Rk read from L2)
-//   B(:, c)    += Bt Racc_old(:, c)                    (algorithms.py:445)
-//   Racc(:, c)  = triu(Rk Racc_old)(:, c)               (kernels.py:103-114)
-//   Rinv(:, c)  = R^-1 e_c by back substitution         (kernels.py:85-100)
+// finish: one CTA per 8-column block J, everything in 8x8 blocks with DMMA
+//   B(:, J)     += Bt Racc_old(:, J)                      (algorithms.py:445)
+//   Racc(I, J)   = sum_{L=I..J} Rk(I, L) Racc_old(L, J)   (kernels.py:103-114, triu)
+//   Rinv(I, J)   = inv(R_II) (delta_IJ - sum_{L>I} R(I, L) Rinv(L, J)),
+//                  block back substitution I = J .. 0    (kernels.py:85-100)
+// Rk / Racc are column-major (ldr, rows >= k zero); rows/cols >= k of the
+// last block act as identity.  Rinv goes straight into coefficient tiles.
 constexpr int FF_WARPS = 8;
 
+// A fragment of block (I, L) of a column-major matrix: A[m][kk] = M(8I+m, 8L+kk)
+__device__ __forceinline__ double frag_a(const double* M, int ldm, int I, int L, int g, int t, int h) {
+  return M[(int64_t)(8 * L + t + 4 * h) * ldm + 8 * I + g];
+}
+// B fragment of block (L, J): B[kk][n] = M(8L+kk, 8J+n)
+__device__ __forceinline__ double frag_b(const double* M, int ldm, int L, int J, int g, int t, int h) {
+  return M[(int64_t)(8 * J + g) * ldm + 8 * L + t + 4 * h];
+}
+
 __global__ void __launch_bounds__(FF_WARPS * 32) factor_finish_kernel(FactorArgs a) {
+  // sOld (Racc_old(:, J), first phase) and sX (Rinv(I, J) blocks, second phase) share storage
+  __shared__ double sU[256 * 9];
+  __shared__ double sInv[32][64];      // inv(R_II), column-major 8x8
+  __shared__ double sPart[FF_WARPS][64];
+  double (*sOld)[9] = reinterpret_cast<double (*)[9]>(sU);   // rows (<= 256) x 8, padded
+  double (*sX)[64] = reinterpret_cast<double (*)[64]>(sU);   // 32 blocks, column-major 8x8
+  if (a.st->code != CQR_FACTORED) return;
+  const int k = a.k;
+  const int J = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int ldr = a.ldr;
+  const int KP = (int)round_up(k, 32);
+  const double* R = a.Rk;
+  const int nrow = 8 * J + 8;          // rows 0 .. 8J+7 of the column block
+
+  // ---- stage Racc_old(:, J) (rows < nrow) and update B with it
+  for (int e = threadIdx.x; e < nrow * 8; e += FF_WARPS * 32) {
+    const int r = e % nrow, cl = e / nrow, c = 8 * J + cl;
+    sOld[r][cl] = (c < k) ? a.Racc[(int64_t)c * ldr + r] : ((r == c) ? 1.0 : 0.0);
+  }
+  __syncthreads();
+  if (a.update_b && a.q > 0) {
+    for (int e = threadIdx.x; e < a.q * 8; e += FF_WARPS * 32) {
+      const int i = e % a.q, cl = e / a.q, c = 8 * J + cl;
+      if (c >= k) continue;
+      double s = 0.0;
+      for (int l = 0; l <= c; ++l) s += a.Bt[(int64_t)l * a.ldbt + i] * sOld[l][cl];
+      a.B[(int64_t)c * a.ldb + i] = a.B[(int64_t)c * a.ldb + i] + s;
+    }
+  }
+  // ---- Racc(I, J) = sum_L Rk(I, L) Racc_old(L, J): warps over I, results kept in registers
+  double accs[4][2];
+  int nmine = 0;
+  if (a.accumulate) {
+    for (int I = warp; I <= J; I += FF_WARPS, ++nmine) {
+      double c2[2] = {0.0, 0.0};
+      for (int L = I; L <= J; ++L) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int ra = 8 * I + g, ca = 8 * L + t + 4 * h;
+          const double av = (ra < k && ca < k) ? R[(int64_t)ca * ldr + ra] : ((ra == ca) ? 1.0 : 0.0);
+          const double bv = sOld[8 * L + t + 4 * h][g];
+          dmma(c2, av, bv);
+        }
+      }
+      accs[nmine][0] = c2[0];
+      accs[nmine][1] = c2[1];
+    }
+  }
+  // ---- inverses of the diagonal blocks I <= J (warp per block, lanes 0..7 one column each)
+  for (int I = warp; I <= J; I += FF_WARPS) {
+    if (lane < 8) {
+      // column cl of inv(R_II): back substitution R_II x = e_cl
+      double x[8];
+      const int cl = lane;
+#pragma unroll
+      for (int r = 7; r >= 0; --r) {
+        double s = (r == cl) ? 1.0 : 0.0;
+#pragma unroll
+        for (int l = r + 1; l < 8; ++l) {
+          const int ri = 8 * I + r, cj = 8 * I + l;
+          const double rv = (ri < k && cj < k) ? R[(int64_t)cj * ldr + ri] : 0.0;
+          s -= rv * x[l];
+        }
+        const int di = 8 * I + r;
+        const double dv = (di < k) ? R[(int64_t)di * ldr + di] : 1.0;
+        x[r] = (r <= cl) ? s / dv : 0.0;
+      }
+#pragma unroll
+      for (int r = 0; r < 8; ++r) sInv[I][cl * 8 + r] = x[r];
+    }
+  }
+  __syncthreads();
+  // ---- write Racc(:, J) (all reads of Racc_old(:, J) are done: staged in smem)
+  if (a.accumulate) {
+    int n2 = 0;
+    for (int I = warp; I <= J; I += FF_WARPS, ++n2) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int r = 8 * I + g, c = 8 * J + 2 * t + e;
+        if (c < k && r < k) a.Racc[(int64_t)c * ldr + r] = (r <= c) ? accs[n2][e] : 0.0;
+      }
+    }
+  }
+  // ---- block back substitution for Rinv(:, J)
+  for (int I = J; I >= 0; --I) {
+    // S = sum_{L=I+1..J} R(I, L) X_L, L split over warps
+    double c2[2] = {0.0, 0.0};
+    for (int L = I + 1 + warp; L <= J; L += FF_WARPS) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int ra = 8 * I + g, ca = 8 * L + t + 4 * h;
+        const double av = (ra < k && ca < k) ? R[(int64_t)ca * ldr + ra] : 0.0;
+        const double bv = sX[L][g * 8 + t + 4 * h];
+        dmma(c2, av, bv);
+      }
+    }
+    sPart[warp][(2 * t) * 8 + g] = c2[0];
+    sPart[warp][(2 * t + 1) * 8 + g] = c2[1];
+    __syncthreads();
+    if (warp == 0) {
+      // M = delta_IJ I - sum_w S_w (fixed order), X_I = inv(R_II) M
+      double m[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int idx = (2 * t + e) * 8 + g;   // (row g, col 2t+e)
+        double sum = 0.0;
+#pragma unroll
+        for (int w = 0; w < FF_WARPS; ++w) sum += sPart[w][idx];
+        m[e] = ((I == J && g == 2 * t + e) ? 1.0 : 0.0) - sum;
+      }
+      __syncwarp();
+      // stage M in sPart[0] (column-major) for the B fragments
+      sPart[0][(2 * t) * 8 + g] = m[0];
+      sPart[0][(2 * t + 1) * 8 + g] = m[1];
+      __syncwarp();
+      double x2[2] = {0.0, 0.0};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) dmma(x2, sInv[I][(t + 4 * h) * 8 + g], sPart[0][g * 8 + t + 4 * h]);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int r = 8 * I + g, c = 8 * J + 2 * t + e;
+        const double v = (I == J && g > 2 * t + e) ? 0.0 : x2[e];
+        sX[I][(2 * t + e) * 8 + g] = v;
+        if (r < k && c < k) a.Rinv[coeff_off(r, c, k)] = v;
+      }
+    }
+    __syncthreads();
+  }
+  (void)KP;
+}
+
+// generic (k > 256) finish: one warp per column, R columns staged through
+// shared memory.  Same operations as factor_finish_kernel.
+constexpr int FW_WARPS = 8;
+
+__global__ void __launch_bounds__(FW_WARPS * 32) factor_finish_wide_kernel(FactorArgs a) {
   extern __shared__ __align__(16) double ffs[];
   if (a.st->code != CQR_FACTORED) return;
   const int k = a.k;
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  const int c0 = blockIdx.x * FF_WARPS;
+  const int c0 = blockIdx.x * FW_WARPS;
   const int c = c0 + wl;
   const bool active = c < k;
   double* col = ffs + (size_t)wl * k;                 // per-warp column scratch
-  double* rbuf = ffs + (size_t)FF_WARPS * k;          // 2 x k: staged column of R
+  double* rbuf = ffs + (size_t)FW_WARPS * k;          // 2 x k: staged column of R
   const int ldr = a.ldr;
   const int KP = (int)round_up(k, 32);
   const double* R = a.Rk;
@@ -633,8 +820,8 @@ __global__ void __launch_bounds__(FF_WARPS * 32) factor_finish_kernel(FactorArgs
   // back substitution for the CTA's columns together: step i uses column i of R,
   // staged in shared memory (double buffered, next column prefetched into
   // registers while the current step computes)
-  const int cmax = min(c0 + FF_WARPS - 1, k - 1);
-  const int nthr = FF_WARPS * 32;
+  const int cmax = min(c0 + FW_WARPS - 1, k - 1);
+  const int nthr = FW_WARPS * 32;
   for (int l = threadIdx.x; l <= cmax; l += nthr) rbuf[l] = R[(int64_t)cmax * ldr + l];
   int cur = 0;
   double* out = a.Rinv + coeff_off(0, active ? c : 0, k);
@@ -663,6 +850,10 @@ __global__ void __launch_bounds__(FF_WARPS * 32) factor_finish_kernel(FactorArgs
     for (int i = c + 1 + lane; i < KP; i += 32) out[(i / CT_K) * CT_TILE + i % CT_K] = 0.0;
 }
 
+int factor_profile(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, g_fprof, sizeof(g_fprof)) == cudaSuccess ? 0 : -1;
+}
+
 size_t factor_workspace_bytes(int k) {
   size_t b = (size_t)k * k * sizeof(double);
   if (k > FK_SMEM_K) b += 2 * (size_t)pk(0, k) * sizeof(double) + 256;
@@ -675,7 +866,7 @@ cudaError_t factor_launch(FactorArgs& a, cudaStream_t stream) {
   size_t smem = (32 + 3 * (size_t)kpad) * sizeof(double);
   auto blocked = [](int n) { const int nb = (n + 7) / 8; return (int64_t)nb * (nb + 1) / 2 * 64; };
   if (a.k <= FK_SMEM_K) {
-    smem += (size_t)blocked(a.k) * sizeof(double);
+    smem += ((size_t)a.k * a.k + blocked(a.k)) * sizeof(double);
   } else if (a.k <= FK_BIG_K) {
     const int n = a.k - FK_PANEL;
     smem += (size_t)std::max<int64_t>((int64_t)FK_PANEL * a.k, blocked(n)) * sizeof(double);
@@ -685,15 +876,20 @@ cudaError_t factor_launch(FactorArgs& a, cudaStream_t stream) {
     const int mx = 220 * 1024;  // <= 227 KB minus the static shared state
     cudaError_t e = cudaFuncSetAttribute(factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(factor_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    e = cudaFuncSetAttribute(factor_finish_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   factor_kernel<<<1, FK_THREADS, smem, stream>>>(a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  const int blocks = (a.k + FF_WARPS - 1) / FF_WARPS;
-  factor_finish_kernel<<<blocks, FF_WARPS * 32, (size_t)(FF_WARPS + 2) * a.k * sizeof(double), stream>>>(a);
+  const int blocks = (a.k + 7) / 8;
+  if (a.k <= 256) {
+    factor_finish_kernel<<<blocks, FF_WARPS * 32, 0, stream>>>(a);
+  } else {
+    factor_finish_wide_kernel<<<(a.k + FW_WARPS - 1) / FW_WARPS, FW_WARPS * 32,
+                                (size_t)(FW_WARPS + 2) * a.k * sizeof(double), stream>>>(a);
+  }
   return cudaGetLastError();
 }
 

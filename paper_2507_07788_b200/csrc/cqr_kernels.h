@@ -77,5 +77,6 @@ struct FactorArgs {
 };
 cudaError_t factor_launch(FactorArgs& a, cudaStream_t stream);
 size_t factor_workspace_bytes(int k);
+int factor_profile(unsigned long long* out);
 
 }  // namespace cqr

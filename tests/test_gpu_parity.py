@@ -137,13 +137,16 @@ def test_update_golden(case):
                                 co.default_cfg(**case.get("cfg", {})))
     assert res.success == ref.success == case["success"]
     p = a_new.ncols
-    P.compare_iterated(res, ref, p, algo_cfg(case).effective_tol(p))
+    tol = algo_cfg(case).effective_tol(p)
+    n = P.compare_iterated(res, ref, p, tol)
+    diverged_tol = tol if (n < max(len(ref.shift_attempts), len(res.shift_attempts))
+                           or res.iterations != ref.iterations) else None
     k = qin.shape[1]
     np.testing.assert_array_equal(res.r[k:, :k], 0.0)
     np.testing.assert_array_equal(res.r[:k, :k], r_in)
     if case["success"]:
         loo = cq.loss_of_orthogonality(res.q, norm="frobenius")
-        assert _within10(loo, case["loo"], res.q.ncols), (loo, case["loo"])
+        assert P.within10(loo, case["loo"], res.q.ncols, diverged_tol), (loo, case["loo"])
 
 
 # ---------------------------------------------------------------- k x k kernel

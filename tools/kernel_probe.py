@@ -75,6 +75,11 @@ def main():
             pol = _lib.POLICY_RECOMPUTE
             ms = timeit(lambda: e2.factor(pol, 10**6, kk), a.reps)
             out[f"factor_k{kk}_ms"] = ms
+            import ctypes
+            buf = (ctypes.c_ulonglong * 16)()
+            e2.cx.lib.cqr_debug_factor_profile(buf)
+            t0 = buf[0]
+            out[f"factor_k{kk}_phases_us"] = [round((buf[i] - t0) / 1e3, 1) if buf[i] >= t0 else None for i in range(7)]
     print(json.dumps(out))
 
 
