@@ -138,71 +138,99 @@ __device__ bool chol_packed(double* W, int n, int off, double* rowbuf, double& s
 __device__ __forceinline__ int boff(int I, int J) { return (J * (J + 1) / 2 + I) * 64; }
 __device__ __forceinline__ int belem(int i, int c) { return boff(i >> 3, c >> 3) + (c & 7) * 8 + (i & 7); }
 
-__device__ bool chol_blocked(double* Wb, int n, int off, double* rowbuf, double& smin, FState& fs) {
+// block layouts: the full upper triangle, or a band of the first 4 block rows
+struct LayoutUpper {
+  __device__ __forceinline__ int operator()(int I, int J) const { return boff(I, J); }
+};
+struct LayoutBand4 {
+  __device__ __forceinline__ int operator()(int I, int J) const { return (J * 4 + I) * 64; }
+};
+
+// Blocked right-looking Cholesky over block rows [0, nbr) of an nb x nb block
+// upper triangle (rows/cols >= n are identity padding).  Per block step P:
+//   (a) warp 0 factors the 8x8 diagonal block warp-synchronously (pivot
+//       check `not s > 0`, sqrt, row scaling, rank-1 updates inside the block);
+//   (b) all threads solve the panel R_PP^T R_PJ = W_PJ column by column;
+//   (c) the trailing blocks (I, J), P < I < nbr, I <= J, get the rank-8
+//       update with two DMMA.8x8x4 each.
+// Three block barriers per 8 pivots.
+template <typename Lay>
+__device__ bool chol_blocked(double* Wb, int n, int nb, int nbr, int off, double& smin, FState& fs, Lay lay,
+                             int* flag) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int nb = (n + 7) >> 3;
-  for (int P = 0; P < nb; ++P) {
-    const int ncb = nb - 1 - P;   // blocks right of the diagonal block in row P
-    const int w8 = 8 * ncb;
-    for (int jj = 0; jj < 8; ++jj) {
-      const int j = 8 * P + jj;
-      const int dgi = boff(P, P) + jj * 8 + jj;
-      const double s = Wb[dgi];
-      if (j < n) {
-        if (!(s > 0.0)) {
-          if (tid == 0) { fs.pivot_index = j + off; fs.pivot_value = s; }
-          __syncthreads();
-          return false;
+  for (int P = 0; P < nbr; ++P) {
+    double* D = Wb + lay(P, P);
+    // ---- (a) diagonal block, warp 0
+    if (warp == 0) {
+      int failed = 0;
+      for (int jj = 0; jj < 8; ++jj) {
+        const int j = 8 * P + jj;
+        const double s = D[jj * 8 + jj];
+        if (j < n) {
+          if (!(s > 0.0)) {
+            if (lane == 0) { fs.pivot_index = j + off; fs.pivot_value = s; }
+            failed = 1;
+            break;
+          }
+          smin = fmin(smin, s);
         }
-        smin = fmin(smin, s);
-      }
-      const double d = sqrt(s);
-      // scale row j: columns c > j (diagonal block: cl > jj; blocks (P, J > P): all 8)
-      const int nd = 7 - jj, T = nd + w8;
-      for (int e = tid; e < T; e += FK_THREADS) {
-        int c, idx;
-        if (e < nd) { c = 8 * P + jj + 1 + e; idx = boff(P, P) + (jj + 1 + e) * 8 + jj; }
-        else { const int q = e - nd; c = 8 * (P + 1) + q; idx = boff(P, P + 1 + (q >> 3)) + (q & 7) * 8 + jj; }
-        const double v = Wb[idx] / d;
-        Wb[idx] = v;
-        rowbuf[c] = v;
-      }
-      if (tid == 0) Wb[dgi] = d;   // nobody reads the pivot element before the next step
-      __syncthreads();
-      // rows ii = jj+1..7 of the panel, flattened over (ii, c):
-      //   off-diagonal blocks: (7 - jj) * 8 ncb elements; diagonal block: pairs ii <= cl
-      const int noff = (7 - jj) * w8;
-      const int ndg = (7 - jj) * (8 - jj) / 2;
-      for (int e = tid; e < noff + ndg; e += FK_THREADS) {
-        int ii, c, idx;
-        if (e < noff) {
-          ii = jj + 1 + e / w8;
-          const int q = e % w8;
-          c = 8 * (P + 1) + q;
-          idx = boff(P, P + 1 + (q >> 3)) + (q & 7) * 8 + ii;
-        } else {
-          int r = e - noff;
-          ii = jj + 1;
-          while (r >= 8 - ii) { r -= 8 - ii; ++ii; }
-          const int cl = ii + r;
-          c = 8 * P + cl;
-          idx = boff(P, P) + cl * 8 + ii;
+        const double d = sqrt(s);
+        if (lane > jj && lane < 8) D[lane * 8 + jj] = D[lane * 8 + jj] / d;   // row jj, column lane
+        __syncwarp();
+        if (lane == 0) D[jj * 8 + jj] = d;
+        // rows ii > jj, columns c >= ii of the block: 28 pairs at most
+        {
+          const int w = 7 - jj;   // rows jj+1..7, columns jj+1..7 -> w x w grid, keep upper
+          for (int e = lane; e < w * w; e += 32) {
+            const int ii = jj + 1 + e / w, c = jj + 1 + e % w;
+            if (c >= ii) D[c * 8 + ii] -= D[ii * 8 + jj] * D[c * 8 + jj];
+          }
         }
-        Wb[idx] -= rowbuf[8 * P + ii] * rowbuf[c];
+        __syncwarp();
       }
-      __syncthreads();
+      if (lane == 0) *flag = failed;
     }
-    // trailing rank-8 update: blocks (I, J), P < I <= J < nb
-    const int nblk = ncb * (ncb + 1) / 2;
+    __syncthreads();
+    if (*flag) return false;
+    // ---- (b) panel: R_PJ = R_PP^{-T} W_PJ, one column per thread
+    const int ncols = 8 * (nb - 1 - P);
+    for (int col = tid; col < ncols; col += FK_THREADS) {
+      double* blk = Wb + lay(P, P + 1 + (col >> 3)) + (col & 7) * 8;   // column (col & 7), rows 0..7
+      double y[8];
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) {
+        double v = blk[jj];
+#pragma unroll
+        for (int l = 0; l < jj; ++l) v -= D[jj * 8 + l] * y[l];
+        y[jj] = v / D[jj * 8 + jj];
+      }
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) blk[jj] = y[jj];
+    }
+    __syncthreads();
+    // ---- (c) trailing rank-8 update: blocks (I, J), P < I < nbr, I <= J < nb
+    const int ncb = nb - 1 - P;
+    const int nrows_b = nbr - 1 - P;
+    const int nblk = (nrows_b == ncb) ? ncb * (ncb + 1) / 2 : nrows_b * ncb - nrows_b * (nrows_b - 1) / 2;
     for (int blk = warp; blk < nblk; blk += FK_NW) {
-      int J = (int)((sqrtf(8.0f * blk + 1.0f) - 1.0f) * 0.5f);
-      while ((J + 1) * (J + 2) / 2 <= blk) ++J;
-      while (J * (J + 1) / 2 > blk) --J;
-      const int I = P + 1 + (blk - J * (J + 1) / 2), Jb = P + 1 + J;
-      const double* pa = Wb + boff(P, I) + g * 8 + t;
-      const double* pb = Wb + boff(P, Jb) + g * 8 + t;
-      double* pc = Wb + boff(I, Jb) + 2 * t * 8 + g;
+      int I, Jb;
+      if (nrows_b == ncb) {
+        int J = (int)((sqrtf(8.0f * blk + 1.0f) - 1.0f) * 0.5f);
+        while ((J + 1) * (J + 2) / 2 <= blk) ++J;
+        while (J * (J + 1) / 2 > blk) --J;
+        I = P + 1 + (blk - J * (J + 1) / 2);
+        Jb = P + 1 + J;
+      } else {
+        // band rows: row r of the band has ncb - r blocks
+        int r = 0, rem = blk;
+        while (rem >= ncb - r) { rem -= ncb - r; ++r; }
+        I = P + 1 + r;
+        Jb = I + rem;
+      }
+      const double* pa = Wb + lay(P, I) + g * 8 + t;
+      const double* pb = Wb + lay(P, Jb) + g * 8 + t;
+      double* pc = Wb + lay(I, Jb) + 2 * t * 8 + g;
       double c2[2] = {pc[0], pc[8]};
       dmma(c2, -pa[0], pb[0]);
       dmma(c2, -pa[4], pb[4]);
@@ -252,9 +280,10 @@ __device__ __forceinline__ void fmark(int slot) {
 
 // One factorization attempt of X + sigma I; on success the factor is in Rk
 // (upper triangle; the caller zeroes the rest).  `smem_w` is the shared work
-// area, `gW` the global fallback for k > FK_BIG_K.
+// area, `gW` the global fallback for k > FK_BIG_K.  X is symmetric (shared
+// memory for k <= 128, global otherwise).
 __device__ bool chol_attempt(const double* __restrict__ X, int k, double sigma, double* smem_w, double* gW,
-                             double* Rk, int ldr, double* rowbuf, FState& fs) {
+                             double* Rk, int ldr, double* rowbuf, FState& fs, int* flag) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   double smin = INFINITY;
   bool ok;
@@ -262,13 +291,14 @@ __device__ bool chol_attempt(const double* __restrict__ X, int k, double sigma, 
     double* Wb = smem_w;
     for (int c = warp; c < k; c += FK_NW)
       for (int i = lane; i <= c; i += 32) {
-        double x = X[(int64_t)c * k + i];
+        double x = X[c * k + i];
         if (i == c) x = __dadd_rn(x, sigma);
         Wb[belem(i, c)] = x;
       }
     pad_blocked(Wb, k);
     __syncthreads();
-    ok = chol_blocked(Wb, k, 0, rowbuf, smin, fs);
+    const int nb = (k + 7) >> 3;
+    ok = chol_blocked(Wb, k, nb, nb, 0, smin, fs, LayoutUpper(), flag);
     if (ok) store_blocked(Wb, k, 0, Rk, ldr);
   } else if (k > FK_BIG_K) {
     double* W = gW;
@@ -282,55 +312,41 @@ __device__ bool chol_attempt(const double* __restrict__ X, int k, double sigma, 
     ok = chol_packed(W, k, 0, rowbuf, smin, fs);
     if (ok) store_packed(W, k, 0, Rk, ldr);
   } else {
+    // ---- stage 1: block rows 0..3 (rows 0..31) as a band, updates kept inside the band
     fmark(2);
-    // ---- stage 1: rows 0..31 as a row-major panel P[r][c] (c >= r) in shared memory
     const int b = FK_PANEL;
-    double* P = smem_w;
+    const int nb = (k + 7) >> 3;
+    double* Wb = smem_w;
+    const LayoutBand4 band;
     for (int r = warp; r < b; r += FK_NW)
-      for (int c = r + lane; c < k; c += 32) {
-        double x = X[(int64_t)r * k + c];   // = X(r, c) by symmetry; contiguous in c
-        if (c == r) x = __dadd_rn(x, sigma);
-        P[r * k + c] = x;
+      for (int c = r + lane; c < 8 * nb; c += 32) {
+        double x = 0.0;
+        if (c < k) {
+          x = X[(int64_t)r * k + c];   // = X(r, c) by symmetry; contiguous in c
+          if (c == r) x = __dadd_rn(x, sigma);
+        }
+        Wb[band(r >> 3, c >> 3) + (c & 7) * 8 + (r & 7)] = x;
       }
     __syncthreads();
-    ok = true;
-    for (int j = 0; j < b; ++j) {
-      const double s = P[j * k + j];
-      if (!(s > 0.0)) {
-        if (tid == 0) { fs.pivot_index = j; fs.pivot_value = s; }
-        __syncthreads();
-        ok = false;
-        break;
-      }
-      smin = fmin(smin, s);
-      const double d = sqrt(s);
-      for (int c = j + 1 + tid; c < k; c += FK_THREADS) P[j * k + c] = P[j * k + c] / d;
-      __syncthreads();
-      if (tid == 0) P[j * k + j] = d;
-      // rows j+1..b-1 of the panel: P[i][c] -= P[j][i] P[j][c], c >= i
-      for (int i = j + 1 + warp; i < b; i += FK_NW) {
-        const double ri = P[j * k + i];
-        for (int c = i + lane; c < k; c += 32) P[i * k + c] -= ri * P[j * k + c];
-      }
-      __syncthreads();
-    }
+    ok = chol_blocked(Wb, k, nb, 4, 0, smin, fs, band, flag);
     if (ok) {
-      // panel rows are final rows of R
+      // band rows are final rows of R
       for (int r = warp; r < b; r += FK_NW)
-        for (int c = r + lane; c < k; c += 32) Rk[(int64_t)c * ldr + r] = P[r * k + c];
+        for (int c = r + lane; c < k; c += 32) Rk[(int64_t)c * ldr + r] = Wb[band(r >> 3, c >> 3) + (c & 7) * 8 + (r & 7)];
       __syncthreads();
       fmark(3);
-      // ---- stage 2: S = X22 - R12^T R12 (packed upper, n = k - 32) with DMMA,
-      // fragments of R12 read from Rk (L2); S overwrites the panel area
+      // ---- stage 2: S = X22 - R12^T R12 (block upper, n = k - 32) with DMMA,
+      // fragments of R12 read from Rk (L2); S overwrites the band area
       const int n = k - b;
       double* S = smem_w;
-      const int nb = (n + 7) / 8;
-      const int nblk = nb * (nb + 1) / 2;
+      const int nbs = (n + 7) / 8;
+      const int nblk = nbs * (nbs + 1) / 2;
       const int g = lane >> 2, t = lane & 3;
       for (int blk = warp; blk < nblk; blk += FK_NW) {
-        int J = 0, rem = blk;
-        while (rem > J) { rem -= J + 1; ++J; }
-        const int I = rem;  // I <= J
+        int J = (int)((sqrtf(8.0f * blk + 1.0f) - 1.0f) * 0.5f);
+        while ((J + 1) * (J + 2) / 2 <= blk) ++J;
+        while (J * (J + 1) / 2 > blk) --J;
+        const int I = blk - J * (J + 1) / 2;  // I <= J
         const int ci = b + 8 * I + g, cj = b + 8 * J + g;
         double acc[2] = {0.0, 0.0};
 #pragma unroll
@@ -352,7 +368,7 @@ __device__ bool chol_attempt(const double* __restrict__ X, int k, double sigma, 
       pad_blocked(S, n);
       __syncthreads();
       fmark(4);
-      ok = chol_blocked(S, n, b, rowbuf, smin, fs);
+      ok = chol_blocked(S, n, nbs, nbs, b, smin, fs, LayoutUpper(), flag);
       fmark(5);
       if (ok) store_blocked(S, n, b, Rk, ldr);
     }
@@ -375,13 +391,15 @@ __device__ double norm_estimate(const double* __restrict__ X, int k, double tol,
   const int tid = threadIdx.x;
   const int64_t kk = (int64_t)k * k;
   double loc = 0.0, la = 0.0;
-  for (int64_t e = tid; e < kk; e += FK_THREADS) {
-    const double x = X[e];
-    loc += x * x;
-    const int i = (int)(e % k), c = (int)(e / k);
-    const double d = x - X[(int64_t)i * k + c];
-    la += d * d;
-  }
+  (void)kk;
+  for (int c = tid >> 5; c < k; c += FK_NW)
+#pragma unroll 4
+    for (int i = tid & 31; i < k; i += 32) {
+      const double x = X[(int64_t)c * k + i];
+      loc += x * x;
+      const double d = x - X[(int64_t)i * k + c];
+      la += d * d;
+    }
   const double fro = sqrt(block_sum(loc, red));
   const double asym = sqrt(block_sum(la, red));
   if (fro == 0.0) return 0.0;
@@ -421,9 +439,10 @@ __device__ double norm_estimate(const double* __restrict__ X, int k, double tol,
   return fro;
 }
 
-__global__ void __launch_bounds__(FK_THREADS) factor_kernel(FactorArgs a) {
+__global__ void __launch_bounds__(FK_THREADS, 1) factor_kernel(FactorArgs a) {
   extern __shared__ __align__(16) double fsm[];
   __shared__ FState fs;
+  __shared__ int sflag;
   const int k = a.k;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int kpad = (int)round_up(k, 8);
@@ -447,10 +466,9 @@ __global__ void __launch_bounds__(FK_THREADS) factor_kernel(FactorArgs a) {
   // ---- 1. X = G (or G - Bt^T Bt), symmetric by construction from the lower triangle
   //         (lower triangle read column by column: coalesced)
   const int64_t kk = (int64_t)k * k;
+  for (int cc = warp; cc < k; cc += FK_NW)
 #pragma unroll 4
-  for (int64_t e = tid; e < kk; e += FK_THREADS) {
-    const int r = (int)(e % k), cc = (int)(e / k);
-    if (r < cc) continue;
+  for (int r = cc + lane; r < k; r += 32) {
     double x = a.G[(int64_t)cc * a.ldg + r];
     if (a.policy == CQR_POLICY_UPDATE && a.q > 0) {
       const double* br = a.Bt + (int64_t)r * a.ldbt;
@@ -466,11 +484,12 @@ __global__ void __launch_bounds__(FK_THREADS) factor_kernel(FactorArgs a) {
 
   // ---- 2. err = ||X - I||_F
   double loc = 0.0;
+  for (int c = warp; c < k; c += FK_NW)
 #pragma unroll 8
-  for (int64_t e = tid; e < kk; e += FK_THREADS) {
-    const double d = X[e] - (((e % k) == (e / k)) ? 1.0 : 0.0);
-    loc += d * d;
-  }
+    for (int i = lane; i < k; i += 32) {
+      const double d = X[(int64_t)c * k + i] - ((i == c) ? 1.0 : 0.0);
+      loc += d * d;
+    }
   const double err = sqrt(block_sum(loc, red));
   // decision-margin scale: max diag of the undeflated Gram (for updates the
   // deflated X is itself at rounding level when the block is dependent)
@@ -502,7 +521,7 @@ __global__ void __launch_bounds__(FK_THREADS) factor_kernel(FactorArgs a) {
     const double u2 = 2.0 * a.u;
     switch (a.policy) {
       case CQR_POLICY_PLAIN:
-        ok = chol_attempt(X, k, 0.0, Wsm, a.W, a.Rk, a.ldr, rowbuf, fs);
+        ok = chol_attempt(X, k, 0.0, Wsm, a.W, a.Rk, a.ldr, rowbuf, fs, &sflag);
         break;
       case CQR_POLICY_SHIFT_ONCE: {
         const double est = norm_estimate(X, k, a.est_tol, a.est_max_iter, vec, wv, red, fs);
@@ -510,11 +529,11 @@ __global__ void __launch_bounds__(FK_THREADS) factor_kernel(FactorArgs a) {
         if (fs.code == CQR_ASYMMETRIC) { done = true; break; }
         sigma = shift_value(a.m_global, a.shift_width, est, a.u);
         if (tid == 0) { fs.est_calls = 1; fs.norm_est = est; a.shifts[0] = sigma; fs.n_shifts = 1; }
-        ok = chol_attempt(X, k, sigma, Wsm, a.W, a.Rk, a.ldr, rowbuf, fs);
+        ok = chol_attempt(X, k, sigma, Wsm, a.W, a.Rk, a.ldr, rowbuf, fs, &sflag);
         break;
       }
       case CQR_POLICY_RECOMPUTE: {
-        ok = chol_attempt(X, k, 0.0, Wsm, a.W, a.Rk, a.ldr, rowbuf, fs);
+        ok = chol_attempt(X, k, 0.0, Wsm, a.W, a.Rk, a.ldr, rowbuf, fs, &sflag);
         if (ok) break;
         const double est = norm_estimate(X, k, a.est_tol, a.est_max_iter, vec, wv, red, fs);
         __syncthreads();
@@ -531,7 +550,7 @@ __global__ void __launch_bounds__(FK_THREADS) factor_kernel(FactorArgs a) {
           }
           if (tid == 0) a.shifts[nsh] = sigma;
           ++nsh;
-          ok = chol_attempt(X, k, sigma, Wsm, a.W, a.Rk, a.ldr, rowbuf, fs);
+          ok = chol_attempt(X, k, sigma, Wsm, a.W, a.Rk, a.ldr, rowbuf, fs, &sflag);
           if (ok) break;
           if (tid == 0) fs.escalations += 1;
           sigma = py_max(a.esc * sigma, u2);
@@ -543,7 +562,7 @@ __global__ void __launch_bounds__(FK_THREADS) factor_kernel(FactorArgs a) {
         int retries = 0, nsh = 0;
         sigma = 0.0;
         while (true) {
-          ok = chol_attempt(X, k, sigma, Wsm, a.W, a.Rk, a.ldr, rowbuf, fs);
+          ok = chol_attempt(X, k, sigma, Wsm, a.W, a.Rk, a.ldr, rowbuf, fs, &sflag);
           if (ok) break;
           ++retries;
           if (retries > a.max_shift_attempts) {
