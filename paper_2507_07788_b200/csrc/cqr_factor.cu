@@ -146,55 +146,60 @@ struct LayoutBand4 {
   __device__ __forceinline__ int operator()(int I, int J) const { return (J * 4 + I) * 64; }
 };
 
+// 8x8 diagonal block factorization by one warp (block column-major in shared
+// memory).  Pivot j is s = Schur diagonal, breakdown on `not s > 0`
+// (kernels.py:76); d = s * rsqrt(s), the row is scaled by rsqrt(s) and the
+// reciprocal is kept in inv[] for the panel solve.  Returns 1 on breakdown.
+__device__ int diag_block_warp(double* D, int P, int n, int off, double* inv, double& smin, FState& fs) {
+  const int lane = threadIdx.x & 31;
+  // (ii, c) pairs with ii <= c of the 7x7, 6x6, ... trailing parts: precomputed per lane
+  for (int jj = 0; jj < 8; ++jj) {
+    const int j = 8 * P + jj;
+    const double s = D[jj * 8 + jj];
+    if (j < n) {
+      if (!(s > 0.0)) {
+        if (lane == 0) { fs.pivot_index = j + off; fs.pivot_value = s; }
+        return 1;
+      }
+      smin = fmin(smin, s);
+    }
+    const double r = rsqrt(s);
+    if (lane > jj && lane < 8) D[lane * 8 + jj] *= r;    // row jj, column lane
+    if (lane == jj) { D[jj * 8 + jj] = s * r; inv[j] = r; }
+    __syncwarp();
+    const int w = 7 - jj;
+    for (int e = lane; e < w * w; e += 32) {
+      const int ii = jj + 1 + e / w, c = jj + 1 + e % w;
+      if (c >= ii) D[c * 8 + ii] -= D[ii * 8 + jj] * D[c * 8 + jj];
+    }
+    __syncwarp();
+  }
+  return 0;
+}
+
 // Blocked right-looking Cholesky over block rows [0, nbr) of an nb x nb block
 // upper triangle (rows/cols >= n are identity padding).  Per block step P:
-//   (a) warp 0 factors the 8x8 diagonal block warp-synchronously (pivot
-//       check `not s > 0`, sqrt, row scaling, rank-1 updates inside the block);
 //   (b) all threads solve the panel R_PP^T R_PJ = W_PJ column by column;
-//   (c) the trailing blocks (I, J), P < I < nbr, I <= J, get the rank-8
-//       update with two DMMA.8x8x4 each.
-// Three block barriers per 8 pivots.
+//   (c) the trailing blocks (I, J), P < I < nbr, I <= J get the rank-8 update
+//       with two DMMA.8x8x4 each -- warp 0 takes block (P+1, P+1) first and
+//       then factors it (lookahead), the other warps take the rest.
+// Two block barriers per 8 pivots.
 template <typename Lay>
-__device__ bool chol_blocked(double* Wb, int n, int nb, int nbr, int off, double& smin, FState& fs, Lay lay,
-                             int* flag) {
+__device__ bool chol_blocked(double* Wb, int n, int nb, int nbr, int off, double* inv, double& smin, FState& fs,
+                             Lay lay, int* flag) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
+  if (warp == 0) {
+    const int f = diag_block_warp(Wb + lay(0, 0), 0, n, off, inv, smin, fs);
+    if (lane == 0) *flag = f;
+  }
+  __syncthreads();
+  if (*flag) return false;
   for (int P = 0; P < nbr; ++P) {
-    double* D = Wb + lay(P, P);
-    // ---- (a) diagonal block, warp 0
-    if (warp == 0) {
-      int failed = 0;
-      for (int jj = 0; jj < 8; ++jj) {
-        const int j = 8 * P + jj;
-        const double s = D[jj * 8 + jj];
-        if (j < n) {
-          if (!(s > 0.0)) {
-            if (lane == 0) { fs.pivot_index = j + off; fs.pivot_value = s; }
-            failed = 1;
-            break;
-          }
-          smin = fmin(smin, s);
-        }
-        const double d = sqrt(s);
-        if (lane > jj && lane < 8) D[lane * 8 + jj] = D[lane * 8 + jj] / d;   // row jj, column lane
-        __syncwarp();
-        if (lane == 0) D[jj * 8 + jj] = d;
-        // rows ii > jj, columns c >= ii of the block: 28 pairs at most
-        {
-          const int w = 7 - jj;   // rows jj+1..7, columns jj+1..7 -> w x w grid, keep upper
-          for (int e = lane; e < w * w; e += 32) {
-            const int ii = jj + 1 + e / w, c = jj + 1 + e % w;
-            if (c >= ii) D[c * 8 + ii] -= D[ii * 8 + jj] * D[c * 8 + jj];
-          }
-        }
-        __syncwarp();
-      }
-      if (lane == 0) *flag = failed;
-    }
-    __syncthreads();
-    if (*flag) return false;
+    const double* D = Wb + lay(P, P);
     // ---- (b) panel: R_PJ = R_PP^{-T} W_PJ, one column per thread
     const int ncols = 8 * (nb - 1 - P);
+    const double* iv = inv + 8 * P;
     for (int col = tid; col < ncols; col += FK_THREADS) {
       double* blk = Wb + lay(P, P + 1 + (col >> 3)) + (col & 7) * 8;   // column (col & 7), rows 0..7
       double y[8];
@@ -203,7 +208,7 @@ __device__ bool chol_blocked(double* Wb, int n, int nb, int nbr, int off, double
         double v = blk[jj];
 #pragma unroll
         for (int l = 0; l < jj; ++l) v -= D[jj * 8 + l] * y[l];
-        y[jj] = v / D[jj * 8 + jj];
+        y[jj] = v * iv[jj];
       }
 #pragma unroll
       for (int jj = 0; jj < 8; ++jj) blk[jj] = y[jj];
@@ -213,31 +218,49 @@ __device__ bool chol_blocked(double* Wb, int n, int nb, int nbr, int off, double
     const int ncb = nb - 1 - P;
     const int nrows_b = nbr - 1 - P;
     const int nblk = (nrows_b == ncb) ? ncb * (ncb + 1) / 2 : nrows_b * ncb - nrows_b * (nrows_b - 1) / 2;
-    for (int blk = warp; blk < nblk; blk += FK_NW) {
-      int I, Jb;
-      if (nrows_b == ncb) {
-        int J = (int)((sqrtf(8.0f * blk + 1.0f) - 1.0f) * 0.5f);
-        while ((J + 1) * (J + 2) / 2 <= blk) ++J;
-        while (J * (J + 1) / 2 > blk) --J;
-        I = P + 1 + (blk - J * (J + 1) / 2);
-        Jb = P + 1 + J;
-      } else {
-        // band rows: row r of the band has ncb - r blocks
-        int r = 0, rem = blk;
-        while (rem >= ncb - r) { rem -= ncb - r; ++r; }
-        I = P + 1 + r;
-        Jb = I + rem;
+    int f = 0;
+    if (warp == 0) {
+      if (nrows_b > 0) {
+        // block (P+1, P+1) (index 0 in both enumerations), then factor it
+        const double* pa = Wb + lay(P, P + 1) + g * 8 + t;
+        double* pc = Wb + lay(P + 1, P + 1) + 2 * t * 8 + g;
+        double c2[2] = {pc[0], pc[8]};
+        dmma(c2, -pa[0], pa[0]);
+        dmma(c2, -pa[4], pa[4]);
+        pc[0] = c2[0];
+        pc[8] = c2[1];
+        __syncwarp();
+        f = diag_block_warp(Wb + lay(P + 1, P + 1), P + 1, n, off, inv, smin, fs);
       }
-      const double* pa = Wb + lay(P, I) + g * 8 + t;
-      const double* pb = Wb + lay(P, Jb) + g * 8 + t;
-      double* pc = Wb + lay(I, Jb) + 2 * t * 8 + g;
-      double c2[2] = {pc[0], pc[8]};
-      dmma(c2, -pa[0], pb[0]);
-      dmma(c2, -pa[4], pb[4]);
-      pc[0] = c2[0];
-      pc[8] = c2[1];
+      if (lane == 0) *flag = f;
+    } else {
+      for (int blk = warp; blk < nblk; blk += FK_NW - 1) {   // blk 0 is warp 0's
+        int I, Jb;
+        if (nrows_b == ncb) {
+          int J = (int)((sqrtf(8.0f * blk + 1.0f) - 1.0f) * 0.5f);
+          while ((J + 1) * (J + 2) / 2 <= blk) ++J;
+          while (J * (J + 1) / 2 > blk) --J;
+          I = P + 1 + (blk - J * (J + 1) / 2);
+          Jb = P + 1 + J;
+        } else {
+          // band rows: row r of the band has ncb - r blocks
+          int r = 0, rem = blk;
+          while (rem >= ncb - r) { rem -= ncb - r; ++r; }
+          I = P + 1 + r;
+          Jb = I + rem;
+        }
+        const double* pa = Wb + lay(P, I) + g * 8 + t;
+        const double* pb = Wb + lay(P, Jb) + g * 8 + t;
+        double* pc = Wb + lay(I, Jb) + 2 * t * 8 + g;
+        double c2[2] = {pc[0], pc[8]};
+        dmma(c2, -pa[0], pb[0]);
+        dmma(c2, -pa[4], pb[4]);
+        pc[0] = c2[0];
+        pc[8] = c2[1];
+      }
     }
     __syncthreads();
+    if (*flag) return false;
   }
   return true;
 }
@@ -298,7 +321,7 @@ __device__ bool chol_attempt(const double* __restrict__ X, int k, double sigma, 
     pad_blocked(Wb, k);
     __syncthreads();
     const int nb = (k + 7) >> 3;
-    ok = chol_blocked(Wb, k, nb, nb, 0, smin, fs, LayoutUpper(), flag);
+    ok = chol_blocked(Wb, k, nb, nb, 0, rowbuf, smin, fs, LayoutUpper(), flag);
     if (ok) store_blocked(Wb, k, 0, Rk, ldr);
   } else if (k > FK_BIG_K) {
     double* W = gW;
@@ -328,7 +351,7 @@ __device__ bool chol_attempt(const double* __restrict__ X, int k, double sigma, 
         Wb[band(r >> 3, c >> 3) + (c & 7) * 8 + (r & 7)] = x;
       }
     __syncthreads();
-    ok = chol_blocked(Wb, k, nb, 4, 0, smin, fs, band, flag);
+    ok = chol_blocked(Wb, k, nb, 4, 0, rowbuf, smin, fs, band, flag);
     if (ok) {
       // band rows are final rows of R
       for (int r = warp; r < b; r += FK_NW)
@@ -368,7 +391,7 @@ __device__ bool chol_attempt(const double* __restrict__ X, int k, double sigma, 
       pad_blocked(S, n);
       __syncthreads();
       fmark(4);
-      ok = chol_blocked(S, n, nbs, nbs, b, smin, fs, LayoutUpper(), flag);
+      ok = chol_blocked(S, n, nbs, nbs, b, rowbuf, smin, fs, LayoutUpper(), flag);
       fmark(5);
       if (ok) store_blocked(S, n, b, Rk, ldr);
     }
