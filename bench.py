@@ -223,6 +223,7 @@ def run_ours():
     # ---- warm-up
     res = None
     for _ in range(ARGS.warmup):
+        res = None            # drop the previous Q before the next one is allocated (config 5: 61 GB each)
         res = algo(a)
     barrier()
 
@@ -235,6 +236,7 @@ def run_ours():
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(ARGS.steps):
+            res = None
             res = algo(a)
         e1.record()
         barrier()
@@ -271,6 +273,7 @@ def run_ours():
             torch.cuda.synchronize()
             return r.r
 
+        res = None
         e2e_step()
         barrier()
         t0 = time.perf_counter()

@@ -59,15 +59,15 @@ class DeviceContext:
 
     def row_range(self, m):
         """Rows [lo, hi) of a global row count m owned by this rank."""
-        lo = m * self.rank // self.world
-        hi = m * (self.rank + 1) // self.world
-        return lo, hi
+        from .dist import row_range
 
-    def allreduce_(self, t):
+        return row_range(m, self.rank, self.world)
+
+    def allreduce_(self, t, symmetric=False):
         """Sum a small device tensor over ranks (NCCL); no-op on one rank."""
-        if self.world > 1:
-            torch.distributed.all_reduce(t)
-        return t
+        from .dist import allreduce_gram_
+
+        return allreduce_gram_(t, symmetric=symmetric)
 
     def allgather_rows(self, local, m):
         """Concatenate per-rank row blocks (host numpy, m_local x k) to m x k."""

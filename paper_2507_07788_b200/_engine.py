@@ -49,8 +49,7 @@ def gram_device(arr, out=None):
         cx.timer.stop("gram", t0, (arr.m_local, k))
     cx.launches += 2
     if cx.world > 1:
-        cx.allreduce_(g)
-        _symmetrize_(g)
+        cx.allreduce_(g, symmetric=True)
     return g
 
 
