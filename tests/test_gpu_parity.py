@@ -379,3 +379,36 @@ def test_panel_nan_annotated():
         with pytest.raises(cq.ShiftAttemptLimitError) as info:
             cq.pn_chol_qr(cq.CudaVectorArray.from_numpy(blk), 2, cq.AlgoConfig(max_shift_attempts=3))
     assert info.value.panel_index == 1
+
+
+@pytest.mark.parametrize("m,k", [(300, 10), (1000, 1), (4100, 33), (2048, 64), (5000, 100), (3001, 128),
+                                 (777, 96), (1200, 200)])
+@pytest.mark.parametrize("inplace", [False, True])
+def test_apply_gram_matches_separate_ops(m, k, inplace):
+    """cqr_apply_gram (fused for k <= 64 and 97..128) == TRMM then Gram."""
+    cq = _cq()
+    from paper_2507_07788_b200 import _lib
+    from paper_2507_07788_b200._engine import Engine
+
+    rng = np.random.default_rng(m + k)
+    x = rng.normal(size=(m, k))
+    g = rng.normal(size=(k, k))
+    spd = g @ g.T + k * np.eye(k)
+    eng = Engine(k, cq.AlgoConfig())
+    import torch
+    eng.G.copy_(torch.from_numpy(spd))
+    st = eng.factor(_lib.POLICY_PLAIN, m, k)
+    assert st.code == _lib.FACTORED
+    a = cq.CudaVectorArray.from_numpy(x)
+    if inplace and not eng.in_place_gram_ok():
+        pytest.skip("in place needs the fused kernel or k <= 64")
+    dst = a if inplace else cq.CudaVectorArray.zeros(a.space, k)
+    eng.apply(a, dst, with_gram=True)
+    g_dev = eng.G.cpu().numpy()
+    r = eng.Rk[:, :k].cpu().numpy().T
+    q_ref = x @ np.linalg.inv(r)
+    q = dst.to_numpy()
+    np.testing.assert_allclose(q, q_ref, rtol=0, atol=1e-11 * np.max(np.abs(q_ref)))
+    ref_g = q.T @ q
+    np.testing.assert_array_equal(g_dev, g_dev.T)
+    assert np.max(np.abs(g_dev - ref_g)) <= 1e-12 * np.max(np.abs(ref_g)) * max(1.0, np.log2(m))
