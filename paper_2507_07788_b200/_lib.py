@@ -85,6 +85,7 @@ SIGNATURES = {
     "cqr_coeff_doubles": (_SZ, [_I, _I]),
     "cqr_pack_coeffs": (_I, [_P, _I, _I, _I, _P, _P]),
     "cqr_apply_gram_workspace_bytes": (_SZ, [_I64, _I]),
+    "cqr_set_fused": (None, [_I]),
     "cqr_apply_gram_launches": (_I, [_I]),
     "cqr_apply_gram_inplace_ok": (_I, [_I]),
     "cqr_apply_gram": (_I, [_P, _I64, _I64, _I, _P, _P, _I64, _P, _I, _P, _SZ, _P]),

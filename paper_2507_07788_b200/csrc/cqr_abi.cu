@@ -145,6 +145,8 @@ size_t cqr_apply_gram_workspace_bytes(int64_t m, int k) {
   return a;
 }
 
+void cqr_set_fused(int enable) { cqr::set_fused(enable); }
+
 int cqr_apply_gram_launches(int k) { return cqr::apply_gram_fused_supported(k) ? 2 : 3; }
 
 int cqr_apply_gram_inplace_ok(int k) { return (k <= 64 || cqr::apply_gram_fused_supported(k)) ? 1 : 0; }

@@ -305,7 +305,12 @@ static int fused_kp(int k) {
   return 0;   // 65..96: unfused path
 }
 
-bool apply_gram_fused_supported(int k) { return k >= 1 && fused_kp(k) != 0; }
+// Off by default: measured slower than TRMM + Gram on B200 in round 1 (two CTA
+// barriers per panel keep the 8 warps in lockstep).  Enabled
+// with cqr_set_fused(1) (tests exercise it).
+static int g_fused_enabled = 0;
+void set_fused(int on) { g_fused_enabled = on ? 1 : 0; }
+bool apply_gram_fused_supported(int k) { return g_fused_enabled && k >= 1 && fused_kp(k) != 0; }
 
 static int fused_ctas(int64_t rows, int kp) {
   const int br = (kp >= 128) ? 32 : 64;

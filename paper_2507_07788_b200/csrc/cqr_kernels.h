@@ -54,6 +54,7 @@ cudaError_t apply_gram_fused_launch(const double* X, int64_t ldx, int k, const d
                                     cudaStream_t stream);
 size_t apply_gram_fused_ws_bytes(int64_t rows, int k);
 bool apply_gram_fused_supported(int k);
+void set_fused(int on);
 
 // ------------------------------------------------------------- k x k stage (K4)
 struct FactorArgs {

@@ -384,12 +384,23 @@ def test_panel_nan_annotated():
 @pytest.mark.parametrize("m,k", [(300, 10), (1000, 1), (4100, 33), (2048, 64), (5000, 100), (3001, 128),
                                  (777, 96), (1200, 200)])
 @pytest.mark.parametrize("inplace", [False, True])
-def test_apply_gram_matches_separate_ops(m, k, inplace):
-    """cqr_apply_gram (fused for k <= 64 and 97..128) == TRMM then Gram."""
+@pytest.mark.parametrize("fused", [0, 1])
+def test_apply_gram_matches_separate_ops(m, k, inplace, fused):
+    """cqr_apply_gram (both the fused kernel and the two-kernel path) ==
+    TRMM then Gram."""
     cq = _cq()
     from paper_2507_07788_b200 import _lib
+    from paper_2507_07788_b200._device import ctx
     from paper_2507_07788_b200._engine import Engine
 
+    ctx().lib.cqr_set_fused(fused)
+    try:
+        _apply_gram_case(cq, _lib, Engine, m, k, inplace)
+    finally:
+        ctx().lib.cqr_set_fused(0)
+
+
+def _apply_gram_case(cq, _lib, Engine, m, k, inplace):
     rng = np.random.default_rng(m + k)
     x = rng.normal(size=(m, k))
     g = rng.normal(size=(k, k))
