@@ -41,7 +41,7 @@ def _args():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 5])
+    p.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4, 5])
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--rows", type=int, default=None, help="override global rows (testing)")
     p.add_argument("--no-e2e", action="store_true")
@@ -67,6 +67,9 @@ CFG = {
             cond=None, cpu_rows=1_000_000),
     3: dict(workload="rs_chol_qr 2000000x256 kappa=1e15 (BASELINE config 3)", m=2_000_000, k=256,
             algo="rs_chol_qr", cond=15.0, cpu_rows=200_000),
+    4: dict(workload="chol_qr_update chain 8000000 x (16 + 31 x 16), A_j = Q_prev C_j + 1e-8 G_j "
+                     "(BASELINE config 4)", m=8_000_000, k=512, p=16, blocks=31, algo="chol_qr_update",
+            cond=None, cpu_rows=200_000),
     5: dict(workload="chol_qr2 128000000x64 N(0,1) (BASELINE config 5)", m=128_000_000, k=64, algo="chol_qr2",
             cond=None, cpu_rows=4_000_000),
 }
@@ -74,15 +77,41 @@ SEED = 2025
 
 
 def _metric():
+    if ARGS.config == 4:
+        return "block-append update rows*cols/s (cols = 512)"
     return "shifted CholQR3 rows*cols/s" if ARGS.config in (1, 3) else "CholQR2 rows*cols/s"
 
 
 # ---------------------------------------------------------------------------- CPU legs
+def _cpu_update_chain(rows, blocks, p=16, seed=SEED):
+    """Oracle block-append chain on `rows` rows; returns the seconds spent in
+    chol_qr_update calls (block generation excluded, as on the GPU)."""
+    from oracle import cholqr_oracle as co
+    from paper_2507_07788_b200.workloads import next_block
+
+    rng = np.random.default_rng(seed)
+    q0 = np.linalg.qr(rng.standard_normal((rows, p)))[0]
+    res = co.rs_chol_qr(q0)
+    q, r = res.q, res.r
+    spent = 0.0
+    for _ in range(blocks):
+        a = next_block(q, rng, p)
+        t0 = time.perf_counter()
+        res = co.chol_qr_update(q, r, a)
+        spent += time.perf_counter() - t0
+        q, r = res.q, res.r
+    return spent
+
+
 def _cpu_run(cfg, rows, reps):
     """Time the oracle (reference restatement) on `rows` rows of the config's
     construction; returns (seconds per call, sample description)."""
     from oracle import cholqr_oracle as co
     from paper_2507_07788_b200.workloads import host_config
+
+    if ARGS.config == 4:
+        sec = _cpu_update_chain(rows, cfg["blocks"])
+        return sec, f"31 chol_qr_update calls on {rows} rows (16 -> 512 columns), block generation excluded"
 
     x = host_config(ARGS.config, m=rows, seed=SEED)
     fn = {"s_chol_qr3": co.s_chol_qr3, "chol_qr2": co.chol_qr2, "rs_chol_qr": co.rs_chol_qr}[cfg["algo"]]
@@ -106,14 +135,18 @@ def run_reference():
     from oracle import cholqr_oracle as co  # noqa: F401
     from paper_2507_07788_b200.workloads import host_config
 
-    x = host_config(ARGS.config, m=rows, seed=SEED)
-    fn = {"s_chol_qr3": co.s_chol_qr3, "chol_qr2": co.chol_qr2, "rs_chol_qr": co.rs_chol_qr}[cfg["algo"]]
-    for _ in range(ARGS.warmup):
-        fn(x)
-    t0 = time.perf_counter()
-    for _ in range(ARGS.steps):
-        fn(x)
-    dt = (time.perf_counter() - t0) / ARGS.steps
+    if ARGS.config == 4:
+        _cpu_update_chain(rows, 2)
+        dt = sum(_cpu_update_chain(rows, cfg["blocks"]) for _ in range(ARGS.steps)) / ARGS.steps
+    else:
+        x = host_config(ARGS.config, m=rows, seed=SEED)
+        fn = {"s_chol_qr3": co.s_chol_qr3, "chol_qr2": co.chol_qr2, "rs_chol_qr": co.rs_chol_qr}[cfg["algo"]]
+        for _ in range(ARGS.warmup):
+            fn(x)
+        t0 = time.perf_counter()
+        for _ in range(ARGS.steps):
+            fn(x)
+        dt = (time.perf_counter() - t0) / ARGS.steps
     value = rows * cfg["k"] / dt
     cores = os.cpu_count()
     line = {
@@ -201,6 +234,8 @@ def run_ours():
         lo, hi = cx.row_range(m)
         return cq.CudaVectorArray.from_device_colmajor(space, x_full[lo:hi].T)
 
+    if ARGS.config == 4:
+        return run_update_chain(cq, cx, cfg, m, world, rank, local)
     if cfg["cond"] is not None:
         u_from = "householder" if ARGS.config == 1 else "cholqr2"
         a = device_svd_matrix(from_global, m, k, cfg["cond"], SEED, u_from=u_from)
@@ -291,6 +326,8 @@ def run_ours():
     if rank == 0 and world == 1 and not ARGS.no_cpu:
         try:
             sec, sample = _cpu_run(cfg, cfg["cpu_rows"], 1)
+            if ARGS.config == 4:
+                sec = sec
             cpu = {"value": cfg["cpu_rows"] * k / sec, "unit": "rows*cols/s", "cores": os.cpu_count(),
                    "kind": "port", "sample": sample + f", {os.cpu_count()} BLAS threads"}
         except Exception as exc:  # pragma: no cover
@@ -317,6 +354,103 @@ def run_ours():
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_update_chain(cq, cx, cfg, m, world, rank, local):
+    """Config 4: 31 chained chol_qr_update calls (16 -> 512 columns).  Each
+    new block is A_j = Q_prev C_j + 1e-8 G_j built from the algorithm's own
+    Q_prev (BASELINE.json config 4); the timed quantity is the sum of the
+    update calls' CUDA-event times (block generation between calls is not
+    part of the update path)."""
+    import torch
+    import torch.distributed as dist
+
+    p, nblk = cfg["p"], cfg["blocks"]
+    space = cq.VectorSpace(m)
+    gen = torch.Generator(device="cuda").manual_seed(SEED + rank)
+    from paper_2507_07788_b200 import _device
+    from paper_2507_07788_b200.workloads import device_gaussian
+
+    g0 = device_gaussian(cq.CudaVectorArray.zeros(space, p), SEED + 17 * rank)
+    base = cq.rs_chol_qr(g0)
+    q0 = cq.CudaVectorArray.zeros(space, 0, capacity=p * (nblk + 1))
+    q0.append(base.q)
+    r0 = base.r
+    hgen = np.random.default_rng(SEED)
+
+    def chain(timer_events):
+        q, r = q0.copy(), r0
+        q.reserve(p * (nblk + 1))
+        passes = []
+        for j in range(nblk):
+            c = hgen.standard_normal((q.ncols, p))
+            a = q.lincomb(c)
+            noise = cq.CudaVectorArray.zeros(space, p)
+            device_gaussian(noise, int(hgen.integers(1 << 30)) + rank)
+            a.axpy(1e-8, noise)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            res = cq.chol_qr_update(q, r, a)
+            e1.record()
+            timer_events.append((e0, e1))
+            passes.append(res.shift_attempts)
+            q, r = res.q, res.r
+        return q, r, passes
+
+    for _ in range(max(1, ARGS.warmup)):
+        ev = []
+        chain(ev)
+    torch.cuda.synchronize()
+    cx.timer = _device.KernelTimer()
+    launches0 = cx.launches
+    totals = []
+    with ClockSampler(local) as clocks:
+        for _ in range(ARGS.steps):
+            ev = []
+            q, r, passes = chain(ev)
+            torch.cuda.synchronize()
+            totals.append(sum(a.elapsed_time(b) for a, b in ev))
+    ktimes = cx.timer.summary()
+    cx.timer = None
+    launches = (cx.launches - launches0) // ARGS.steps
+    ms = float(np.mean(totals))
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=cx.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = m * 512 / (ms * 1e-3)
+    loo = cq.loss_of_orthogonality(q, norm="frobenius")
+    # dominant kernel: the fused update pass; flops per launch
+    up = ktimes.get("update_pass", {"ms": [1.0], "work": [(0, 0, 0, 0)]})
+    fl = 0.0
+    for rows_, qq, pp, init in up["work"]:
+        fl += (2.0 * rows_ * qq * pp + rows_ * pp * (pp + 1)) * (1 if init else 2)
+    tfs = fl / (sum(up["ms"]) * 1e-3) / 1e12
+    cpu = None
+    if rank == 0 and world == 1 and not ARGS.no_cpu:
+        rows = cfg["cpu_rows"]
+        sec = _cpu_update_chain(rows, cfg["blocks"])
+        cpu = {"value": rows * 512 / sec, "unit": "rows*cols/s", "cores": os.cpu_count(), "kind": "port",
+               "sample": f"oracle: 31 chol_qr_update calls on {rows} rows (16 -> 512 columns), block "
+                         f"generation excluded, {os.cpu_count()} BLAS threads"}
+    if rank == 0:
+        print(json.dumps({
+            "metric": _metric(), "value": value, "unit": "rows*cols/s", "n_gpus": world, "steps": ARGS.steps,
+            "warmup": ARGS.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, built in HBM)",
+            "config": {"workload": cfg["workload"], "rows": m, "cols": 512, "block": p, "blocks": nblk,
+                       "parallelism": f"row-sharded dp{world}", "timed": "sum of update-call event times",
+                       "update_passes": passes[:3] + ["..."] + passes[-2:], "final_loo_fro": loo},
+            "roofline": {"bound": "fp64", "kernel": "update_pass", "achieved": tfs, "peak": FP64_PEAK_TFS,
+                         "unit": "TFLOP/s", "frac": tfs / FP64_PEAK_TFS, "traffic": None,
+                         "peak_source": FP64_PEAK_SRC,
+                         "flops_model": "2 m q p (projection) + 2 m q p (cross Gram) + 2 m p (p+1) per pass"},
+            "kernels": {n: {"launches_per_step": len(v["ms"]) / ARGS.steps, "mean_ms": float(np.mean(v["ms"]))}
+                        for n, v in ktimes.items()},
+            "gpu_launches": launches, "clocks": clocks.summary(), "e2e": None, "cpu_baseline": cpu}), flush=True)
     if world > 1:
         dist.destroy_process_group()
 

@@ -153,6 +153,19 @@ int cqr_apply_gram_inplace_ok(int k);
 int cqr_apply_gram(const double* X, int64_t ldx, int64_t m, int k, const double* Rinv_tiles, double* Q,
                    int64_t ldq, double* G, int ldg, void* ws, size_t ws_bytes, void* stream);
 
+/* Fused block-update pass (Alg. 2, p <= 16, 1 <= q <= 512), one sweep over
+ * the rows with Q_in read from HBM once:
+ *   initial = 1:  Bt_next = Q_in^T Q, G = Q^T Q            (algorithms.py:430-431)
+ *   initial = 0:  Q <- (Q - Q_in Bt) R^-1 in place, then
+ *                 Bt_next = Q_in^T Q, G = Q^T Q             (algorithms.py:442-450)
+ * Bt (q x p, ldbt) and Bt_next (q x p, ld q) may alias; R^-1 in coefficient
+ * tiles (p x p); G lower triangle mirrored (ldg). */
+int cqr_update_supported(int q, int p);
+size_t cqr_update_workspace_bytes(int64_t m, int q, int p);
+int cqr_update_pass(const double* Qin, int64_t ldqin, int q, double* Q, int64_t ldq, int p, int64_t m,
+                    const double* Bt, int ldbt, const double* Rinv_tiles, int initial, double* Bt_next, double* G,
+                    int ldg, void* ws, size_t ws_bytes, void* stream);
+
 /* The k x k stage of one pass, one launch: forms X (G, or the deflated
  * G - Bt^T Bt for updates), measures ||X - I||_F, runs the policy's
  * factorization attempts with breakdown detection, power-iteration norm

@@ -372,12 +372,16 @@ def chol_qr_update(q_in, r_in, a_new, cfg=None, ledger=None):
     tol = cfg.effective_tol(p)
     width = k if cfg.update_shift_width == "existing" else p
     eng = Engine(p, cfg, q=k)
+    fused = k > 0 and eng.cx.lib.cqr_update_supported(k, p) == 1
 
     def deflated_gram(qq):
         # bt = Q_in^T Q (device, q x p), G = Q^T Q; deflation happens in the factor kernel
-        if k:
-            cross_gram_device(q_in, qq, out=eng.Bt)
-        eng.gram(qq)
+        if fused:
+            eng.update_pass(q_in, qq, initial=True)
+        else:
+            if k:
+                cross_gram_device(q_in, qq, out=eng.Bt)
+            eng.gram(qq)
         _charge(ledger, "gemm", _flops.gemm_flops(m, k, p))
         _charge(ledger, "gemm", _flops.gemm_flops(m, p, p))
         _charge(ledger, "gemm", _flops.gemm_flops(p, k, p) + p * p)
@@ -417,6 +421,20 @@ def chol_qr_update(q_in, r_in, a_new, cfg=None, ledger=None):
             _charge(ledger, "gemm", _flops.gemm_flops(m, k, p))
             _charge(ledger, "gemm", _flops.gemm_flops(m, p, p))
             _charge(ledger, "gemm", _flops.gemm_flops(p, k, p) + p * p)
+        elif fused:
+            # one sweep: Q <- (Q - Q_in Bt) R^-1, Bt <- Q_in^T Q, G <- Q^T Q
+            if q is None:
+                q = a_new.copy()
+            eng.update_pass(q_in, q, initial=False)
+            _charge(ledger, "gemm", _flops.gemm_flops(m, k, p))
+            _charge(ledger, "gemm", m * p)
+            _charge(ledger, "trtri", _flops.tri_inverse_flops(p))
+            _charge(ledger, "gemm", _flops.gemm_flops(m, p, p))
+            _charge(ledger, "gemm", _flops.gemm_flops(k, p, p) + k * p)
+            _charge(ledger, "trmm", _flops.trmm_flops(p))
+            _charge(ledger, "gemm", _flops.gemm_flops(m, k, p))
+            _charge(ledger, "gemm", _flops.gemm_flops(m, p, p))
+            _charge(ledger, "gemm", _flops.gemm_flops(p, k, p) + p * p)
         else:
             proj = _lincomb_device(q_in, eng.Bt, k, p)
             _charge(ledger, "gemm", _flops.gemm_flops(m, k, p))
@@ -435,9 +453,7 @@ def chol_qr_update(q_in, r_in, a_new, cfg=None, ledger=None):
         its += 1
     if q is None:
         q = a_new.copy()
-    q_out = q_in.copy()
-    q_out.reserve(k + p)
-    q_out.append(q)
+    q_out = q_in.extended(q)
     b = eng.b_host() if k else np.zeros((0, p))
     r_out = np.block([[r_in, b], [np.zeros((p, k)), eng.r_host()]])
     return QRResult(q_out, r_out, its, shifts, attempts, success=success, orth_error=st.err,

@@ -24,6 +24,7 @@ libcqr pack / unpack kernels, in row chunks.
 
 from __future__ import annotations
 
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -77,13 +78,49 @@ def upload_coeffs(c):
     return coeff_tiles(dev, k, n, max(k, 1))
 
 
+class _Storage:
+    """A device buffer possibly shared by several arrays (zero-copy append:
+    the augmented basis of an update is a view that extends its input's
+    buffer).  `claimed` = columns in use by the widest view; mutation of a
+    shared buffer detaches (copy on write) so every array keeps the
+    reference's value semantics."""
+
+    __slots__ = ("claimed", "views", "__weakref__")
+
+    def __init__(self, claimed):
+        self.claimed = claimed
+        self.views = 0
+
+    def release(self):
+        self.views -= 1
+
+
 class CudaVectorArray:
     """Tall fp64 array on the local B200, columns-only interface."""
 
-    def __init__(self, space, buf, ncols):
+    def __init__(self, space, buf, ncols, storage=None):
         self.space = space
         self._buf = buf          # (m_pad/4, capacity, 4) float64
         self._k = int(ncols)
+        self._attach(storage or _Storage(self._k))
+
+    def _attach(self, storage):
+        self._st = storage
+        storage.views += 1
+        if self._k > storage.claimed:
+            storage.claimed = self._k
+        self._fin = weakref.finalize(self, storage.release)
+
+    def _detach(self):
+        """Copy on write: give this array a private buffer before mutating."""
+        if self._st.views <= 1:
+            return
+        old = CudaVectorArray(self.space, self._buf, self._k, self._st)
+        buf = self._alloc(self.space, max(self._k, 1))
+        self._fin()
+        self._buf = buf
+        self._attach(_Storage(self._k))
+        self._gather(old, j0=0, n=self._k)
 
     # ------------------------------------------------------------ construction
     @staticmethod
@@ -215,20 +252,41 @@ class CudaVectorArray:
         return out
 
     def reserve(self, capacity):
-        """Grow the column capacity (keeps contents)."""
-        if capacity <= self.capacity:
+        """Grow the column capacity (keeps contents; detaches from shared storage)."""
+        if capacity <= self.capacity and self._st.views <= 1:
             return
-        old = CudaVectorArray(self.space, self._buf, self._k)
-        self._buf = self._alloc(self.space, capacity)
+        old = CudaVectorArray(self.space, self._buf, self._k, self._st)
+        buf = self._alloc(self.space, max(capacity, self._k))
+        self._fin()
+        self._buf = buf
+        self._attach(_Storage(self._k))
         self._gather(old, j0=0, n=self._k)
+
+    def _tail_free(self, n):
+        return self._k + n <= self.capacity and self._st.claimed == self._k
 
     def append(self, other):
         self._check_space(other)
         need = self._k + other._k
-        if need > self.capacity:
+        if not self._tail_free(other._k):
             self.reserve(max(need, 2 * self.capacity))
         self._gather(other, j0=0, n=other._k, dcol0=self._k)
         self._k = need
+        self._st.claimed = max(self._st.claimed, need)
+
+    def extended(self, other):
+        """q_in.copy() + append(other) as a new array (reference
+        algorithms.py:453-454).  When this array owns free capacity after its
+        columns, the result shares the buffer (no O(m k) copy); both arrays
+        keep value semantics through copy on write."""
+        self._check_space(other)
+        if not self._tail_free(other._k):
+            out = self.copy()
+            out.reserve(self._k + other._k)
+            out.append(other)
+            return out
+        self._gather(other, j0=0, n=other._k, dcol0=self._k)
+        return CudaVectorArray(self.space, self._buf, self._k + other._k, self._st)
 
     def gramian(self, other=None):
         from . import _engine
@@ -259,6 +317,7 @@ class CudaVectorArray:
         if other._k != self._k:
             raise ValueError(f"column count mismatch: {self._k} vs {other._k}")
         if self._k:
+            self._detach()
             cx = ctx()
             _lib.check(cx.lib.cqr_axpy(self.ptr(), self.ld, float(alpha), other.ptr(), other.ld, self.m_local,
                                        self._k, cx.stream), "axpy")
@@ -269,7 +328,9 @@ class CudaVectorArray:
         keep = [j for j in range(self._k) if j not in idx]
         out = CudaVectorArray(self.space, self._alloc(self.space, len(keep), zero=False), len(keep))
         out._gather(self, idx=keep)
+        self._fin()
         self._buf, self._k = out._buf, out._k
+        self._attach(_Storage(self._k))
 
     def to_numpy(self):
         """Copy of the full m x k block (Fortran order), gathered over ranks."""
