@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define CQR_ABI_VERSION 3
+#define CQR_ABI_VERSION 4
 
 #define CQR_OK 0
 #define CQR_EINVAL (-1)
@@ -58,6 +58,7 @@ extern "C" {
 #define CQR_SHIFT_LIMIT 4  /* ShiftAttemptLimitError (algorithms.py:47-56,309-310,384) */
 #define CQR_TRI_SINGULAR 5 /* TriangularSingularError (kernels.py:42-47,94-99)        */
 #define CQR_ASYMMETRIC 6   /* ValueError of spectral_norm_estimate (kernels.py:148-153) */
+#define CQR_ESTIMATED 7    /* CQR_POLICY_ESTIMATE: norm_est / est_flag written only     */
 
 /* cqr_factor_config.policy: which reference factorization rule runs */
 #define CQR_POLICY_PLAIN 0      /* cholesky(x)                       algorithms.py:209-210 */
@@ -67,6 +68,9 @@ extern "C" {
                                                                      algorithms.py:344-349, 295-317 */
 #define CQR_POLICY_UPDATE 3     /* deflated x = G - Bt^T Bt; sigma = 0, recomputed, escalated
                                                                      algorithms.py:358-397 */
+#define CQR_POLICY_FIXED_SHIFT 4 /* cholesky(x + fixed_shift I), breakdown propagates
+                                                                     algorithms.py:284 (is_chol_qr) */
+#define CQR_POLICY_ESTIMATE 5   /* spectral_norm_estimate(x) only    algorithms.py:279-283 */
 
 typedef struct cqr_factor_config {
   int32_t policy;
@@ -82,6 +86,7 @@ typedef struct cqr_factor_config {
   int32_t update_b;           /* 1: B <- B + Bt Racc_old   (algorithms.py:445)       */
   int32_t est_max_iter;       /* power-iteration cap (100, kernels.py:126)           */
   double est_tol;             /* power-iteration settling tolerance (1e-2)           */
+  double fixed_shift;         /* CQR_POLICY_FIXED_SHIFT: the shift                   */
 } cqr_factor_config;
 
 typedef struct cqr_factor_status {

@@ -318,6 +318,53 @@ def rs_chol_qr(a, cfg=None):
     return out
 
 
+def is_chol_qr(a, cfg=None):
+    """Iterated passes with one fixed shift taken from the initial Gramian's
+    norm estimate at the first breakdown; no escalation
+    (`algorithms.py:247-292`)."""
+    cfg = cfg or default_cfg()
+    a = np.asfortranarray(a, dtype=float)
+    m, n = a.shape
+    tol = effective_tol(cfg, n)
+    q = a.copy(order="F")
+    r = np.eye(n)
+    x = gram(q)
+    first = x
+    sigma0 = None
+    shifts, attempts, margins, dms = [], [], [], []
+    its = 0
+    err = identity_distance(x)
+    hist = [err]
+    while not err < tol:
+        if its == cfg["max_iter"]:
+            out = Result(q, r, its, shifts, attempts, False, err, margins)
+            out.err_history, out.decision_margins = hist, dms
+            return out
+        rk, dm, _ = _attempt(x)
+        dms.append(dm)
+        if rk is not None:
+            attempts.append(0)
+            xs = x
+        else:
+            if sigma0 is None:
+                est, _ = spectral_estimate(first)
+                sigma0 = shift_value(m, n, est, cfg["u"])
+            xs = _with_shift(x, sigma0)
+            rk = cholesky_upper(xs)
+            shifts.append(sigma0)
+            attempts.append(1)
+        margins.append(_margin(xs, rk))
+        q = lincomb(q, tri_inverse(rk))
+        r = tri_mult(rk, r)
+        x = gram(q)
+        its += 1
+        err = identity_distance(x)
+        hist.append(err)
+    out = Result(q, r, its, shifts, attempts, True, err, margins)
+    out.err_history, out.decision_margins = hist, dms
+    return out
+
+
 def _deflated(q, bt):
     """Deflated, symmetrized Gramian (`algorithms.py:358-366`)."""
     x = gram(q) - bt.T @ bt

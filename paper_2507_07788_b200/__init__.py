@@ -15,6 +15,7 @@ from .algorithms import (
     chol_qr,
     chol_qr2,
     chol_qr_update,
+    is_chol_qr,
     panel_widths,
     pn_chol_qr,
     rs_chol_qr,

@@ -118,14 +118,15 @@ class Engine:
             self.B = self.Bt = None
 
     # ------------------------------------------------------------ k x k stage
-    def factor(self, policy, m_global, width, *, tol=0.0, check_tol=False, stop=False, update_b=False):
+    def factor(self, policy, m_global, width, *, tol=0.0, check_tol=False, stop=False, update_b=False,
+               fixed_shift=0.0):
         cx = self.cx
         cfg = self.cfg
         fc = _lib.FactorConfig(
             policy=policy, shift_width=width, m_global=m_global, unit_roundoff=cfg.unit_roundoff,
             shift_escalation=cfg.shift_escalation, max_shift_attempts=cfg.max_shift_attempts,
             check_tol=1 if check_tol else 0, tol=tol, stop=1 if stop else 0, accumulate=1,
-            update_b=1 if update_b else 0, est_max_iter=100, est_tol=1e-2)
+            update_b=1 if update_b else 0, est_max_iter=100, est_tol=1e-2, fixed_shift=fixed_shift)
         bt = self.Bt.data_ptr() if self.Bt is not None else None
         b = self.B.data_ptr() if self.B is not None else None
         base = self.stat.data_ptr()

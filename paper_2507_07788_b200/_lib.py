@@ -18,8 +18,8 @@ CQR_OK = 0
 CQR_EINVAL = -1
 CQR_ECUDA = -2
 
-FACTORED, CONVERGED, CAPPED, BREAKDOWN, SHIFT_LIMIT, TRI_SINGULAR, ASYMMETRIC = range(7)
-POLICY_PLAIN, POLICY_SHIFT_ONCE, POLICY_RECOMPUTE, POLICY_UPDATE = range(4)
+FACTORED, CONVERGED, CAPPED, BREAKDOWN, SHIFT_LIMIT, TRI_SINGULAR, ASYMMETRIC, ESTIMATED = range(8)
+POLICY_PLAIN, POLICY_SHIFT_ONCE, POLICY_RECOMPUTE, POLICY_UPDATE, POLICY_FIXED_SHIFT, POLICY_ESTIMATE = range(6)
 
 c_double_p = ctypes.c_void_p  # device pointers are passed as integers
 
@@ -41,6 +41,7 @@ class FactorConfig(ctypes.Structure):
         ("update_b", ctypes.c_int32),
         ("est_max_iter", ctypes.c_int32),
         ("est_tol", ctypes.c_double),
+        ("fixed_shift", ctypes.c_double),
     ]
 
 

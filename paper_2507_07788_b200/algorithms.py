@@ -346,6 +346,73 @@ def rs_chol_qr(a, cfg=None, ledger=None):
                     success=True, orth_error=st.err, pivot_margins=margins, decision_margins=dms)
 
 
+def is_chol_qr(a, cfg=None, ledger=None):
+    """Iterated passes with one fixed shift (algorithms.py:247-292): at the
+    first breakdown the shift is derived from the INITIAL Gramian's norm
+    estimate and reused unchanged; a breakdown of the shifted factorization
+    propagates (no escalation)."""
+    import torch
+
+    from .kernels import compute_shift
+
+    cfg = cfg or AlgoConfig()
+    a = _device_array(a)
+    if a.ncols < 1:
+        raise ValueError("need at least one column")
+    m, n = a.space.dim, a.ncols
+    tol = cfg.effective_tol(n)
+    eng = Engine(n, cfg)
+    eng.gram(a)
+    first = torch.empty_like(eng.G)
+    first.copy_(eng.G)
+    _charge(ledger, "gemm", _flops.gemm_flops(m, n, n))
+    q = None
+    sigma0 = None
+    shifts, attempts, margins, dms = [], [], [], []
+    its = 0
+    while True:
+        st = eng.factor(_lib.POLICY_PLAIN, m, n, tol=tol, check_tol=True, stop=(its == cfg.max_iter))
+        _charge(ledger, "fro_norm", _flops.frobenius_flops(n))
+        if st.code == _lib.CONVERGED:
+            break
+        if st.code == _lib.CAPPED:
+            return QRResult(q if q is not None else a.copy(), eng.r_host(), its, shifts, attempts,
+                            success=False, orth_error=st.err, pivot_margins=margins, decision_margins=dms)
+        _charge_plain_attempt(ledger, n)
+        dms.append(st.plain_margin)
+        err = st.err
+        if st.code == _lib.BREAKDOWN:
+            if sigma0 is None:
+                cur = torch.empty_like(eng.G)
+                cur.copy_(eng.G)
+                eng.G.copy_(first)
+                est = eng.factor(_lib.POLICY_ESTIMATE, m, n)
+                eng.G.copy_(cur)
+                _emit_estimate_warning(est)
+                _raise_for(est)
+                _charge(ledger, "eig_est", _flops.eig_estimate_flops(n))
+                sigma0 = compute_shift(m, n, est.norm_est, cfg.unit_roundoff)
+            _charge(ledger, "potrf", n)
+            _charge_plain_attempt(ledger, n)
+            st = eng.factor(_lib.POLICY_FIXED_SHIFT, m, n, fixed_shift=sigma0)
+            _raise_for(st)
+            shifts.append(sigma0)
+            attempts.append(1)
+        else:
+            _raise_for(st)
+            attempts.append(0)
+        margins.append(st.min_pivot_rel)
+        _charge(ledger, "trtri", _flops.tri_inverse_flops(n))
+        q = _apply_gram_into(eng, a if q is None else q, fresh_ok=q is None)
+        _charge(ledger, "gemm", _flops.gemm_flops(m, n, n))
+        _charge(ledger, "trmm", _flops.trmm_flops(n))
+        _charge(ledger, "gemm", _flops.gemm_flops(m, n, n))
+        its += 1
+        del err
+    return QRResult(q if q is not None else a.copy(), eng.r_host(), its, shifts, attempts,
+                    success=True, orth_error=st.err, pivot_margins=margins, decision_margins=dms)
+
+
 # ----------------------------------------------------------------------------
 # block-append update (Alg. 2) and the panel fold (Alg. 3)
 # ----------------------------------------------------------------------------

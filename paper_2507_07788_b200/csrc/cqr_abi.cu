@@ -211,7 +211,7 @@ int cqr_factor(const cqr_factor_config* cfg, int k, const double* G, int ldg, co
   if (G == nullptr || ldg < k) return fail(CQR_EINVAL, "cqr_factor: bad G / ldg");
   if (Rk == nullptr || Rinv == nullptr || Racc == nullptr || ldr < cqr::round_up(k, 32))
     return fail(CQR_EINVAL, "cqr_factor: bad R buffers / ldr");
-  if (cfg->policy < CQR_POLICY_PLAIN || cfg->policy > CQR_POLICY_UPDATE)
+  if (cfg->policy < CQR_POLICY_PLAIN || cfg->policy > CQR_POLICY_ESTIMATE)
     return fail(CQR_EINVAL, "cqr_factor: unknown policy");
   if (cfg->policy == CQR_POLICY_UPDATE && q > 0 && (Bt == nullptr || ldbt < q))
     return fail(CQR_EINVAL, "cqr_factor: update policy needs Bt (q x k)");
@@ -234,6 +234,7 @@ int cqr_factor(const cqr_factor_config* cfg, int k, const double* G, int ldg, co
   a.stop = cfg->stop;
   a.est_tol = cfg->est_tol;
   a.est_max_iter = cfg->est_max_iter;
+  a.fixed_shift = cfg->fixed_shift;
   a.accumulate = cfg->accumulate;
   a.update_b = cfg->update_b;
   double* w = static_cast<double*>(ws);

@@ -546,6 +546,22 @@ __global__ void __launch_bounds__(FK_THREADS, 1) factor_kernel(FactorArgs a) {
       case CQR_POLICY_PLAIN:
         ok = chol_attempt(X, k, 0.0, Wsm, a.W, a.Rk, a.ldr, rowbuf, fs, &sflag);
         break;
+      case CQR_POLICY_FIXED_SHIFT:
+        sigma = a.fixed_shift;
+        if (tid == 0) { a.shifts[0] = sigma; fs.n_shifts = 1; }
+        ok = chol_attempt(X, k, sigma, Wsm, a.W, a.Rk, a.ldr, rowbuf, fs, &sflag);
+        break;
+      case CQR_POLICY_ESTIMATE: {
+        const double est = norm_estimate(X, k, a.est_tol, a.est_max_iter, vec, wv, red, fs);
+        __syncthreads();
+        if (tid == 0) {
+          if (fs.code != CQR_ASYMMETRIC) fs.code = CQR_ESTIMATED;
+          fs.norm_est = est;
+          fs.est_calls = 1;
+        }
+        done = true;
+        break;
+      }
       case CQR_POLICY_SHIFT_ONCE: {
         const double est = norm_estimate(X, k, a.est_tol, a.est_max_iter, vec, wv, red, fs);
         __syncthreads();

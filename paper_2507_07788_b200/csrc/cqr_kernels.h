@@ -73,6 +73,7 @@ struct FactorArgs {
   double u, esc; int max_shift_attempts;
   double tol; int check_tol; int stop;
   double est_tol; int est_max_iter;
+  double fixed_shift;
   int accumulate; int update_b;
   double* X;       // k*k workspace
   double* W;       // packed-upper workspace (k > smem limit)

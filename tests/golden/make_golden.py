@@ -88,6 +88,12 @@ def main():
         add(f"rs_{m}x{n}_c{x}_s{s}", "rs_chol_qr", blk, res, extra={"loo": loo, "rrr": rrr}, spec=sp)
         if x <= 14:
             try:
+                res = c.is_chol_qr(a)
+                loo, rrr = _metrics(c, blk, res)
+                add(f"is_{m}x{n}_c{x}_s{s}", "is_chol_qr", blk, res, extra={"loo": loo, "rrr": rrr}, spec=sp)
+            except c.CholeskyBreakdown as e:
+                add(f"is_{m}x{n}_c{x}_s{s}", "is_chol_qr", blk, exc=e, spec=sp)
+            try:
                 res = c.s_chol_qr3(a)
                 loo, rrr = _metrics(c, blk, res)
                 add(f"s3_{m}x{n}_c{x}_s{s}", "s_chol_qr3", blk, res, extra={"loo": loo, "rrr": rrr}, spec=sp)

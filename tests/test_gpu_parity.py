@@ -25,7 +25,8 @@ pytestmark = pytest.mark.gpu
 
 G = Golden()
 U = 1.11e-16
-SINGLE = [c for c in G.meta["cases"] if c["algo"] in ("rs_chol_qr", "s_chol_qr3", "chol_qr", "chol_qr2")]
+SINGLE = [c for c in G.meta["cases"]
+          if c["algo"] in ("rs_chol_qr", "is_chol_qr", "s_chol_qr3", "chol_qr", "chol_qr2")]
 UPDATE = [c for c in G.meta["cases"] if c["algo"] == "chol_qr_update"]
 
 
@@ -40,7 +41,7 @@ def _run(case, a):
     algo = getattr(cq, case["algo"])
     with warnings.catch_warnings():
         warnings.simplefilter("ignore")
-        if case["algo"] == "rs_chol_qr":
+        if case["algo"] in ("rs_chol_qr", "is_chol_qr"):
             return algo(a, algo_cfg(case))
         return algo(a)
 
@@ -60,6 +61,7 @@ def _oracle_single(case, blk):
     with warnings.catch_warnings():
         warnings.simplefilter("ignore")
         fn = {"rs_chol_qr": lambda x: co.rs_chol_qr(x, co.default_cfg(**case.get("cfg", {}))),
+              "is_chol_qr": lambda x: co.is_chol_qr(x, co.default_cfg(**case.get("cfg", {}))),
               "s_chol_qr3": co.s_chol_qr3, "chol_qr": co.chol_qr, "chol_qr2": co.chol_qr2}[case["algo"]]
         try:
             return fn(blk), None
@@ -89,7 +91,7 @@ def test_single_input_golden(case):
     assert res.success == ref.success
     np.testing.assert_array_equal(np.tril(res.r, -1), 0.0)
     diverged_tol = None
-    if case["algo"] == "rs_chol_qr":
+    if case["algo"] in ("rs_chol_qr", "is_chol_qr"):
         tol = algo_cfg(case).effective_tol(k)
         n = P.compare_iterated(res, ref, k, tol)
         if n < max(len(ref.shift_attempts), len(res.shift_attempts)) or res.iterations != ref.iterations:

@@ -21,7 +21,8 @@ from oracle import matgen_oracle as mg
 from conftest import Golden, oracle_cfg
 
 G = Golden()
-SINGLE = [c for c in G.meta["cases"] if c["algo"] in ("rs_chol_qr", "s_chol_qr3", "chol_qr", "chol_qr2")]
+SINGLE = [c for c in G.meta["cases"]
+          if c["algo"] in ("rs_chol_qr", "is_chol_qr", "s_chol_qr3", "chol_qr", "chol_qr2")]
 UPDATE = [c for c in G.meta["cases"] if c["algo"] == "chol_qr_update"]
 
 
@@ -31,6 +32,8 @@ def _run_single(case, a):
         warnings.simplefilter("ignore")
         if algo == "rs_chol_qr":
             return co.rs_chol_qr(a, oracle_cfg(case))
+        if algo == "is_chol_qr":
+            return co.is_chol_qr(a, oracle_cfg(case))
         if algo == "s_chol_qr3":
             return co.s_chol_qr3(a)
         if algo == "chol_qr":
