@@ -234,8 +234,8 @@ __device__ bool chol_blocked(double* Wb, int n, int nb, int nbr, int off, double
       }
       if (lane == 0) *flag = f;
     } else {
-      for (int blk = warp; blk < nblk; blk += FK_NW - 1) {   // blk 0 is warp 0's
-        int I, Jb;
+      // two blocks per iteration: all loads first, then the DMMAs (ILP)
+      auto decode = [&](int blk, int& I, int& Jb) {
         if (nrows_b == ncb) {
           int J = (int)((sqrtf(8.0f * blk + 1.0f) - 1.0f) * 0.5f);
           while ((J + 1) * (J + 2) / 2 <= blk) ++J;
@@ -249,14 +249,34 @@ __device__ bool chol_blocked(double* Wb, int n, int nb, int nbr, int off, double
           I = P + 1 + r;
           Jb = I + rem;
         }
-        const double* pa = Wb + lay(P, I) + g * 8 + t;
-        const double* pb = Wb + lay(P, Jb) + g * 8 + t;
-        double* pc = Wb + lay(I, Jb) + 2 * t * 8 + g;
-        double c2[2] = {pc[0], pc[8]};
-        dmma(c2, -pa[0], pb[0]);
-        dmma(c2, -pa[4], pb[4]);
-        pc[0] = c2[0];
-        pc[8] = c2[1];
+      };
+      for (int blk = warp; blk < nblk; blk += 2 * (FK_NW - 1)) {   // blk 0 is warp 0's
+        const int blk2 = blk + (FK_NW - 1);
+        const bool two = blk2 < nblk;
+        int I0, J0, I1 = 0, J1 = 0;
+        decode(blk, I0, J0);
+        if (two) decode(blk2, I1, J1);
+        const double* pa0 = Wb + lay(P, I0) + g * 8 + t;
+        const double* pb0 = Wb + lay(P, J0) + g * 8 + t;
+        double* pc0 = Wb + lay(I0, J0) + 2 * t * 8 + g;
+        double c0[2] = {pc0[0], pc0[8]};
+        const double a00 = -pa0[0], a01 = -pa0[4], b00 = pb0[0], b01 = pb0[4];
+        double c1[2] = {0.0, 0.0}, a10 = 0.0, a11 = 0.0, b10 = 0.0, b11 = 0.0;
+        double* pc1 = pc0;
+        if (two) {
+          const double* pa1 = Wb + lay(P, I1) + g * 8 + t;
+          const double* pb1 = Wb + lay(P, J1) + g * 8 + t;
+          pc1 = Wb + lay(I1, J1) + 2 * t * 8 + g;
+          c1[0] = pc1[0]; c1[1] = pc1[8];
+          a10 = -pa1[0]; a11 = -pa1[4]; b10 = pb1[0]; b11 = pb1[4];
+        }
+        dmma(c0, a00, b00);
+        if (two) dmma(c1, a10, b10);
+        dmma(c0, a01, b01);
+        if (two) dmma(c1, a11, b11);
+        pc0[0] = c0[0];
+        pc0[8] = c0[1];
+        if (two) { pc1[0] = c1[0]; pc1[8] = c1[1]; }
       }
     }
     __syncthreads();
@@ -488,31 +508,40 @@ __global__ void __launch_bounds__(FK_THREADS, 1) factor_kernel(FactorArgs a) {
   fmark(0);
   // ---- 1. X = G (or G - Bt^T Bt), symmetric by construction from the lower triangle
   //         (lower triangle read column by column: coalesced)
-  const int64_t kk = (int64_t)k * k;
-  for (int cc = warp; cc < k; cc += FK_NW)
-#pragma unroll 4
-  for (int r = cc + lane; r < k; r += 32) {
-    double x = a.G[(int64_t)cc * a.ldg + r];
-    if (a.policy == CQR_POLICY_UPDATE && a.q > 0) {
-      const double* br = a.Bt + (int64_t)r * a.ldbt;
-      const double* bc = a.Bt + (int64_t)cc * a.ldbt;
-      double d = 0.0;
-      for (int l = 0; l < a.q; ++l) d += br[l] * bc[l];
-      x = x - d;
+  //         and 2. err = ||X - I||_F in the same sweep; loads are batched 16
+  //         per thread before any store (the L2 latency, not bandwidth, bounds
+  //         this phase)
+  const int kk32 = k * k;
+  double loc = 0.0;
+  for (int base = tid; base < kk32; base += 16 * FK_THREADS) {
+    double v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int e = base + j * FK_THREADS;
+      const int r = e % k, c = e / k;
+      v[j] = (e < kk32 && r >= c) ? a.G[(int64_t)c * a.ldg + r] : 0.0;
     }
-    X[(int64_t)cc * k + r] = x;
-    X[(int64_t)r * k + cc] = x;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int e = base + j * FK_THREADS;
+      const int r = e % k, c = e / k;
+      if (e < kk32 && r >= c) {
+        double x = v[j];
+        if (a.policy == CQR_POLICY_UPDATE && a.q > 0) {
+          const double* br = a.Bt + (int64_t)r * a.ldbt;
+          const double* bc = a.Bt + (int64_t)c * a.ldbt;
+          double d = 0.0;
+          for (int l = 0; l < a.q; ++l) d += br[l] * bc[l];
+          x = x - d;
+        }
+        X[(int64_t)c * k + r] = x;
+        X[(int64_t)r * k + c] = x;
+        const double d = x - ((r == c) ? 1.0 : 0.0);
+        loc += ((r == c) ? 1.0 : 2.0) * (d * d);
+      }
+    }
   }
   __syncthreads();
-
-  // ---- 2. err = ||X - I||_F
-  double loc = 0.0;
-  for (int c = warp; c < k; c += FK_NW)
-#pragma unroll 8
-    for (int i = lane; i < k; i += 32) {
-      const double d = X[(int64_t)c * k + i] - ((i == c) ? 1.0 : 0.0);
-      loc += d * d;
-    }
   const double err = sqrt(block_sum(loc, red));
   // decision-margin scale: max diag of the undeflated Gram (for updates the
   // deflated X is itself at rounding level when the block is dependent)
@@ -781,19 +810,35 @@ __global__ void __launch_bounds__(FF_WARPS * 32) factor_finish_kernel(FactorArgs
       }
     }
   }
-  // ---- block back substitution for Rinv(:, J)
-  for (int I = J; I >= 0; --I) {
-    // S = sum_{L=I+1..J} R(I, L) X_L, L split over warps
-    double c2[2] = {0.0, 0.0};
-    for (int L = I + 1 + warp; L <= J; L += FF_WARPS) {
+  // ---- block back substitution for Rinv(:, J); the R(I, L) fragments of the
+  // next step are prefetched into registers while the current step runs
+  auto load_row = [&](int I, double (&fr)[4][2]) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int L = I + 1 + warp + FF_WARPS * j;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int ra = 8 * I + g, ca = 8 * L + t + 4 * h;
-        const double av = (ra < k && ca < k) ? R[(int64_t)ca * ldr + ra] : 0.0;
-        const double bv = sX[L][g * 8 + t + 4 * h];
-        dmma(c2, av, bv);
+        fr[j][h] = (I >= 0 && L <= J && ra < k && ca < k) ? R[(int64_t)ca * ldr + ra] : 0.0;
       }
     }
+  };
+  double cur[4][2], nxt[4][2];
+  load_row(J, cur);
+  for (int I = J; I >= 0; --I) {
+    load_row(I - 1, nxt);
+    // S = sum_{L=I+1..J} R(I, L) X_L, L split over warps
+    double c2[2] = {0.0, 0.0};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int L = I + 1 + warp + FF_WARPS * j;
+      if (L <= J) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) dmma(c2, cur[j][h], sX[L][g * 8 + t + 4 * h]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) { cur[j][0] = nxt[j][0]; cur[j][1] = nxt[j][1]; }
     sPart[warp][(2 * t) * 8 + g] = c2[0];
     sPart[warp][(2 * t + 1) * 8 + g] = c2[1];
     __syncthreads();
