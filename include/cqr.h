@@ -120,6 +120,10 @@ size_t cqr_gram_workspace_bytes(int64_t m, int ka, int kb, int self);
 int cqr_gram(const double* X, int64_t ldx, int64_t m, int k, double* G, int ldg, void* ws, size_t ws_bytes,
              void* stream);
 
+/* Select the self-Gram schedule: 1 (default) = block-row pairs over full-row
+ * panels (k <= 256), 0 = 64x64 tile items. */
+void cqr_set_gram_pairs(int enable);
+
 /* Cross Gram G = A^T B (ka x kb).  Replaces gramian(other) (varray.py:154-155). */
 int cqr_cross_gram(const double* A, int64_t lda, int ka, const double* B, int64_t ldb, int kb, int64_t m, double* G,
                    int ldg, void* ws, size_t ws_bytes, void* stream);

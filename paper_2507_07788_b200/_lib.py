@@ -77,6 +77,7 @@ SIGNATURES = {
     "cqr_last_error": (ctypes.c_char_p, []),
     "cqr_gram_workspace_bytes": (_SZ, [_I64, _I, _I, _I]),
     "cqr_gram": (_I, [_P, _I64, _I64, _I, _P, _I, _P, _SZ, _P]),
+    "cqr_set_gram_pairs": (None, [_I]),
     "cqr_cross_gram": (_I, [_P, _I64, _I, _P, _I64, _I, _I64, _P, _I, _P, _SZ, _P]),
     "cqr_lincomb": (_I, [_P, _I64, _I64, _I, _P, _I, _I, _P, _I64, _P]),
     "cqr_axpy": (_I, [_P, _I64, ctypes.c_double, _P, _I64, _I64, _I, _P]),

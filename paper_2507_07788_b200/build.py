@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 LIB = os.path.join(HERE, "libcqr.so")
-SOURCES = ["cqr_abi.cu", "cqr_gram.cu", "cqr_gemm.cu", "cqr_layout.cu", "cqr_fused.cu", "cqr_update.cu", "cqr_factor.cu"]
+SOURCES = ["cqr_abi.cu", "cqr_gram.cu", "cqr_gram_pairs.cu", "cqr_gemm.cu", "cqr_layout.cu", "cqr_fused.cu", "cqr_update.cu", "cqr_factor.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -41,10 +41,18 @@ int cqr_abi_version(void) { return CQR_ABI_VERSION; }
 
 const char* cqr_last_error(void) { return g_last_error.c_str(); }
 
+static int g_gram_pairs = 1;   // block-row-pair self-Gram kernel (k <= 256)
+void cqr_set_gram_pairs(int enable) { g_gram_pairs = enable ? 1 : 0; }
+
 size_t cqr_gram_workspace_bytes(int64_t m, int ka, int kb, int self) {
   if (ka <= 0 || kb <= 0) return 256;
   cqr::GramArgs a = cqr::gram_plan(nullptr, 0, ka, nullptr, 0, kb, cqr::round_up(m, 16), self != 0);
-  return cqr::gram_workspace_bytes(a) + 256;
+  size_t b = cqr::gram_workspace_bytes(a) + 256;
+  if (self && cqr::gram_pairs_supported(ka)) {
+    const size_t b2 = cqr::gram_pairs_ws_bytes(cqr::round_up(m, 16), ka);
+    if (b2 > b) b = b2;
+  }
+  return b;
 }
 
 static int gram_common(const double* A, int64_t lda, int ka, const double* B, int64_t ldb, int kb, int64_t m,
@@ -57,6 +65,13 @@ static int gram_common(const double* A, int64_t lda, int ka, const double* B, in
   }
   if (ka == 0 || kb == 0) return CQR_OK;
   if (G == nullptr || ldg < ka) return fail(CQR_EINVAL, std::string(who) + ": bad output G / ldg");
+  if (self && g_gram_pairs && cqr::gram_pairs_supported(ka)) {
+    if (ws == nullptr || ws_bytes < cqr::gram_pairs_ws_bytes(cqr::round_up(m, 16), ka))
+      return fail(CQR_EINVAL, std::string(who) + ": workspace too small");
+    return cuda_check(cqr::gram_pairs_launch(A, lda, ka, cqr::round_up(m, 16), G, ldg, static_cast<double*>(ws),
+                                             static_cast<cudaStream_t>(stream)),
+                      who);
+  }
   cqr::GramArgs a = cqr::gram_plan(A, lda, ka, B, ldb, kb, cqr::round_up(m, 16), self);
   if (ws_bytes < cqr::gram_workspace_bytes(a) || ws == nullptr)
     return fail(CQR_EINVAL, std::string(who) + ": workspace too small");

@@ -1,0 +1,237 @@
+// K1 (v2): self Gram by block-row pairs, for k <= 256.
+//
+// Replaces `DenseVectorArray.gramian()` (reference varray.py:150-153) like
+// cqr_gram.cu, with a schedule built for full-row panels:
+//   * the lower triangle of the NB x NB grid of 8x8 blocks (NB = KP/8, KP =
+//     k rounded up to a power of two >= 16) is cut into the NB/2 block-row
+//     pairs (i, NB-1-i); every pair holds exactly NB+1 blocks, so one pair
+//     per warp balances the DMMA work perfectly;
+//   * a CTA (8 warps, one per SM; thread 0 issues the copies) owns 8 pairs -- the whole
+//     triangle for KP <= 128 (KP < 128: several warps per pair, splitting
+//     the k4 steps), half of it for KP = 256 (two CTAs per row range) -- and
+//     streams 32-row panels of ALL k columns (QI layout: one bulk copy per
+//     stage when ldk == KP), so X is read once (twice from L2 for KP = 256)
+//     instead of once per 64x64 tile;
+//   * per k4 step a warp loads the NB-i fragments of its columns once (the
+//     two row fragments are among them) and issues NB+1 DMMA.8x8x4.
+// Per-CTA partial triangles go to a workspace; a fixed-order reduce sums them.
+#include "cqr_common.cuh"
+#include "cqr_kernels.h"
+
+namespace cqr {
+
+constexpr int GP_THREADS = 256;   // 8 warps; thread 0 also issues the bulk copies
+constexpr int GP_BR = 32;         // rows per stage
+constexpr int GP_STAGES = 3;
+
+template <int KP>
+struct GPCfg {
+  static constexpr int NB = KP / 8;
+  static constexpr int PAIRS = NB / 2;
+  static constexpr int ITEMS = (PAIRS > 8) ? PAIRS / 8 : 1;     // CTAs per row range
+  static constexpr int WPP = (PAIRS >= 8) ? 1 : 8 / PAIRS;      // warps per pair
+  static constexpr int STAGE = GP_BR * KP;                      // doubles
+};
+
+template <int KP>
+size_t gp_smem_bytes() {
+  return (size_t)GP_STAGES * GPCfg<KP>::STAGE * sizeof(double) + 2 * GP_STAGES * 8 + 64;
+}
+
+// one pair (i, NB-1-i): acc[0..i] = row i (cols 0..i), acc[i+1..NB] = row NB-1-i (cols 0..NB-1-i)
+template <int NB, int I>
+__device__ __forceinline__ void pair_steps(double (&acc)[NB + 1][2], const double* fp, int ks0, int ks1, int kst) {
+  constexpr int J = NB - 1 - I;
+  for (int ks = ks0; ks < ks1; ks += kst) {
+    const double* q = fp + ks * (NB * 32);   // quad ks of a [quad][KP][4] panel
+    double f[J + 1];
+#pragma unroll
+    for (int c = 0; c <= J; ++c) f[c] = q[32 * c];
+#pragma unroll
+    for (int c = 0; c <= I; ++c) dmma(acc[c], f[I], f[c]);
+#pragma unroll
+    for (int c = 0; c <= J; ++c) dmma(acc[I + 1 + c], f[J], f[c]);
+  }
+}
+
+template <int NB, int I>
+__device__ __forceinline__ void pair_store(const double (&acc)[NB + 1][2], double* out, int g, int t) {
+  constexpr int J = NB - 1 - I;
+  constexpr int KP = 8 * NB;
+  // out: KP x KP column-major partial
+#pragma unroll
+  for (int c = 0; c <= I; ++c)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) out[(8 * c + 2 * t + e) * KP + 8 * I + g] += acc[c][e];
+#pragma unroll
+  for (int c = 0; c <= J; ++c)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) out[(8 * c + 2 * t + e) * KP + 8 * J + g] += acc[I + 1 + c][e];
+}
+
+template <int NB, int I>
+struct PairDispatch {
+  __device__ static void run(int pair, double (&acc)[NB + 1][2], const double* fp, int ks0, int ks1, int kst) {
+    if (pair == I) pair_steps<NB, I>(acc, fp, ks0, ks1, kst);
+    else PairDispatch<NB, I + 1>::run(pair, acc, fp, ks0, ks1, kst);
+  }
+  __device__ static void store(int pair, const double (&acc)[NB + 1][2], double* out, int g, int t) {
+    if (pair == I) pair_store<NB, I>(acc, out, g, t);
+    else PairDispatch<NB, I + 1>::store(pair, acc, out, g, t);
+  }
+};
+template <int NB>
+struct PairDispatch<NB, NB / 2> {
+  __device__ static void run(int, double (&)[NB + 1][2], const double*, int, int, int) {}
+  __device__ static void store(int, const double (&)[NB + 1][2], double*, int, int) {}
+};
+
+template <int KP>
+__global__ void __launch_bounds__(GP_THREADS, 1) gram_pairs_kernel(const double* __restrict__ X, int64_t ldx, int k,
+                                                                   int64_t rows, int nsplit, double* ws) {
+  using C = GPCfg<KP>;
+  constexpr int NB = C::NB;
+  extern __shared__ __align__(128) double smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + GP_STAGES * C::STAGE);
+  uint64_t* empty = full + GP_STAGES;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int item = blockIdx.x % C::ITEMS, split = blockIdx.x / C::ITEMS;
+  const int64_t npan = ceil_div(rows, GP_BR);
+  const int64_t p0 = npan * split / nsplit, p1 = npan * (split + 1) / nsplit;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < GP_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 8); }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  auto issue = [&](int64_t p, int st) {
+    const int64_t r0 = p * GP_BR;
+    const int nq = (int)imin64(GP_BR, rows - r0) >> 2;
+    double* dst = smem + st * C::STAGE;
+    const double* src = X + (r0 >> 2) * 4 * ldx;
+    mbar_arrive_expect_tx(&full[st], (uint32_t)nq * k * 32);
+    if (ldx == KP && k == KP) {
+      bulk_g2s(dst, src, (uint32_t)nq * KP * 32, &full[st]);
+    } else {
+      for (int q = 0; q < nq; ++q) bulk_g2s(dst + q * 4 * KP, src + q * 4 * ldx, (uint32_t)k * 32, &full[st]);
+    }
+  };
+  if (threadIdx.x == 0)
+    for (int j = 0; j < GP_STAGES - 1 && p0 + j < p1; ++j) issue(p0 + j, j);
+
+  const int g = lane >> 2, t = lane & 3;
+  const int pair = item * 8 + warp / C::WPP;       // pair index handled by this warp
+  const int sub = warp % C::WPP;                   // k4-step phase when several warps share a pair
+  double acc[NB + 1][2];
+#pragma unroll
+  for (int c = 0; c <= NB; ++c) { acc[c][0] = 0.0; acc[c][1] = 0.0; }
+  const double* fbase = smem + 4 * g + t;           // (column g, row t) of quad 0
+  const bool active = pair < C::PAIRS;
+  int it = 0;
+  for (int64_t p = p0; p < p1; ++p, ++it) {
+    const int s = it % GP_STAGES;
+    if (threadIdx.x == 0 && p + GP_STAGES - 1 < p1) {
+      // refill the stage consumed GP_STAGES - 1 panels ago
+      const int it2 = it + GP_STAGES - 1;
+      const int s2 = it2 % GP_STAGES;
+      if (it2 >= GP_STAGES) mbar_wait(&empty[s2], ((it2 / GP_STAGES) - 1) & 1);
+      issue(p + GP_STAGES - 1, s2);
+    }
+    mbar_wait(&full[s], (it / GP_STAGES) & 1);
+    const int nk4 = (int)imin64(GP_BR, rows - p * GP_BR) >> 2;
+    if (active) {
+      const double* fp = fbase + s * C::STAGE;
+      // columns >= k of the staged panel hold stale data: only outputs in
+      // rows/cols >= k see them, and those are never read back
+      PairDispatch<NB, 0>::run(pair, acc, fp, sub, nk4, C::WPP);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+
+  // ---- per-CTA partial (KP x KP column-major, lower triangle), warps in fixed order
+  double* out = ws + ((int64_t)split * C::ITEMS + item) * KP * KP;
+  for (int e = threadIdx.x; e < KP * KP; e += 256) out[e] = 0.0;
+  asm volatile("bar.sync 1, 256;" ::: "memory");
+  for (int w = 0; w < 8; ++w) {
+    if (warp == w && active) PairDispatch<NB, 0>::store(pair, acc, out, g, t);
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+  }
+}
+
+__global__ void gram_pairs_reduce(const double* __restrict__ ws, int nparts, int KP, int k, double* G, int ldg) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)k * k;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e % k), c = (int)(e / k);
+    if (r < c) continue;
+    double s = 0.0;
+    for (int p = 0; p < nparts; ++p) s += ws[(int64_t)p * KP * KP + (int64_t)c * KP + r];
+    G[(int64_t)c * ldg + r] = s;
+    G[(int64_t)r * ldg + c] = s;
+  }
+}
+
+static int gp_kp(int k) {
+  if (k <= 16) return 16;
+  if (k <= 32) return 32;
+  if (k <= 64) return 64;
+  if (k <= 128) return 128;
+  if (k <= 256) return 256;
+  return 0;
+}
+
+bool gram_pairs_supported(int k) { return k >= 1 && gp_kp(k) != 0; }
+
+static void gp_grid(int64_t rows, int kp, int& items, int& nsplit) {
+  items = (kp == 256) ? 2 : 1;
+  const int64_t npan = ceil_div(rows, GP_BR);
+  int64_t ns = num_sms() / items;
+  if (ns > npan) ns = npan;
+  if (ns < 1) ns = 1;
+  nsplit = (int)ns;
+}
+
+size_t gram_pairs_ws_bytes(int64_t rows, int k) {
+  const int kp = gp_kp(k);
+  if (!kp) return 0;
+  int items, nsplit;
+  gp_grid(rows, kp, items, nsplit);
+  return (size_t)items * nsplit * kp * kp * sizeof(double) + 256;
+}
+
+template <int KP>
+static cudaError_t launch_gp(const double* X, int64_t ldx, int k, int64_t rows, double* G, int ldg, double* ws,
+                             cudaStream_t s) {
+  static bool attr = false;
+  const size_t smem = gp_smem_bytes<KP>();
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(gram_pairs_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  int items, nsplit;
+  gp_grid(rows, KP, items, nsplit);
+  gram_pairs_kernel<KP><<<items * nsplit, GP_THREADS, smem, s>>>(X, ldx, k, rows, nsplit, ws);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const int64_t nel = (int64_t)k * k;
+  int blocks = (int)imin64(ceil_div(nel, 256), 4 * num_sms());
+  gram_pairs_reduce<<<blocks < 1 ? 1 : blocks, 256, 0, s>>>(ws, items * nsplit, KP, k, G, ldg);
+  return cudaGetLastError();
+}
+
+cudaError_t gram_pairs_launch(const double* X, int64_t ldx, int k, int64_t rows, double* G, int ldg, double* ws,
+                              cudaStream_t s) {
+  switch (gp_kp(k)) {
+    case 16: return launch_gp<16>(X, ldx, k, rows, G, ldg, ws, s);
+    case 32: return launch_gp<32>(X, ldx, k, rows, G, ldg, ws, s);
+    case 64: return launch_gp<64>(X, ldx, k, rows, G, ldg, ws, s);
+    case 128: return launch_gp<128>(X, ldx, k, rows, G, ldg, ws, s);
+    case 256: return launch_gp<256>(X, ldx, k, rows, G, ldg, ws, s);
+    default: return cudaErrorNotSupported;
+  }
+}
+
+}  // namespace cqr

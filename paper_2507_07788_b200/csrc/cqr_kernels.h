@@ -26,6 +26,11 @@ GramArgs gram_plan(const double* A, int64_t lda, int ka, const double* B, int64_
 size_t gram_workspace_bytes(const GramArgs& a);
 cudaError_t gram_launch(GramArgs& a, double* G, int ldg, cudaStream_t stream);
 
+bool gram_pairs_supported(int k);
+size_t gram_pairs_ws_bytes(int64_t rows, int k);
+cudaError_t gram_pairs_launch(const double* X, int64_t ldx, int k, int64_t rows, double* G, int ldg, double* ws,
+                              cudaStream_t s);
+
 // ------------------------------------------------------------- row-panel GEMM (K2 building block)
 struct GemmArgs {
   const double* X; int64_t ldx; int kx;   // QI m x kx (ldx = column capacity)
