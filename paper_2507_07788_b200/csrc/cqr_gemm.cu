@@ -3,7 +3,8 @@
 //
 // Replaces `DenseVectorArray.lincomb` (reference varray.py:157-163: X @ C plus
 // a Fortran re-layout copy).  CTA tile = 64 rows x 64 output columns, four
-// consumer warps in a 2x2 grid of 32x32 register tiles, one producer warp.
+// consumer warps in a 2x2 grid of 32-row x (4 interleaved 8-column blocks)
+// register tiles, one producer warp.
 // The K dimension is streamed in chunks of 32 columns: per chunk one stage
 // holds X[64 rows, 32 cols] (16 bulk copies of one 1 KB quad run each) and
 // the 32 x 64 coefficient tile (one 18 KB bulk copy of the pre-tiled C,
@@ -33,6 +34,12 @@ __device__ __forceinline__ int group_tiles(int grp, int T, int upper, int (&tile
   if (upper && T - 1 - grp != grp) { tiles[1] = T - 1 - grp; return 2; }
   return 1;
 }
+
+// 8-column block j (0..3) of warp column wj: wj = 0 owns blocks {0,3,4,7},
+// wj = 1 owns {1,2,5,6}.  On the diagonal 64x64 block of a triangular C,
+// block b needs b+1 k-octets, so both sets cost 18 -- the two warp columns
+// (and the SM sub-partitions they run on) get equal DMMA work.
+__device__ __forceinline__ int col_block(int j, int wj) { return 2 * j + (wj ^ (j & 1)); }
 
 __global__ void __launch_bounds__(GM_THREADS, 2) gemm_kernel(GemmArgs args) {
   extern __shared__ __align__(128) double smem[];
@@ -102,9 +109,35 @@ __global__ void __launch_bounds__(GM_THREADS, 2) gemm_kernel(GemmArgs args) {
         const double* Cs = Xs + GM_XS;
         // A fragment (row 32wi+8i+g, col kc+4ks+t): quad 8wi+2i+g/4, offset 4(4ks+t) + g%4
         const double* xp = Xs + (8 * wi + (g >> 2)) * (GM_KC * 4) + 4 * t + (g & 3);
-        const double* cp = Cs + (32 * wj + g) * CT_LD + t;
+        const double* cp = Cs + g * CT_LD + t;
         const bool tail = kc + GM_KC > args.kx;   // X columns past kx hold stale data
-        const int colmax = n0 + 32 * wj + 31;     // last output column of this warp
+        const int colmax = n0 + 63 - 8 * wj;      // last output column of this warp
+        if (!tail && (!args.upper || kc + GM_KC <= n0)) {
+          // full chunk (no zero blocks, no stale columns): fully unrolled,
+          // next k4 step's fragments loaded while this step's DMMAs issue
+          double a[2][4], b[2][4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) a[0][i] = xp[2 * i * (GM_KC * 4)];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) b[0][j] = cp[8 * col_block(j, wj) * CT_LD];
+#pragma unroll
+          for (int ks = 0; ks < GM_KC / 4; ++ks) {
+            const int cur = ks & 1;
+            if (ks + 1 < GM_KC / 4) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) a[cur ^ 1][i] = xp[2 * i * (GM_KC * 4) + 16 * (ks + 1)];
+#pragma unroll
+              for (int j = 0; j < 4; ++j) b[cur ^ 1][j] = cp[8 * col_block(j, wj) * CT_LD + 4 * (ks + 1)];
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+              for (int i = 0; i < 4; ++i) dmma(acc[i][j], a[cur][i], b[cur][j]);
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[s]);
+          continue;
+        }
 #pragma unroll 2
         for (int ks = 0; ks < GM_KC / 4; ++ks) {
           const int k4 = kc + 4 * ks;
@@ -115,10 +148,10 @@ __global__ void __launch_bounds__(GM_THREADS, 2) gemm_kernel(GemmArgs args) {
 #pragma unroll
           for (int i = 0; i < 4; ++i) a[i] = kval ? xp[2 * i * (GM_KC * 4) + 16 * ks] : 0.0;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) b[j] = cp[8 * j * CT_LD + 4 * ks];
+          for (int j = 0; j < 4; ++j) b[j] = cp[8 * col_block(j, wj) * CT_LD + 4 * ks];
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            if (args.upper && k4 > n0 + 32 * wj + 8 * j + 7) continue;  // block of zeros
+            if (args.upper && k4 > n0 + 8 * col_block(j, wj) + 7) continue;  // block of zeros
 #pragma unroll
             for (int i = 0; i < 4; ++i) dmma(acc[i][j], a[i], b[j]);
           }
@@ -136,7 +169,7 @@ __global__ void __launch_bounds__(GM_THREADS, 2) gemm_kernel(GemmArgs args) {
         for (int j = 0; j < 4; ++j)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const int col = n0 + 32 * wj + 8 * j + 2 * t + e;
+            const int col = n0 + 8 * col_block(j, wj) + 2 * t + e;
             if (col < args.n) yq[4 * (int64_t)col] = acc[i][j][e];
           }
       }

@@ -22,7 +22,6 @@ namespace cqr {
 
 constexpr int GP_THREADS = 256;   // 8 warps; thread 0 also issues the bulk copies
 constexpr int GP_BR = 32;         // rows per stage
-constexpr int GP_STAGES = 3;
 
 template <int KP>
 struct GPCfg {
@@ -31,11 +30,15 @@ struct GPCfg {
   static constexpr int ITEMS = (PAIRS > 8) ? PAIRS / 8 : 1;     // CTAs per row range
   static constexpr int WPP = (PAIRS >= 8) ? 1 : 8 / PAIRS;      // warps per pair
   static constexpr int STAGE = GP_BR * KP;                      // doubles
+  // ring depth: ~192 KB of panels in flight per SM (HBM latency x per-SM
+  // bandwidth needs >= 64 KB outstanding), at most 8 stages
+  static constexpr int S_FIT = (192 * 1024) / (STAGE * 8);
+  static constexpr int STAGES = S_FIT > 8 ? 8 : (S_FIT < 3 ? 3 : S_FIT);
 };
 
 template <int KP>
 size_t gp_smem_bytes() {
-  return (size_t)GP_STAGES * GPCfg<KP>::STAGE * sizeof(double) + 2 * GP_STAGES * 8 + 64;
+  return (size_t)GPCfg<KP>::STAGES * GPCfg<KP>::STAGE * sizeof(double) + 2 * GPCfg<KP>::STAGES * 8 + 64;
 }
 
 // one pair (i, NB-1-i): acc[0..i] = row i (cols 0..i), acc[i+1..NB] = row NB-1-i (cols 0..NB-1-i)
@@ -91,6 +94,7 @@ __global__ void __launch_bounds__(GP_THREADS, 1) gram_pairs_kernel(const double*
                                                                    int64_t rows, int nsplit, double* ws) {
   using C = GPCfg<KP>;
   constexpr int NB = C::NB;
+  constexpr int GP_STAGES = C::STAGES;
   extern __shared__ __align__(128) double smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + GP_STAGES * C::STAGE);
   uint64_t* empty = full + GP_STAGES;
