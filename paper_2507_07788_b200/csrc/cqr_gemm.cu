@@ -41,6 +41,34 @@ __device__ __forceinline__ int group_tiles(int grp, int T, int upper, int (&tile
 // (and the SM sub-partitions they run on) get equal DMMA work.
 __device__ __forceinline__ int col_block(int j, int wj) { return 2 * j + (wj ^ (j & 1)); }
 
+// Diagonal chunk CH (0/1) of a 64-column tile of an upper-triangular C for
+// warp column WJ: every block/step condition is a compile-time constant, so
+// no DMMA is issued for a zero block (predicated-off DMMAs still occupy the
+// tensor pipe).  Block b is live at k4 step ks iff 4 CH + ks/2 <= b.
+template <int WJ, int CH>
+__device__ __forceinline__ void diag_chunk(double (&acc)[4][4][2], const double* xp, const double* cp) {
+  constexpr int bmax = WJ == 0 ? 7 : 6;
+#pragma unroll
+  for (int ks = 0; ks < GM_KC / 4; ++ks) {
+    if (4 * CH + ks / 2 > bmax) break;
+    double a[4], b[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = xp[2 * i * (GM_KC * 4) + 16 * ks];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int cb = 2 * j + (WJ ^ (j & 1));
+      if (4 * CH + ks / 2 <= cb) b[j] = cp[8 * cb * CT_LD + 4 * ks];
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int cb = 2 * j + (WJ ^ (j & 1));
+      if (4 * CH + ks / 2 > cb) continue;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) dmma(acc[i][j], a[i], b[j]);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(GM_THREADS, 2) gemm_kernel(GemmArgs args) {
   extern __shared__ __align__(128) double smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + GM_STAGES * GM_STAGE_DOUBLES);
@@ -134,6 +162,14 @@ __global__ void __launch_bounds__(GM_THREADS, 2) gemm_kernel(GemmArgs args) {
 #pragma unroll
               for (int i = 0; i < 4; ++i) dmma(acc[i][j], a[cur][i], b[cur][j]);
           }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[s]);
+          continue;
+        }
+        if (args.upper && !tail && kc >= n0) {
+          const int ch = (kc - n0) >> 5;   // 0 or 1
+          if (wj == 0) { if (ch == 0) diag_chunk<0, 0>(acc, xp, cp); else diag_chunk<0, 1>(acc, xp, cp); }
+          else         { if (ch == 0) diag_chunk<1, 0>(acc, xp, cp); else diag_chunk<1, 1>(acc, xp, cp); }
           __syncwarp();
           if (lane == 0) mbar_arrive(&empty[s]);
           continue;
