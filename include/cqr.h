@@ -152,8 +152,9 @@ int cqr_pack_coeffs(const double* src, int ld, int k, int n, double* dst, void* 
  * over X (Q may alias X).  Replaces the lincomb + gramian pair of one
  * iteration (algorithms.py:350,352 / :238,:240 / :211 + :209). */
 size_t cqr_apply_gram_workspace_bytes(int64_t m, int k);
-/* Select the single-kernel fused TRMM + Gram pass for k <= 64 and 97..128
- * (default off; the two-kernel path is faster on B200 in this release). */
+/* Select the single-kernel fused TRMM + Gram pass for 33 <= k <= 64 and
+ * 97 <= k <= 128 (default off: the two-kernel TRMM then Gram path is faster on
+ * B200, where these passes are FP64-pipe bound, not HBM bound). */
 void cqr_set_fused(int enable);
 /* Number of kernel launches one cqr_apply_gram call issues for width k. */
 int cqr_apply_gram_launches(int k);

@@ -1,288 +1,279 @@
-// K2 fused pass for k <= 128: Q = X R^-1 (R^-1 upper triangular) and
-// G = Q^T Q in one stream over X (Q may alias X).
+// K2 fused pass for 33 <= k <= 64 and 97 <= k <= 128: Q = X R^-1 (R^-1
+// upper triangular) and G = Q^T Q in one stream over X (Q may alias X).
 //
 // Replaces the lincomb + gramian pair of one iteration (reference
 // algorithms.py:350,352 / :238,:240 / :211 + chol_qr2's second Gram) with one
 // HBM read of X and one write of Q per pass (the unfused pair reads Q again).
 //
-// CTA = 8 consumer warps + 1 producer warp, persistent over row panels of BR
-// rows (one wave, one CTA per SM).  At start the CTA loads the R^-1
-// coefficient tiles it needs (upper part only) into shared memory.  Per
-// panel: the producer stages X (QI layout: one run per quad) into a 2-stage
-// ring; the consumers
-//   1. compute the Q panel with DMMA -- warp w owns a row group and the
-//      column-block pair (c, NC-1-c), so every warp gets the same triangular
-//      work -- and store it to HBM straight from registers;
-//   2. after a CTA barrier overwrite the staged X with Q (QI layout) and
-//      accumulate the lower-triangular Gram from it (32x32 register
-//      sub-tiles, diagonal ones skipping upper blocks, shared sub-tiles split
-//      over k4 steps);
-//   3. release the stage.
-// Partials are summed inside the CTA in a fixed warp order and written once
-// per CTA; gram_fused_reduce sums them over CTAs in a fixed order.
+// Warp-specialised, one CTA per SM, persistent over 32-row panels.  With
+// NB = KP/8 column blocks and P = NB/2:
+//   * P TRMM warps: warp c owns the column-block pair (c, NB-1-c) for all 32
+//     rows of a panel -- every pair costs 2(NB+1) k4 steps, so the warps are
+//     balanced -- reads the X panel from a TMA ring (XST stages) and writes
+//     Q into a ring of Q panels in shared memory;
+//   * P Gram warps: warp i owns the block-row pair (i, NB-1-i) of the lower
+//     triangle (NB+1 blocks each) and accumulates it from the Q ring in
+//     registers over the whole sweep; one lane of Gram warp 0 stores each Q
+//     panel to HBM with bulk copies from the ring.
+// Per 8 rows both halves issue NB(NB+1) DMMA.8x8x4, all from compile-time
+// loops (no predicated-off DMMA occupies the tensor pipe).  The groups hand
+// panels over through mbarriers only (no CTA-wide barrier in the sweep).
+// Thread 0 issues the bulk copies.  Per-CTA partial triangles are summed in a
+// fixed warp order, then over CTAs by gram_fused_reduce in a fixed order.
 #include "cqr_common.cuh"
 #include "cqr_kernels.h"
+#include "cqr_pairs.cuh"
 
 namespace cqr {
 
-constexpr int FU_THREADS = 256;   // 8 warps; thread 0 also issues the bulk copies
+constexpr int FU_BR = 32;   // rows per panel = 8 k4 steps
 
 template <int KP>
-struct FusedCfg {
-  static constexpr int NC = KP / 8;                       // 8-column blocks
-  static constexpr int BR = (KP >= 128) ? 32 : 64;        // rows per panel
-  static constexpr int NR = BR / 8;                       // 8-row blocks per panel
-  static constexpr int PAIRS = NC / 2;                    // column-block pairs
-  static constexpr int RGROUPS = 8 / PAIRS;               // row groups (warps = RGROUPS * PAIRS)
-  static constexpr int RB = NR / RGROUPS;                 // row blocks per warp
-  static constexpr int STAGE = BR * KP;                   // doubles per staged panel
-  static constexpr int NKT = KP / CT_K;                   // coefficient k tiles
-  static constexpr int NNT = (KP + CT_N - 1) / CT_N;      // coefficient n tiles
-  static constexpr int T = KP / 32;                       // 32x32 Gram sub-tiles per side
+struct FuCfg {
+  static constexpr int NB = KP / 8;
+  static constexpr int PAIRS = NB / 2;        // TRMM warps = Gram warps
+  // KP = 64: a dedicated producer warp issues the X copies; KP = 128 (16
+  // compute warps, 128 registers each) keeps the producer inline on thread 0
+  static constexpr bool PRODUCER = KP == 64;
+  static constexpr int THREADS = 64 * PAIRS + (PRODUCER ? 32 : 0);
+  static constexpr int NKT = KP / CT_K;       // 32-row coefficient k tiles
+  static constexpr int NNT = KP / CT_N;       // 64-column coefficient n tiles
+  static constexpr int STAGE = FU_BR * KP;    // doubles per panel
+  static constexpr int XST = (KP == 64) ? 6 : 2;
+  static constexpr int QB = (KP == 64) ? 3 : 1;
 };
 
-// coefficient tiles of R^-1 needed (kt*32 < (nt+1)*64), in order; index -> slot
+// coefficient tiles of R^-1 that hold upper-triangle entries (kt*32 < (nt+1)*64), packed in order
 template <int KP>
-__device__ __forceinline__ int tile_slot(int kt, int nt) {
+__host__ __device__ constexpr int tile_slot(int kt, int nt) {
   int slot = 0;
-  for (int n = 0; n < nt; ++n) slot += min(FusedCfg<KP>::NKT, 2 * (n + 1));
+  for (int n = 0; n < nt; ++n) slot += (FuCfg<KP>::NKT < 2 * (n + 1)) ? FuCfg<KP>::NKT : 2 * (n + 1);
   return slot + kt;
 }
 template <int KP>
 __host__ __device__ constexpr int n_tiles_needed() {
-  int s = 0;
-  for (int n = 0; n < FusedCfg<KP>::NNT; ++n) s += (FusedCfg<KP>::NKT < 2 * (n + 1)) ? FusedCfg<KP>::NKT : 2 * (n + 1);
-  return s;
+  return tile_slot<KP>(0, FuCfg<KP>::NNT);
 }
-
 template <int KP>
 __host__ __device__ constexpr size_t fused_smem_doubles() {
-  return ((size_t)n_tiles_needed<KP>() * CT_TILE + 2 * FusedCfg<KP>::STAGE) > (size_t)KP * KP
-             ? (size_t)n_tiles_needed<KP>() * CT_TILE + 2 * FusedCfg<KP>::STAGE
-             : (size_t)KP * KP;
+  return (size_t)n_tiles_needed<KP>() * CT_TILE + (size_t)(FuCfg<KP>::XST + FuCfg<KP>::QB) * FuCfg<KP>::STAGE;
 }
 
-// Gram work of warp w: (sub-tile i, j, diag, k4 start, k4 stride)
-template <int KP>
-__device__ __forceinline__ void gram_role(int w, int& si, int& sj, int& k0, int& kst) {
-  if constexpr (KP == 128) {
-    // 6 off-diagonal sub-tiles (warps 0-5), 4 diagonal ones in pairs (warps 6, 7)
-    // off sub-tiles (1,0) (2,0) (3,0) (2,1) (3,1) (3,2) for warps 0..5
-    if (w < 6) {
-      si = (w < 3) ? w + 1 : (w < 5 ? w - 1 : 3);
-      sj = (w < 3) ? 0 : (w < 5 ? 1 : 2);
-    } else {
-      si = sj = (w - 6) * 2;   // and si + 1
+// Q[32 rows, blocks CA and CB] of one panel; xp -> (row g, col t) of the
+// staged X panel, rp -> (col g, k t) of the coefficient tile area.  The
+// fragments of k4 step ks+1 are loaded before the DMMAs of step ks issue.
+template <int KP, int CA, bool KFULL>
+__device__ __forceinline__ void fu_trmm(double (&acc)[4][2][2], const double* xp, const double* rp, int t, int k) {
+  constexpr int NB = KP / 8, CB = NB - 1 - CA;
+  constexpr int NKA = 2 * (CA + 1), NKB = 2 * (CB + 1);
+#pragma unroll
+  for (int rb = 0; rb < 4; ++rb)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) { acc[rb][c][0] = 0.0; acc[rb][c][1] = 0.0; }
+  double a[2][4], bA[2], bB[2];
+  auto load = [&](int ks, int buf) {
+    const bool kv = KFULL || (4 * ks + t < k);   // X columns >= k of the stage are stale
+#pragma unroll
+    for (int rb = 0; rb < 4; ++rb) a[buf][rb] = kv ? xp[rb * 8 * KP + 16 * ks] : 0.0;
+    bB[buf] = rp[tile_slot<KP>(ks / 8, CB / 8) * CT_TILE + ((8 * CB) & 63) * CT_LD + 4 * (ks % 8)];
+    if (ks < NKA) bA[buf] = rp[tile_slot<KP>(ks / 8, CA / 8) * CT_TILE + ((8 * CA) & 63) * CT_LD + 4 * (ks % 8)];
+  };
+  load(0, 0);
+#pragma unroll
+  for (int ks = 0; ks < NKB; ++ks) {
+    const int cur = ks & 1;
+    if (ks + 1 < NKB) load(ks + 1, cur ^ 1);
+#pragma unroll
+    for (int rb = 0; rb < 4; ++rb) dmma(acc[rb][1], a[cur][rb], bB[cur]);
+    if (ks < NKA) {
+#pragma unroll
+      for (int rb = 0; rb < 4; ++rb) dmma(acc[rb][0], a[cur][rb], bA[cur]);
     }
-    k0 = 0; kst = 1;
-  } else if constexpr (KP == 64) {
-    // off (1,0) over warps 0-3 (k4 mod 4), diag (0,0) over 4-5, diag (1,1) over 6-7 (k4 mod 2)
-    if (w < 4) { si = 1; sj = 0; k0 = w; kst = 4; }
-    else if (w < 6) { si = sj = 0; k0 = w - 4; kst = 2; }
-    else { si = sj = 1; k0 = w - 6; kst = 2; }
-  } else {
-    si = sj = 0; k0 = w; kst = 8;
   }
 }
 
-template <int KP>
-__global__ void __launch_bounds__(FU_THREADS, 1) apply_gram_fused_kernel(const double* X, int64_t ldx,
-                                                                          int k, const double* __restrict__ Rt,
-                                                                          double* Q, int64_t ldq, int64_t rows,
-                                                                          double* __restrict__ ws) {
-  using C = FusedCfg<KP>;
+template <int KP, int C, bool KFULL>
+struct TrmmDispatch {
+  __device__ static void run(int pair, double (&acc)[4][2][2], const double* xp, const double* rp, int t, int k) {
+    if (pair == C) fu_trmm<KP, C, KFULL>(acc, xp, rp, t, k);
+    else TrmmDispatch<KP, C + 1, KFULL>::run(pair, acc, xp, rp, t, k);
+  }
+};
+template <int KP, bool KFULL>
+struct TrmmDispatch<KP, KP / 16, KFULL> {
+  __device__ static void run(int, double (&)[4][2][2], const double*, const double*, int, int) {}
+};
+
+template <int KP, bool KFULL>
+__global__ void __launch_bounds__(FuCfg<KP>::THREADS, 1)
+    apply_gram_fused_kernel(const double* X, int64_t ldx, int k, const double* __restrict__ Rt, double* Q,
+                            int64_t ldq, int64_t rows, double* __restrict__ ws) {
+  using C = FuCfg<KP>;
+  constexpr int NB = C::NB, P = C::PAIRS, XST = C::XST, QB = C::QB;
+  // thread 0 keeps XD panels in flight and refills the stage of panel j-XLAG,
+  // so warp 0 does not wait for the slowest TRMM warp every panel
+  constexpr int XLAG = XST >= 6 ? 2 : 1, XD = XST - XLAG;
   extern __shared__ __align__(128) double smem[];
-  double* rt_s = smem;                                        // R^-1 tiles
-  double* stg = rt_s + n_tiles_needed<KP>() * CT_TILE;        // 2 x STAGE
-  double* red = smem;   // KP x KP partial Gram (column-major), reuses tiles + stages after the loop
-  __shared__ __align__(8) uint64_t bars[6];
-  uint64_t* full = bars;
-  uint64_t* empty = bars + 2;
-  uint64_t* rbar = bars + 4;
+  double* rt_s = smem;                                   // R^-1 tiles
+  double* xst = rt_s + n_tiles_needed<KP>() * CT_TILE;   // XST X panels
+  double* qbuf = xst + XST * C::STAGE;                   // QB Q panels
+  double* red = smem;                                    // KP x KP partial, after the sweep
+  static_assert((size_t)KP * KP <= (size_t)n_tiles_needed<KP>() * CT_TILE + (size_t)XST * C::STAGE,
+                "the partial must not overlap the Q ring");
+  __shared__ __align__(8) uint64_t bars[2 * XST + 2 * QB + 1];
+  uint64_t* xfull = bars;
+  uint64_t* xempty = xfull + XST;
+  uint64_t* qfull = xempty + XST;
+  uint64_t* qempty = qfull + QB;
+  uint64_t* rbar = qempty + QB;
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int64_t npan = ceil_div(rows, C::BR);
+  const int64_t npan = ceil_div(rows, FU_BR);
+  const int64_t mine = (npan > blockIdx.x) ? ceil_div(npan - blockIdx.x, gridDim.x) : 0;
+  constexpr bool kfull = KFULL;   // k == KP
 
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < 2; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 8); }
+  if (tid == 0) {
+    for (int s = 0; s < XST; ++s) { mbar_init(&xfull[s], 1); mbar_init(&xempty[s], P); }
+    for (int s = 0; s < QB; ++s) { mbar_init(&qfull[s], 32 * P); mbar_init(&qempty[s], P); }
     mbar_init(rbar, 1);
     fence_mbar_init();
   }
   __syncthreads();
-  (void)lane;
 
-  // bulk-copy issue (thread 0): R^-1 tiles once, X panels one ahead
-  auto issue_panel = [&](int64_t p, int st) {
-    const int64_t r0 = p * C::BR;
-    const int nq = (int)imin64(C::BR, rows - r0) >> 2;
-    double* dst = stg + st * C::STAGE;
-    mbar_arrive_expect_tx(&full[st], (uint32_t)nq * k * 32);
+  auto issue = [&](int64_t j, int st) {
+    const int64_t r0 = (blockIdx.x + j * gridDim.x) * FU_BR;
+    const int nq = (int)imin64(FU_BR, rows - r0) >> 2;
+    double* dst = xst + st * C::STAGE;
     const double* src = X + (r0 >> 2) * 4 * ldx;
-    if (ldx == KP && k == KP) {
-      bulk_g2s(dst, src, (uint32_t)nq * KP * 32, &full[st]);
+    mbar_arrive_expect_tx(&xfull[st], (uint32_t)nq * k * 32);
+    if (ldx == KP && kfull) {
+      bulk_g2s(dst, src, (uint32_t)nq * KP * 32, &xfull[st]);
     } else {
-      for (int q = 0; q < nq; ++q) bulk_g2s(dst + q * 4 * KP, src + q * 4 * ldx, (uint32_t)k * 32, &full[st]);
+      for (int q = 0; q < nq; ++q) bulk_g2s(dst + q * 4 * KP, src + q * 4 * ldx, (uint32_t)k * 32, &xfull[st]);
     }
   };
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     mbar_arrive_expect_tx(rbar, n_tiles_needed<KP>() * CT_TILE * 8);
     for (int nt = 0; nt < C::NNT; ++nt)
       for (int kt = 0; kt < min(C::NKT, 2 * (nt + 1)); ++kt)
         bulk_g2s(rt_s + tile_slot<KP>(kt, nt) * CT_TILE, Rt + ((int64_t)nt * C::NKT + kt) * CT_TILE, CT_TILE * 8,
                  rbar);
-    if (blockIdx.x < npan) issue_panel(blockIdx.x, 0);
+    if (!C::PRODUCER)
+      for (int j = 0; j < XD && j < mine; ++j) issue(j, j);
   }
-
-  // ---------------- consumers
-  // TRMM role: row blocks [rg*RB, rg*RB + RB), column blocks cA = pair, cB = NC-1-pair
-  const int pair = warp % C::PAIRS, rg = warp / C::PAIRS;
-  const int cA = pair, cB = C::NC - 1 - pair;
-  int si, sj, k0, kst;
-  gram_role<KP>(warp, si, sj, k0, kst);
-  const bool dg = (si == sj);
-
-  constexpr int NX = (KP == 128) ? 2 : 1;   // KP = 128: the diagonal warps own two sub-tiles
-  double gacc[NX][4][4][2];
-#pragma unroll
-  for (int x = 0; x < NX; ++x)
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) { gacc[x][i][j][0] = 0.0; gacc[x][i][j][1] = 0.0; }
-
-  mbar_wait(rbar, 0);
-  int it = 0;
-  for (int64_t p = blockIdx.x; p < npan; p += gridDim.x, ++it) {
-    const int s = it & 1;
-    if (threadIdx.x == 0 && p + gridDim.x < npan) {
-      // stage s^1 held panel it-1: wait until every warp released it, then refill
-      if (it >= 1) mbar_wait(&empty[s ^ 1], ((it - 1) >> 1) & 1);
-      issue_panel(p + gridDim.x, s ^ 1);
-    }
-    mbar_wait(&full[s], (it >> 1) & 1);
-    const int64_t r0 = p * C::BR;
-    const int nrows = (int)imin64(C::BR, rows - r0);
-    double* P = stg + s * C::STAGE;
-
-    // ---- 1. TRMM: qacc[rb][cb] for rb < RB, cb in {cA, cB}
-    double qacc[C::RB][2][2];
-#pragma unroll
-    for (int rb = 0; rb < C::RB; ++rb)
-#pragma unroll
-      for (int c = 0; c < 2; ++c) { qacc[rb][c][0] = 0.0; qacc[rb][c][1] = 0.0; }
-    // K loop over k4 steps; column block c needs K < 8(c+1)
-    const int kmaxB = min(2 * (cB + 1), (k + 3) / 4);
-    const int kmaxA = min(2 * (cA + 1), (k + 3) / 4);
-    for (int ks = 0; ks < kmaxB; ++ks) {
-      const int kc = 4 * ks + t;   // X column of this lane's A fragment
-      double a[C::RB];
-#pragma unroll
-      for (int rb = 0; rb < C::RB; ++rb) {
-        const int row = 8 * (rg * C::RB + rb) + g;
-        a[rb] = (kc < k) ? P[(row >> 2) * 4 * KP + 4 * kc + (row & 3)] : 0.0;
-      }
-      // B fragment: R^-1(kc, 8 cb + g) from tile (kc/32, (8cb+g)/64)
-      const int nB = 8 * cB + g;
-      const double bB = rt_s[tile_slot<KP>(kc >> 5, nB >> 6) * CT_TILE + (nB & 63) * CT_LD + (kc & 31)];
-#pragma unroll
-      for (int rb = 0; rb < C::RB; ++rb) dmma(qacc[rb][1], a[rb], bB);
-      if (ks < kmaxA) {
-        const int nA = 8 * cA + g;
-        const double bA = rt_s[tile_slot<KP>(kc >> 5, nA >> 6) * CT_TILE + (nA & 63) * CT_LD + (kc & 31)];
-#pragma unroll
-        for (int rb = 0; rb < C::RB; ++rb) dmma(qacc[rb][0], a[rb], bA);
-      }
-    }
-    // store Q to HBM (QI) straight from registers
-#pragma unroll
-    for (int rb = 0; rb < C::RB; ++rb) {
-      const int row = 8 * (rg * C::RB + rb) + g;
-      if (row < nrows) {
-        double* qrow = Q + ((r0 + row) >> 2) * 4 * ldq + (row & 3);
-#pragma unroll
-        for (int c = 0; c < 2; ++c)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int col = 8 * (c ? cB : cA) + 2 * t + e;
-            if (col < k) qrow[4 * (int64_t)col] = qacc[rb][c][e];
-          }
-      }
-    }
-    // ---- 2. overwrite the staged X with Q, then the Gram
-    asm volatile("bar.sync 1, 256;" ::: "memory");
-#pragma unroll
-    for (int rb = 0; rb < C::RB; ++rb) {
-      const int row = 8 * (rg * C::RB + rb) + g;
-#pragma unroll
-      for (int c = 0; c < 2; ++c)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int col = 8 * (c ? cB : cA) + 2 * t + e;
-          P[(row >> 2) * 4 * KP + 4 * col + (row & 3)] = (row < nrows && col < k) ? qacc[rb][c][e] : 0.0;
-        }
-    }
-    asm volatile("bar.sync 1, 256;" ::: "memory");
-    {
-      const int nk4 = nrows >> 2;
-      const double* base = P + 4 * g + t;   // (column g, row t) inside quad 0
-      for (int ks = k0; ks < nk4; ks += kst) {
-        const double* qd = base + ks * 4 * KP;
-        double a[4], b[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) a[i] = qd[4 * (32 * si + 8 * i)];
-        if (dg) {
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j <= i; ++j) dmma(gacc[0][i][j], a[i], a[j]);
-          if constexpr (NX == 2) {
-#pragma unroll
-            for (int i = 0; i < 4; ++i) b[i] = qd[4 * (32 * (si + 1) + 8 * i)];
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-              for (int j = 0; j <= i; ++j) dmma(gacc[NX - 1][i][j], b[i], b[j]);
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) b[j] = qd[4 * (32 * sj + 8 * j)];
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) dmma(gacc[0][i][j], a[i], b[j]);
+  if constexpr (C::PRODUCER) {
+    if (warp == 2 * P) {
+      if (lane == 0) {
+        int s = 0;
+        uint32_t ph = 0;
+        for (int64_t j = 0; j < mine; ++j) {
+          if (j >= XST) mbar_wait(&xempty[s], ph ^ 1);
+          issue(j, s);
+          if (++s == XST) { s = 0; ph ^= 1; }
         }
       }
+      return;
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
   }
 
-  // ---- CTA reduction of the Gram partials into red (KP x KP column-major), fixed warp order
-  asm volatile("bar.sync 1, 256;" ::: "memory");   // every warp is done with the tiles and stages
-  for (int e = threadIdx.x; e < KP * KP; e += 256) red[e] = 0.0;
-  asm volatile("bar.sync 1, 256;" ::: "memory");
-  for (int w = 0; w < 8; ++w) {
-    if (warp == w) {
+  if (warp < P) {
+    // ---------------- TRMM warps
+    const int cA = warp, cB = NB - 1 - warp;
+    const double* rp = rt_s + g * CT_LD + t;
+    mbar_wait(rbar, 0);
+    int s = 0, qs = 0;          // ring slots of panel j
+    uint32_t xph = 0, qph = 0;  // (j / XST) & 1, (j / QB) & 1
+    for (int64_t j = 0; j < mine; ++j) {
+      if (!C::PRODUCER && tid == 0 && j + XD < mine) {
+        // stage s2 last held panel j - XLAG (released by every TRMM warp)
+        const int64_t j2 = j + XD;
+        const int s2 = (int)(j2 % XST);
+        if (j2 >= XST) mbar_wait(&xempty[s2], (uint32_t)((j2 / XST) - 1) & 1);
+        issue(j2, s2);
+      }
+      mbar_wait(&xfull[s], xph);
+      const int64_t r0 = (blockIdx.x + j * gridDim.x) * FU_BR;
+      const int nrows = (int)imin64(FU_BR, rows - r0);
+      const double* xp = xst + s * C::STAGE + (g >> 2) * 4 * KP + 4 * t + (g & 3);
+      double acc[4][2][2];
+      TrmmDispatch<KP, 0, KFULL>::run(warp, acc, xp, rp, t, k);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&xempty[s]);
+      // Q -> the Q ring (zeros past the last row / column); a Gram lane
+      // stores the panel to HBM from there with one bulk copy per quad
+      if (j >= QB) mbar_wait(&qempty[qs], qph ^ 1);
+      double* qd = qbuf + qs * C::STAGE + (g >> 2) * 4 * KP + (g & 3);
+      if (KFULL && nrows == FU_BR) {
 #pragma unroll
-      for (int x = 0; x < NX; ++x) {
-        if (x == 1 && !dg) break;
-        const int ti = si + x, tj = sj + x;
+        for (int rb = 0; rb < 4; ++rb)
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+          for (int c = 0; c < 2; ++c)
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
+            for (int e = 0; e < 2; ++e) qd[rb * 8 * KP + 4 * (8 * (c ? cB : cA) + 2 * t + e)] = acc[rb][c][e];
+      } else {
+#pragma unroll
+        for (int rb = 0; rb < 4; ++rb) {
+          const int row = 8 * rb + g;
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-              const int r = 32 * ti + 8 * i + g, c = 32 * tj + 8 * j + 2 * t + e;
-              if (!dg || i >= j) red[c * KP + r] += gacc[x][i][j][e];
+              const int col = 8 * (c ? cB : cA) + 2 * t + e;
+              qd[rb * 8 * KP + 4 * col] = (row < nrows && col < k) ? acc[rb][c][e] : 0.0;
             }
+        }
       }
+      fence_proxy_async_smem();  // the bulk store reads the ring through the async proxy
+      mbar_arrive(&qfull[qs]);   // every lane: its own stores are released
+      if (++s == XST) { s = 0; xph ^= 1; }
+      if (++qs == QB) { qs = 0; qph ^= 1; }
     }
-    asm volatile("bar.sync 1, 256;" ::: "memory");
+  } else {
+    // ---------------- Gram warps
+    const int pr = warp - P;
+    const double* fb = qbuf + 4 * g + t;
+    double gacc[NB + 1][2];
+#pragma unroll
+    for (int c = 0; c <= NB; ++c) { gacc[c][0] = 0.0; gacc[c][1] = 0.0; }
+    int qs = 0;
+    uint32_t qph = 0;
+    const bool storer = (pr == 0 && lane == 0);
+    for (int64_t j = 0; j < mine; ++j) {
+      mbar_wait(&qfull[qs], qph);
+      if (storer) {
+        const int64_t r0 = (blockIdx.x + j * gridDim.x) * FU_BR;
+        const int nq = (int)imin64(FU_BR, rows - r0) >> 2;
+        const double* src = qbuf + qs * C::STAGE;
+        double* dst = Q + (r0 >> 2) * 4 * ldq;
+        if (ldq == KP && KFULL) {
+          bulk_s2g(dst, src, (uint32_t)nq * KP * 32);
+        } else {
+          for (int q = 0; q < nq; ++q) bulk_s2g(dst + q * 4 * ldq, src + q * 4 * KP, (uint32_t)k * 32);
+        }
+        bulk_commit();
+      }
+      PairDispatch<NB, 0>::run(pr, gacc, fb + qs * C::STAGE, 0, FU_BR / 4, 1);
+      if (storer) bulk_wait_read<0>();   // the slot may be refilled once the store has read it
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&qempty[qs]);
+      if (++qs == QB) { qs = 0; qph ^= 1; }
+    }
+    if (storer) bulk_wait<0>();
+    // ---- per-CTA partial (KP x KP column-major, lower triangle), Gram warps in
+    // fixed order.  Every TRMM warp finished with the tiles and X stages before
+    // its last qfull arrive, and red (KP*KP doubles) ends before the Q ring.
+    const int gt = tid - 32 * P;
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * P) : "memory");
+    for (int e = gt; e < KP * KP; e += 32 * P) red[e] = 0.0;
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * P) : "memory");
+    for (int w = 0; w < P; ++w) {
+      if (pr == w) PairDispatch<NB, 0>::store(w, gacc, red, g, t);
+      asm volatile("bar.sync 1, %0;" ::"r"(32 * P) : "memory");
+    }
+    double* out = ws + (int64_t)blockIdx.x * KP * KP;
+    for (int e = gt; e < KP * KP; e += 32 * P) out[e] = red[e];
   }
-  double* out = ws + (int64_t)blockIdx.x * KP * KP;
-  for (int e = threadIdx.x; e < KP * KP; e += 256) out[e] = red[e];
 }
 
 // fixed-order sum over CTAs of the per-CTA KP x KP partials; lower triangle, mirrored
@@ -299,22 +290,22 @@ __global__ void gram_fused_reduce(const double* __restrict__ ws, int nparts, int
 }
 
 static int fused_kp(int k) {
-  if (k <= 32) return 32;
-  if (k <= 64) return 64;
+  if (k > 32 && k <= 64) return 64;
   if (k > 96 && k <= 128) return 128;
-  return 0;   // 65..96: unfused path
+  return 0;   // k <= 32 and 65..96: unfused path
 }
 
-// Off by default: measured slower than TRMM + Gram on B200 in round 1 (two CTA
-// barriers per panel keep the 8 warps in lockstep).  Enabled
-// with cqr_set_fused(1) (tests exercise it).
+// Off by default: on B200 every pass with k >= 64 is bound by the FP64 tensor
+// pipe, not HBM, so saving the second read of Q does not pay; measured
+// (tools/kernel_probe.py): k=64 fused 10.85 ms vs TRMM 5.24 + Gram 4.99 ms at
+// m=32M, k=128 fused 5.89 ms vs 2.21 + 2.10 ms at m=4M.  cqr_set_fused(1)
+// selects it (tests exercise both).
 static int g_fused_enabled = 0;
 void set_fused(int on) { g_fused_enabled = on ? 1 : 0; }
 bool apply_gram_fused_supported(int k) { return g_fused_enabled && k >= 1 && fused_kp(k) != 0; }
 
-static int fused_ctas(int64_t rows, int kp) {
-  const int br = (kp >= 128) ? 32 : 64;
-  int64_t n = ceil_div(rows, br);
+static int fused_ctas(int64_t rows) {
+  int64_t n = ceil_div(rows, FU_BR);
   int64_t c = num_sms();
   return (int)(n < c ? (n < 1 ? 1 : n) : c);
 }
@@ -322,7 +313,7 @@ static int fused_ctas(int64_t rows, int kp) {
 size_t apply_gram_fused_ws_bytes(int64_t rows, int k) {
   const int kp = fused_kp(k);
   if (!kp) return 0;
-  return (size_t)fused_ctas(rows, kp) * kp * kp * sizeof(double) + 256;
+  return (size_t)fused_ctas(rows) * kp * kp * sizeof(double) + 256;
 }
 
 template <int KP>
@@ -331,13 +322,19 @@ static cudaError_t launch_fused(const double* X, int64_t ldx, int k, const doubl
   static bool attr = false;
   const size_t smem = fused_smem_doubles<KP>() * sizeof(double);
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(apply_gram_fused_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(apply_gram_fused_kernel<KP, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(apply_gram_fused_kernel<KP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const int ctas = fused_ctas(rows, KP);
-  apply_gram_fused_kernel<KP><<<ctas, FU_THREADS, smem, s>>>(X, ldx, k, Rt, Q, ldq, rows, ws);
+  const int ctas = fused_ctas(rows);
+  if (k == KP)
+    apply_gram_fused_kernel<KP, true><<<ctas, FuCfg<KP>::THREADS, smem, s>>>(X, ldx, k, Rt, Q, ldq, rows, ws);
+  else
+    apply_gram_fused_kernel<KP, false><<<ctas, FuCfg<KP>::THREADS, smem, s>>>(X, ldx, k, Rt, Q, ldq, rows, ws);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int64_t nel = (int64_t)k * k;
@@ -351,7 +348,6 @@ cudaError_t apply_gram_fused_launch(const double* X, int64_t ldx, int k, const d
                                     cudaStream_t stream) {
   (void)ws_bytes;
   switch (fused_kp(k)) {
-    case 32: return launch_fused<32>(X, ldx, k, Rinv_tiles, Q, ldq, rows, G, ldg, ws, stream);
     case 64: return launch_fused<64>(X, ldx, k, Rinv_tiles, Q, ldq, rows, G, ldg, ws, stream);
     case 128: return launch_fused<128>(X, ldx, k, Rinv_tiles, Q, ldq, rows, G, ldg, ws, stream);
     default: return cudaErrorNotSupported;

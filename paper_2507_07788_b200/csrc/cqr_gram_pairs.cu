@@ -6,7 +6,8 @@
 //     k rounded up to a power of two >= 16) is cut into the NB/2 block-row
 //     pairs (i, NB-1-i); every pair holds exactly NB+1 blocks, so one pair
 //     per warp balances the DMMA work perfectly;
-//   * a CTA (8 warps, one per SM; thread 0 issues the copies) owns 8 pairs -- the whole
+//   * a CTA (8 compute warps + a producer warp, one CTA per SM; for KP = 256
+//     thread 0 issues the copies inline) owns 8 pairs -- the whole
 //     triangle for KP <= 128 (KP < 128: several warps per pair, splitting
 //     the k4 steps), half of it for KP = 256 (two CTAs per row range) -- and
 //     streams 32-row panels of ALL k columns (QI layout: one bulk copy per
@@ -17,11 +18,10 @@
 // Per-CTA partial triangles go to a workspace; a fixed-order reduce sums them.
 #include "cqr_common.cuh"
 #include "cqr_kernels.h"
+#include "cqr_pairs.cuh"
 
 namespace cqr {
 
-constexpr int GP_THREADS = 256;   // 8 warps; thread 0 also issues the bulk copies
-constexpr int GP_BR = 32;         // rows per stage
 
 template <int KP>
 struct GPCfg {
@@ -29,11 +29,18 @@ struct GPCfg {
   static constexpr int PAIRS = NB / 2;
   static constexpr int ITEMS = (PAIRS > 8) ? PAIRS / 8 : 1;     // CTAs per row range
   static constexpr int WPP = (PAIRS >= 8) ? 1 : 8 / PAIRS;      // warps per pair
-  static constexpr int STAGE = GP_BR * KP;                      // doubles
+  // rows per stage: 32, more for narrow panels so a stage is >= 16 KB (bulk
+  // copies below 16 KB stream measurably slower, profiles/r01_bulk_stream.jsonl)
+  static constexpr int BR = (KP >= 64) ? 32 : 2048 / KP;
+  static constexpr int STAGE = BR * KP;                         // doubles
   // ring depth: ~192 KB of panels in flight per SM (HBM latency x per-SM
   // bandwidth needs >= 64 KB outstanding), at most 8 stages
   static constexpr int S_FIT = (192 * 1024) / (STAGE * 8);
   static constexpr int STAGES = S_FIT > 8 ? 8 : (S_FIT < 3 ? 3 : S_FIT);
+  // a dedicated producer warp (9 warps) where the consumers' registers allow
+  // it; KP = 256 needs ~250 registers per thread, so thread 0 issues inline
+  static constexpr bool PRODUCER = KP <= 128;
+  static constexpr int THREADS = PRODUCER ? 288 : 256;
 };
 
 template <int KP>
@@ -41,56 +48,8 @@ size_t gp_smem_bytes() {
   return (size_t)GPCfg<KP>::STAGES * GPCfg<KP>::STAGE * sizeof(double) + 2 * GPCfg<KP>::STAGES * 8 + 64;
 }
 
-// one pair (i, NB-1-i): acc[0..i] = row i (cols 0..i), acc[i+1..NB] = row NB-1-i (cols 0..NB-1-i)
-template <int NB, int I>
-__device__ __forceinline__ void pair_steps(double (&acc)[NB + 1][2], const double* fp, int ks0, int ks1, int kst) {
-  constexpr int J = NB - 1 - I;
-  for (int ks = ks0; ks < ks1; ks += kst) {
-    const double* q = fp + ks * (NB * 32);   // quad ks of a [quad][KP][4] panel
-    double f[J + 1];
-#pragma unroll
-    for (int c = 0; c <= J; ++c) f[c] = q[32 * c];
-#pragma unroll
-    for (int c = 0; c <= I; ++c) dmma(acc[c], f[I], f[c]);
-#pragma unroll
-    for (int c = 0; c <= J; ++c) dmma(acc[I + 1 + c], f[J], f[c]);
-  }
-}
-
-template <int NB, int I>
-__device__ __forceinline__ void pair_store(const double (&acc)[NB + 1][2], double* out, int g, int t) {
-  constexpr int J = NB - 1 - I;
-  constexpr int KP = 8 * NB;
-  // out: KP x KP column-major partial
-#pragma unroll
-  for (int c = 0; c <= I; ++c)
-#pragma unroll
-    for (int e = 0; e < 2; ++e) out[(8 * c + 2 * t + e) * KP + 8 * I + g] += acc[c][e];
-#pragma unroll
-  for (int c = 0; c <= J; ++c)
-#pragma unroll
-    for (int e = 0; e < 2; ++e) out[(8 * c + 2 * t + e) * KP + 8 * J + g] += acc[I + 1 + c][e];
-}
-
-template <int NB, int I>
-struct PairDispatch {
-  __device__ static void run(int pair, double (&acc)[NB + 1][2], const double* fp, int ks0, int ks1, int kst) {
-    if (pair == I) pair_steps<NB, I>(acc, fp, ks0, ks1, kst);
-    else PairDispatch<NB, I + 1>::run(pair, acc, fp, ks0, ks1, kst);
-  }
-  __device__ static void store(int pair, const double (&acc)[NB + 1][2], double* out, int g, int t) {
-    if (pair == I) pair_store<NB, I>(acc, out, g, t);
-    else PairDispatch<NB, I + 1>::store(pair, acc, out, g, t);
-  }
-};
-template <int NB>
-struct PairDispatch<NB, NB / 2> {
-  __device__ static void run(int, double (&)[NB + 1][2], const double*, int, int, int) {}
-  __device__ static void store(int, const double (&)[NB + 1][2], double*, int, int) {}
-};
-
 template <int KP>
-__global__ void __launch_bounds__(GP_THREADS, 1) gram_pairs_kernel(const double* __restrict__ X, int64_t ldx, int k,
+__global__ void __launch_bounds__(GPCfg<KP>::THREADS, 1) gram_pairs_kernel(const double* __restrict__ X, int64_t ldx, int k,
                                                                    int64_t rows, int nsplit, double* ws) {
   using C = GPCfg<KP>;
   constexpr int NB = C::NB;
@@ -100,7 +59,7 @@ __global__ void __launch_bounds__(GP_THREADS, 1) gram_pairs_kernel(const double*
   uint64_t* empty = full + GP_STAGES;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int item = blockIdx.x % C::ITEMS, split = blockIdx.x / C::ITEMS;
-  const int64_t npan = ceil_div(rows, GP_BR);
+  const int64_t npan = ceil_div(rows, C::BR);
   const int64_t p0 = npan * split / nsplit, p1 = npan * (split + 1) / nsplit;
 
   if (threadIdx.x == 0) {
@@ -110,8 +69,8 @@ __global__ void __launch_bounds__(GP_THREADS, 1) gram_pairs_kernel(const double*
   __syncthreads();
 
   auto issue = [&](int64_t p, int st) {
-    const int64_t r0 = p * GP_BR;
-    const int nq = (int)imin64(GP_BR, rows - r0) >> 2;
+    const int64_t r0 = p * C::BR;
+    const int nq = (int)imin64(C::BR, rows - r0) >> 2;
     double* dst = smem + st * C::STAGE;
     const double* src = X + (r0 >> 2) * 4 * ldx;
     mbar_arrive_expect_tx(&full[st], (uint32_t)nq * k * 32);
@@ -121,8 +80,25 @@ __global__ void __launch_bounds__(GP_THREADS, 1) gram_pairs_kernel(const double*
       for (int q = 0; q < nq; ++q) bulk_g2s(dst + q * 4 * KP, src + q * 4 * ldx, (uint32_t)k * 32, &full[st]);
     }
   };
-  if (threadIdx.x == 0)
-    for (int j = 0; j < GP_STAGES - 1 && p0 + j < p1; ++j) issue(p0 + j, j);
+  if constexpr (C::PRODUCER) {
+    if (warp == 8) {
+      // producer warp: refill each stage as soon as the 8 consumers release it
+      if (lane == 0) {
+        int it = 0;
+        for (int64_t p = p0; p < p1; ++p, ++it) {
+          const int s = it % GP_STAGES;
+          if (it >= GP_STAGES) mbar_wait(&empty[s], ((it / GP_STAGES) - 1) & 1);
+          issue(p, s);
+        }
+      }
+      return;
+    }
+  }
+  // inline producer (thread 0): D panels in flight, refills the stage of panel it-LAG
+  constexpr int LAG = GP_STAGES >= 6 ? 2 : 1;
+  constexpr int D = GP_STAGES - LAG;
+  if (!C::PRODUCER && threadIdx.x == 0)
+    for (int j = 0; j < D && p0 + j < p1; ++j) issue(p0 + j, j);
 
   const int g = lane >> 2, t = lane & 3;
   const int pair = item * 8 + warp / C::WPP;       // pair index handled by this warp
@@ -135,15 +111,15 @@ __global__ void __launch_bounds__(GP_THREADS, 1) gram_pairs_kernel(const double*
   int it = 0;
   for (int64_t p = p0; p < p1; ++p, ++it) {
     const int s = it % GP_STAGES;
-    if (threadIdx.x == 0 && p + GP_STAGES - 1 < p1) {
-      // refill the stage consumed GP_STAGES - 1 panels ago
-      const int it2 = it + GP_STAGES - 1;
+    if (!C::PRODUCER && threadIdx.x == 0 && p + D < p1) {
+      // stage s2 last held panel it - LAG
+      const int it2 = it + D;
       const int s2 = it2 % GP_STAGES;
       if (it2 >= GP_STAGES) mbar_wait(&empty[s2], ((it2 / GP_STAGES) - 1) & 1);
-      issue(p + GP_STAGES - 1, s2);
+      issue(p + D, s2);
     }
     mbar_wait(&full[s], (it / GP_STAGES) & 1);
-    const int nk4 = (int)imin64(GP_BR, rows - p * GP_BR) >> 2;
+    const int nk4 = (int)imin64(C::BR, rows - p * C::BR) >> 2;
     if (active) {
       const double* fp = fbase + s * C::STAGE;
       // columns >= k of the staged panel hold stale data: only outputs in
@@ -189,7 +165,7 @@ bool gram_pairs_supported(int k) { return k >= 1 && gp_kp(k) != 0; }
 
 static void gp_grid(int64_t rows, int kp, int& items, int& nsplit) {
   items = (kp == 256) ? 2 : 1;
-  const int64_t npan = ceil_div(rows, GP_BR);
+  const int64_t npan = ceil_div(rows, (kp >= 64) ? 32 : 2048 / kp);
   int64_t ns = num_sms() / items;
   if (ns > npan) ns = npan;
   if (ns < 1) ns = 1;
@@ -217,7 +193,7 @@ static cudaError_t launch_gp(const double* X, int64_t ldx, int k, int64_t rows, 
   }
   int items, nsplit;
   gp_grid(rows, KP, items, nsplit);
-  gram_pairs_kernel<KP><<<items * nsplit, GP_THREADS, smem, s>>>(X, ldx, k, rows, nsplit, ws);
+  gram_pairs_kernel<KP><<<items * nsplit, GPCfg<KP>::THREADS, smem, s>>>(X, ldx, k, rows, nsplit, ws);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int64_t nel = (int64_t)k * k;

@@ -1,0 +1,58 @@
+// Block-row pair helpers shared by the self-Gram kernels (cqr_gram_pairs.cu,
+// cqr_fused.cu).  The lower triangle of the NB x NB grid of 8x8 blocks is cut
+// into the NB/2 block-row pairs (i, NB-1-i), each exactly NB+1 blocks.  A
+// staged panel is QI with ldk = KP: fp points at (column g, row t) of quad 0.
+#pragma once
+#include "cqr_common.cuh"
+
+namespace cqr {
+
+// one pair (i, NB-1-i): acc[0..i] = row i (cols 0..i), acc[i+1..NB] = row NB-1-i (cols 0..NB-1-i)
+template <int NB, int I>
+__device__ __forceinline__ void pair_steps(double (&acc)[NB + 1][2], const double* fp, int ks0, int ks1, int kst) {
+  constexpr int J = NB - 1 - I;
+  for (int ks = ks0; ks < ks1; ks += kst) {
+    const double* q = fp + ks * (NB * 32);   // quad ks of a [quad][KP][4] panel
+    double f[J + 1];
+#pragma unroll
+    for (int c = 0; c <= J; ++c) f[c] = q[32 * c];
+#pragma unroll
+    for (int c = 0; c <= I; ++c) dmma(acc[c], f[I], f[c]);
+#pragma unroll
+    for (int c = 0; c <= J; ++c) dmma(acc[I + 1 + c], f[J], f[c]);
+  }
+}
+
+template <int NB, int I>
+__device__ __forceinline__ void pair_store(const double (&acc)[NB + 1][2], double* out, int g, int t) {
+  constexpr int J = NB - 1 - I;
+  constexpr int KP = 8 * NB;
+  // out: KP x KP column-major partial
+#pragma unroll
+  for (int c = 0; c <= I; ++c)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) out[(8 * c + 2 * t + e) * KP + 8 * I + g] += acc[c][e];
+#pragma unroll
+  for (int c = 0; c <= J; ++c)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) out[(8 * c + 2 * t + e) * KP + 8 * J + g] += acc[I + 1 + c][e];
+}
+
+template <int NB, int I>
+struct PairDispatch {
+  __device__ static void run(int pair, double (&acc)[NB + 1][2], const double* fp, int ks0, int ks1, int kst) {
+    if (pair == I) pair_steps<NB, I>(acc, fp, ks0, ks1, kst);
+    else PairDispatch<NB, I + 1>::run(pair, acc, fp, ks0, ks1, kst);
+  }
+  __device__ static void store(int pair, const double (&acc)[NB + 1][2], double* out, int g, int t) {
+    if (pair == I) pair_store<NB, I>(acc, out, g, t);
+    else PairDispatch<NB, I + 1>::store(pair, acc, out, g, t);
+  }
+};
+template <int NB>
+struct PairDispatch<NB, NB / 2> {
+  __device__ static void run(int, double (&)[NB + 1][2], const double*, int, int, int) {}
+  __device__ static void store(int, const double (&)[NB + 1][2], double*, int, int) {}
+};
+
+}  // namespace cqr

@@ -384,7 +384,7 @@ def test_panel_nan_annotated():
 
 
 @pytest.mark.parametrize("m,k", [(300, 10), (1000, 1), (4100, 33), (2048, 64), (5000, 100), (3001, 128),
-                                 (777, 96), (1200, 200)])
+                                 (777, 96), (1200, 200), (40000, 50), (70000, 128), (90000, 64)])
 @pytest.mark.parametrize("inplace", [False, True])
 @pytest.mark.parametrize("fused", [0, 1])
 def test_apply_gram_matches_separate_ops(m, k, inplace, fused):
