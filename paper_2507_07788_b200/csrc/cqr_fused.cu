@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(FuCfg<KP>::THREADS, 1)
         }
         bulk_commit();
       }
-      PairDispatch<NB, 0>::run(pr, gacc, fb + qs * C::STAGE, 0, FU_BR / 4, 1);
+      PairDispatch<NB, 0>::template run<(KP == 64)>(pr, gacc, fb + qs * C::STAGE, 0, FU_BR / 4, 1);
       if (storer) bulk_wait_read<0>();   // the slot may be refilled once the store has read it
       __syncwarp();
       if (lane == 0) mbar_arrive(&qempty[qs]);

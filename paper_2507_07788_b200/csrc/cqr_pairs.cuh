@@ -9,17 +9,41 @@ namespace cqr {
 
 // one pair (i, NB-1-i): acc[0..i] = row i (cols 0..i), acc[i+1..NB] = row NB-1-i (cols 0..NB-1-i)
 template <int NB, int I>
-__device__ __forceinline__ void pair_steps(double (&acc)[NB + 1][2], const double* fp, int ks0, int ks1, int kst) {
+__device__ __forceinline__ void pair_load(double (&f)[NB - I], const double* fp, int ks) {
+  const double* q = fp + ks * (NB * 32);   // quad ks of a [quad][KP][4] panel
+#pragma unroll
+  for (int c = 0; c < NB - I; ++c) f[c] = q[32 * c];
+}
+template <int NB, int I>
+__device__ __forceinline__ void pair_mma(double (&acc)[NB + 1][2], const double (&f)[NB - I]) {
   constexpr int J = NB - 1 - I;
-  for (int ks = ks0; ks < ks1; ks += kst) {
-    const double* q = fp + ks * (NB * 32);   // quad ks of a [quad][KP][4] panel
-    double f[J + 1];
 #pragma unroll
-    for (int c = 0; c <= J; ++c) f[c] = q[32 * c];
+  for (int c = 0; c <= I; ++c) dmma(acc[c], f[I], f[c]);
 #pragma unroll
-    for (int c = 0; c <= I; ++c) dmma(acc[c], f[I], f[c]);
-#pragma unroll
-    for (int c = 0; c <= J; ++c) dmma(acc[I + 1 + c], f[J], f[c]);
+  for (int c = 0; c <= J; ++c) dmma(acc[I + 1 + c], f[J], f[c]);
+}
+// k4 steps ks0, ks0 + kst, ... < ks1.  PF: the fragments of the next step are
+// loaded before this step's DMMAs issue (needs twice the fragment registers).
+template <int NB, int I, bool PF>
+__device__ __forceinline__ void pair_steps(double (&acc)[NB + 1][2], const double* fp, int ks0, int ks1, int kst) {
+  if constexpr (!PF) {
+    for (int ks = ks0; ks < ks1; ks += kst) {
+      double f[NB - I];
+      pair_load<NB, I>(f, fp, ks);
+      pair_mma<NB, I>(acc, f);
+    }
+  } else {
+    if (ks0 >= ks1) return;
+    double f0[NB - I], f1[NB - I];
+    pair_load<NB, I>(f0, fp, ks0);
+    for (int ks = ks0; ks < ks1; ks += 2 * kst) {
+      const bool has1 = ks + kst < ks1;
+      if (has1) pair_load<NB, I>(f1, fp, ks + kst);
+      pair_mma<NB, I>(acc, f0);
+      if (!has1) break;
+      if (ks + 2 * kst < ks1) pair_load<NB, I>(f0, fp, ks + 2 * kst);
+      pair_mma<NB, I>(acc, f1);
+    }
   }
 }
 
@@ -40,9 +64,10 @@ __device__ __forceinline__ void pair_store(const double (&acc)[NB + 1][2], doubl
 
 template <int NB, int I>
 struct PairDispatch {
+  template <bool PF = false>
   __device__ static void run(int pair, double (&acc)[NB + 1][2], const double* fp, int ks0, int ks1, int kst) {
-    if (pair == I) pair_steps<NB, I>(acc, fp, ks0, ks1, kst);
-    else PairDispatch<NB, I + 1>::run(pair, acc, fp, ks0, ks1, kst);
+    if (pair == I) pair_steps<NB, I, PF>(acc, fp, ks0, ks1, kst);
+    else PairDispatch<NB, I + 1>::template run<PF>(pair, acc, fp, ks0, ks1, kst);
   }
   __device__ static void store(int pair, const double (&acc)[NB + 1][2], double* out, int g, int t) {
     if (pair == I) pair_store<NB, I>(acc, out, g, t);
@@ -51,6 +76,7 @@ struct PairDispatch {
 };
 template <int NB>
 struct PairDispatch<NB, NB / 2> {
+  template <bool PF = false>
   __device__ static void run(int, double (&)[NB + 1][2], const double*, int, int, int) {}
   __device__ static void store(int, const double (&)[NB + 1][2], double*, int, int) {}
 };
