@@ -8,79 +8,80 @@
 // (algorithms.py:430-431): Bt = Q_in^T Q, G = Q^T Q.
 //
 // The reference streams Q_in three times per iteration (projection, cross
-// Gram, and the copy of the basis); here Q_in is read from HBM once.  The
-// rows are cut into 16-row sub-panels; a sub-panel of Q_in (4 quads x q
-// columns, one bulk copy per quad) and of the block go through a 2-stage
-// ring, and everything the iteration needs from those rows is done before
-// the stage is released (work split per sub-panel: see the kernel).  CTA =
-// 8 warps, persistent over sub-panels; thread 0 issues the bulk copies.
-// Per-CTA partials [Bt'(q x 16) | G'(16 x 16)] are summed by a fixed-order
-// reduce kernel.
+// Gram, and the copy of the basis); here Q_in is read from HBM once.  Rows go
+// in 16-row sub-panels through a TMA ring (Q_in: 4 quads x q columns, block:
+// 4 quads x p), one CTA per SM, persistent.  The CTA is warp-specialised:
+//   * 8 projection warps: warp w owns the column slices [64c + 8w, +8) of
+//     Q_in (its Bt rows live in registers): proj partial = Q_in Bt over its
+//     slices, fixed-order sum of the 8 partials in shared memory, t = Q - proj,
+//     Q' = t R^-1 (warps 0-3, one 8x8 block each), Q' -> HBM (in place) and
+//     into a 2-slot ring of Q' sub-panels;
+//   * 8 cross-Gram warps: warp w owns the same slices as rows of Bt':
+//     Bt' += Q_in^T Q' in registers over the sweep, G += Q'^T Q' (warps 8-10);
+//     they release the stage, and the last one's lane 0 refills it.
+// Both groups issue q/8 DMMA per warp per sub-panel; the width enters as the
+// template parameter NQ = ceil(q/64) so no DMMA is predicated off.  Groups hand
+// over through mbarriers; the projection group syncs on a named barrier.
+// Per-CTA partials [Bt'(q_pad x 16) | G'(16 x 16)] are written once per CTA
+// and summed by a fixed-order reduce kernel.
 #include "cqr_common.cuh"
 #include "cqr_kernels.h"
 
 namespace cqr {
 
-constexpr int UP_THREADS = 256;
 constexpr int UP_SR = 16;                 // rows per sub-panel (4 quads)
 constexpr int UP_MAXQ = 512;
 constexpr int UP_PB = 16;                 // padded block width
-constexpr int UP_BLD = UP_MAXQ + 4;       // Bt staging: [16][516] (516 = 4 mod 16)
-constexpr int UP_QIN = UP_SR * UP_MAXQ;   // doubles per staged Q_in sub-panel (64 KB)
-constexpr int UP_QB = UP_SR * UP_PB;      // doubles per staged block sub-panel
-constexpr int UP_STAGE = UP_QIN + UP_QB;
-constexpr int UP_MAXCB = UP_MAXQ / 8 / 8; // column blocks of Bt' per warp (8)
+constexpr int UP_THREADS = 512;           // 8 projection + 8 cross-Gram warps
+constexpr int UP_YS = 2;                  // Q' ring slots
+constexpr int UP_MAXNS = 8;               // TMA ring stages (at most)
+constexpr int UP_FIXED = UP_PB * CT_LD + 8 * 256 + 256 + UP_YS * 256;   // doubles before the ring
 
 struct UpdateArgs {
   const double* Qin; int64_t ldqin; int q;
   double* Qb; int64_t ldqb; int p;        // block (updated in place unless initial)
-  int64_t rows;
-  const double* Bt; int ldbt;             // q x p column-major (iteration mode)
+  int64_t rows;                           // multiple of 16
+  const double* Bt; int ldbt;             // p x q as [n][k] (iteration mode)
   const double* Rinv;                     // p x p coefficient tiles (iteration mode)
   int initial;
   double* ws;                             // [ctas][(q_pad + 16) * 16]
+  int qs;                                 // staged column stride (= 4 mod 8)
+  int ns;                                 // ring stages
 };
 
-static size_t update_smem_bytes() {
-  return ((size_t)2 * UP_STAGE + UP_PB * UP_BLD + UP_PB * CT_LD + 8 * 256 + 2 * UP_QB) * sizeof(double) + 64;
+static int up_qs(int q) { return (int)round_up(q, 8) + 4; }
+static int up_stage(int q) { return UP_SR * up_qs(q) + UP_SR * UP_PB; }
+static int up_stages(int q) {
+  const int64_t avail = 227 * 1024 - 512 - (int64_t)UP_FIXED * 8;
+  int64_t ns = avail / ((int64_t)up_stage(q) * 8);
+  return (int)(ns > UP_MAXNS ? UP_MAXNS : ns);
 }
+static size_t update_smem_bytes(int q) { return ((size_t)UP_FIXED + (size_t)up_stages(q) * up_stage(q)) * 8; }
 
-// Per 16-row sub-panel (Q_in rows: 4 quads x q columns, staged with one bulk
-// copy per quad; block rows: 4 quads x p):
-//   proj = Q_in Bt          K = q split over the 8 warps, fixed-order reduce
-//   t    = Q - proj         (iteration mode)
-//   Q'   = t R^-1           warps 0..3 (2 x 2 blocks, K = 16) -> HBM + smem
-//   Bt' += Q_in^T Q'        warp w owns Bt' row blocks w, w+8, ... (registers)
-//   G   += Q'^T Q'          warps 0..2 (lower blocks)
-// Q_in is read from HBM once per pass.
+template <int NQ>
 __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(UpdateArgs a) {
   extern __shared__ __align__(128) double smem[];
-  double* ring = smem;                                   // 2 stages: [Q_in sub-panel | block sub-panel]
-  double* bts = ring + 2 * UP_STAGE;                     // Bt as [n][k] (ld UP_BLD)
-  double* ris = bts + UP_PB * UP_BLD;                    // R^-1 as [n][k] (ld 36)
-  double* red = ris + UP_PB * CT_LD;                     // 8 warps x 256 projection partials
-  double* tq = red + 8 * 256;                            // t (16 x 16, QI)
-  double* qn = tq + UP_QB;                               // Q' (16 x 16, QI)
-  __shared__ __align__(8) uint64_t full[2], empty[2];
+  const int q = a.q, p = a.p, qs = a.qs, ns = a.ns;
+  const int STG = UP_SR * qs + UP_SR * UP_PB;
+  double* ris = smem;                      // R^-1 as [n][k] (ld 36)
+  double* red = ris + UP_PB * CT_LD;       // 8 projection partials (16 x 16, column-major)
+  double* tq = red + 8 * 256;              // t = Q - proj (QI, 16 x 16)
+  double* yring = tq + 256;                // UP_YS x Q' (QI, 16 x 16)
+  double* stg = yring + UP_YS * 256;       // ns x [Q_in sub-panel (4 quads x qs x 4) | block (4 quads x 16 x 4)]
+  __shared__ __align__(8) uint64_t full[UP_MAXNS], empty[UP_MAXNS], yfull[UP_YS], yempty[UP_YS];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int q = a.q, p = a.p;
-  const int qs = (q + 3) & ~3;                           // staged column stride (quad = 4 qs doubles)
-  const int nk4 = (q + 3) / 4;
-  const int ncb = (q + 7) / 8;                           // Bt' row blocks
-  const int64_t nsp = ceil_div(a.rows, UP_SR);
   const bool init = a.initial != 0;
+  const int64_t nsp = a.rows / UP_SR;
+  const int64_t mine = (nsp > blockIdx.x) ? ceil_div(nsp - blockIdx.x, gridDim.x) : 0;
 
   if (tid == 0) {
-    for (int s = 0; s < 2; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 8); }
+    for (int s = 0; s < ns; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 8); }
+    for (int s = 0; s < UP_YS; ++s) { mbar_init(&yfull[s], 256); mbar_init(&yempty[s], 8); }
     fence_mbar_init();
   }
   if (!init) {
-    for (int e = tid; e < UP_PB * UP_BLD; e += UP_THREADS) {
-      const int n = e / UP_BLD, kk = e % UP_BLD;
-      bts[e] = (n < p && kk < q) ? a.Bt[(int64_t)n * a.ldbt + kk] : 0.0;
-    }
     for (int e = tid; e < UP_PB * CT_LD; e += UP_THREADS) {
       const int n = e / CT_LD, kk = e % CT_LD;
       ris[e] = (n < p && kk < p) ? a.Rinv[coeff_off(kk, n, p)] : 0.0;
@@ -88,153 +89,165 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(UpdateArgs a
   }
   __syncthreads();
 
-  auto issue = [&](int64_t sp, int st) {
-    const int64_t r0 = sp * UP_SR;
-    const int nq = (int)imin64(UP_SR, a.rows - r0) >> 2;
-    double* dq = ring + st * UP_STAGE;
-    double* db = dq + UP_QIN;
-    mbar_arrive_expect_tx(&full[st], (uint32_t)nq * (q + p) * 32);
+  auto issue = [&](int64_t j, int st) {
+    const int64_t r0 = (blockIdx.x + j * gridDim.x) * UP_SR;
+    double* dq = stg + st * STG;
+    double* db = dq + UP_SR * qs;
+    mbar_arrive_expect_tx(&full[st], (uint32_t)4 * (q + p) * 32);
     const double* sq = a.Qin + (r0 >> 2) * 4 * a.ldqin;
     const double* sb = a.Qb + (r0 >> 2) * 4 * a.ldqb;
-    for (int qq = 0; qq < nq; ++qq) {
-      bulk_g2s(dq + qq * 4 * qs, sq + qq * 4 * a.ldqin, (uint32_t)q * 32, &full[st]);
-      bulk_g2s(db + qq * 4 * UP_PB, sb + qq * 4 * a.ldqb, (uint32_t)p * 32, &full[st]);
+    for (int qq = 0; qq < 4; ++qq) bulk_g2s(dq + qq * 4 * qs, sq + qq * 4 * a.ldqin, (uint32_t)q * 32, &full[st]);
+    if (a.ldqb == UP_PB && p == UP_PB) {
+      bulk_g2s(db, sb, 4 * UP_PB * 32, &full[st]);
+    } else {
+      for (int qq = 0; qq < 4; ++qq) bulk_g2s(db + qq * 4 * UP_PB, sb + qq * 4 * a.ldqb, (uint32_t)p * 32, &full[st]);
     }
   };
-  if (tid == 0 && blockIdx.x < nsp) issue(blockIdx.x, 0);
+  if (tid == 0)
+    for (int j = 0; j < ns && j < mine; ++j) issue(j, j);
 
-  double ct[UP_MAXCB][2][2];
+  int s = 0, ys = 0;
+  uint32_t ph = 0, yph = 0;
+  if (warp < 8) {
+    // ================= projection group
+    const int wa = warp;
+    double btr[NQ][2][2];   // Bt(64c + 8wa + 4h + t, 8nb + g)
 #pragma unroll
-  for (int i = 0; i < UP_MAXCB; ++i)
+    for (int c = 0; c < NQ; ++c)
 #pragma unroll
-    for (int n = 0; n < 2; ++n) { ct[i][n][0] = 0.0; ct[i][n][1] = 0.0; }
-  double gq[2] = {0.0, 0.0};
-
-  int it = 0;
-  for (int64_t sp = blockIdx.x; sp < nsp; sp += gridDim.x, ++it) {
-    const int s = it & 1;
-    if (tid == 0 && sp + gridDim.x < nsp) {
-      if (it >= 1) mbar_wait(&empty[s ^ 1], ((it - 1) >> 1) & 1);
-      issue(sp + gridDim.x, s ^ 1);
-    }
-    mbar_wait(&full[s], (it >> 1) & 1);
-    const int64_t r0 = sp * UP_SR;
-    const int nrows = (int)imin64(UP_SR, a.rows - r0);
-    const double* Qs = ring + s * UP_STAGE;   // [quad][qs][4]
-    const double* Bs = Qs + UP_QIN;           // [quad][16][4], columns >= p stale
-    const double* src;                        // Q' (or Q in initial mode) as [quad][16][4]
-    if (!init) {
-      // ---- proj partial: warp w takes k4 steps [w*c, (w+1)*c)
-      const int chunk = (nk4 + 7) / 8;
-      const int ks0 = warp * chunk, ks1 = min(nk4, ks0 + chunk);
-      double pr[2][2][2] = {{{0.0, 0.0}, {0.0, 0.0}}, {{0.0, 0.0}, {0.0, 0.0}}};
-      for (int ks = ks0; ks < ks1; ++ks) {
-        const int kc = 4 * ks + t;
-        double av[2];
+      for (int h = 0; h < 2; ++h)
 #pragma unroll
-        for (int rb = 0; rb < 2; ++rb) {
-          const int row = 8 * rb + g;
-          av[rb] = (kc < q) ? Qs[(row >> 2) * 4 * qs + 4 * kc + (row & 3)] : 0.0;
+        for (int nb = 0; nb < 2; ++nb) {
+          const int kk = 64 * c + 8 * wa + 4 * h + t, n = 8 * nb + g;
+          btr[c][h][nb] = (!init && kk < q && n < p) ? a.Bt[(int64_t)n * a.ldbt + kk] : 0.0;
         }
-        const double b0 = bts[g * UP_BLD + kc], b1 = bts[(8 + g) * UP_BLD + kc];
+    const int row = tid & 15, col = tid >> 4;   // element of the t / copy phase (256 threads, 16 x 16)
+    const int qoff = (row >> 2) * 4 * UP_PB + 4 * col + (row & 3);
+    for (int64_t j = 0; j < mine; ++j) {
+      const int64_t r0 = (blockIdx.x + j * gridDim.x) * UP_SR;
+      mbar_wait(&full[s], ph);
+      const double* Qs = stg + s * STG;
+      const double* Ys = Qs + UP_SR * qs;
+      double* yd = yring + ys * 256;
+      if (!init) {
+        double pr[2][2][2] = {{{0.0, 0.0}, {0.0, 0.0}}, {{0.0, 0.0}, {0.0, 0.0}}};
+        const double* xa = Qs + (g >> 2) * 4 * qs + (g & 3) + 4 * t;   // row g, column t
 #pragma unroll
-        for (int rb = 0; rb < 2; ++rb) {
-          dmma(pr[rb][0], av[rb], b0);
-          dmma(pr[rb][1], av[rb], b1);
+        for (int c = 0; c < NQ; ++c)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int kc = 64 * c + 8 * wa + 4 * h;   // + t
+            const bool kv = kc + t < q;               // columns >= q of the stage are stale
+            const double a0 = kv ? xa[4 * kc] : 0.0;
+            const double a1 = kv ? xa[4 * kc + 8 * qs] : 0.0;   // row 8 + g
+            dmma(pr[0][0], a0, btr[c][h][0]);
+            dmma(pr[0][1], a0, btr[c][h][1]);
+            dmma(pr[1][0], a1, btr[c][h][0]);
+            dmma(pr[1][1], a1, btr[c][h][1]);
+          }
+#pragma unroll
+        for (int rb = 0; rb < 2; ++rb)
+#pragma unroll
+          for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) red[wa * 256 + (8 * nb + 2 * t + e) * 16 + 8 * rb + g] = pr[rb][nb][e];
+        asm volatile("bar.sync 2, 256;" ::: "memory");
+        {
+          double sum = 0.0;
+#pragma unroll
+          for (int w = 0; w < 8; ++w) sum += red[w * 256 + col * 16 + row];
+          tq[qoff] = (col < p) ? Ys[qoff] - sum : 0.0;
         }
-      }
-      // partials -> red[w][(col)*16 + row]
+        asm volatile("bar.sync 2, 256;" ::: "memory");
+        if (j >= UP_YS) mbar_wait(&yempty[ys], yph ^ 1);
+        if (wa < 4) {
+          // Q' block (rb, nb) = t(rows 8rb.., :) R^-1(:, cols 8nb..); R^-1 upper: K < 8(nb+1)
+          const int rb = wa >> 1, nb = wa & 1;
+          const int r = 8 * rb + g;
+          const double* tp = tq + (r >> 2) * 4 * UP_PB + (r & 3) + 4 * t;
+          const double* rp = ris + (8 * nb + g) * CT_LD + t;
+          double c2[2] = {0.0, 0.0};
+          if (nb == 0) {
 #pragma unroll
-      for (int rb = 0; rb < 2; ++rb)
+            for (int ks = 0; ks < 2; ++ks) dmma(c2, tp[16 * ks], rp[4 * ks]);
+          } else {
 #pragma unroll
-        for (int nb = 0; nb < 2; ++nb)
+            for (int ks = 0; ks < 4; ++ks) dmma(c2, tp[16 * ks], rp[4 * ks]);
+          }
 #pragma unroll
-          for (int e = 0; e < 2; ++e) red[warp * 256 + (8 * nb + 2 * t + e) * 16 + 8 * rb + g] = pr[rb][nb][e];
-      __syncthreads();
-      {
-        // thread e: proj(row, col) = sum over warps (fixed order); t = Q - proj
-        const int row = tid & 15, col = tid >> 4;
-        double sum = 0.0;
-#pragma unroll
-        for (int w = 0; w < 8; ++w) sum += red[w * 256 + col * 16 + row];
-        const bool v = row < nrows && col < p;
-        const double x = v ? Bs[(row >> 2) * 4 * UP_PB + 4 * col + (row & 3)] : 0.0;
-        tq[(row >> 2) * 4 * UP_PB + 4 * col + (row & 3)] = v ? x - sum : 0.0;
-      }
-      __syncthreads();
-      // ---- Q' = t R^-1: warps 0..3, block (rb = w >> 1, nb = w & 1)
-      if (warp < 4) {
-        const int rb = warp >> 1, nb = warp & 1;
-        const int row = 8 * rb + g;
-        double c2[2] = {0.0, 0.0};
-#pragma unroll
-        for (int ks = 0; ks < UP_PB / 4; ++ks) {
-          const int kc = 4 * ks + t;
-          dmma(c2, tq[(row >> 2) * 4 * UP_PB + 4 * kc + (row & 3)], ris[(8 * nb + g) * CT_LD + kc]);
-        }
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int col = 8 * nb + 2 * t + e;
-          const bool v = row < nrows && col < p;
-          qn[(row >> 2) * 4 * UP_PB + 4 * col + (row & 3)] = v ? c2[e] : 0.0;
-          if (v) a.Qb[((r0 + row) >> 2) * 4 * a.ldqb + 4 * col + (row & 3)] = c2[e];
-        }
-      }
-      __syncthreads();
-      src = qn;
-    } else {
-      // initial mode: Q' = Q; zero its stale padding columns / rows in a copy
-      {
-        const int row = tid & 15, col = tid >> 4;
-        const bool v = row < nrows && col < p;
-        qn[(row >> 2) * 4 * UP_PB + 4 * col + (row & 3)] = v ? Bs[(row >> 2) * 4 * UP_PB + 4 * col + (row & 3)] : 0.0;
-      }
-      __syncthreads();
-      src = qn;
-    }
-    // ---- Bt' += Q_in^T Q' (K = 16 rows); warp w: Bt' row blocks cb = w + 8 i
-    {
-      const double* bq = src + 4 * g + t;   // (column g, row t) of quad 0
-      const int nq = nrows >> 2;
-#pragma unroll
-      for (int i = 0; i < UP_MAXCB; ++i) {
-        const int cb = warp + 8 * i;
-        if (cb < ncb) {
-          const double* xa = Qs + 4 * (8 * cb + g) + t;
-          for (int ks = 0; ks < nq; ++ks) {
-            const double av = xa[ks * 4 * qs];
-            dmma(ct[i][0], av, bq[ks * 4 * UP_PB]);
-            dmma(ct[i][1], av, bq[ks * 4 * UP_PB + 32]);
+          for (int e = 0; e < 2; ++e) {
+            const int cc = 8 * nb + 2 * t + e;
+            const bool v = cc < p;
+            yd[(r >> 2) * 4 * UP_PB + 4 * cc + (r & 3)] = v ? c2[e] : 0.0;
+            if (v) a.Qb[((r0 + r) >> 2) * 4 * a.ldqb + 4 * cc + (r & 3)] = c2[e];
           }
         }
+      } else {
+        // initial mode: Q' = Q (stale padding columns zeroed)
+        if (j >= UP_YS) mbar_wait(&yempty[ys], yph ^ 1);
+        yd[qoff] = (col < p) ? Ys[qoff] : 0.0;
       }
-      if (warp < 3) {
-        const int bi = (warp == 0) ? 0 : 1, bj = (warp == 2) ? 1 : 0;
-        for (int ks = 0; ks < nq; ++ks) dmma(gq, bq[ks * 4 * UP_PB + 32 * bi], bq[ks * 4 * UP_PB + 32 * bj]);
-      }
+      mbar_arrive(&yfull[ys]);   // every projection thread: its own stores are released
+      if (++s == ns) { s = 0; ph ^= 1; }
+      if (++ys == UP_YS) { ys = 0; yph ^= 1; }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-    __syncthreads();   // qn / tq / red are rewritten by the next sub-panel
-  }
-
-  // ---- per-CTA partials: [Bt'(q_pad x 16) | G (16 x 16)] column-major with ld = q_pad + 16
-  const int qp = (int)round_up(q, 64);
-  const int ld = qp + UP_PB;
-  double* out = a.ws + (int64_t)blockIdx.x * ld * UP_PB;
+  } else {
+    // ================= cross-Gram group
+    const int wb = warp - 8;
+    double ct[NQ][2][2];
 #pragma unroll
-  for (int i = 0; i < UP_MAXCB; ++i) {
-    const int cb = warp + 8 * i;
-    if (cb >= ncb) continue;
+    for (int c = 0; c < NQ; ++c)
 #pragma unroll
-    for (int n = 0; n < 2; ++n)
+      for (int n = 0; n < 2; ++n) { ct[c][n][0] = 0.0; ct[c][n][1] = 0.0; }
+    double gq[2] = {0.0, 0.0};
+    const int bi = (wb == 0) ? 0 : 1, bj = (wb == 2) ? 1 : 0;
+    for (int64_t j = 0; j < mine; ++j) {
+      mbar_wait(&yfull[ys], yph);
+      const double* Qs = stg + s * STG;
+      const double* yd = yring + ys * 256;
+      const double* xa = Qs + 4 * (8 * wb + g) + t;   // Q_in(row t, column 8wb + g)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) out[(int64_t)(8 * n + 2 * t + e) * ld + 8 * cb + g] = ct[i][n][e];
-  }
-  if (warp < 3) {
-    const int bi = (warp == 0) ? 0 : 1, bj = (warp == 2) ? 1 : 0;
+      for (int ks = 0; ks < 4; ++ks) {
+        const double b0 = yd[ks * 64 + 4 * g + t], b1 = yd[ks * 64 + 32 + 4 * g + t];
 #pragma unroll
-    for (int e = 0; e < 2; ++e) out[(int64_t)(8 * bj + 2 * t + e) * ld + qp + 8 * bi + g] = gq[e];
+        for (int c = 0; c < NQ; ++c) {
+          const bool v = 64 * c + 8 * wb + g < q;
+          const double av = v ? xa[ks * 4 * qs + 256 * c] : 0.0;
+          dmma(ct[c][0], av, b0);
+          dmma(ct[c][1], av, b1);
+        }
+      }
+      if (wb < 3) {
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) dmma(gq, yd[ks * 64 + 32 * bi + 4 * g + t], yd[ks * 64 + 32 * bj + 4 * g + t]);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&empty[s]);
+        mbar_arrive(&yempty[ys]);
+        if (wb == 7 && j + ns < mine) {
+          mbar_wait(&empty[s], ph);   // all 8 cross-Gram warps are done with the stage
+          issue(j + ns, s);
+        }
+      }
+      __syncwarp();
+      if (++s == ns) { s = 0; ph ^= 1; }
+      if (++ys == UP_YS) { ys = 0; yph ^= 1; }
+    }
+    // ---- per-CTA partials: [Bt'(q_pad x 16) | G (16 x 16)] column-major with ld = q_pad + 16
+    const int qp = (int)round_up(q, 64);
+    const int ld = qp + UP_PB;
+    double* out = a.ws + (int64_t)blockIdx.x * ld * UP_PB;
+#pragma unroll
+    for (int c = 0; c < NQ; ++c)
+#pragma unroll
+      for (int n = 0; n < 2; ++n)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) out[(int64_t)(8 * n + 2 * t + e) * ld + 64 * c + 8 * wb + g] = ct[c][n][e];
+    if (wb < 3) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) out[(int64_t)(8 * bj + 2 * t + e) * ld + qp + 8 * bi + g] = gq[e];
+    }
   }
 }
 
@@ -267,23 +280,32 @@ static int update_ctas(int64_t rows) {
   return (int)(n < c ? (n < 1 ? 1 : n) : c);
 }
 
-bool update_pass_supported(int q, int p) { return q >= 1 && q <= UP_MAXQ && p >= 1 && p <= UP_PB; }
+bool update_pass_supported(int q, int p) {
+  return q >= 1 && q <= UP_MAXQ && p >= 1 && p <= UP_PB && up_stages(q) >= 2;
+}
 
 size_t update_pass_ws_bytes(int64_t rows, int q) {
   const int qp = (int)round_up(q, 64);
   return (size_t)update_ctas(rows) * (qp + UP_PB) * UP_PB * sizeof(double) + 256;
 }
 
+template <int NQ>
+static cudaError_t launch_up(const UpdateArgs& a, int ctas, size_t smem, cudaStream_t s) {
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(update_pass_kernel<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = smem;
+  }
+  update_pass_kernel<NQ><<<ctas, UP_THREADS, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
 cudaError_t update_pass_launch(const double* Qin, int64_t ldqin, int q, double* Qb, int64_t ldqb, int p,
                                int64_t rows, const double* Bt, int ldbt, const double* Rinv_tiles, int initial,
                                double* Bt_next, double* G, int ldg, double* ws, cudaStream_t s) {
-  static bool attr = false;
-  const size_t smem = update_smem_bytes();
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(update_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  if (rows % UP_SR) return cudaErrorInvalidValue;
   UpdateArgs a{};
   a.Qin = Qin; a.ldqin = ldqin; a.q = q;
   a.Qb = Qb; a.ldqb = ldqb; a.p = p;
@@ -291,9 +313,22 @@ cudaError_t update_pass_launch(const double* Qin, int64_t ldqin, int q, double* 
   a.Bt = Bt; a.ldbt = ldbt; a.Rinv = Rinv_tiles;
   a.initial = initial;
   a.ws = ws;
+  a.qs = up_qs(q);
+  a.ns = up_stages(q);
+  const size_t smem = update_smem_bytes(q);
   const int ctas = update_ctas(rows);
-  update_pass_kernel<<<ctas, UP_THREADS, smem, s>>>(a);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e;
+  switch ((q + 63) / 64) {
+    case 1: e = launch_up<1>(a, ctas, smem, s); break;
+    case 2: e = launch_up<2>(a, ctas, smem, s); break;
+    case 3: e = launch_up<3>(a, ctas, smem, s); break;
+    case 4: e = launch_up<4>(a, ctas, smem, s); break;
+    case 5: e = launch_up<5>(a, ctas, smem, s); break;
+    case 6: e = launch_up<6>(a, ctas, smem, s); break;
+    case 7: e = launch_up<7>(a, ctas, smem, s); break;
+    case 8: e = launch_up<8>(a, ctas, smem, s); break;
+    default: return cudaErrorInvalidValue;
+  }
   if (e != cudaSuccess) return e;
   const int qp = (int)round_up(q, 64);
   const int64_t nel = (int64_t)q * p + (int64_t)p * p;

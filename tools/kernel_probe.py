@@ -2,6 +2,7 @@
 captures and quick per-kernel measurements.
 
     python tools/kernel_probe.py --m 2000000 --k 256 [--reps 5] [--only gram|apply|factor]
+    python tools/kernel_probe.py --only update --m 8000000 --q 256 --k 16   (update pass, basis q, block k)
 """
 
 from __future__ import annotations
@@ -24,6 +25,7 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--only", default="all")
     ap.add_argument("--shifted", action="store_true", help="factor a rank-deficient Gram (shift path)")
+    ap.add_argument("--q", type=int, default=256, help="basis width for --only update")
     a = ap.parse_args()
     import paper_2507_07788_b200 as cq
     from paper_2507_07788_b200 import _lib
@@ -31,6 +33,33 @@ def main():
 
     m, k = a.m, a.k
     from paper_2507_07788_b200.workloads import device_gaussian
+
+    if a.only == "update":
+        q_in = device_gaussian(cq.CudaVectorArray.zeros(cq.VectorSpace(m), a.q), 2)
+        qb = device_gaussian(cq.CudaVectorArray.zeros(cq.VectorSpace(m), k), 3)
+        eng = Engine(k, cq.AlgoConfig(), q=a.q)
+        g = torch.randn((k, k), dtype=torch.float64, device="cuda")
+        eng.G.copy_(g @ g.T + k * torch.eye(k, dtype=torch.float64, device="cuda"))
+        st = eng.factor(_lib.POLICY_PLAIN, m, k)
+        assert st.code == _lib.FACTORED, st.code
+        eng.Bt.copy_(1e-3 * torch.randn_like(eng.Bt))
+
+        def run():
+            eng.update_pass(q_in, qb, initial=False)
+
+        run()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(a.reps):
+            run()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / a.reps
+        flops = 4.0 * m * a.q * k + 2.0 * m * k * (k + 1)
+        print(json.dumps({"m": m, "q": a.q, "p": k, "update_ms": ms, "update_tfs": flops / ms / 1e9,
+                          "qin_gbs": m * a.q * 8 / ms / 1e6}))
+        return
 
     x = device_gaussian(cq.CudaVectorArray.zeros(cq.VectorSpace(m), k), 1)
     q = cq.CudaVectorArray.zeros(cq.VectorSpace(m), k)
