@@ -395,7 +395,7 @@ def run_update_chain(cq, cx, cfg, m, world, rank, local):
             res = cq.chol_qr_update(q, r, a)
             e1.record()
             timer_events.append((e0, e1))
-            passes.append(res.shift_attempts)
+            passes.append({"iterations": res.iterations, "shift_attempts": list(res.shift_attempts)})
             q, r = res.q, res.r
         return q, r, passes
 
@@ -442,7 +442,7 @@ def run_update_chain(cq, cx, cfg, m, world, rank, local):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, built in HBM)",
             "config": {"workload": cfg["workload"], "rows": m, "cols": 512, "block": p, "blocks": nblk,
                        "parallelism": f"row-sharded dp{world}", "timed": "sum of update-call event times",
-                       "update_passes": passes[:3] + ["..."] + passes[-2:], "final_loo_fro": loo},
+                       "per_block": passes[:3] + ["..."] + passes[-2:], "final_loo_fro": loo},
             "roofline": {"bound": "fp64", "kernel": "update_pass", "achieved": tfs, "peak": FP64_PEAK_TFS,
                          "unit": "TFLOP/s", "frac": tfs / FP64_PEAK_TFS, "traffic": None,
                          "peak_source": FP64_PEAK_SRC,
