@@ -39,7 +39,7 @@ struct GPCfg {
   static constexpr int STAGES = S_FIT > 8 ? 8 : (S_FIT < 3 ? 3 : S_FIT);
   // a dedicated producer warp (9 warps) where the consumers' registers allow
   // it; KP = 256 needs ~250 registers per thread, so thread 0 issues inline
-  static constexpr bool PRODUCER = KP <= 128;
+  static constexpr bool PRODUCER = true;
   static constexpr int THREADS = PRODUCER ? 288 : 256;
 };
 
@@ -124,7 +124,8 @@ __global__ void __launch_bounds__(GPCfg<KP>::THREADS, 1) gram_pairs_kernel(const
       const double* fp = fbase + s * C::STAGE;
       // columns >= k of the staged panel hold stale data: only outputs in
       // rows/cols >= k see them, and those are never read back
-      PairDispatch<NB, 0>::run(pair, acc, fp, sub, nk4, C::WPP);
+      if constexpr (KP >= 256) PairDispatch<NB, 0>::run_lean(pair, acc, fp, sub, nk4, C::WPP);
+      else PairDispatch<NB, 0>::run(pair, acc, fp, sub, nk4, C::WPP);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);

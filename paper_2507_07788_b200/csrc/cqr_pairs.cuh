@@ -22,6 +22,25 @@ __device__ __forceinline__ void pair_mma(double (&acc)[NB + 1][2], const double 
 #pragma unroll
   for (int c = 0; c <= J; ++c) dmma(acc[I + 1 + c], f[J], f[c]);
 }
+// lean variant for wide panels: only the two row fragments stay live, column
+// fragments stream one at a time (fits the 168-register cap of a 9-warp CTA)
+template <int NB, int I>
+__device__ __forceinline__ void pair_step_lean(double (&acc)[NB + 1][2], const double* q) {
+  constexpr int J = NB - 1 - I;
+  const double fI = q[32 * I], fJ = q[32 * J];
+#pragma unroll
+  for (int c = 0; c <= J; ++c) {
+    const double fc = q[32 * c];
+    if (c <= I) dmma(acc[c], fI, fc);
+    dmma(acc[I + 1 + c], fJ, fc);
+  }
+}
+template <int NB, int I>
+__device__ __forceinline__ void pair_steps_lean(double (&acc)[NB + 1][2], const double* fp, int ks0, int ks1,
+                                                int kst) {
+  for (int ks = ks0; ks < ks1; ks += kst) pair_step_lean<NB, I>(acc, fp + ks * (NB * 32));
+}
+
 // k4 steps ks0, ks0 + kst, ... < ks1.  PF: the fragments of the next step are
 // loaded before this step's DMMAs issue (needs twice the fragment registers).
 template <int NB, int I, bool PF>
@@ -69,6 +88,10 @@ struct PairDispatch {
     if (pair == I) pair_steps<NB, I, PF>(acc, fp, ks0, ks1, kst);
     else PairDispatch<NB, I + 1>::template run<PF>(pair, acc, fp, ks0, ks1, kst);
   }
+  __device__ static void run_lean(int pair, double (&acc)[NB + 1][2], const double* fp, int ks0, int ks1, int kst) {
+    if (pair == I) pair_steps_lean<NB, I>(acc, fp, ks0, ks1, kst);
+    else PairDispatch<NB, I + 1>::run_lean(pair, acc, fp, ks0, ks1, kst);
+  }
   __device__ static void store(int pair, const double (&acc)[NB + 1][2], double* out, int g, int t) {
     if (pair == I) pair_store<NB, I>(acc, out, g, t);
     else PairDispatch<NB, I + 1>::store(pair, acc, out, g, t);
@@ -78,6 +101,7 @@ template <int NB>
 struct PairDispatch<NB, NB / 2> {
   template <bool PF = false>
   __device__ static void run(int, double (&)[NB + 1][2], const double*, int, int, int) {}
+  __device__ static void run_lean(int, double (&)[NB + 1][2], const double*, int, int, int) {}
   __device__ static void store(int, const double (&)[NB + 1][2], double*, int, int) {}
 };
 
