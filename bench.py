@@ -34,6 +34,23 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 FP64_PEAK_TFS = 37.2          # measured DMMA peak, profiles/r01_fp64_peak.json
 FP64_PEAK_SRC = "measured DMMA.8x8x4 microbenchmark (profiles/r01_fp64_peak.json)"
+# DRAM traffic of one dominant-kernel launch from `ncu --set full` captures at
+# the bench's exact per-launch shape (tools/profile_round.sh); per config: the
+# captures summed, and the (rows, cols) they were taken at.
+NCU_SUMMARY = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_ncu_summary.json")
+TRAFFIC_CAPTURES = {3: (("trmm_k256.ncu-rep", "gram_k256.ncu-rep"), (2_000_000, 256))}
+
+
+def _traffic(config, rows, cols):
+    """Measured bytes per launch (read + write) or None when no capture matches."""
+    caps, shape = TRAFFIC_CAPTURES.get(config, ((), None))
+    if not caps or shape != (rows, cols) or not os.path.exists(NCU_SUMMARY):
+        return None
+    with open(NCU_SUMMARY) as fh:
+        by = {d["capture"]: d for d in json.load(fh)}
+    if not all(c in by for c in caps):
+        return None
+    return sum(by[c]["dram_read_bytes"] + by[c]["dram_write_bytes"] for c in caps)
 
 
 def _args():
@@ -343,7 +360,10 @@ def run_ours():
                        "parallelism": f"row-sharded dp{world}",
                        "l2": "inputs larger than L2 (%.1f GB)" % (m * k * 8 / 1e9)},
             "roofline": {"bound": "fp64", "kernel": dom, "achieved": tfs, "peak": FP64_PEAK_TFS,
-                         "unit": "TFLOP/s", "frac": tfs / FP64_PEAK_TFS, "traffic": None,
+                         "unit": "TFLOP/s", "frac": tfs / FP64_PEAK_TFS,
+                         "traffic": _traffic(ARGS.config, lm[0] if lm else 0, k),
+                         "traffic_note": "DRAM bytes per launch, ncu --set full (profiles/r01_ncu_summary.json); "
+                                         "algorithmic: read X + write Q + read Q = 3 m k 8 B",
                          "peak_source": FP64_PEAK_SRC, "kernel_share_of_step": step_share,
                          "flops_model": "TRMM k(k+1) + SYRK k(k+1) flops per row"},
             "kernels": kernel_summary,

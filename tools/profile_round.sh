@@ -1,0 +1,22 @@
+#!/bin/bash
+# Capture the round's profiles on a GPU box (run from the repo root under gpurun):
+#   launch list of the default bench command, and one `ncu --set full` capture
+#   per hot kernel.  Outputs go to gpurun_out/prof/.
+set -u
+mkdir -p gpurun_out/prof
+python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > gpurun_out/prof/bench_plain.log 2>&1 || exit 1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/prof/launches_config3.csv \
+    python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > gpurun_out/prof/ncu_launches.log 2>&1
+full() {  # name, kernel regex, command...
+  local name=$1 kre=$2; shift 2
+  "$@" > /dev/null 2>&1 || { echo "$name: command failed"; return; }
+  ncu --set full --clock-control none --import-source on -k "regex:$kre" -c 1 -o gpurun_out/prof/$name "$@" \
+      > gpurun_out/prof/$name.log 2>&1
+}
+full gram_k256 gram_pairs_kernel python tools/kernel_probe.py --only gram --m 2000000 --k 256 --reps 1
+full trmm_k256 gemm_kernel python tools/kernel_probe.py --only apply --m 2000000 --k 256 --reps 1
+full gram_k64 gram_pairs_kernel python tools/kernel_probe.py --only gram --m 32000000 --k 64 --reps 1
+full trmm_k64 gemm_kernel python tools/kernel_probe.py --only apply --m 32000000 --k 64 --reps 1
+full update_q256 update_pass_kernel python tools/kernel_probe.py --only update --m 8000000 --q 256 --k 16 --reps 1
+full factor_k256 "factor_kernel" python tools/kernel_probe.py --only factor --reps 1
+ls -la gpurun_out/prof
