@@ -22,6 +22,8 @@ from .algorithms import (
     s_chol_qr3,
 )
 from .errors import CholeskyBreakdown, ShiftAttemptLimitError, TriangularSingularError
+from .matgen import MatrixSpec, effective_seed, generate, generate_host, random_orthogonal, singular_values
+from .mmio import load_matrix_market, save_matrix_market, to_dense_block
 from .flops import (
     CATEGORIES,
     FlopLedger,
@@ -33,6 +35,8 @@ from .flops import (
     gemm_flops,
     ledger_report,
     panel_counts,
+    panel_flop_ratio,
+    panel_flop_ratio_limit,
     predict_rscholqr,
     rscholqr_counts,
     tri_inverse_flops,
@@ -57,7 +61,8 @@ def __getattr__(name):
         from . import kernels
 
         return getattr(kernels, name)
-    if name in ("loss_of_orthogonality", "reconstruction_residual", "cholesky_residual"):
+    if name in ("loss_of_orthogonality", "reconstruction_residual", "cholesky_residual", "quality_report",
+                "QualityReport"):
         from . import metrics
 
         return getattr(metrics, name)

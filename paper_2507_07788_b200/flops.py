@@ -141,6 +141,17 @@ def panel_counts(m, panel_widths, profiles):
     return out
 
 
+def panel_flop_ratio(n, r, x):
+    """Predicted panel / plain flop ratio for r panels and x iterations:
+    1/2 + 1/(2r) + x/(4nx + 2n), the m -> infinity limit (flops.py:256-262)."""
+    return 0.5 + 1.0 / (2 * r) + x / (4.0 * n * x + 2.0 * n)
+
+
+def panel_flop_ratio_limit(r):
+    """Its many-iteration limit, 1/2 + 1/(2r) (flops.py:265-267)."""
+    return 0.5 + 1.0 / (2 * r)
+
+
 @dataclass(frozen=True)
 class LedgerComparison:
     measured: dict
