@@ -124,8 +124,14 @@ __global__ void __launch_bounds__(GPCfg<KP>::THREADS, 1) gram_pairs_kernel(const
       const double* fp = fbase + s * C::STAGE;
       // columns >= k of the staged panel hold stale data: only outputs in
       // rows/cols >= k see them, and those are never read back
-      if constexpr (KP >= 256) PairDispatch<NB, 0>::run_lean(pair, acc, fp, sub, nk4, C::WPP);
-      else PairDispatch<NB, 0>::run(pair, acc, fp, sub, nk4, C::WPP);
+      if constexpr (KP >= 256) {
+        PairDispatch<NB, 0>::run_lean(pair, acc, fp, sub, nk4, C::WPP);
+      } else {
+        // full panels of narrow widths: fully unrolled (KP = 128 measured faster with the loop)
+        if (KP <= 64 && nk4 == C::BR / 4)
+          PairDispatch<NB, 0>::template run_fixed<C::BR / 4 / C::WPP>(pair, acc, fp, sub, C::WPP);
+        else PairDispatch<NB, 0>::run(pair, acc, fp, sub, nk4, C::WPP);
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);

@@ -22,6 +22,17 @@ __device__ __forceinline__ void pair_mma(double (&acc)[NB + 1][2], const double 
 #pragma unroll
   for (int c = 0; c <= J; ++c) dmma(acc[I + 1 + c], f[J], f[c]);
 }
+// NS k4 steps ks0, ks0 + kst, ... fully unrolled (full panels: no loop overhead)
+template <int NB, int I, int NS>
+__device__ __forceinline__ void pair_steps_fixed(double (&acc)[NB + 1][2], const double* fp, int ks0, int kst) {
+#pragma unroll
+  for (int j = 0; j < NS; ++j) {
+    double f[NB - I];
+    pair_load<NB, I>(f, fp, ks0 + j * kst);
+    pair_mma<NB, I>(acc, f);
+  }
+}
+
 // lean variant for wide panels: only the two row fragments stay live, column
 // fragments stream one at a time (fits the 168-register cap of a 9-warp CTA)
 template <int NB, int I>
@@ -88,6 +99,11 @@ struct PairDispatch {
     if (pair == I) pair_steps<NB, I, PF>(acc, fp, ks0, ks1, kst);
     else PairDispatch<NB, I + 1>::template run<PF>(pair, acc, fp, ks0, ks1, kst);
   }
+  template <int NS>
+  __device__ static void run_fixed(int pair, double (&acc)[NB + 1][2], const double* fp, int ks0, int kst) {
+    if (pair == I) pair_steps_fixed<NB, I, NS>(acc, fp, ks0, kst);
+    else PairDispatch<NB, I + 1>::template run_fixed<NS>(pair, acc, fp, ks0, kst);
+  }
   __device__ static void run_lean(int pair, double (&acc)[NB + 1][2], const double* fp, int ks0, int ks1, int kst) {
     if (pair == I) pair_steps_lean<NB, I>(acc, fp, ks0, ks1, kst);
     else PairDispatch<NB, I + 1>::run_lean(pair, acc, fp, ks0, ks1, kst);
@@ -101,6 +117,8 @@ template <int NB>
 struct PairDispatch<NB, NB / 2> {
   template <bool PF = false>
   __device__ static void run(int, double (&)[NB + 1][2], const double*, int, int, int) {}
+  template <int NS>
+  __device__ static void run_fixed(int, double (&)[NB + 1][2], const double*, int, int) {}
   __device__ static void run_lean(int, double (&)[NB + 1][2], const double*, int, int, int) {}
   __device__ static void store(int, const double (&)[NB + 1][2], double*, int, int) {}
 };
