@@ -49,6 +49,10 @@ constexpr int FK_MAX_K = 2048;
 
 __host__ __device__ __forceinline__ int64_t pk(int i, int c) { return (int64_t)c * (c + 1) / 2 + i; }
 
+// phase timestamps of the last factor launch (globaltimer ns), for profiling;
+// slots 9..12 accumulate SM cycles of the blocked-Cholesky step phases
+__device__ unsigned long long g_fprof[16];
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -150,12 +154,19 @@ struct LayoutBand4 {
 // memory).  Pivot j is s = Schur diagonal, breakdown on `not s > 0`
 // (kernels.py:76); d = s * rsqrt(s), the row is scaled by rsqrt(s) and the
 // reciprocal is kept in inv[] for the panel solve.  Returns 1 on breakdown.
+// The block lives in registers (lane c owns column c, duplicated across the
+// four lane octets); row jj entries reach other columns by shuffles, so the
+// 8 dependent pivot steps never touch shared memory.
 __device__ int diag_block_warp(double* D, int P, int n, int off, double* inv, double& smin, FState& fs) {
   const int lane = threadIdx.x & 31;
-  // (ii, c) pairs with ii <= c of the 7x7, 6x6, ... trailing parts: precomputed per lane
+  const int c = lane & 7;
+  double d[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) d[r] = D[c * 8 + r];
+#pragma unroll
   for (int jj = 0; jj < 8; ++jj) {
     const int j = 8 * P + jj;
-    const double s = D[jj * 8 + jj];
+    const double s = __shfl_sync(0xffffffffu, d[jj], jj);
     if (j < n) {
       if (!(s > 0.0)) {
         if (lane == 0) { fs.pivot_index = j + off; fs.pivot_value = s; }
@@ -163,17 +174,26 @@ __device__ int diag_block_warp(double* D, int P, int n, int off, double* inv, do
       }
       smin = fmin(smin, s);
     }
+    // the unscaled row jj goes round before rsqrt(s) is known: the rank-1
+    // update is A(ii, c) -= A(jj, ii) A(jj, c) r^2 (r = rsqrt(s)), so only one
+    // multiply follows the rsqrt on the pivot-to-pivot path
+    double aji[8];
+#pragma unroll
+    for (int ii = jj + 1; ii < 8; ++ii) aji[ii] = __shfl_sync(0xffffffffu, d[jj], ii);   // A(jj, ii) from lane ii
     const double r = rsqrt(s);
-    if (lane > jj && lane < 8) D[lane * 8 + jj] *= r;    // row jj, column lane
-    if (lane == jj) { D[jj * 8 + jj] = s * r; inv[j] = r; }
-    __syncwarp();
-    const int w = 7 - jj;
-    for (int e = lane; e < w * w; e += 32) {
-      const int ii = jj + 1 + e / w, c = jj + 1 + e % w;
-      if (c >= ii) D[c * 8 + ii] -= D[ii * 8 + jj] * D[c * 8 + jj];
-    }
-    __syncwarp();
+    const double ajc = d[jj] * (r * r);
+#pragma unroll
+    for (int ii = jj + 1; ii < 8; ++ii)
+      if (c >= ii) d[ii] -= aji[ii] * ajc;
+    if (c > jj) d[jj] *= r;          // row jj, column c
+    if (c == jj) d[jj] = s * r;
+    if (lane == 0) inv[j] = r;
   }
+  if (lane < 8) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) D[c * 8 + r] = d[r];
+  }
+  __syncwarp();
   return 0;
 }
 
@@ -185,17 +205,18 @@ __device__ int diag_block_warp(double* D, int P, int n, int off, double* inv, do
 //       then factors it (lookahead), the other warps take the rest.
 // Two block barriers per 8 pivots.
 template <typename Lay>
-__device__ bool chol_blocked(double* Wb, int n, int nb, int nbr, int off, double* inv, double& smin, FState& fs,
-                             Lay lay, int* flag) {
+__device__ bool chol_blocked(double* Wb, int n, int nb, int P0, int nbr, int off, double* inv, double& smin,
+                             FState& fs, Lay lay, int* flag) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   if (warp == 0) {
-    const int f = diag_block_warp(Wb + lay(0, 0), 0, n, off, inv, smin, fs);
+    const int f = diag_block_warp(Wb + lay(P0, P0), P0, n, off, inv, smin, fs);
     if (lane == 0) *flag = f;
   }
   __syncthreads();
   if (*flag) return false;
-  for (int P = 0; P < nbr; ++P) {
+  for (int P = P0; P < nbr; ++P) {
+    const long long c0 = clock64();
     const double* D = Wb + lay(P, P);
     // ---- (b) panel: R_PJ = R_PP^{-T} W_PJ, one column per thread
     const int ncols = 8 * (nb - 1 - P);
@@ -214,6 +235,7 @@ __device__ bool chol_blocked(double* Wb, int n, int nb, int nbr, int off, double
       for (int jj = 0; jj < 8; ++jj) blk[jj] = y[jj];
     }
     __syncthreads();
+    const long long c1 = clock64();
     // ---- (c) trailing rank-8 update: blocks (I, J), P < I < nbr, I <= J < nb
     const int ncb = nb - 1 - P;
     const int nrows_b = nbr - 1 - P;
@@ -230,7 +252,9 @@ __device__ bool chol_blocked(double* Wb, int n, int nb, int nbr, int off, double
         pc[0] = c2[0];
         pc[8] = c2[1];
         __syncwarp();
+        const long long cd = clock64();
         f = diag_block_warp(Wb + lay(P + 1, P + 1), P + 1, n, off, inv, smin, fs);
+        if (lane == 0) atomicAdd(&g_fprof[12], (unsigned long long)(clock64() - cd));
       }
       if (lane == 0) *flag = f;
     } else {
@@ -280,7 +304,78 @@ __device__ bool chol_blocked(double* Wb, int n, int nb, int nbr, int off, double
       }
     }
     __syncthreads();
+    if (threadIdx.x == 0) {
+      const long long c2 = clock64();
+      g_fprof[9] += (unsigned long long)(c1 - c0);
+      g_fprof[10] += (unsigned long long)(c2 - c1);
+      g_fprof[11] += 1;
+    }
     if (*flag) return false;
+  }
+  return true;
+}
+
+// Rank-(8 (P1-P0)) update of the trailing blocks after a band of block rows
+// [P0, P1) is final: C(I, J) -= sum_P R(P, I)^T R(P, J) for P1 <= I <= J < nb.
+// Each element sees the same DMMA chain (P ascending, k4 0 then 4) as P1-P0
+// separate rank-8 steps, so the result is bitwise the unbanded one.
+template <typename Lay>
+__device__ void band_trailing_update(double* Wb, int nb, int P0, int P1, Lay lay) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int tn = nb - P1;
+  const int nblk = tn * (tn + 1) / 2;
+  auto decode = [&](int blk, int& I, int& J) {
+    J = (int)((sqrtf(8.0f * blk + 1.0f) - 1.0f) * 0.5f);
+    while ((J + 1) * (J + 2) / 2 <= blk) ++J;
+    while (J * (J + 1) / 2 > blk) --J;
+    I = P1 + blk - J * (J + 1) / 2;
+    J += P1;
+  };
+  // two blocks per iteration: two independent DMMA chains in flight
+  for (int blk = warp; blk < nblk; blk += 2 * FK_NW) {
+    const int blk2 = blk + FK_NW;
+    const bool two = blk2 < nblk;
+    int I0, J0, I1 = 0, J1 = 0;
+    decode(blk, I0, J0);
+    if (two) decode(blk2, I1, J1);
+    double* pc0 = Wb + lay(I0, J0) + 2 * t * 8 + g;
+    double* pc1 = two ? Wb + lay(I1, J1) + 2 * t * 8 + g : pc0;
+    double c0[2] = {pc0[0], pc0[8]};
+    double c1[2] = {pc1[0], pc1[8]};
+    for (int P = P0; P < P1; ++P) {
+      const double* pa0 = Wb + lay(P, I0) + g * 8 + t;
+      const double* pb0 = Wb + lay(P, J0) + g * 8 + t;
+      const double* pa1 = Wb + lay(P, I1) + g * 8 + t;
+      const double* pb1 = Wb + lay(P, J1) + g * 8 + t;
+      const double a00 = -pa0[0], a01 = -pa0[4], b00 = pb0[0], b01 = pb0[4];
+      const double a10 = -pa1[0], a11 = -pa1[4], b10 = pb1[0], b11 = pb1[4];
+      dmma(c0, a00, b00);
+      dmma(c1, a10, b10);
+      dmma(c0, a01, b01);
+      dmma(c1, a11, b11);
+    }
+    pc0[0] = c0[0];
+    pc0[8] = c0[1];
+    if (two) { pc1[0] = c1[0]; pc1[8] = c1[1]; }
+  }
+}
+
+// Banded right-looking Cholesky of the nb x nb block upper triangle: bands of
+// 4 block rows (32 pivots) are factored with in-band rank-8 steps, then the
+// rest of the matrix gets one rank-32 update per band (4x fewer barriers and
+// 4x more DMMA per block load than rank-8 steps over the whole matrix).
+// `nbr` limits the factorization to block rows [0, nbr).
+template <typename Lay>
+__device__ bool chol_banded(double* Wb, int n, int nb, int nbr, int off, double* inv, double& smin, FState& fs,
+                            Lay lay, int* flag) {
+  for (int P0 = 0; P0 < nbr; P0 += 4) {
+    const int P1 = min(nbr, P0 + 4);
+    if (!chol_blocked(Wb, n, nb, P0, P1, off, inv, smin, fs, lay, flag)) return false;
+    if (P1 < nbr) {
+      band_trailing_update(Wb, nb, P0, P1, lay);
+      __syncthreads();
+    }
   }
   return true;
 }
@@ -311,8 +406,7 @@ __device__ void store_packed(const double* W, int n, int off, double* Rk, int ld
 
 constexpr int FK_PANEL = 32;
 
-// phase timestamps of the last factor launch (globaltimer ns), for profiling
-__device__ unsigned long long g_fprof[16];
+
 __device__ __forceinline__ void fmark(int slot) {
   if (threadIdx.x == 0) {
     unsigned long long t;
@@ -325,7 +419,7 @@ __device__ __forceinline__ void fmark(int slot) {
 // (upper triangle; the caller zeroes the rest).  `smem_w` is the shared work
 // area, `gW` the global fallback for k > FK_BIG_K.  X is symmetric (shared
 // memory for k <= 128, global otherwise).
-__device__ bool chol_attempt(const double* __restrict__ X, int k, double sigma, double* smem_w, double* gW,
+__device__ __noinline__ bool chol_attempt(const double* __restrict__ X, int k, double sigma, double* smem_w, double* gW,
                              double* Rk, int ldr, double* rowbuf, FState& fs, int* flag) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   double smin = INFINITY;
@@ -341,7 +435,7 @@ __device__ bool chol_attempt(const double* __restrict__ X, int k, double sigma, 
     pad_blocked(Wb, k);
     __syncthreads();
     const int nb = (k + 7) >> 3;
-    ok = chol_blocked(Wb, k, nb, nb, 0, rowbuf, smin, fs, LayoutUpper(), flag);
+    ok = chol_banded(Wb, k, nb, nb, 0, rowbuf, smin, fs, LayoutUpper(), flag);
     if (ok) store_blocked(Wb, k, 0, Rk, ldr);
   } else if (k > FK_BIG_K) {
     double* W = gW;
@@ -371,7 +465,7 @@ __device__ bool chol_attempt(const double* __restrict__ X, int k, double sigma, 
         Wb[band(r >> 3, c >> 3) + (c & 7) * 8 + (r & 7)] = x;
       }
     __syncthreads();
-    ok = chol_blocked(Wb, k, nb, 4, 0, rowbuf, smin, fs, band, flag);
+    ok = chol_banded(Wb, k, nb, 4, 0, rowbuf, smin, fs, band, flag);
     if (ok) {
       // band rows are final rows of R
       for (int r = warp; r < b; r += FK_NW)
@@ -411,7 +505,7 @@ __device__ bool chol_attempt(const double* __restrict__ X, int k, double sigma, 
       pad_blocked(S, n);
       __syncthreads();
       fmark(4);
-      ok = chol_blocked(S, n, nbs, nbs, b, rowbuf, smin, fs, LayoutUpper(), flag);
+      ok = chol_banded(S, n, nbs, nbs, b, rowbuf, smin, fs, LayoutUpper(), flag);
       fmark(5);
       if (ok) store_blocked(S, n, b, Rk, ldr);
     }
@@ -453,32 +547,58 @@ __device__ double norm_estimate(const double* __restrict__ X, int k, double tol,
   const double v0 = 1.0 / sqrt((double)k);
   for (int i = tid; i < k; i += FK_THREADS) vec[i] = v0;
   __syncthreads();
+  const int warp = tid >> 5, lane = tid & 31;
   bool have_prev = false;
   double prev = 0.0;
   for (int it = 0; it < max_iter; ++it) {
-    double nw_loc = 0.0;
-    for (int i = tid; i < k; i += FK_THREADS) {
-      double s = 0.0;
-#pragma unroll 8
-      for (int c = 0; c < k; ++c) s += X[(int64_t)c * k + i] * vec[c];
-      wv[i] = s;
-      nw_loc += s * s;
+    // w = X v: warp w owns rows w, w + 16, ... (4 rows in flight); lanes stride
+    // the row (X symmetric: row i is contiguous), fixed-order butterfly sums
+    for (int i0 = warp; i0 < k; i0 += 4 * FK_NW) {
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int c = lane; c < k; c += 32) {
+        const double vc = vec[c];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int i = i0 + r * FK_NW;
+          if (i < k) acc[r] += X[(int64_t)i * k + c] * vc;
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const double sr = warp_sum(acc[r]);
+        const int i = i0 + r * FK_NW;
+        if (lane == 0 && i < k) wv[i] = sr;
+      }
     }
-    const double nw = sqrt(block_sum(nw_loc, red));
+    __syncthreads();
+    // ||w||^2 and v.w in one two-value reduction
+    double ww = 0.0, vw = 0.0;
+    for (int i = tid; i < k; i += FK_THREADS) {
+      ww += wv[i] * wv[i];
+      vw += vec[i] * wv[i];
+    }
+    ww = warp_sum(ww);
+    vw = warp_sum(vw);
+    if (lane == 0) { red[warp] = ww; red[FK_NW + warp] = vw; }
+    __syncthreads();
+    double nw2 = 0.0, lam = 0.0;
+#pragma unroll
+    for (int w = 0; w < FK_NW; ++w) { nw2 += red[w]; lam += red[FK_NW + w]; }
+    const double nw = sqrt(nw2);
     if (nw == 0.0) {
       if (tid == 0) fs.est_flag = 1;
       return fro;
     }
-    double vw_loc = 0.0;
-    for (int i = tid; i < k; i += FK_THREADS) vw_loc += vec[i] * wv[i];
-    const double lam = block_sum(vw_loc, red);
     for (int i = tid; i < k; i += FK_THREADS) vec[i] = wv[i] / nw;
-    __syncthreads();
-    if (have_prev && fabs(lam - prev) <= tol * fabs(lam)) return fabs(lam);
+    __syncthreads();   // also: red is rewritten next iteration only after this
+    if (have_prev && fabs(lam - prev) <= tol * fabs(lam)) {
+      if (tid == 0) g_fprof[8] = it + 1;   // iterations of the last estimate (profiling)
+      return fabs(lam);
+    }
     prev = lam;
     have_prev = true;
   }
-  if (tid == 0) fs.est_flag = 2;
+  if (tid == 0) { fs.est_flag = 2; g_fprof[8] = max_iter; }
   return fro;
 }
 
@@ -505,6 +625,7 @@ __global__ void __launch_bounds__(FK_THREADS, 1) factor_kernel(FactorArgs a) {
     fs.sigma = 0.0; fs.attempts = 0; fs.plain_margin = 0.0; fs.diag_max = 0.0; fs.min_pivot = 0.0;
   }
 
+  if (tid == 0) { g_fprof[9] = 0; g_fprof[10] = 0; g_fprof[11] = 0; g_fprof[12] = 0; }
   fmark(0);
   // ---- 1. X = G (or G - Bt^T Bt), symmetric by construction from the lower triangle
   //         (lower triangle read column by column: coalesced)
