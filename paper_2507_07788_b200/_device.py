@@ -38,6 +38,7 @@ class DeviceContext:
         torch.cuda.set_device(self.device)
         self._ws = torch.empty(0, dtype=torch.uint8, device=self.device)
         self._ws2 = torch.empty(0, dtype=torch.uint8, device=self.device)
+        self._pinned = {}   # shape -> free pinned host buffers (status slots; cudaHostAlloc is slow)
         self.launches = 0   # libcqr kernel launches issued (bench bookkeeping)
         self.timer = None   # optional KernelTimer (bench): CUDA events per libcqr call
 
@@ -45,6 +46,14 @@ class DeviceContext:
     @property
     def stream(self):
         return torch.cuda.current_stream(self.device).cuda_stream
+
+    def acquire_pinned(self, shape):
+        """A pinned uint8 host buffer of `shape` from the free list (or a new one)."""
+        free = self._pinned.setdefault(tuple(shape), [])
+        return free.pop() if free else torch.empty(shape, dtype=torch.uint8, pin_memory=True)
+
+    def release_pinned(self, buf):
+        self._pinned.setdefault(tuple(buf.shape), []).append(buf)
 
     def workspace(self, nbytes, which=0):
         """Reusable device scratch (grown on demand)."""

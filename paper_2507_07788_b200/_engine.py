@@ -104,12 +104,16 @@ class Engine:
         self.G = torch.empty((k, k), dtype=torch.float64, device=dev)
         self.Rk = torch.zeros((k, self.ldr), dtype=torch.float64, device=dev)
         self.Rinv = torch.zeros(max(cx.lib.cqr_coeff_doubles(k, k), 1), dtype=torch.float64, device=dev)  # tiles
-        self.Racc = torch.zeros((k, self.ldr), dtype=torch.float64, device=dev)
-        self.Racc[:, :k] = torch.eye(k, dtype=torch.float64, device=dev)
+        self.Racc = torch.eye(k, self.ldr, dtype=torch.float64, device=dev)   # [I | 0]
         self.cap = cfg.max_shift_attempts + 1
         nbytes = STATUS_BYTES + 8 * self.cap
-        self.stat = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
-        self.stat_host = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+        # status slots: fixed-schedule algorithms enqueue several factor calls and
+        # read their statuses once at the end (factor_async / collect)
+        self.nslots = 4
+        self.stat_all = torch.empty((self.nslots, nbytes), dtype=torch.uint8, device=dev)
+        self.stat_host_all = cx.acquire_pinned((self.nslots, nbytes))
+        self.stat, self.stat_host = self.stat_all[0], self.stat_host_all[0]
+        self._next_slot = 0
         self.fws = torch.empty(cx.lib.cqr_factor_workspace_bytes(k), dtype=torch.uint8, device=dev)
         if q:
             self.B = torch.zeros((k, q), dtype=torch.float64, device=dev)     # (p, q): column-major q x p
@@ -117,10 +121,36 @@ class Engine:
         else:
             self.B = self.Bt = None
 
+    def __del__(self):
+        try:
+            self.cx.release_pinned(self.stat_host_all)
+        except Exception:   # interpreter shutdown
+            pass
+
     # ------------------------------------------------------------ k x k stage
     def factor(self, policy, m_global, width, *, tol=0.0, check_tol=False, stop=False, update_b=False,
                fixed_shift=0.0):
+        """Run the k x k stage and return its status (one host sync)."""
+        h = self.factor_async(policy, m_global, width, tol=tol, check_tol=check_tol, stop=stop, update_b=update_b,
+                              fixed_shift=fixed_shift)
+        return self.collect([h])[0]
+
+    def collect(self, handles):
+        """Statuses of enqueued factor calls, in order, after one stream sync."""
+        torch.cuda.current_stream(self.cx.device).synchronize()
+        out = []
+        for h in handles:
+            raw = self.stat_host_all[h].numpy()
+            out.append(PassStatus(raw.tobytes(), raw[STATUS_BYTES:].view(np.float64)))
+        return out
+
+    def factor_async(self, policy, m_global, width, *, tol=0.0, check_tol=False, stop=False, update_b=False,
+                     fixed_shift=0.0):
+        """Enqueue the k x k stage; its status lands in a pinned host slot
+        (returned handle) without a sync.  Up to `nslots` calls may be pending."""
         cx = self.cx
+        slot = self._next_slot
+        self._next_slot = (slot + 1) % self.nslots
         cfg = self.cfg
         fc = _lib.FactorConfig(
             policy=policy, shift_width=width, m_global=m_global, unit_roundoff=cfg.unit_roundoff,
@@ -129,7 +159,7 @@ class Engine:
             update_b=1 if update_b else 0, est_max_iter=100, est_tol=1e-2, fixed_shift=fixed_shift)
         bt = self.Bt.data_ptr() if self.Bt is not None else None
         b = self.B.data_ptr() if self.B is not None else None
-        base = self.stat.data_ptr()
+        base = self.stat_all[slot].data_ptr()
         t0 = cx.timer.start() if cx.timer else None
         _lib.check(cx.lib.cqr_factor(ctypes.byref(fc), self.k, self.G.data_ptr(), self.k, bt, max(self.q, 1),
                                      self.q, self.Rk.data_ptr(), self.Rinv.data_ptr(), self.ldr,
@@ -138,11 +168,8 @@ class Engine:
         if t0 is not None:
             cx.timer.stop("factor", t0, (self.k,))
         cx.launches += 2
-        self.stat_host.copy_(self.stat, non_blocking=True)
-        torch.cuda.current_stream(cx.device).synchronize()
-        raw = self.stat_host.numpy()
-        shifts = raw[STATUS_BYTES:].view(np.float64)
-        return PassStatus(raw.tobytes(), shifts)
+        self.stat_host_all[slot].copy_(self.stat_all[slot], non_blocking=True)
+        return slot
 
     # ------------------------------------------------------------ tall passes
     def gram(self, arr):

@@ -180,7 +180,11 @@ def _charge_update(ledger, p, st):
 # ----------------------------------------------------------------------------
 
 def chol_qr(a, cfg=None, ledger=None):
-    """One plain pass: Q = A R^-1 with R from the Gramian; breakdown propagates."""
+    """One plain pass: Q = A R^-1 with R from the Gramian; breakdown propagates.
+
+    Fixed schedule: the kernels are enqueued back to back and the factor status
+    is read once at the end; charges and raises replay the reference's order
+    (algorithms.py:201-212), so a breakdown raises with the same ledger state."""
     cfg = cfg or AlgoConfig()
     a = _device_array(a)
     if a.ncols < 1:
@@ -188,13 +192,14 @@ def chol_qr(a, cfg=None, ledger=None):
     m, n = a.space.dim, a.ncols
     eng = Engine(n, cfg)
     eng.gram(a)
-    _charge(ledger, "gemm", _flops.gemm_flops(m, n, n))
-    _charge_plain_attempt(ledger, n)
-    st = eng.factor(_lib.POLICY_PLAIN, m, n)
-    _raise_for(st)
-    _charge(ledger, "trtri", _flops.tri_inverse_flops(n))
+    h = eng.factor_async(_lib.POLICY_PLAIN, m, n)
     q = _fresh_like(a, n)
     eng.apply(a, q, with_gram=False)
+    (st,) = eng.collect([h])
+    _charge(ledger, "gemm", _flops.gemm_flops(m, n, n))
+    _charge_plain_attempt(ledger, n)
+    _raise_for(st)
+    _charge(ledger, "trtri", _flops.tri_inverse_flops(n))
     _charge(ledger, "gemm", _flops.gemm_flops(m, n, n))
     return QRResult(q=q, r=eng.r_host(), iterations=1, pivot_margins=[st.min_pivot_rel],
                     decision_margins=[st.plain_margin])
@@ -207,32 +212,31 @@ def _fresh_like(a, n):
 def chol_qr2(a, cfg=None, ledger=None):
     """Two plain passes, factors multiplied (algorithms.py:215-220).
 
-    Device schedule: Gram(A) | factor | Q1 = A R1^-1 fused with Gram(Q1) |
-    factor | Q = Q1 R2^-1 in place -- 5 m k doubles of HBM traffic."""
+    Device schedule: Gram(A) | factor | Q1 = A R1^-1 + Gram(Q1) | factor |
+    Q = Q1 R2^-1 in place, enqueued without a host sync; both statuses are read
+    at the end and the reference's charge / raise sequence is replayed."""
     cfg = cfg or AlgoConfig()
     a = _device_array(a)
     if a.ncols < 1:
         raise ValueError("need at least one column")
     m, n = a.space.dim, a.ncols
     eng = Engine(n, cfg)
-    margins = []
     eng.gram(a)
-    _charge(ledger, "gemm", _flops.gemm_flops(m, n, n))
-    _charge_plain_attempt(ledger, n)
-    st = eng.factor(_lib.POLICY_PLAIN, m, n)
-    _raise_for(st)
-    margins.append(st.min_pivot_rel)
-    _charge(ledger, "trtri", _flops.tri_inverse_flops(n))
+    h1 = eng.factor_async(_lib.POLICY_PLAIN, m, n)
     q = _fresh_like(a, n)
     eng.apply(a, q, with_gram=True)
-    _charge(ledger, "gemm", _flops.gemm_flops(m, n, n))          # lincomb of pass 1
-    _charge(ledger, "gemm", _flops.gemm_flops(m, n, n))          # Gram of pass 2
-    _charge_plain_attempt(ledger, n)
-    st = eng.factor(_lib.POLICY_PLAIN, m, n)
-    _raise_for(st)
-    margins.append(st.min_pivot_rel)
-    _charge(ledger, "trtri", _flops.tri_inverse_flops(n))
+    h2 = eng.factor_async(_lib.POLICY_PLAIN, m, n)
     _apply_last(eng, q)
+    st1, st2 = eng.collect([h1, h2])
+    margins = []
+    for i, st in enumerate((st1, st2)):
+        if i == 1:
+            _charge(ledger, "gemm", _flops.gemm_flops(m, n, n))      # lincomb of pass 1
+        _charge(ledger, "gemm", _flops.gemm_flops(m, n, n))          # Gram of this pass
+        _charge_plain_attempt(ledger, n)
+        _raise_for(st)
+        margins.append(st.min_pivot_rel)
+        _charge(ledger, "trtri", _flops.tri_inverse_flops(n))
     _charge(ledger, "gemm", _flops.gemm_flops(m, n, n))
     _charge(ledger, "trmm", _flops.trmm_flops(n))
     return QRResult(q=q, r=eng.r_host(), iterations=2, pivot_margins=margins)
@@ -261,39 +265,44 @@ def _apply_gram_into(eng, src, fresh_ok):
 
 def s_chol_qr3(a, cfg=None, ledger=None):
     """Shifted first pass (sigma from the first Gram's norm estimate), then two
-    plain passes; a breakdown in any pass propagates (algorithms.py:223-244)."""
+    plain passes; a breakdown in any pass propagates (algorithms.py:223-244).
+
+    Fixed schedule: all three passes are enqueued without a host sync, the three
+    statuses are read once, then the reference's warnings, charges and raises
+    are replayed in order."""
     cfg = cfg or AlgoConfig()
     a = _device_array(a)
     if a.ncols < 1:
         raise ValueError("need at least one column")
     m, n = a.space.dim, a.ncols
     eng = Engine(n, cfg)
-    margins = []
     eng.gram(a)
+    hs = [eng.factor_async(_lib.POLICY_SHIFT_ONCE, m, n)]
+    q = _fresh_like(a, n)
+    eng.apply(a, q, with_gram=True)
+    hs.append(eng.factor_async(_lib.POLICY_PLAIN, m, n))
+    q = _apply_gram_into(eng, q, fresh_ok=False)
+    hs.append(eng.factor_async(_lib.POLICY_PLAIN, m, n))
+    _apply_last(eng, q)
+    sts = eng.collect(hs)
+
+    st = sts[0]
     _charge(ledger, "gemm", _flops.gemm_flops(m, n, n))
-    st = eng.factor(_lib.POLICY_SHIFT_ONCE, m, n)
     _emit_estimate_warning(st)
     _charge(ledger, "eig_est", _flops.eig_estimate_flops(n))
     _charge(ledger, "potrf", n)
     _charge_plain_attempt(ledger, n)
     _raise_for(st)
     sigma = st.shifts[0]
-    margins.append(st.min_pivot_rel)
+    margins = [st.min_pivot_rel]
     _charge(ledger, "trtri", _flops.tri_inverse_flops(n))
-    q = _fresh_like(a, n)
-    eng.apply(a, q, with_gram=True)
     _charge(ledger, "gemm", _flops.gemm_flops(m, n, n))
-    for p in range(2):
+    for st in sts[1:]:
         _charge(ledger, "gemm", _flops.gemm_flops(m, n, n))      # Gram of this pass
         _charge_plain_attempt(ledger, n)
-        st = eng.factor(_lib.POLICY_PLAIN, m, n)
         _raise_for(st)
         margins.append(st.min_pivot_rel)
         _charge(ledger, "trtri", _flops.tri_inverse_flops(n))
-        if p == 0:
-            q = _apply_gram_into(eng, q, fresh_ok=False)
-        else:
-            _apply_last(eng, q)
         _charge(ledger, "gemm", _flops.gemm_flops(m, n, n))
         _charge(ledger, "trmm", _flops.trmm_flops(n))
     return QRResult(q=q, r=eng.r_host(), iterations=3, shifts_applied=[sigma], pivot_margins=margins)
