@@ -19,8 +19,9 @@
 //   * 8 cross-Gram warps: warp w owns the same slices as rows of Bt':
 //     Bt' += Q_in^T Q' in registers over the sweep, G += Q'^T Q' (warps 8-10);
 //     they release the stage, and the last one's lane 0 refills it.
-// Both groups issue q/8 DMMA per warp per sub-panel; the width enters as the
-// template parameter NQ = ceil(q/64) so no DMMA is predicated off.  Groups hand
+// Both groups issue q/8 DMMA per warp per 16 rows; the width enters as the
+// template parameter NQ = ceil(q/64) so no DMMA is predicated off.  Bases up to
+// 192 columns use 32-row sub-panels (half the per-row synchronisation).  Groups hand
 // over through mbarriers; the projection group syncs on a named barrier.
 // Per-CTA partials [Bt'(q_pad x 16) | G'(16 x 16)] are written once per CTA
 // and summed by a fixed-order reduce kernel.
@@ -29,13 +30,18 @@
 
 namespace cqr {
 
-constexpr int UP_SR = 16;                 // rows per sub-panel (4 quads)
 constexpr int UP_MAXQ = 512;
 constexpr int UP_PB = 16;                 // padded block width
 constexpr int UP_THREADS = 512;           // 8 projection + 8 cross-Gram warps
 constexpr int UP_YS = 2;                  // Q' ring slots
 constexpr int UP_MAXNS = 8;               // TMA ring stages (at most)
-constexpr int UP_FIXED = UP_PB * CT_LD + 8 * 256 + 256 + UP_YS * 256;   // doubles before the ring
+
+// SR = rows per sub-panel (16 or 32): 32 halves the per-row cost of the
+// projection group's barriers and reduction, used where the stage still
+// leaves room for a deep ring (narrow bases).
+__host__ __device__ constexpr int up_fixed(int SR) {   // doubles before the ring
+  return UP_PB * CT_LD + 8 * SR * UP_PB + SR * UP_PB + UP_YS * SR * UP_PB;
+}
 
 struct UpdateArgs {
   const double* Qin; int64_t ldqin; int q;
@@ -50,30 +56,36 @@ struct UpdateArgs {
 };
 
 static int up_qs(int q) { return (int)round_up(q, 8) + 4; }
-static int up_stage(int q) { return UP_SR * up_qs(q) + UP_SR * UP_PB; }
-static int up_stages(int q) {
-  const int64_t avail = 227 * 1024 - 512 - (int64_t)UP_FIXED * 8;
-  int64_t ns = avail / ((int64_t)up_stage(q) * 8);
+static int up_sr(int q) { return q <= 192 ? 32 : 16; }
+static int up_stage(int q, int sr) { return sr * up_qs(q) + sr * UP_PB; }
+static int up_stages(int q, int sr) {
+  const int64_t avail = 227 * 1024 - 512 - (int64_t)up_fixed(sr) * 8;
+  int64_t ns = avail / ((int64_t)up_stage(q, sr) * 8);
   return (int)(ns > UP_MAXNS ? UP_MAXNS : ns);
 }
-static size_t update_smem_bytes(int q) { return ((size_t)UP_FIXED + (size_t)up_stages(q) * up_stage(q)) * 8; }
+static size_t update_smem_bytes(int q, int sr) {
+  return ((size_t)up_fixed(sr) + (size_t)up_stages(q, sr) * up_stage(q, sr)) * 8;
+}
 
-template <int NQ>
+template <int NQ, int SR>
 __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(UpdateArgs a) {
+  constexpr int RB = SR / 8;        // 8-row blocks per sub-panel
+  constexpr int Q4 = SR / 4;        // quads (k4 steps of the cross Gram) per sub-panel
+  constexpr int TE = SR * UP_PB;    // elements of a 16-wide sub-panel
   extern __shared__ __align__(128) double smem[];
   const int q = a.q, p = a.p, qs = a.qs, ns = a.ns;
-  const int STG = UP_SR * qs + UP_SR * UP_PB;
+  const int STG = SR * qs + SR * UP_PB;
   double* ris = smem;                      // R^-1 as [n][k] (ld 36)
-  double* red = ris + UP_PB * CT_LD;       // 8 projection partials (16 x 16, column-major)
-  double* tq = red + 8 * 256;              // t = Q - proj (QI, 16 x 16)
-  double* yring = tq + 256;                // UP_YS x Q' (QI, 16 x 16)
-  double* stg = yring + UP_YS * 256;       // ns x [Q_in sub-panel (4 quads x qs x 4) | block (4 quads x 16 x 4)]
+  double* red = ris + UP_PB * CT_LD;       // 8 projection partials (QI, SR x 16)
+  double* tq = red + 8 * TE;               // t = Q - proj (QI, SR x 16)
+  double* yring = tq + TE;                 // UP_YS x Q' (QI, SR x 16)
+  double* stg = yring + UP_YS * TE;        // ns x [Q_in sub-panel (Q4 quads x qs x 4) | block (Q4 quads x 16 x 4)]
   __shared__ __align__(8) uint64_t full[UP_MAXNS], empty[UP_MAXNS], yfull[UP_YS], yempty[UP_YS];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   const bool init = a.initial != 0;
-  const int64_t nsp = a.rows / UP_SR;
+  const int64_t nsp = ceil_div(a.rows, SR);
   const int64_t mine = (nsp > blockIdx.x) ? ceil_div(nsp - blockIdx.x, gridDim.x) : 0;
 
   if (tid == 0) {
@@ -90,17 +102,18 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(UpdateArgs a
   __syncthreads();
 
   auto issue = [&](int64_t j, int st) {
-    const int64_t r0 = (blockIdx.x + j * gridDim.x) * UP_SR;
+    const int64_t r0 = (blockIdx.x + j * gridDim.x) * SR;
+    const int nq = (int)imin64(SR, a.rows - r0) >> 2;
     double* dq = stg + st * STG;
-    double* db = dq + UP_SR * qs;
-    mbar_arrive_expect_tx(&full[st], (uint32_t)4 * (q + p) * 32);
+    double* db = dq + SR * qs;
+    mbar_arrive_expect_tx(&full[st], (uint32_t)nq * (q + p) * 32);
     const double* sq = a.Qin + (r0 >> 2) * 4 * a.ldqin;
     const double* sb = a.Qb + (r0 >> 2) * 4 * a.ldqb;
-    for (int qq = 0; qq < 4; ++qq) bulk_g2s(dq + qq * 4 * qs, sq + qq * 4 * a.ldqin, (uint32_t)q * 32, &full[st]);
+    for (int qq = 0; qq < nq; ++qq) bulk_g2s(dq + qq * 4 * qs, sq + qq * 4 * a.ldqin, (uint32_t)q * 32, &full[st]);
     if (a.ldqb == UP_PB && p == UP_PB) {
-      bulk_g2s(db, sb, 4 * UP_PB * 32, &full[st]);
+      bulk_g2s(db, sb, (uint32_t)nq * UP_PB * 32, &full[st]);
     } else {
-      for (int qq = 0; qq < 4; ++qq) bulk_g2s(db + qq * 4 * UP_PB, sb + qq * 4 * a.ldqb, (uint32_t)p * 32, &full[st]);
+      for (int qq = 0; qq < nq; ++qq) bulk_g2s(db + qq * 4 * UP_PB, sb + qq * 4 * a.ldqb, (uint32_t)p * 32, &full[st]);
     }
   };
   if (tid == 0)
@@ -121,16 +134,25 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(UpdateArgs a
           const int kk = 64 * c + 8 * wa + 4 * h + t, n = 8 * nb + g;
           btr[c][h][nb] = (!init && kk < q && n < p) ? a.Bt[(int64_t)n * a.ldbt + kk] : 0.0;
         }
-    const int row = tid & 15, col = tid >> 4;   // element of the t / copy phase (256 threads, 16 x 16)
-    const int qoff = (row >> 2) * 4 * UP_PB + 4 * col + (row & 3);
     for (int64_t j = 0; j < mine; ++j) {
-      const int64_t r0 = (blockIdx.x + j * gridDim.x) * UP_SR;
+      const int64_t r0 = (blockIdx.x + j * gridDim.x) * SR;
+      const int nrows = (int)imin64(SR, a.rows - r0);
       mbar_wait(&full[s], ph);
       const double* Qs = stg + s * STG;
-      const double* Ys = Qs + UP_SR * qs;
-      double* yd = yring + ys * 256;
+      const double* Ys = Qs + SR * qs;
+      double* yd = yring + ys * TE;
+      if (SR > 16 && nrows < SR) {
+        // ragged last sub-panel: the stage's rows >= nrows are stale; zero them
+        // for the cross-Gram group (it multiplies them by Q' rows that are 0)
+        double* Qz = stg + s * STG + nrows * qs;
+        for (int e = tid; e < (SR - nrows) * qs; e += 256) Qz[e] = 0.0;
+      }
       if (!init) {
-        double pr[2][2][2] = {{{0.0, 0.0}, {0.0, 0.0}}, {{0.0, 0.0}, {0.0, 0.0}}};
+        double pr[RB][2][2];
+#pragma unroll
+        for (int rb = 0; rb < RB; ++rb)
+#pragma unroll
+          for (int nb = 0; nb < 2; ++nb) { pr[rb][nb][0] = 0.0; pr[rb][nb][1] = 0.0; }
         const double* xa = Qs + (g >> 2) * 4 * qs + (g & 3) + 4 * t;   // row g, column t
 #pragma unroll
         for (int c = 0; c < NQ; ++c)
@@ -138,29 +160,35 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(UpdateArgs a
           for (int h = 0; h < 2; ++h) {
             const int kc = 64 * c + 8 * wa + 4 * h;   // + t
             const bool kv = kc + t < q;               // columns >= q of the stage are stale
-            const double a0 = kv ? xa[4 * kc] : 0.0;
-            const double a1 = kv ? xa[4 * kc + 8 * qs] : 0.0;   // row 8 + g
-            dmma(pr[0][0], a0, btr[c][h][0]);
-            dmma(pr[0][1], a0, btr[c][h][1]);
-            dmma(pr[1][0], a1, btr[c][h][0]);
-            dmma(pr[1][1], a1, btr[c][h][1]);
-          }
+            double av[RB];
 #pragma unroll
-        for (int rb = 0; rb < 2; ++rb)
+            for (int rb = 0; rb < RB; ++rb) av[rb] = kv ? xa[4 * kc + rb * 8 * qs] : 0.0;   // row 8 rb + g
+#pragma unroll
+            for (int rb = 0; rb < RB; ++rb) {
+              dmma(pr[rb][0], av[rb], btr[c][h][0]);
+              dmma(pr[rb][1], av[rb], btr[c][h][1]);
+            }
+          }
+        // partials in the QI layout of the sub-panel (as tq, yd and the stage)
+#pragma unroll
+        for (int rb = 0; rb < RB; ++rb)
 #pragma unroll
           for (int nb = 0; nb < 2; ++nb)
 #pragma unroll
-            for (int e = 0; e < 2; ++e) red[wa * 256 + (8 * nb + 2 * t + e) * 16 + 8 * rb + g] = pr[rb][nb][e];
+            for (int e = 0; e < 2; ++e)
+              red[wa * TE + (2 * rb + (g >> 2)) * 4 * UP_PB + 4 * (8 * nb + 2 * t + e) + (g & 3)] = pr[rb][nb][e];
         asm volatile("bar.sync 2, 256;" ::: "memory");
-        {
+        for (int e = tid; e < TE; e += 256) {
+          // e is the QI offset itself: a warp touches 32 consecutive doubles
+          const int row = 4 * (e >> 6) + (e & 3), col = (e >> 2) & 15;
           double sum = 0.0;
 #pragma unroll
-          for (int w = 0; w < 8; ++w) sum += red[w * 256 + col * 16 + row];
-          tq[qoff] = (col < p) ? Ys[qoff] - sum : 0.0;
+          for (int w = 0; w < 8; ++w) sum += red[w * TE + e];
+          tq[e] = (col < p && row < nrows) ? Ys[e] - sum : 0.0;
         }
         asm volatile("bar.sync 2, 256;" ::: "memory");
         if (j >= UP_YS) mbar_wait(&yempty[ys], yph ^ 1);
-        if (wa < 4) {
+        if (wa < 2 * RB) {
           // Q' block (rb, nb) = t(rows 8rb.., :) R^-1(:, cols 8nb..); R^-1 upper: K < 8(nb+1)
           const int rb = wa >> 1, nb = wa & 1;
           const int r = 8 * rb + g;
@@ -179,13 +207,16 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(UpdateArgs a
             const int cc = 8 * nb + 2 * t + e;
             const bool v = cc < p;
             yd[(r >> 2) * 4 * UP_PB + 4 * cc + (r & 3)] = v ? c2[e] : 0.0;
-            if (v) a.Qb[((r0 + r) >> 2) * 4 * a.ldqb + 4 * cc + (r & 3)] = c2[e];
+            if (v && r < nrows) a.Qb[((r0 + r) >> 2) * 4 * a.ldqb + 4 * cc + (r & 3)] = c2[e];
           }
         }
       } else {
-        // initial mode: Q' = Q (stale padding columns zeroed)
+        // initial mode: Q' = Q (stale padding columns / rows zeroed)
         if (j >= UP_YS) mbar_wait(&yempty[ys], yph ^ 1);
-        yd[qoff] = (col < p) ? Ys[qoff] : 0.0;
+        for (int e = tid; e < TE; e += 256) {
+          const int row = 4 * (e >> 6) + (e & 3), col = (e >> 2) & 15;
+          yd[e] = (col < p && row < nrows) ? Ys[e] : 0.0;
+        }
       }
       mbar_arrive(&yfull[ys]);   // every projection thread: its own stores are released
       if (++s == ns) { s = 0; ph ^= 1; }
@@ -204,10 +235,10 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(UpdateArgs a
     for (int64_t j = 0; j < mine; ++j) {
       mbar_wait(&yfull[ys], yph);
       const double* Qs = stg + s * STG;
-      const double* yd = yring + ys * 256;
+      const double* yd = yring + ys * TE;
       const double* xa = Qs + 4 * (8 * wb + g) + t;   // Q_in(row t, column 8wb + g)
 #pragma unroll
-      for (int ks = 0; ks < 4; ++ks) {
+      for (int ks = 0; ks < Q4; ++ks) {
         const double b0 = yd[ks * 64 + 4 * g + t], b1 = yd[ks * 64 + 32 + 4 * g + t];
 #pragma unroll
         for (int c = 0; c < NQ; ++c) {
@@ -219,7 +250,7 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(UpdateArgs a
       }
       if (wb < 3) {
 #pragma unroll
-        for (int ks = 0; ks < 4; ++ks) dmma(gq, yd[ks * 64 + 32 * bi + 4 * g + t], yd[ks * 64 + 32 * bj + 4 * g + t]);
+        for (int ks = 0; ks < Q4; ++ks) dmma(gq, yd[ks * 64 + 32 * bi + 4 * g + t], yd[ks * 64 + 32 * bj + 4 * g + t]);
       }
       __syncwarp();
       if (lane == 0) {
@@ -275,13 +306,13 @@ __global__ void update_reduce_kernel(const double* __restrict__ ws, int nparts, 
 }
 
 static int update_ctas(int64_t rows) {
-  int64_t n = ceil_div(rows, UP_SR);
+  int64_t n = ceil_div(rows, 16);
   int64_t c = num_sms();
   return (int)(n < c ? (n < 1 ? 1 : n) : c);
 }
 
 bool update_pass_supported(int q, int p) {
-  return q >= 1 && q <= UP_MAXQ && p >= 1 && p <= UP_PB && up_stages(q) >= 2;
+  return q >= 1 && q <= UP_MAXQ && p >= 1 && p <= UP_PB && up_stages(q, up_sr(q)) >= 2;
 }
 
 size_t update_pass_ws_bytes(int64_t rows, int q) {
@@ -289,23 +320,23 @@ size_t update_pass_ws_bytes(int64_t rows, int q) {
   return (size_t)update_ctas(rows) * (qp + UP_PB) * UP_PB * sizeof(double) + 256;
 }
 
-template <int NQ>
+template <int NQ, int SR>
 static cudaError_t launch_up(const UpdateArgs& a, int ctas, size_t smem, cudaStream_t s) {
   static size_t attr = 0;
   if (smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(update_pass_kernel<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(update_pass_kernel<NQ, SR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
     attr = smem;
   }
-  update_pass_kernel<NQ><<<ctas, UP_THREADS, smem, s>>>(a);
+  update_pass_kernel<NQ, SR><<<ctas, UP_THREADS, smem, s>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t update_pass_launch(const double* Qin, int64_t ldqin, int q, double* Qb, int64_t ldqb, int p,
                                int64_t rows, const double* Bt, int ldbt, const double* Rinv_tiles, int initial,
                                double* Bt_next, double* G, int ldg, double* ws, cudaStream_t s) {
-  if (rows % UP_SR) return cudaErrorInvalidValue;
+  if (rows % 16) return cudaErrorInvalidValue;
   UpdateArgs a{};
   a.Qin = Qin; a.ldqin = ldqin; a.q = q;
   a.Qb = Qb; a.ldqb = ldqb; a.p = p;
@@ -314,19 +345,20 @@ cudaError_t update_pass_launch(const double* Qin, int64_t ldqin, int q, double* 
   a.initial = initial;
   a.ws = ws;
   a.qs = up_qs(q);
-  a.ns = up_stages(q);
-  const size_t smem = update_smem_bytes(q);
+  const int sr = up_sr(q);
+  a.ns = up_stages(q, sr);
+  const size_t smem = update_smem_bytes(q, sr);
   const int ctas = update_ctas(rows);
   cudaError_t e;
   switch ((q + 63) / 64) {
-    case 1: e = launch_up<1>(a, ctas, smem, s); break;
-    case 2: e = launch_up<2>(a, ctas, smem, s); break;
-    case 3: e = launch_up<3>(a, ctas, smem, s); break;
-    case 4: e = launch_up<4>(a, ctas, smem, s); break;
-    case 5: e = launch_up<5>(a, ctas, smem, s); break;
-    case 6: e = launch_up<6>(a, ctas, smem, s); break;
-    case 7: e = launch_up<7>(a, ctas, smem, s); break;
-    case 8: e = launch_up<8>(a, ctas, smem, s); break;
+    case 1: e = launch_up<1, 32>(a, ctas, smem, s); break;
+    case 2: e = launch_up<2, 32>(a, ctas, smem, s); break;
+    case 3: e = (sr == 32) ? launch_up<3, 32>(a, ctas, smem, s) : launch_up<3, 16>(a, ctas, smem, s); break;
+    case 4: e = launch_up<4, 16>(a, ctas, smem, s); break;
+    case 5: e = launch_up<5, 16>(a, ctas, smem, s); break;
+    case 6: e = launch_up<6, 16>(a, ctas, smem, s); break;
+    case 7: e = launch_up<7, 16>(a, ctas, smem, s); break;
+    case 8: e = launch_up<8, 16>(a, ctas, smem, s); break;
     default: return cudaErrorInvalidValue;
   }
   if (e != cudaSuccess) return e;
