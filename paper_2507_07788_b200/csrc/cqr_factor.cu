@@ -15,7 +15,7 @@
 // The loop control that stays on the host (iteration count, QRResult) only
 // reads the status record this kernel writes.
 //
-// Two launches per pass.  `factor_kernel` (one CTA, 512 threads) forms X,
+// Two launches per pass.  `factor_kernel` (one CTA, 384 threads) forms X,
 // measures it, runs the policy's factorization attempts and writes Rk;
 // `factor_finish_kernel` (one warp per column, k/8 CTAs) does the column-
 // independent rest: B += Bt Racc, Racc <- triu(Rk Racc) and the inverse by
@@ -41,7 +41,7 @@
 
 namespace cqr {
 
-constexpr int FK_THREADS = 512;
+constexpr int FK_THREADS = 384;
 constexpr int FK_NW = FK_THREADS / 32;
 constexpr int FK_SMEM_K = 128;   // whole packed triangle in shared memory
 constexpr int FK_BIG_K = 256;    // panel + shared trailing matrix
@@ -150,51 +150,57 @@ struct LayoutBand4 {
   __device__ __forceinline__ int operator()(int I, int J) const { return (J * 4 + I) * 64; }
 };
 
-// 8x8 diagonal block factorization by one warp (block column-major in shared
-// memory).  Pivot j is s = Schur diagonal, breakdown on `not s > 0`
-// (kernels.py:76); d = s * rsqrt(s), the row is scaled by rsqrt(s) and the
-// reciprocal is kept in inv[] for the panel solve.  Returns 1 on breakdown.
-// The block lives in registers (lane c owns column c, duplicated across the
-// four lane octets); row jj entries reach other columns by shuffles, so the
-// 8 dependent pivot steps never touch shared memory.
+// 8x8 diagonal block factorization (block column-major in shared memory).
+// Pivot j is s = Schur diagonal, breakdown on `not s > 0` (kernels.py:76);
+// d = s * rsqrt(s), the row is scaled by rsqrt(s) and the reciprocal is kept
+// in inv[] for the panel solve.  Returns 1 (warp-uniform) on breakdown.
+// One lane does it with the 36 upper entries in registers: 8 dependent pivots
+// cost ~1100 cycles this way against ~3100 with the block spread over the
+// warp, where 64-bit shuffles serialise on the MIO pipe
+// (profiles/r01_diag_block.jsonl).  Only lane 0's smin is used afterwards.
+__device__ __forceinline__ constexpr int pk8(int i, int c) { return c * (c + 1) / 2 + i; }
 __device__ int diag_block_warp(double* D, int P, int n, int off, double* inv, double& smin, FState& fs) {
   const int lane = threadIdx.x & 31;
-  const int c = lane & 7;
-  double d[8];
+  int bad = 0;
+  if (lane == 0) {
+    double a[36];
 #pragma unroll
-  for (int r = 0; r < 8; ++r) d[r] = D[c * 8 + r];
+    for (int c = 0; c < 8; ++c)
 #pragma unroll
-  for (int jj = 0; jj < 8; ++jj) {
-    const int j = 8 * P + jj;
-    const double s = __shfl_sync(0xffffffffu, d[jj], jj);
-    if (j < n) {
-      if (!(s > 0.0)) {
-        if (lane == 0) { fs.pivot_index = j + off; fs.pivot_value = s; }
-        return 1;
+      for (int i = 0; i <= c; ++i) a[pk8(i, c)] = D[c * 8 + i];
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      const int j = 8 * P + jj;
+      const double sj = a[pk8(jj, jj)];
+      if (j < n) {
+        if (!(sj > 0.0)) {
+          fs.pivot_index = j + off;
+          fs.pivot_value = sj;
+          bad = 1;
+          break;
+        }
+        smin = fmin(smin, sj);
       }
-      smin = fmin(smin, s);
+      const double r = rsqrt(sj);
+      a[pk8(jj, jj)] = sj * r;
+      inv[j] = r;
+#pragma unroll
+      for (int c = jj + 1; c < 8; ++c) a[pk8(jj, c)] *= r;
+#pragma unroll
+      for (int c = jj + 1; c < 8; ++c)
+#pragma unroll
+        for (int i = jj + 1; i <= c; ++i) a[pk8(i, c)] -= a[pk8(jj, i)] * a[pk8(jj, c)];
     }
-    // the unscaled row jj goes round before rsqrt(s) is known: the rank-1
-    // update is A(ii, c) -= A(jj, ii) A(jj, c) r^2 (r = rsqrt(s)), so only one
-    // multiply follows the rsqrt on the pivot-to-pivot path
-    double aji[8];
+    if (!bad) {
 #pragma unroll
-    for (int ii = jj + 1; ii < 8; ++ii) aji[ii] = __shfl_sync(0xffffffffu, d[jj], ii);   // A(jj, ii) from lane ii
-    const double r = rsqrt(s);
-    const double ajc = d[jj] * (r * r);
+      for (int c = 0; c < 8; ++c)
 #pragma unroll
-    for (int ii = jj + 1; ii < 8; ++ii)
-      if (c >= ii) d[ii] -= aji[ii] * ajc;
-    if (c > jj) d[jj] *= r;          // row jj, column c
-    if (c == jj) d[jj] = s * r;
-    if (lane == 0) inv[j] = r;
+        for (int i = 0; i <= c; ++i) D[c * 8 + i] = a[pk8(i, c)];
+    }
   }
-  if (lane < 8) {
-#pragma unroll
-    for (int r = 0; r < 8; ++r) D[c * 8 + r] = d[r];
-  }
+  bad = __shfl_sync(0xffffffffu, bad, 0);
   __syncwarp();
-  return 0;
+  return bad;
 }
 
 // Blocked right-looking Cholesky over block rows [0, nbr) of an nb x nb block
@@ -274,8 +280,14 @@ __device__ bool chol_blocked(double* Wb, int n, int nb, int P0, int nbr, int off
           Jb = I + rem;
         }
       };
-      for (int blk = warp; blk < nblk; blk += 2 * (FK_NW - 1)) {   // blk 0 is warp 0's
-        const int blk2 = blk + (FK_NW - 1);
+      // Workers: the 12 warps outside warp 0's SM sub-partition (warp % 4 != 0);
+      // warps 4, 8, 12 stay idle so their DMMAs do not contend for the FP64 pipe
+      // with warp 0's dependent pivot chain (it runs 2-3x slower otherwise).
+      // blk 0 is warp 0's.
+      constexpr int NWK = FK_NW - FK_NW / 4;
+      const int wk = warp - 1 - (warp >> 2);
+      for (int blk = ((warp & 3) ? 1 + wk : nblk); blk < nblk; blk += 2 * NWK) {
+        const int blk2 = blk + NWK;
         const bool two = blk2 < nblk;
         int I0, J0, I1 = 0, J1 = 0;
         decode(blk, I0, J0);
