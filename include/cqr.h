@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define CQR_ABI_VERSION 4
+#define CQR_ABI_VERSION 5
 
 #define CQR_OK 0
 #define CQR_EINVAL (-1)
@@ -175,6 +175,12 @@ size_t cqr_update_workspace_bytes(int64_t m, int q, int p);
 int cqr_update_pass(const double* Qin, int64_t ldqin, int q, double* Q, int64_t ldq, int p, int64_t m,
                     const double* Bt, int ldbt, const double* Rinv_tiles, int initial, double* Bt_next, double* G,
                     int ldg, void* ws, size_t ws_bytes, void* stream);
+/* Same pass reading the block from Q and writing Q' to Qout (iteration mode;
+ * Qout must not overlap Q), so the first iteration needs no copy of the
+ * caller's block (the reference copies it, algorithms.py:427). */
+int cqr_update_pass_to(const double* Qin, int64_t ldqin, int q, const double* Q, int64_t ldq, double* Qout,
+                       int64_t ldqout, int p, int64_t m, const double* Bt, int ldbt, const double* Rinv_tiles,
+                       int initial, double* Bt_next, double* G, int ldg, void* ws, size_t ws_bytes, void* stream);
 
 /* The k x k stage of one pass, one launch: forms X (G, or the deflated
  * G - Bt^T Bt for updates), measures ||X - I||_F, runs the policy's

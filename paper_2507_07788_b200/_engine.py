@@ -196,17 +196,19 @@ class Engine:
                 cx.timer.stop("apply", t0, (src.m_local, self.k))
             cx.launches += 1
 
-    def update_pass(self, q_in, qb, initial):
-        """Fused block-update pass (cqr_update_pass): Bt, G from Q_in and the
+    def update_pass(self, q_in, qb, initial, out=None):
+        """Fused block-update pass (cqr_update_pass_to): Bt, G from Q_in and the
         block; in iteration mode the block is first replaced by
-        (Q - Q_in Bt) R^-1 in place."""
+        (Q - Q_in Bt) R^-1, in place or written to `out`."""
         cx = self.cx
+        dst = qb if out is None else out
         ws = cx.workspace(cx.lib.cqr_update_workspace_bytes(qb.m_local, q_in.ncols, self.k), which=1)
         t0 = cx.timer.start() if cx.timer else None
-        _lib.check(cx.lib.cqr_update_pass(q_in.ptr(), q_in.ld, q_in.ncols, qb.ptr(), qb.ld, self.k, qb.m_local,
-                                          self.Bt.data_ptr(), q_in.ncols, self.Rinv.data_ptr(),
-                                          1 if initial else 0, self.Bt.data_ptr(), self.G.data_ptr(), self.k,
-                                          ws.data_ptr(), ws.numel(), cx.stream), "update_pass")
+        _lib.check(cx.lib.cqr_update_pass_to(q_in.ptr(), q_in.ld, q_in.ncols, qb.ptr(), qb.ld, dst.ptr(), dst.ld,
+                                             self.k, qb.m_local, self.Bt.data_ptr(), q_in.ncols,
+                                             self.Rinv.data_ptr(), 1 if initial else 0, self.Bt.data_ptr(),
+                                             self.G.data_ptr(), self.k, ws.data_ptr(), ws.numel(), cx.stream),
+                   "update_pass")
         if t0 is not None:
             cx.timer.stop("update_pass", t0, (qb.m_local, q_in.ncols, self.k, 1 if initial else 0))
         cx.launches += 2

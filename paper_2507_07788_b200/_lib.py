@@ -94,6 +94,7 @@ SIGNATURES = {
     "cqr_update_supported": (_I, [_I, _I]),
     "cqr_update_workspace_bytes": (_SZ, [_I64, _I, _I]),
     "cqr_update_pass": (_I, [_P, _I64, _I, _P, _I64, _I, _I64, _P, _I, _P, _I, _P, _P, _I, _P, _SZ, _P]),
+    "cqr_update_pass_to": (_I, [_P, _I64, _I, _P, _I64, _P, _I64, _I, _I64, _P, _I, _P, _I, _P, _P, _I, _P, _SZ, _P]),
     "cqr_factor_workspace_bytes": (_SZ, [_I]),
     "cqr_debug_factor_profile": (_I, [ctypes.POINTER(ctypes.c_ulonglong)]),
     "cqr_factor": (_I, [ctypes.POINTER(FactorConfig), _I, _P, _I, _P, _I, _I, _P, _P, _I, _P, _P, _I, _P, _P,

@@ -498,10 +498,13 @@ def chol_qr_update(q_in, r_in, a_new, cfg=None, ledger=None):
             _charge(ledger, "gemm", _flops.gemm_flops(m, p, p))
             _charge(ledger, "gemm", _flops.gemm_flops(p, k, p) + p * p)
         elif fused:
-            # one sweep: Q <- (Q - Q_in Bt) R^-1, Bt <- Q_in^T Q, G <- Q^T Q
+            # one sweep: Q <- (Q - Q_in Bt) R^-1, Bt <- Q_in^T Q, G <- Q^T Q; the
+            # first one reads the caller's block and writes a fresh Q (no copy)
             if q is None:
-                q = a_new.copy()
-            eng.update_pass(q_in, q, initial=False)
+                q = _fresh_like(a_new, p)
+                eng.update_pass(q_in, a_new, initial=False, out=q)
+            else:
+                eng.update_pass(q_in, q, initial=False)
             _charge(ledger, "gemm", _flops.gemm_flops(m, k, p))
             _charge(ledger, "gemm", m * p)
             _charge(ledger, "trtri", _flops.tri_inverse_flops(p))

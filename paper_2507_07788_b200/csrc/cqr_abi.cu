@@ -195,23 +195,42 @@ size_t cqr_update_workspace_bytes(int64_t m, int q, int p) {
   return q >= 1 ? cqr::update_pass_ws_bytes(cqr::round_up(m, 16), q) : 256;
 }
 
-int cqr_update_pass(const double* Qin, int64_t ldqin, int q, double* Q, int64_t ldq, int p, int64_t m,
-                    const double* Bt, int ldbt, const double* Rinv_tiles, int initial, double* Bt_next, double* G,
-                    int ldg, void* ws, size_t ws_bytes, void* stream) {
+int cqr_update_pass_to(const double* Qin, int64_t ldqin, int q, const double* Q, int64_t ldq, double* Qout,
+                       int64_t ldqout, int p, int64_t m, const double* Bt, int ldbt, const double* Rinv_tiles,
+                       int initial, double* Bt_next, double* G, int ldg, void* ws, size_t ws_bytes, void* stream) {
   if (!cqr::update_pass_supported(q, p)) return fail(CQR_EINVAL, "cqr_update_pass: needs 1 <= q <= 512, 1 <= p <= 16");
   int rc = check_tall(Qin, ldqin, m, q, "cqr_update_pass(Qin)");
   if (rc) return rc;
   rc = check_tall(Q, ldq, m, p, "cqr_update_pass(Q)");
   if (rc) return rc;
+  if (!initial) {
+    rc = check_tall(Qout, ldqout, m, p, "cqr_update_pass(Qout)");
+    if (rc) return rc;
+    if (Qout != Q && Qout != nullptr && Q != nullptr) {
+      // out of place: the output must not overlap the block it reads
+      const char* lo = reinterpret_cast<const char*>(Q);
+      const char* hi = lo + 8 * ((cqr::round_up(m, 16) / 4 - 1) * 4 * ldq + 4 * p);
+      const char* o = reinterpret_cast<const char*>(Qout);
+      if (o >= lo && o < hi) return fail(CQR_EINVAL, "cqr_update_pass: Qout overlaps Q (use Qout == Q for in place)");
+    }
+  }
   if (!initial && (Bt == nullptr || ldbt < q || Rinv_tiles == nullptr))
     return fail(CQR_EINVAL, "cqr_update_pass: iteration mode needs Bt (ldbt >= q) and R^-1 tiles");
   if (Bt_next == nullptr || G == nullptr || ldg < p) return fail(CQR_EINVAL, "cqr_update_pass: bad outputs");
   if (ws == nullptr || ws_bytes < cqr::update_pass_ws_bytes(cqr::round_up(m, 16), q))
     return fail(CQR_EINVAL, "cqr_update_pass: workspace too small");
-  return cuda_check(cqr::update_pass_launch(Qin, ldqin, q, Q, ldq, p, cqr::round_up(m, 16), Bt, ldbt, Rinv_tiles,
+  return cuda_check(cqr::update_pass_launch(Qin, ldqin, q, Q, ldq, initial ? const_cast<double*>(Q) : Qout,
+                                            initial ? ldq : ldqout, p, cqr::round_up(m, 16), Bt, ldbt, Rinv_tiles,
                                             initial, Bt_next, G, ldg, static_cast<double*>(ws),
                                             static_cast<cudaStream_t>(stream)),
                     "cqr_update_pass");
+}
+
+int cqr_update_pass(const double* Qin, int64_t ldqin, int q, double* Q, int64_t ldq, int p, int64_t m,
+                    const double* Bt, int ldbt, const double* Rinv_tiles, int initial, double* Bt_next, double* G,
+                    int ldg, void* ws, size_t ws_bytes, void* stream) {
+  return cqr_update_pass_to(Qin, ldqin, q, Q, ldq, Q, ldq, p, m, Bt, ldbt, Rinv_tiles, initial, Bt_next, G, ldg, ws,
+                            ws_bytes, stream);
 }
 
 int cqr_debug_factor_profile(unsigned long long* out16) { return cqr::factor_profile(out16); }

@@ -64,9 +64,9 @@ void set_fused(int on);
 // ------------------------------------------------------------- fused update pass (K3)
 bool update_pass_supported(int q, int p);
 size_t update_pass_ws_bytes(int64_t rows, int q);
-cudaError_t update_pass_launch(const double* Qin, int64_t ldqin, int q, double* Qb, int64_t ldqb, int p,
-                               int64_t rows, const double* Bt, int ldbt, const double* Rinv_tiles, int initial,
-                               double* Bt_next, double* G, int ldg, double* ws, cudaStream_t s);
+cudaError_t update_pass_launch(const double* Qin, int64_t ldqin, int q, const double* Qb, int64_t ldqb, double* Qo,
+                               int64_t ldqo, int p, int64_t rows, const double* Bt, int ldbt, const double* Rinv_tiles,
+                               int initial, double* Bt_next, double* G, int ldg, double* ws, cudaStream_t s);
 
 // ------------------------------------------------------------- k x k stage (K4)
 struct FactorArgs {

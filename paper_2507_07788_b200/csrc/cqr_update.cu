@@ -45,7 +45,8 @@ __host__ __device__ constexpr int up_fixed(int SR) {   // doubles before the rin
 
 struct UpdateArgs {
   const double* Qin; int64_t ldqin; int q;
-  double* Qb; int64_t ldqb; int p;        // block (updated in place unless initial)
+  const double* Qb; int64_t ldqb; int p;  // block read by the pass
+  double* Qo; int64_t ldqo;               // where Q' goes (iteration mode; may be Qb)
   int64_t rows;                           // multiple of 16
   const double* Bt; int ldbt;             // p x q as [n][k] (iteration mode)
   const double* Rinv;                     // p x p coefficient tiles (iteration mode)
@@ -207,7 +208,7 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(UpdateArgs a
             const int cc = 8 * nb + 2 * t + e;
             const bool v = cc < p;
             yd[(r >> 2) * 4 * UP_PB + 4 * cc + (r & 3)] = v ? c2[e] : 0.0;
-            if (v && r < nrows) a.Qb[((r0 + r) >> 2) * 4 * a.ldqb + 4 * cc + (r & 3)] = c2[e];
+            if (v && r < nrows) a.Qo[((r0 + r) >> 2) * 4 * a.ldqo + 4 * cc + (r & 3)] = c2[e];
           }
         }
       } else {
@@ -333,13 +334,14 @@ static cudaError_t launch_up(const UpdateArgs& a, int ctas, size_t smem, cudaStr
   return cudaGetLastError();
 }
 
-cudaError_t update_pass_launch(const double* Qin, int64_t ldqin, int q, double* Qb, int64_t ldqb, int p,
-                               int64_t rows, const double* Bt, int ldbt, const double* Rinv_tiles, int initial,
-                               double* Bt_next, double* G, int ldg, double* ws, cudaStream_t s) {
+cudaError_t update_pass_launch(const double* Qin, int64_t ldqin, int q, const double* Qb, int64_t ldqb, double* Qo,
+                               int64_t ldqo, int p, int64_t rows, const double* Bt, int ldbt, const double* Rinv_tiles,
+                               int initial, double* Bt_next, double* G, int ldg, double* ws, cudaStream_t s) {
   if (rows % 16) return cudaErrorInvalidValue;
   UpdateArgs a{};
   a.Qin = Qin; a.ldqin = ldqin; a.q = q;
   a.Qb = Qb; a.ldqb = ldqb; a.p = p;
+  a.Qo = Qo; a.ldqo = ldqo;
   a.rows = rows;
   a.Bt = Bt; a.ldbt = ldbt; a.Rinv = Rinv_tiles;
   a.initial = initial;

@@ -425,3 +425,46 @@ def _apply_gram_case(cq, _lib, Engine, m, k, inplace):
     ref_g = q.T @ q
     np.testing.assert_array_equal(g_dev, g_dev.T)
     assert np.max(np.abs(g_dev - ref_g)) <= 1e-12 * np.max(np.abs(ref_g)) * max(1.0, np.log2(m))
+
+
+@pytest.mark.parametrize("q,p,m", [(64, 16, 5000), (200, 16, 40016), (33, 7, 3001)])
+def test_update_pass_out_of_place_matches_in_place(q, p, m):
+    """cqr_update_pass_to (read the block, write Q' elsewhere) is bitwise the
+    in-place pass, and rejects an output that overlaps its input."""
+    cq = _cq()
+    import torch
+    from paper_2507_07788_b200 import _lib
+    from paper_2507_07788_b200._engine import Engine
+
+    rng = np.random.default_rng(q + p)
+    qin = cq.CudaVectorArray.from_numpy(np.linalg.qr(rng.standard_normal((m, q)))[0])
+    blk = cq.CudaVectorArray.from_numpy(rng.standard_normal((m, p)))
+    outs = [Engine(p, cq.AlgoConfig(), q=q) for _ in range(2)]
+    g = np.random.default_rng(1).standard_normal((p, p))
+    spd = g @ g.T + p * np.eye(p)
+    bt = 1e-2 * np.random.default_rng(2).standard_normal(outs[0].Bt.shape)
+    results = []
+    for mode, eng in zip(("in", "out"), outs):
+        eng.G.copy_(torch.from_numpy(spd))
+        assert eng.factor(_lib.POLICY_PLAIN, m, p).code == _lib.FACTORED
+        eng.Bt.copy_(torch.from_numpy(bt))
+        if mode == "in":
+            y = blk.copy()
+            eng.update_pass(qin, y, initial=False)
+        else:
+            y = cq.CudaVectorArray.zeros(blk.space, p)
+            eng.update_pass(qin, blk, initial=False, out=y)
+        results.append((y.to_numpy(), eng.Bt.cpu().numpy(), eng.G.cpu().numpy()))
+    for a_, b_ in zip(results[0], results[1]):
+        np.testing.assert_array_equal(a_, b_)
+    # the caller's block is untouched by the out-of-place pass
+    assert not np.array_equal(blk.to_numpy(), results[1][0])
+    eng = outs[1]
+    with pytest.raises(_lib.CqrError, match="overlaps"):
+        from paper_2507_07788_b200._device import ctx
+        cx = ctx()
+        ws = cx.workspace(cx.lib.cqr_update_workspace_bytes(blk.m_local, q, p), which=1)
+        _lib.check(cx.lib.cqr_update_pass_to(qin.ptr(), qin.ld, q, blk.ptr(), blk.ld, blk.ptr() + 8 * 4, blk.ld, p,
+                                             blk.m_local, eng.Bt.data_ptr(), q, eng.Rinv.data_ptr(), 0,
+                                             eng.Bt.data_ptr(), eng.G.data_ptr(), p, ws.data_ptr(), ws.numel(),
+                                             cx.stream), "update_pass")
