@@ -417,6 +417,85 @@ __device__ void store_packed(const double* W, int n, int off, double* Rk, int ld
 }
 
 constexpr int FK_PANEL = 32;
+constexpr int FK_BAND_K = 768;   // banded global path: the 32-row band fits in shared memory
+
+// 256 < k <= 768: right-looking Cholesky by 32-row bands with the working
+// matrix W (upper triangle, column-major k x k, L2 resident).  Per band:
+// stage rows [r0, r0+32) x cols [r0, k) in shared memory (band layout),
+// factor them with in-band rank-8 steps (chol_banded), write them to Rk, then
+// apply the rank-32 update to the trailing upper triangle of W with DMMA
+// (fragments of the band from shared memory, C read-modify-write in L2).
+__device__ bool chol_bands_global(double* W, int k, double* Wb, double* Rk, int ldr, double* inv, double& smin,
+                                  FState& fs, int* flag) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const LayoutBand4 band;
+  for (int r0 = 0; r0 < k; r0 += FK_PANEL) {
+    const int n = k - r0;                 // order of the remaining matrix
+    const int nb = (n + 7) >> 3;
+    const int nbr = min(4, nb);
+    for (int r = warp; r < 8 * nbr; r += FK_NW)
+      for (int c = r + lane; c < 8 * nb; c += 32) {
+        double x = (c == r) ? 1.0 : 0.0;   // identity padding past n
+        if (c < n && r < n) x = W[(int64_t)(r0 + c) * k + r0 + r];
+        Wb[band(r >> 3, c >> 3) + (c & 7) * 8 + (r & 7)] = x;
+      }
+    __syncthreads();
+    if (!chol_banded(Wb, n, nb, nbr, r0, inv, smin, fs, band, flag)) return false;
+    for (int r = warp; r < min(FK_PANEL, n); r += FK_NW)
+      for (int c = r + lane; c < n; c += 32)
+        Rk[(int64_t)(r0 + c) * ldr + r0 + r] = Wb[band(r >> 3, c >> 3) + (c & 7) * 8 + (r & 7)];
+    if (nb > 4) {
+      // trailing blocks (I, J), 4 <= I <= J < nb (band-relative), two per iteration
+      const int tn = nb - 4;
+      const int nblk = tn * (tn + 1) / 2;
+      auto decode = [&](int blk, int& I, int& J) {
+        J = (int)((sqrtf(8.0f * blk + 1.0f) - 1.0f) * 0.5f);
+        while ((J + 1) * (J + 2) / 2 <= blk) ++J;
+        while (J * (J + 1) / 2 > blk) --J;
+        I = 4 + blk - J * (J + 1) / 2;
+        J += 4;
+      };
+      for (int blk = warp; blk < nblk; blk += 2 * FK_NW) {
+        const int blk2 = blk + FK_NW;
+        const bool two = blk2 < nblk;
+        int I0, J0, I1 = 4, J1 = 4;
+        decode(blk, I0, J0);
+        if (two) decode(blk2, I1, J1);
+        // C fragment (row g, cols 2t, 2t+1) of block (I, J): W(r0 + 8I + g, r0 + 8J + 2t + e)
+        const int ri0 = 8 * I0 + g, ri1 = 8 * I1 + g;
+        double c0[2], c1[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int cj0 = 8 * J0 + 2 * t + e, cj1 = 8 * J1 + 2 * t + e;
+          c0[e] = (ri0 < n && cj0 < n) ? W[(int64_t)(r0 + cj0) * k + r0 + ri0] : 0.0;
+          c1[e] = (two && ri1 < n && cj1 < n) ? W[(int64_t)(r0 + cj1) * k + r0 + ri1] : 0.0;
+        }
+#pragma unroll
+        for (int P = 0; P < 4; ++P) {
+          const double* pa0 = Wb + band(P, I0) + g * 8 + t;
+          const double* pb0 = Wb + band(P, J0) + g * 8 + t;
+          const double* pa1 = Wb + band(P, I1) + g * 8 + t;
+          const double* pb1 = Wb + band(P, J1) + g * 8 + t;
+          const double a00 = -pa0[0], a01 = -pa0[4], b00 = pb0[0], b01 = pb0[4];
+          const double a10 = -pa1[0], a11 = -pa1[4], b10 = pb1[0], b11 = pb1[4];
+          dmma(c0, a00, b00);
+          dmma(c1, a10, b10);
+          dmma(c0, a01, b01);
+          dmma(c1, a11, b11);
+        }
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int cj0 = 8 * J0 + 2 * t + e, cj1 = 8 * J1 + 2 * t + e;
+          if (ri0 < n && cj0 < n && ri0 <= cj0) W[(int64_t)(r0 + cj0) * k + r0 + ri0] = c0[e];
+          if (two && ri1 < n && cj1 < n && ri1 <= cj1) W[(int64_t)(r0 + cj1) * k + r0 + ri1] = c1[e];
+        }
+      }
+    }
+    __syncthreads();   // W updates (global, this CTA) and the band area before the next band
+  }
+  return true;
+}
 
 
 __device__ __forceinline__ void fmark(int slot) {
@@ -449,6 +528,16 @@ __device__ __noinline__ bool chol_attempt(const double* __restrict__ X, int k, d
     const int nb = (k + 7) >> 3;
     ok = chol_banded(Wb, k, nb, nb, 0, rowbuf, smin, fs, LayoutUpper(), flag);
     if (ok) store_blocked(Wb, k, 0, Rk, ldr);
+  } else if (k > FK_BIG_K && k <= FK_BAND_K) {
+    double* W = gW;   // k x k upper (column-major): X + sigma I, factored in place by bands
+    for (int c = warp; c < k; c += FK_NW)
+      for (int i = lane; i <= c; i += 32) {
+        double x = X[(int64_t)c * k + i];
+        if (i == c) x = __dadd_rn(x, sigma);
+        W[(int64_t)c * k + i] = x;
+      }
+    __syncthreads();
+    ok = chol_bands_global(W, k, smem_w, Rk, ldr, rowbuf, smin, fs, flag);
   } else if (k > FK_BIG_K) {
     double* W = gW;
     for (int c = warp; c < k; c += FK_NW)
@@ -1106,6 +1195,8 @@ cudaError_t factor_launch(FactorArgs& a, cudaStream_t stream) {
   } else if (a.k <= FK_BIG_K) {
     const int n = a.k - FK_PANEL;
     smem += (size_t)std::max<int64_t>((int64_t)FK_PANEL * a.k, blocked(n)) * sizeof(double);
+  } else if (a.k <= FK_BAND_K) {
+    smem += (size_t)FK_PANEL * kpad * sizeof(double);   // one 32-row band
   }
   static bool attr_set = false;
   if (!attr_set) {

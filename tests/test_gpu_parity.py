@@ -468,3 +468,47 @@ def test_update_pass_out_of_place_matches_in_place(q, p, m):
                                              blk.m_local, eng.Bt.data_ptr(), q, eng.Rinv.data_ptr(), 0,
                                              eng.Bt.data_ptr(), eng.G.data_ptr(), p, ws.data_ptr(), ws.numel(),
                                              cx.stream), "update_pass")
+
+
+@pytest.mark.parametrize("k", [264, 384, 520, 800])
+def test_wide_chol_qr2_matches_oracle(k):
+    """Widths past 256: the banded L2 factorization (256 < k <= 768) and the
+    packed fallback (k > 768) against the oracle on a well-conditioned block."""
+    cq = _cq()
+    from oracle import cholqr_oracle as co
+
+    m = 3 * k + 17
+    x = np.random.default_rng(k).standard_normal((m, k))
+    res = cq.chol_qr2(cq.CudaVectorArray.from_numpy(x))
+    ref = co.chol_qr2(x)
+    assert np.max(np.abs(res.r - ref.r)) <= 1e-10 * np.max(np.abs(ref.r))
+    np.testing.assert_array_equal(np.tril(res.r, -1), 0.0)
+    loo = cq.loss_of_orthogonality(res.q, norm="frobenius")
+    assert P.within10(loo, co.loo_fro(ref.q), k)
+
+
+def test_wide_rs_chol_qr_shifts_match_oracle():
+    """k = 384 with kappa = 1e10: shifted passes through the banded factor."""
+    cq = _cq()
+    from oracle import cholqr_oracle as co
+    from oracle import matgen_oracle as mg
+
+    k, m = 384, 3000
+    rng = np.random.default_rng(7)
+    u = np.linalg.qr(rng.standard_normal((m, k)))[0]
+    v = np.linalg.qr(rng.standard_normal((k, k)))[0]
+    x = (u * np.logspace(0, -10, k)) @ v
+    res = cq.rs_chol_qr(cq.CudaVectorArray.from_numpy(x))
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        ref = co.rs_chol_qr(x, co.default_cfg())
+    tol = cq.AlgoConfig().effective_tol(k)
+    n = P.compare_iterated(res, ref, k, tol)
+    diverged = tol if (n < max(len(ref.shift_attempts), len(res.shift_attempts))
+                       or res.iterations != ref.iterations) else None
+    assert res.success == ref.success
+    loo = cq.loss_of_orthogonality(res.q, norm="frobenius")
+    rrr = cq.reconstruction_residual(cq.CudaVectorArray.from_numpy(x), res.q, res.r, norm="frobenius")
+    assert P.within10(loo, co.loo_fro(ref.q), k, diverged)
+    assert P.within10(rrr, co.rrr_fro(x, ref.q, ref.r), k, diverged)
+    assert sum(res.shift_attempts) >= 1   # the shifted attempts ran through the banded path

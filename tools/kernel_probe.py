@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--only", default="all")
     ap.add_argument("--shifted", action="store_true", help="factor a rank-deficient Gram (shift path)")
     ap.add_argument("--q", type=int, default=256, help="basis width for --only update")
+    ap.add_argument("--fk", default="64,128,256", help="widths for --only factor")
     a = ap.parse_args()
     import paper_2507_07788_b200 as cq
     from paper_2507_07788_b200 import _lib
@@ -93,7 +94,7 @@ def main():
         out["trmm_ms"] = ms
         out["trmm_tfs"] = flops / ms / 1e9
     if a.only in ("all", "factor"):
-        for kk in (64, 128, 256):
+        for kk in [int(v) for v in a.fk.split(",")]:
             e2 = Engine(kk, cq.AlgoConfig())
             g = torch.randn((kk, kk), dtype=torch.float64, device="cuda")
             spd = g @ g.T + kk * torch.eye(kk, dtype=torch.float64, device="cuda")
