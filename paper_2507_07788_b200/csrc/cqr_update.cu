@@ -33,7 +33,7 @@ namespace cqr {
 constexpr int UP_MAXQ = 512;
 constexpr int UP_PB = 16;                 // padded block width
 constexpr int UP_THREADS = 512;           // 8 projection + 8 cross-Gram warps
-constexpr int UP_YS = 2;                  // Q' ring slots
+constexpr int UP_YS = 4;                  // Q' ring slots
 constexpr int UP_MAXNS = 8;               // TMA ring stages (at most)
 
 // SR = rows per sub-panel (16 or 32): 32 halves the per-row cost of the
