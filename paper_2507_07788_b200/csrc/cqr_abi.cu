@@ -275,6 +275,15 @@ int cqr_factor(const cqr_factor_config* cfg, int k, const double* G, int ldg, co
   a.X = w;
   a.W = w + (size_t)k * k;
   a.Ri = a.W + (size_t)k * (k + 1) / 2;
+  {
+    const size_t ldr1 = (size_t)cqr::round_up(k, 32);
+    double* x = a.Ri + (size_t)k * (k + 1) / 2;
+    a.Rk1 = x; a.ldr1 = (int)ldr1; x += (size_t)k * ldr1;
+    a.W1 = x; x += (size_t)k * (k + 1);
+    a.shifts1 = x; x += 1024;
+    a.pub = x;
+    a.spec = (cfg->policy == CQR_POLICY_RECOMPUTE && cfg->max_shift_attempts < 1000) ? 1 : 0;
+  }
   a.Rk = Rk; a.Rinv = Rinv; a.ldr = ldr;
   a.Racc = Racc;
   a.B = B; a.ldb = ldb;

@@ -88,6 +88,11 @@ struct FactorArgs {
   double* B; int ldb;
   double* shifts;
   cqr_factor_status* st;
+  // speculative shifted branch (RECOMPUTE policy): a second CTA runs the
+  // estimate + shifted attempts into private buffers while CTA 0 tries the
+  // plain factorization; CTA 0 publishes its outcome in `pub` (epoch-tagged)
+  int spec; unsigned epoch;
+  double* Rk1; int ldr1; double* W1; double* shifts1; double* pub;
 };
 cudaError_t factor_launch(FactorArgs& a, cudaStream_t stream);
 size_t factor_workspace_bytes(int k);
