@@ -99,7 +99,20 @@ __device__ __forceinline__ double shift_value(int64_t m, int64_t w, double norm,
 struct FState {
   int code, retries, n_shifts, pivot_index, est_calls, est_flag, escalations, singular_index, attempts;
   double pivot_value, err, norm_est, last_shift, min_pivot_rel, sigma, plain_margin, diag_max, min_pivot;
+  // speculative CTA: the flag CTA 0 publishes and the value meaning "plain attempt held"
+  const volatile unsigned long long* spec_flag;
+  unsigned long long spec_done;
+  int aborted;
 };
+
+// Speculative CTA only: has CTA 0's plain attempt already succeeded?  Polled at
+// band boundaries (all threads must call it; it holds a barrier).
+__device__ bool spec_should_stop(FState& fs) {
+  if (fs.spec_flag == nullptr) return false;
+  if (threadIdx.x == 0 && !fs.aborted && *fs.spec_flag == fs.spec_done) fs.aborted = 1;
+  __syncthreads();
+  return fs.aborted != 0;
+}
 
 // Unblocked right-looking Cholesky of the packed upper n x n matrix W (already
 // loaded).  Pivot indices are reported offset by `off`; `smin` carries the
@@ -383,6 +396,7 @@ __device__ bool chol_banded(double* Wb, int n, int nb, int nbr, int off, double*
                             Lay lay, int* flag) {
   for (int P0 = 0; P0 < nbr; P0 += 4) {
     const int P1 = min(nbr, P0 + 4);
+    if (spec_should_stop(fs)) return false;
     if (!chol_blocked(Wb, n, nb, P0, P1, off, inv, smin, fs, lay, flag)) return false;
     if (P1 < nbr) {
       band_trailing_update(Wb, nb, P0, P1, lay);
@@ -573,6 +587,7 @@ __device__ __noinline__ bool chol_attempt(const double* __restrict__ X, int k, d
         for (int c = r + lane; c < k; c += 32) Rk[(int64_t)c * ldr + r] = Wb[band(r >> 3, c >> 3) + (c & 7) * 8 + (r & 7)];
       __syncthreads();
       fmark(3);
+      if (spec_should_stop(fs)) return false;
       // ---- stage 2: S = X22 - R12^T R12 (block upper, n = k - 32) with DMMA,
       // fragments of R12 read from Rk (L2); S overwrites the band area
       const int n = k - b;
@@ -731,6 +746,11 @@ __global__ void __launch_bounds__(FK_THREADS, 1) factor_kernel(FactorArgs a) {
     fs.est_flag = 0; fs.escalations = 0; fs.singular_index = -1;
     fs.pivot_value = 0.0; fs.err = 0.0; fs.norm_est = 0.0; fs.last_shift = 0.0; fs.min_pivot_rel = 0.0;
     fs.sigma = 0.0; fs.attempts = 0; fs.plain_margin = 0.0; fs.diag_max = 0.0; fs.min_pivot = 0.0;
+    fs.spec_flag = nullptr; fs.spec_done = 0; fs.aborted = 0;
+    if (a.spec && blockIdx.x == 1) {
+      fs.spec_flag = reinterpret_cast<const volatile unsigned long long*>(a.pub);
+      fs.spec_done = (0xC9F0A5ull << 40) | ((unsigned long long)a.epoch << 2) | 1ull;
+    }
   }
 
   if (tid == 0 && blockIdx.x == 0) { g_fprof[9] = 0; g_fprof[10] = 0; g_fprof[11] = 0; g_fprof[12] = 0; }
@@ -842,6 +862,7 @@ __global__ void __launch_bounds__(FK_THREADS, 1) factor_kernel(FactorArgs a) {
         const double est = norm_estimate(X, k, a.est_tol, a.est_max_iter, vec, wv, red, fs);
         __syncthreads();
         if (fs.code == CQR_ASYMMETRIC) { done = true; break; }
+        if (spec_should_stop(fs)) { done = true; break; }
         sigma = shift_value(a.m_global, a.shift_width, est, a.u);
         if (tid == 0) { fs.est_calls = 1; fs.norm_est = est; }
         int retries = 0, nsh = 0;
@@ -856,6 +877,7 @@ __global__ void __launch_bounds__(FK_THREADS, 1) factor_kernel(FactorArgs a) {
           ++nsh;
           ok = chol_attempt(X, k, sigma, Wsm, gWx, Rkx, ldrx, rowbuf, fs, &sflag);
           if (ok) break;
+          if (fs.aborted) { done = true; break; }   // speculative CTA: the plain attempt held
           if (tid == 0) fs.escalations += 1;
           sigma = py_max(a.esc * sigma, u2);
         }
@@ -1011,6 +1033,8 @@ __global__ void __launch_bounds__(FF_WARPS * 32) factor_finish_kernel(FactorArgs
   if (a.st->code != CQR_FACTORED) return;
   const int k = a.k;
   const int J = blockIdx.x;
+  const bool prof = (J == (int)gridDim.x - 1 && threadIdx.x == 0);   // the longest column block
+  long long fc0 = prof ? clock64() : 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int ldr = a.ldr;
@@ -1039,37 +1063,59 @@ __global__ void __launch_bounds__(FF_WARPS * 32) factor_finish_kernel(FactorArgs
   if (a.accumulate) {
     for (int I = warp; I <= J; I += FF_WARPS, ++nmine) {
       double c2[2] = {0.0, 0.0};
-      for (int L = I; L <= J; ++L) {
+      const int ra = 8 * I + g;
+      // Rk(I, L) fragments come from L2: load 4 L steps at once so the
+      // latencies overlap (the DMMA order over L is unchanged)
+      for (int L0 = I; L0 <= J; L0 += 4) {
+        double av[4][2];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int ra = 8 * I + g, ca = 8 * L + t + 4 * h;
-          const double av = (ra < k && ca < k) ? R[(int64_t)ca * ldr + ra] : ((ra == ca) ? 1.0 : 0.0);
-          const double bv = sOld[8 * L + t + 4 * h][g];
-          dmma(c2, av, bv);
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int L = L0 + j, ca = 8 * L + t + 4 * h;
+            av[j][h] = (L <= J) ? ((ra < k && ca < k) ? R[(int64_t)ca * ldr + ra] : ((ra == ca) ? 1.0 : 0.0)) : 0.0;
+          }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int L = L0 + j;
+          if (L > J) break;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) dmma(c2, av[j][h], sOld[8 * L + t + 4 * h][g]);
         }
       }
       accs[nmine][0] = c2[0];
       accs[nmine][1] = c2[1];
     }
   }
+  if (prof) g_fprof[13] = (unsigned long long)(clock64() - fc0);
   // ---- inverses of the diagonal blocks I <= J (warp per block, lanes 0..7 one column each)
-  for (int I = warp; I <= J; I += FF_WARPS) {
-    if (lane < 8) {
-      // column cl of inv(R_II): back substitution R_II x = e_cl
-      double x[8];
-      const int cl = lane;
+  // all 32 lanes: lane = 8 * sub + cl handles block I = warp + 8 (4 i + sub)
+  // column cl (four blocks per warp at once); the 8 diagonal reciprocals are
+  // independent divisions, so the substitution chain itself is FMA only
+  for (int I0 = warp; I0 <= J; I0 += 4 * FF_WARPS) {
+    const int I = I0 + FF_WARPS * (lane >> 3);
+    const int cl = lane & 7;
+    if (I <= J) {
+      double rr[8][8];   // R_II(r, l), upper part
+      double dinv[8];
 #pragma unroll
-      for (int r = 7; r >= 0; --r) {
-        double s = (r == cl) ? 1.0 : 0.0;
+      for (int r = 0; r < 8; ++r) {
 #pragma unroll
         for (int l = r + 1; l < 8; ++l) {
           const int ri = 8 * I + r, cj = 8 * I + l;
-          const double rv = (ri < k && cj < k) ? R[(int64_t)cj * ldr + ri] : 0.0;
-          s -= rv * x[l];
+          rr[r][l] = (ri < k && cj < k) ? R[(int64_t)cj * ldr + ri] : 0.0;
         }
         const int di = 8 * I + r;
-        const double dv = (di < k) ? R[(int64_t)di * ldr + di] : 1.0;
-        x[r] = (r <= cl) ? s / dv : 0.0;
+        dinv[r] = 1.0 / ((di < k) ? R[(int64_t)di * ldr + di] : 1.0);
+      }
+      // column cl of inv(R_II): back substitution R_II x = e_cl
+      double x[8];
+#pragma unroll
+      for (int r = 7; r >= 0; --r) {
+        double sacc = (r == cl) ? 1.0 : 0.0;
+#pragma unroll
+        for (int l = r + 1; l < 8; ++l) sacc -= rr[r][l] * x[l];
+        x[r] = (r <= cl) ? sacc * dinv[r] : 0.0;
       }
 #pragma unroll
       for (int r = 0; r < 8; ++r) sInv[I][cl * 8 + r] = x[r];
@@ -1100,6 +1146,7 @@ __global__ void __launch_bounds__(FF_WARPS * 32) factor_finish_kernel(FactorArgs
       }
     }
   };
+  if (prof) g_fprof[14] = (unsigned long long)(clock64() - fc0);
   double cur[4][2], nxt[4][2];
   load_row(J, cur);
   for (int I = J; I >= 0; --I) {
@@ -1148,6 +1195,7 @@ __global__ void __launch_bounds__(FF_WARPS * 32) factor_finish_kernel(FactorArgs
     }
     __syncthreads();
   }
+  if (prof) g_fprof[15] = (unsigned long long)(clock64() - fc0);
   (void)KP;
 }
 

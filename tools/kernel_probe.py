@@ -111,6 +111,8 @@ def main():
             t0 = buf[0]
             out[f"factor_k{kk}_phases_us"] = [round((buf[i] - t0) / 1e3, 1) if buf[i] >= t0 else None for i in range(7)]
             out[f"factor_k{kk}_est_iters"] = int(buf[8]) if buf[8] < 1000 else None
+            out[f"factor_k{kk}_finish_cycles"] = {"racc": int(buf[13]), "diag_inv": int(buf[14]),
+                                                   "backsub_end": int(buf[15])}
             if buf[11]:
                 out[f"factor_k{kk}_step_cycles"] = {"steps": int(buf[11]), "solve": int(buf[9] // buf[11]),
                                                     "update": int(buf[10] // buf[11]),
