@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define CQR_ABI_VERSION 5
+#define CQR_ABI_VERSION 6
 
 #define CQR_OK 0
 #define CQR_EINVAL (-1)
@@ -59,6 +59,7 @@ extern "C" {
 #define CQR_TRI_SINGULAR 5 /* TriangularSingularError (kernels.py:42-47,94-99)        */
 #define CQR_ASYMMETRIC 6   /* ValueError of spectral_norm_estimate (kernels.py:148-153) */
 #define CQR_ESTIMATED 7    /* CQR_POLICY_ESTIMATE: norm_est / est_flag written only     */
+#define CQR_SKIPPED 8      /* gated off: cfg.gate pointed at a status that is not FACTORED */
 
 /* cqr_factor_config.policy: which reference factorization rule runs */
 #define CQR_POLICY_PLAIN 0      /* cholesky(x)                       algorithms.py:209-210 */
@@ -87,6 +88,9 @@ typedef struct cqr_factor_config {
   int32_t est_max_iter;       /* power-iteration cap (100, kernels.py:126)           */
   double est_tol;             /* power-iteration settling tolerance (1e-2)           */
   double fixed_shift;         /* CQR_POLICY_FIXED_SHIFT: the shift                   */
+  const int32_t* gate;        /* NULL, or the code field of an earlier pass's status in
+                                 device memory: unless it is CQR_FACTORED the launch only
+                                 writes code = CQR_SKIPPED (lets a host loop run ahead) */
 } cqr_factor_config;
 
 typedef struct cqr_factor_status {
@@ -162,6 +166,13 @@ int cqr_apply_gram_launches(int k);
 int cqr_apply_gram_inplace_ok(int k);
 int cqr_apply_gram(const double* X, int64_t ldx, int64_t m, int k, const double* Rinv_tiles, double* Q,
                    int64_t ldq, double* G, int ldg, void* ws, size_t ws_bytes, void* stream);
+/* Same, as a no-op on the device unless *gate == CQR_FACTORED (gate: the code
+ * field of the factor status this pass applies; NULL = always run).  With the
+ * gated factor (cqr_factor_config.gate) a host loop can enqueue pass i+1
+ * before reading pass i's status. */
+int cqr_apply_gram_gated(const double* X, int64_t ldx, int64_t m, int k, const double* Rinv, double* Q,
+                         int64_t ldq, double* G, int ldg, void* ws, size_t ws_bytes, const int32_t* gate,
+                         void* stream);
 
 /* Fused block-update pass (Alg. 2, p <= 16, 1 <= q <= 512), one sweep over
  * the rows with Q_in read from HBM once:
@@ -181,6 +192,11 @@ int cqr_update_pass(const double* Qin, int64_t ldqin, int q, double* Q, int64_t 
 int cqr_update_pass_to(const double* Qin, int64_t ldqin, int q, const double* Q, int64_t ldq, double* Qout,
                        int64_t ldqout, int p, int64_t m, const double* Bt, int ldbt, const double* Rinv_tiles,
                        int initial, double* Bt_next, double* G, int ldg, void* ws, size_t ws_bytes, void* stream);
+/* cqr_update_pass_to gated like cqr_apply_gram_gated. */
+int cqr_update_pass_gated(const double* Qin, int64_t ldqin, int q, const double* Q, int64_t ldq, double* Qout,
+                          int64_t ldqout, int p, int64_t m, const double* Bt, int ldbt, const double* Rinv_tiles,
+                          int initial, double* Bt_next, double* G, int ldg, void* ws, size_t ws_bytes,
+                          const int32_t* gate, void* stream);
 
 /* The k x k stage of one pass, one launch: forms X (G, or the deflated
  * G - Bt^T Bt for updates), measures ||X - I||_F, runs the policy's

@@ -107,15 +107,20 @@ class KernelTimer:
         e.record()
         return e
 
-    def stop(self, name, start, work=None):
+    def stop(self, name, start, work=None, gate=None):
+        """`gate`: the device status slot a gated launch depended on; a copy of
+        its code is kept so launches the device skipped are left out."""
         e = torch.cuda.Event(enable_timing=True)
         e.record()
-        self.events.append((name, start, e, work))
+        code = gate[:4].clone() if gate is not None else None
+        self.events.append((name, start, e, work, code))
 
     def summary(self):
         torch.cuda.synchronize()
         out = {}
-        for name, s, e, work in self.events:
+        for name, s, e, work, code in self.events:
+            if code is not None and int(code.view(torch.int32).item()) != 0:
+                continue   # gated off on the device (the pass after convergence)
             d = out.setdefault(name, {"ms": [], "work": []})
             d["ms"].append(s.elapsed_time(e))
             d["work"].append(work)

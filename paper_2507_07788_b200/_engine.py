@@ -114,6 +114,7 @@ class Engine:
         self.stat_host_all = cx.acquire_pinned((self.nslots, nbytes))
         self.stat, self.stat_host = self.stat_all[0], self.stat_host_all[0]
         self._next_slot = 0
+        self._stat_ev = [None] * self.nslots   # event after each slot's status copy
         self.fws = torch.empty(cx.lib.cqr_factor_workspace_bytes(k), dtype=torch.uint8, device=dev)
         if q:
             self.B = torch.zeros((k, q), dtype=torch.float64, device=dev)     # (p, q): column-major q x p
@@ -135,9 +136,20 @@ class Engine:
                               fixed_shift=fixed_shift)
         return self.collect([h])[0]
 
+    def gate(self, handle):
+        """Device address of the status code of an enqueued factor call: the
+        gate of the launches that must only run if that call factored."""
+        return self.stat_all[handle].data_ptr()
+
     def collect(self, handles):
-        """Statuses of enqueued factor calls, in order, after one stream sync."""
-        torch.cuda.current_stream(self.cx.device).synchronize()
+        """Statuses of enqueued factor calls, in order: waits only for their own
+        status copies, so later enqueued work keeps the GPU busy meanwhile."""
+        for h in handles:
+            ev = self._stat_ev[h]
+            if ev is None:
+                torch.cuda.current_stream(self.cx.device).synchronize()
+            else:
+                ev.synchronize()
         out = []
         for h in handles:
             raw = self.stat_host_all[h].numpy()
@@ -145,7 +157,7 @@ class Engine:
         return out
 
     def factor_async(self, policy, m_global, width, *, tol=0.0, check_tol=False, stop=False, update_b=False,
-                     fixed_shift=0.0):
+                     fixed_shift=0.0, gate=None, gate_slot=None):
         """Enqueue the k x k stage; its status lands in a pinned host slot
         (returned handle) without a sync.  Up to `nslots` calls may be pending."""
         cx = self.cx
@@ -156,7 +168,7 @@ class Engine:
             policy=policy, shift_width=width, m_global=m_global, unit_roundoff=cfg.unit_roundoff,
             shift_escalation=cfg.shift_escalation, max_shift_attempts=cfg.max_shift_attempts,
             check_tol=1 if check_tol else 0, tol=tol, stop=1 if stop else 0, accumulate=1,
-            update_b=1 if update_b else 0, est_max_iter=100, est_tol=1e-2, fixed_shift=fixed_shift)
+            update_b=1 if update_b else 0, est_max_iter=100, est_tol=1e-2, fixed_shift=fixed_shift, gate=gate)
         bt = self.Bt.data_ptr() if self.Bt is not None else None
         b = self.B.data_ptr() if self.B is not None else None
         base = self.stat_all[slot].data_ptr()
@@ -166,37 +178,45 @@ class Engine:
                                      self.Racc.data_ptr(), b, max(self.q, 1), base + STATUS_BYTES, base,
                                      self.fws.data_ptr(), self.fws.numel(), cx.stream), "factor")
         if t0 is not None:
-            cx.timer.stop("factor", t0, (self.k,))
+            cx.timer.stop("factor", t0, (self.k,),
+                          gate=self.stat_all[gate_slot] if gate_slot is not None else None)
         cx.launches += 2
         self.stat_host_all[slot].copy_(self.stat_all[slot], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(cx.device))
+        self._stat_ev[slot] = ev
         return slot
 
     # ------------------------------------------------------------ tall passes
     def gram(self, arr):
         gram_device(arr, self.G)
 
-    def apply(self, src, dst, with_gram=True):
-        """dst = src R^-1 (TRMM); with_gram also forms G = dst^T dst."""
+    def apply(self, src, dst, with_gram=True, gate=None, gate_slot=None):
+        """dst = src R^-1 (TRMM); with_gram also forms G = dst^T dst.  With a
+        gate (Engine.gate of a factor call) the device skips it unless that
+        call factored."""
         cx = self.cx
         t0 = cx.timer.start() if cx.timer else None
         if with_gram:
             ws = cx.workspace(cx.lib.cqr_apply_gram_workspace_bytes(src.m_local, self.k))
-            _lib.check(cx.lib.cqr_apply_gram(src.ptr(), src.ld, src.m_local, self.k, self.Rinv.data_ptr(),
-                                             dst.ptr(), dst.ld, self.G.data_ptr(), self.k,
-                                             ws.data_ptr(), ws.numel(), cx.stream), "apply_gram")
+            _lib.check(cx.lib.cqr_apply_gram_gated(src.ptr(), src.ld, src.m_local, self.k, self.Rinv.data_ptr(),
+                                                   dst.ptr(), dst.ld, self.G.data_ptr(), self.k,
+                                                   ws.data_ptr(), ws.numel(), gate, cx.stream), "apply_gram")
             cx.launches += cx.lib.cqr_apply_gram_launches(self.k)
             if t0 is not None:
-                cx.timer.stop("apply_gram", t0, (src.m_local, self.k))
+                cx.timer.stop("apply_gram", t0, (src.m_local, self.k),
+                              gate=self.stat_all[gate_slot] if gate_slot is not None else None)
             if cx.world > 1:
                 cx.allreduce_(self.G)
         else:
+            assert gate is None, "gated TRMM without Gram is not needed by any schedule"
             _lib.check(cx.lib.cqr_lincomb(src.ptr(), src.ld, src.m_local, self.k, self.Rinv.data_ptr(),
                                           self.k, 1, dst.ptr(), dst.ld, cx.stream), "apply")
             if t0 is not None:
                 cx.timer.stop("apply", t0, (src.m_local, self.k))
             cx.launches += 1
 
-    def update_pass(self, q_in, qb, initial, out=None):
+    def update_pass(self, q_in, qb, initial, out=None, gate=None):
         """Fused block-update pass (cqr_update_pass_to): Bt, G from Q_in and the
         block; in iteration mode the block is first replaced by
         (Q - Q_in Bt) R^-1, in place or written to `out`."""
@@ -204,10 +224,11 @@ class Engine:
         dst = qb if out is None else out
         ws = cx.workspace(cx.lib.cqr_update_workspace_bytes(qb.m_local, q_in.ncols, self.k), which=1)
         t0 = cx.timer.start() if cx.timer else None
-        _lib.check(cx.lib.cqr_update_pass_to(q_in.ptr(), q_in.ld, q_in.ncols, qb.ptr(), qb.ld, dst.ptr(), dst.ld,
-                                             self.k, qb.m_local, self.Bt.data_ptr(), q_in.ncols,
-                                             self.Rinv.data_ptr(), 1 if initial else 0, self.Bt.data_ptr(),
-                                             self.G.data_ptr(), self.k, ws.data_ptr(), ws.numel(), cx.stream),
+        _lib.check(cx.lib.cqr_update_pass_gated(q_in.ptr(), q_in.ld, q_in.ncols, qb.ptr(), qb.ld, dst.ptr(),
+                                                dst.ld, self.k, qb.m_local, self.Bt.data_ptr(), q_in.ncols,
+                                                self.Rinv.data_ptr(), 1 if initial else 0, self.Bt.data_ptr(),
+                                                self.G.data_ptr(), self.k, ws.data_ptr(), ws.numel(), gate,
+                                                cx.stream),
                    "update_pass")
         if t0 is not None:
             cx.timer.stop("update_pass", t0, (qb.m_local, q_in.ncols, self.k, 1 if initial else 0))

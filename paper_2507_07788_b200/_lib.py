@@ -18,7 +18,7 @@ CQR_OK = 0
 CQR_EINVAL = -1
 CQR_ECUDA = -2
 
-FACTORED, CONVERGED, CAPPED, BREAKDOWN, SHIFT_LIMIT, TRI_SINGULAR, ASYMMETRIC, ESTIMATED = range(8)
+FACTORED, CONVERGED, CAPPED, BREAKDOWN, SHIFT_LIMIT, TRI_SINGULAR, ASYMMETRIC, ESTIMATED, SKIPPED = range(9)
 POLICY_PLAIN, POLICY_SHIFT_ONCE, POLICY_RECOMPUTE, POLICY_UPDATE, POLICY_FIXED_SHIFT, POLICY_ESTIMATE = range(6)
 
 c_double_p = ctypes.c_void_p  # device pointers are passed as integers
@@ -42,6 +42,7 @@ class FactorConfig(ctypes.Structure):
         ("est_max_iter", ctypes.c_int32),
         ("est_tol", ctypes.c_double),
         ("fixed_shift", ctypes.c_double),
+        ("gate", ctypes.c_void_p),
     ]
 
 
@@ -91,10 +92,13 @@ SIGNATURES = {
     "cqr_apply_gram_launches": (_I, [_I]),
     "cqr_apply_gram_inplace_ok": (_I, [_I]),
     "cqr_apply_gram": (_I, [_P, _I64, _I64, _I, _P, _P, _I64, _P, _I, _P, _SZ, _P]),
+    "cqr_apply_gram_gated": (_I, [_P, _I64, _I64, _I, _P, _P, _I64, _P, _I, _P, _SZ, _P, _P]),
     "cqr_update_supported": (_I, [_I, _I]),
     "cqr_update_workspace_bytes": (_SZ, [_I64, _I, _I]),
     "cqr_update_pass": (_I, [_P, _I64, _I, _P, _I64, _I, _I64, _P, _I, _P, _I, _P, _P, _I, _P, _SZ, _P]),
     "cqr_update_pass_to": (_I, [_P, _I64, _I, _P, _I64, _P, _I64, _I, _I64, _P, _I, _P, _I, _P, _P, _I, _P, _SZ, _P]),
+    "cqr_update_pass_gated": (_I, [_P, _I64, _I, _P, _I64, _P, _I64, _I, _I64, _P, _I, _P, _I, _P, _P, _I, _P, _SZ,
+                                   _P, _P]),
     "cqr_factor_workspace_bytes": (_SZ, [_I]),
     "cqr_debug_factor_profile": (_I, [ctypes.POINTER(ctypes.c_ulonglong)]),
     "cqr_factor": (_I, [ctypes.POINTER(FactorConfig), _I, _P, _I, _P, _I, _I, _P, _P, _I, _P, _P, _I, _P, _P,

@@ -317,7 +317,14 @@ def rs_chol_qr(a, cfg=None, ledger=None):
     (algorithms.py:320-355): plain attempt first; on breakdown the shift is
     re-derived from the current Gramian's norm estimate and escalated until
     the shifted factorization succeeds.  Stops when ||Q^T Q - I||_F < tol;
-    the iteration cap returns success=False with the last distance."""
+    the iteration cap returns success=False with the last distance.
+
+    Host loop one pass ahead of the device: pass i+1 (factor, then TRMM +
+    Gram) is enqueued before pass i's status is read; its launches are gated
+    on the device by pass i's (resp. its own) factor status, so after the
+    convergence / cap / error pass they do nothing.  The status is then read
+    while the GPU already runs the next pass, and the reference's charges,
+    warnings and raises are replayed in its order."""
     cfg = cfg or AlgoConfig()
     a = _device_array(a)
     if a.ncols < 1:
@@ -327,16 +334,35 @@ def rs_chol_qr(a, cfg=None, ledger=None):
     eng = Engine(n, cfg)
     eng.gram(a)
     _charge(ledger, "gemm", _flops.gemm_flops(m, n, n))
-    q = None                       # the reference's q = a.copy(), taken lazily
+    handles, outs = [], []
+
+    def enqueue(p):
+        prev = handles[p - 1] if p else None
+        h = eng.factor_async(_lib.POLICY_RECOMPUTE, m, n, tol=tol, check_tol=True, stop=(p == cfg.max_iter),
+                             gate=eng.gate(prev) if p else None, gate_slot=prev)
+        src = a if p == 0 else outs[p - 1]
+        # the reference's q = a.copy(), taken lazily: pass 0 writes a fresh array,
+        # later passes work in place where the kernels allow it
+        dst = src if (p > 0 and eng.in_place_gram_ok()) else _fresh_like(src, n)
+        if p < cfg.max_iter:
+            eng.apply(src, dst, with_gram=True, gate=eng.gate(h), gate_slot=h)
+        handles.append(h)
+        outs.append(dst)
+
+    enqueue(0)
     shifts, attempts, margins, dms = [], [], [], []
     its = 0
     while True:
-        st = eng.factor(_lib.POLICY_RECOMPUTE, m, n, tol=tol, check_tol=True, stop=(its == cfg.max_iter))
+        if its + 1 <= cfg.max_iter:
+            enqueue(its + 1)
+        (st,) = eng.collect([handles[its]])
+        if its >= 2:
+            outs[its - 2] = None   # no longer a source or a result
         _charge(ledger, "fro_norm", _flops.frobenius_flops(n))
         if st.code == _lib.CONVERGED:
             break
         if st.code == _lib.CAPPED:
-            return QRResult(q if q is not None else a.copy(), eng.r_host(), its, shifts, attempts,
+            return QRResult(outs[its - 1] if its else a.copy(), eng.r_host(), its, shifts, attempts,
                             success=False, orth_error=st.err, pivot_margins=margins, decision_margins=dms)
         _emit_estimate_warning(st)
         _charge_recompute(ledger, n, st)
@@ -346,12 +372,11 @@ def rs_chol_qr(a, cfg=None, ledger=None):
         shifts.extend(st.shifts)
         margins.append(st.min_pivot_rel)
         _charge(ledger, "trtri", _flops.tri_inverse_flops(n))
-        q = _apply_gram_into(eng, a if q is None else q, fresh_ok=q is None)
         _charge(ledger, "gemm", _flops.gemm_flops(m, n, n))
         _charge(ledger, "trmm", _flops.trmm_flops(n))
         _charge(ledger, "gemm", _flops.gemm_flops(m, n, n))
         its += 1
-    return QRResult(q if q is not None else a.copy(), eng.r_host(), its, shifts, attempts,
+    return QRResult(outs[its - 1] if its else a.copy(), eng.r_host(), its, shifts, attempts,
                     success=True, orth_error=st.err, pivot_margins=margins, decision_margins=dms)
 
 

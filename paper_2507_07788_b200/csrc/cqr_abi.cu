@@ -56,7 +56,8 @@ size_t cqr_gram_workspace_bytes(int64_t m, int ka, int kb, int self) {
 }
 
 static int gram_common(const double* A, int64_t lda, int ka, const double* B, int64_t ldb, int kb, int64_t m,
-                       bool self, double* G, int ldg, void* ws, size_t ws_bytes, void* stream, const char* who) {
+                       bool self, double* G, int ldg, void* ws, size_t ws_bytes, void* stream, const char* who,
+                       const int* gate = nullptr) {
   int rc = check_tall(A, lda, m, ka, who);
   if (rc) return rc;
   if (!self) {
@@ -69,13 +70,14 @@ static int gram_common(const double* A, int64_t lda, int ka, const double* B, in
     if (ws == nullptr || ws_bytes < cqr::gram_pairs_ws_bytes(cqr::round_up(m, 16), ka))
       return fail(CQR_EINVAL, std::string(who) + ": workspace too small");
     return cuda_check(cqr::gram_pairs_launch(A, lda, ka, cqr::round_up(m, 16), G, ldg, static_cast<double*>(ws),
-                                             static_cast<cudaStream_t>(stream)),
+                                             static_cast<cudaStream_t>(stream), gate),
                       who);
   }
   cqr::GramArgs a = cqr::gram_plan(A, lda, ka, B, ldb, kb, cqr::round_up(m, 16), self);
   if (ws_bytes < cqr::gram_workspace_bytes(a) || ws == nullptr)
     return fail(CQR_EINVAL, std::string(who) + ": workspace too small");
   a.ws = static_cast<double*>(ws);
+  a.gate = gate;
   return cuda_check(cqr::gram_launch(a, G, ldg, static_cast<cudaStream_t>(stream)), who);
 }
 
@@ -89,8 +91,8 @@ int cqr_cross_gram(const double* A, int64_t lda, int ka, const double* B, int64_
   return gram_common(A, lda, ka, B, ldb, kb, m, false, G, ldg, ws, ws_bytes, stream, "cqr_cross_gram");
 }
 
-int cqr_lincomb(const double* X, int64_t ldx, int64_t m, int k, const double* C, int n, int upper, double* Y,
-                int64_t ldy, void* stream) {
+static int lincomb_impl(const double* X, int64_t ldx, int64_t m, int k, const double* C, int n, int upper, double* Y,
+                        int64_t ldy, void* stream, const int* gate) {
   int rc = check_tall(X, ldx, m, k, "cqr_lincomb(X)");
   if (rc) return rc;
   rc = check_tall(Y, ldy, m, n, "cqr_lincomb(Y)");
@@ -106,7 +108,12 @@ int cqr_lincomb(const double* X, int64_t ldx, int64_t m, int k, const double* C,
   a.Y = Y; a.ldy = ldy; a.n = n;
   a.rows = cqr::round_up(m, 16);
   a.upper = upper ? 1 : 0;
+  a.gate = gate;
   return cuda_check(cqr::gemm_launch(a, static_cast<cudaStream_t>(stream)), "cqr_lincomb");
+}
+int cqr_lincomb(const double* X, int64_t ldx, int64_t m, int k, const double* C, int n, int upper, double* Y,
+                int64_t ldy, void* stream) {
+  return lincomb_impl(X, ldx, m, k, C, n, upper, Y, ldy, stream, nullptr);
 }
 
 int cqr_axpy(double* Y, int64_t ldy, double alpha, const double* X, int64_t ldx, int64_t m, int n, void* stream) {
@@ -166,8 +173,9 @@ int cqr_apply_gram_launches(int k) { return cqr::apply_gram_fused_supported(k) ?
 
 int cqr_apply_gram_inplace_ok(int k) { return (k <= 64 || cqr::apply_gram_fused_supported(k)) ? 1 : 0; }
 
-int cqr_apply_gram(const double* X, int64_t ldx, int64_t m, int k, const double* Rinv, double* Q, int64_t ldq,
-                   double* G, int ldg, void* ws, size_t ws_bytes, void* stream) {
+int cqr_apply_gram_gated(const double* X, int64_t ldx, int64_t m, int k, const double* Rinv, double* Q,
+                         int64_t ldq, double* G, int ldg, void* ws, size_t ws_bytes, const int32_t* gate,
+                         void* stream) {
   int rc = check_tall(X, ldx, m, k, "cqr_apply_gram(X)");
   if (rc) return rc;
   rc = check_tall(Q, ldq, m, k, "cqr_apply_gram(Q)");
@@ -180,12 +188,17 @@ int cqr_apply_gram(const double* X, int64_t ldx, int64_t m, int k, const double*
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (cqr::apply_gram_fused_supported(k))
     return cuda_check(cqr::apply_gram_fused_launch(X, ldx, k, Rinv, Q, ldq, cqr::round_up(m, 16), G, ldg,
-                                                   static_cast<double*>(ws), ws_bytes, s),
+                                                   static_cast<double*>(ws), ws_bytes, s, gate),
                       "cqr_apply_gram(fused)");
   if (X == Q && k > 64) return fail(CQR_EINVAL, "cqr_apply_gram: in place needs the fused kernel (k <= 128)");
-  rc = cqr_lincomb(X, ldx, m, k, Rinv, k, 1, Q, ldq, stream);
+  rc = lincomb_impl(X, ldx, m, k, Rinv, k, 1, Q, ldq, stream, gate);
   if (rc) return rc;
-  return cqr_gram(Q, ldq, m, k, G, ldg, ws, ws_bytes, stream);
+  return gram_common(Q, ldq, k, Q, ldq, k, m, true, G, ldg, ws, ws_bytes, stream, "cqr_apply_gram(gram)", gate);
+}
+
+int cqr_apply_gram(const double* X, int64_t ldx, int64_t m, int k, const double* Rinv, double* Q, int64_t ldq,
+                   double* G, int ldg, void* ws, size_t ws_bytes, void* stream) {
+  return cqr_apply_gram_gated(X, ldx, m, k, Rinv, Q, ldq, G, ldg, ws, ws_bytes, nullptr, stream);
 }
 
 int cqr_update_supported(int q, int p) { return cqr::update_pass_supported(q, p) ? 1 : 0; }
@@ -195,9 +208,10 @@ size_t cqr_update_workspace_bytes(int64_t m, int q, int p) {
   return q >= 1 ? cqr::update_pass_ws_bytes(cqr::round_up(m, 16), q) : 256;
 }
 
-int cqr_update_pass_to(const double* Qin, int64_t ldqin, int q, const double* Q, int64_t ldq, double* Qout,
-                       int64_t ldqout, int p, int64_t m, const double* Bt, int ldbt, const double* Rinv_tiles,
-                       int initial, double* Bt_next, double* G, int ldg, void* ws, size_t ws_bytes, void* stream) {
+int cqr_update_pass_gated(const double* Qin, int64_t ldqin, int q, const double* Q, int64_t ldq, double* Qout,
+                          int64_t ldqout, int p, int64_t m, const double* Bt, int ldbt, const double* Rinv_tiles,
+                          int initial, double* Bt_next, double* G, int ldg, void* ws, size_t ws_bytes,
+                          const int32_t* gate, void* stream) {
   if (!cqr::update_pass_supported(q, p)) return fail(CQR_EINVAL, "cqr_update_pass: needs 1 <= q <= 512, 1 <= p <= 16");
   int rc = check_tall(Qin, ldqin, m, q, "cqr_update_pass(Qin)");
   if (rc) return rc;
@@ -222,8 +236,15 @@ int cqr_update_pass_to(const double* Qin, int64_t ldqin, int q, const double* Q,
   return cuda_check(cqr::update_pass_launch(Qin, ldqin, q, Q, ldq, initial ? const_cast<double*>(Q) : Qout,
                                             initial ? ldq : ldqout, p, cqr::round_up(m, 16), Bt, ldbt, Rinv_tiles,
                                             initial, Bt_next, G, ldg, static_cast<double*>(ws),
-                                            static_cast<cudaStream_t>(stream)),
+                                            static_cast<cudaStream_t>(stream), gate),
                     "cqr_update_pass");
+}
+
+int cqr_update_pass_to(const double* Qin, int64_t ldqin, int q, const double* Q, int64_t ldq, double* Qout,
+                       int64_t ldqout, int p, int64_t m, const double* Bt, int ldbt, const double* Rinv_tiles,
+                       int initial, double* Bt_next, double* G, int ldg, void* ws, size_t ws_bytes, void* stream) {
+  return cqr_update_pass_gated(Qin, ldqin, q, Q, ldq, Qout, ldqout, p, m, Bt, ldbt, Rinv_tiles, initial, Bt_next, G,
+                               ldg, ws, ws_bytes, nullptr, stream);
 }
 
 int cqr_update_pass(const double* Qin, int64_t ldqin, int q, double* Q, int64_t ldq, int p, int64_t m,
@@ -289,6 +310,7 @@ int cqr_factor(const cqr_factor_config* cfg, int k, const double* G, int ldg, co
   a.B = B; a.ldb = ldb;
   a.shifts = shifts;
   a.st = status;
+  a.gate = cfg->gate;
   return cuda_check(cqr::factor_launch(a, static_cast<cudaStream_t>(stream)), "cqr_factor");
 }
 

@@ -719,6 +719,11 @@ __device__ double norm_estimate(const double* __restrict__ X, int k, double tol,
 }
 
 __global__ void __launch_bounds__(FK_THREADS, 1) factor_kernel(FactorArgs a) {
+  if (a.gate != nullptr && *a.gate != CQR_FACTORED) {
+    // gated off (the previous pass did not factor): record it, touch nothing else
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.st->code = CQR_SKIPPED;
+    return;
+  }
   extern __shared__ __align__(16) double fsm[];
   __shared__ FState fs;
   __shared__ int sflag;

@@ -107,7 +107,8 @@ struct TrmmDispatch<KP, KP / 16, KFULL> {
 template <int KP, bool KFULL>
 __global__ void __launch_bounds__(FuCfg<KP>::THREADS, 1)
     apply_gram_fused_kernel(const double* X, int64_t ldx, int k, const double* __restrict__ Rt, double* Q,
-                            int64_t ldq, int64_t rows, double* __restrict__ ws) {
+                            int64_t ldq, int64_t rows, double* __restrict__ ws, const int* gate) {
+  if (gate != nullptr && *gate != 0) return;   // gated off
   using C = FuCfg<KP>;
   constexpr int NB = C::NB, P = C::PAIRS, XST = C::XST, QB = C::QB;
   // thread 0 keeps XD panels in flight and refills the stage of panel j-XLAG,
@@ -277,7 +278,9 @@ __global__ void __launch_bounds__(FuCfg<KP>::THREADS, 1)
 }
 
 // fixed-order sum over CTAs of the per-CTA KP x KP partials; lower triangle, mirrored
-__global__ void gram_fused_reduce(const double* __restrict__ ws, int nparts, int KP, int k, double* G, int ldg) {
+__global__ void gram_fused_reduce(const double* __restrict__ ws, int nparts, int KP, int k, double* G, int ldg,
+                                  const int* gate) {
+  if (gate != nullptr && *gate != 0) return;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)k * k;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int r = (int)(e % k), c = (int)(e / k);
@@ -318,7 +321,7 @@ size_t apply_gram_fused_ws_bytes(int64_t rows, int k) {
 
 template <int KP>
 static cudaError_t launch_fused(const double* X, int64_t ldx, int k, const double* Rt, double* Q, int64_t ldq,
-                                int64_t rows, double* G, int ldg, double* ws, cudaStream_t s) {
+                                int64_t rows, double* G, int ldg, double* ws, cudaStream_t s, const int* gate) {
   static bool attr = false;
   const size_t smem = fused_smem_doubles<KP>() * sizeof(double);
   if (!attr) {
@@ -332,24 +335,24 @@ static cudaError_t launch_fused(const double* X, int64_t ldx, int k, const doubl
   }
   const int ctas = fused_ctas(rows);
   if (k == KP)
-    apply_gram_fused_kernel<KP, true><<<ctas, FuCfg<KP>::THREADS, smem, s>>>(X, ldx, k, Rt, Q, ldq, rows, ws);
+    apply_gram_fused_kernel<KP, true><<<ctas, FuCfg<KP>::THREADS, smem, s>>>(X, ldx, k, Rt, Q, ldq, rows, ws, gate);
   else
-    apply_gram_fused_kernel<KP, false><<<ctas, FuCfg<KP>::THREADS, smem, s>>>(X, ldx, k, Rt, Q, ldq, rows, ws);
+    apply_gram_fused_kernel<KP, false><<<ctas, FuCfg<KP>::THREADS, smem, s>>>(X, ldx, k, Rt, Q, ldq, rows, ws, gate);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int64_t nel = (int64_t)k * k;
   int blocks = (int)imin64(ceil_div(nel, 256), 2 * num_sms());
-  gram_fused_reduce<<<blocks < 1 ? 1 : blocks, 256, 0, s>>>(ws, ctas, KP, k, G, ldg);
+  gram_fused_reduce<<<blocks < 1 ? 1 : blocks, 256, 0, s>>>(ws, ctas, KP, k, G, ldg, gate);
   return cudaGetLastError();
 }
 
 cudaError_t apply_gram_fused_launch(const double* X, int64_t ldx, int k, const double* Rinv_tiles, double* Q,
                                     int64_t ldq, int64_t rows, double* G, int ldg, double* ws, size_t ws_bytes,
-                                    cudaStream_t stream) {
+                                    cudaStream_t stream, const int* gate) {
   (void)ws_bytes;
   switch (fused_kp(k)) {
-    case 64: return launch_fused<64>(X, ldx, k, Rinv_tiles, Q, ldq, rows, G, ldg, ws, stream);
-    case 128: return launch_fused<128>(X, ldx, k, Rinv_tiles, Q, ldq, rows, G, ldg, ws, stream);
+    case 64: return launch_fused<64>(X, ldx, k, Rinv_tiles, Q, ldq, rows, G, ldg, ws, stream, gate);
+    case 128: return launch_fused<128>(X, ldx, k, Rinv_tiles, Q, ldq, rows, G, ldg, ws, stream, gate);
     default: return cudaErrorNotSupported;
   }
 }

@@ -70,6 +70,7 @@ __device__ __forceinline__ void diag_chunk(double (&acc)[4][4][2], const double*
 }
 
 __global__ void __launch_bounds__(GM_THREADS, 2) gemm_kernel(GemmArgs args) {
+  if (args.gate != nullptr && *args.gate != 0) return;   // gated off
   extern __shared__ __align__(128) double smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + GM_STAGES * GM_STAGE_DOUBLES);
   uint64_t* empty = full + GM_STAGES;

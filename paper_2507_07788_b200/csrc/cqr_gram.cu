@@ -116,6 +116,7 @@ __device__ __forceinline__ void stage_block(double* dst, const double* src, int6
 }
 
 __global__ void __launch_bounds__(GR_THREADS, 2) gram_kernel(GramArgs args) {
+  if (args.gate != nullptr && *args.gate != 0) return;   // gated off
   extern __shared__ __align__(128) double smem[];
   double* stage_base = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + GR_STAGES * GR_STAGE_DOUBLES);
@@ -234,6 +235,7 @@ __global__ void __launch_bounds__(GR_THREADS, 2) gram_kernel(GramArgs args) {
 // Fixed-order sum of the split partials.  One thread per output element of
 // the (lower) tile set; writes G and, for the self Gram, its mirror.
 __global__ void gram_reduce_kernel(GramArgs args, double* G, int ldg) {
+  if (args.gate != nullptr && *args.gate != 0) return;
   const int64_t n_el = (int64_t)args.ka * args.kb;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_el; e += (int64_t)gridDim.x * blockDim.x) {
     const int gi = (int)(e % args.ka), gj = (int)(e / args.ka);

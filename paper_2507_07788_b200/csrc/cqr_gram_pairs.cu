@@ -50,7 +50,9 @@ size_t gp_smem_bytes() {
 
 template <int KP>
 __global__ void __launch_bounds__(GPCfg<KP>::THREADS, 1) gram_pairs_kernel(const double* __restrict__ X, int64_t ldx, int k,
-                                                                   int64_t rows, int nsplit, double* ws) {
+                                                                   int64_t rows, int nsplit, double* ws,
+                                                                   const int* gate) {
+  if (gate != nullptr && *gate != 0) return;   // gated off
   using C = GPCfg<KP>;
   constexpr int NB = C::NB;
   constexpr int GP_STAGES = C::STAGES;
@@ -147,7 +149,9 @@ __global__ void __launch_bounds__(GPCfg<KP>::THREADS, 1) gram_pairs_kernel(const
   }
 }
 
-__global__ void gram_pairs_reduce(const double* __restrict__ ws, int nparts, int KP, int k, double* G, int ldg) {
+__global__ void gram_pairs_reduce(const double* __restrict__ ws, int nparts, int KP, int k, double* G, int ldg,
+                                  const int* gate) {
+  if (gate != nullptr && *gate != 0) return;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)k * k;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int r = (int)(e % k), c = (int)(e / k);
@@ -189,7 +193,7 @@ size_t gram_pairs_ws_bytes(int64_t rows, int k) {
 
 template <int KP>
 static cudaError_t launch_gp(const double* X, int64_t ldx, int k, int64_t rows, double* G, int ldg, double* ws,
-                             cudaStream_t s) {
+                             cudaStream_t s, const int* gate) {
   static bool attr = false;
   const size_t smem = gp_smem_bytes<KP>();
   if (!attr) {
@@ -200,23 +204,23 @@ static cudaError_t launch_gp(const double* X, int64_t ldx, int k, int64_t rows, 
   }
   int items, nsplit;
   gp_grid(rows, KP, items, nsplit);
-  gram_pairs_kernel<KP><<<items * nsplit, GPCfg<KP>::THREADS, smem, s>>>(X, ldx, k, rows, nsplit, ws);
+  gram_pairs_kernel<KP><<<items * nsplit, GPCfg<KP>::THREADS, smem, s>>>(X, ldx, k, rows, nsplit, ws, gate);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int64_t nel = (int64_t)k * k;
   int blocks = (int)imin64(ceil_div(nel, 256), 4 * num_sms());
-  gram_pairs_reduce<<<blocks < 1 ? 1 : blocks, 256, 0, s>>>(ws, items * nsplit, KP, k, G, ldg);
+  gram_pairs_reduce<<<blocks < 1 ? 1 : blocks, 256, 0, s>>>(ws, items * nsplit, KP, k, G, ldg, gate);
   return cudaGetLastError();
 }
 
 cudaError_t gram_pairs_launch(const double* X, int64_t ldx, int k, int64_t rows, double* G, int ldg, double* ws,
-                              cudaStream_t s) {
+                              cudaStream_t s, const int* gate) {
   switch (gp_kp(k)) {
-    case 16: return launch_gp<16>(X, ldx, k, rows, G, ldg, ws, s);
-    case 32: return launch_gp<32>(X, ldx, k, rows, G, ldg, ws, s);
-    case 64: return launch_gp<64>(X, ldx, k, rows, G, ldg, ws, s);
-    case 128: return launch_gp<128>(X, ldx, k, rows, G, ldg, ws, s);
-    case 256: return launch_gp<256>(X, ldx, k, rows, G, ldg, ws, s);
+    case 16: return launch_gp<16>(X, ldx, k, rows, G, ldg, ws, s, gate);
+    case 32: return launch_gp<32>(X, ldx, k, rows, G, ldg, ws, s, gate);
+    case 64: return launch_gp<64>(X, ldx, k, rows, G, ldg, ws, s, gate);
+    case 128: return launch_gp<128>(X, ldx, k, rows, G, ldg, ws, s, gate);
+    case 256: return launch_gp<256>(X, ldx, k, rows, G, ldg, ws, s, gate);
     default: return cudaErrorNotSupported;
   }
 }

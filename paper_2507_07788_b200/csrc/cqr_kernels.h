@@ -20,6 +20,7 @@ struct GramArgs {
   int nsplit;
   int64_t npanels;
   double* ws;         // [nsplit][nitems][2][64*64]
+  const int* gate = nullptr;   // launch is a no-op unless *gate == CQR_FACTORED (0)
 };
 GramArgs gram_plan(const double* A, int64_t lda, int ka, const double* B, int64_t ldb, int kb, int64_t rows,
                    bool self);
@@ -29,7 +30,7 @@ cudaError_t gram_launch(GramArgs& a, double* G, int ldg, cudaStream_t stream);
 bool gram_pairs_supported(int k);
 size_t gram_pairs_ws_bytes(int64_t rows, int k);
 cudaError_t gram_pairs_launch(const double* X, int64_t ldx, int k, int64_t rows, double* G, int ldg, double* ws,
-                              cudaStream_t s);
+                              cudaStream_t s, const int* gate = nullptr);
 
 // ------------------------------------------------------------- row-panel GEMM (K2 building block)
 struct GemmArgs {
@@ -40,6 +41,7 @@ struct GemmArgs {
   int upper;                              // C upper triangular: skip zero blocks
   int ntile_n;
   int64_t nrow_tiles;
+  const int* gate = nullptr;   // launch is a no-op unless *gate == CQR_FACTORED (0)
 };
 cudaError_t gemm_launch(GemmArgs& a, cudaStream_t stream);
 
@@ -56,7 +58,7 @@ cudaError_t pack_coeff_launch(const double* src, int ld, int k, int n, double* d
 // ------------------------------------------------------------- fused TRMM + Gram (K2, k <= 128)
 cudaError_t apply_gram_fused_launch(const double* X, int64_t ldx, int k, const double* Rinv_tiles, double* Q,
                                     int64_t ldq, int64_t rows, double* G, int ldg, double* ws, size_t ws_bytes,
-                                    cudaStream_t stream);
+                                    cudaStream_t stream, const int* gate = nullptr);
 size_t apply_gram_fused_ws_bytes(int64_t rows, int k);
 bool apply_gram_fused_supported(int k);
 void set_fused(int on);
@@ -66,7 +68,8 @@ bool update_pass_supported(int q, int p);
 size_t update_pass_ws_bytes(int64_t rows, int q);
 cudaError_t update_pass_launch(const double* Qin, int64_t ldqin, int q, const double* Qb, int64_t ldqb, double* Qo,
                                int64_t ldqo, int p, int64_t rows, const double* Bt, int ldbt, const double* Rinv_tiles,
-                               int initial, double* Bt_next, double* G, int ldg, double* ws, cudaStream_t s);
+                               int initial, double* Bt_next, double* G, int ldg, double* ws, cudaStream_t s,
+                               const int* gate = nullptr);
 
 // ------------------------------------------------------------- k x k stage (K4)
 struct FactorArgs {
@@ -88,6 +91,7 @@ struct FactorArgs {
   double* B; int ldb;
   double* shifts;
   cqr_factor_status* st;
+  const int* gate;   // nullptr, or: skip the pass unless *gate == CQR_FACTORED
   // speculative shifted branch (RECOMPUTE policy): a second CTA runs the
   // estimate + shifted attempts into private buffers while CTA 0 tries the
   // plain factorization; CTA 0 publishes its outcome in `pub` (epoch-tagged)

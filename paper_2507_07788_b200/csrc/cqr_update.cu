@@ -54,6 +54,7 @@ struct UpdateArgs {
   double* ws;                             // [ctas][(q_pad + 16) * 16]
   int qs;                                 // staged column stride (= 4 mod 8)
   int ns;                                 // ring stages
+  const int* gate;                        // no-op unless *gate == CQR_FACTORED
 };
 
 static int up_qs(int q) { return (int)round_up(q, 8) + 4; }
@@ -70,6 +71,7 @@ static size_t update_smem_bytes(int q, int sr) {
 
 template <int NQ, int SR>
 __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(UpdateArgs a) {
+  if (a.gate != nullptr && *a.gate != 0) return;   // gated off
   constexpr int RB = SR / 8;        // 8-row blocks per sub-panel
   constexpr int Q4 = SR / 4;        // quads (k4 steps of the cross Gram) per sub-panel
   constexpr int TE = SR * UP_PB;    // elements of a 16-wide sub-panel
@@ -285,7 +287,8 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(UpdateArgs a
 
 // fixed-order sum over CTAs; Bt' (q x p, ld ldbt) and G (p x p, lower mirrored, ld ldg)
 __global__ void update_reduce_kernel(const double* __restrict__ ws, int nparts, int q, int p, int qp,
-                                     double* Bt, int ldbt, double* G, int ldg) {
+                                     double* Bt, int ldbt, double* G, int ldg, const int* gate) {
+  if (gate != nullptr && *gate != 0) return;
   const int ld = qp + UP_PB;
   const int64_t nbt = (int64_t)q * p, ng = (int64_t)p * p;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nbt + ng;
@@ -336,7 +339,8 @@ static cudaError_t launch_up(const UpdateArgs& a, int ctas, size_t smem, cudaStr
 
 cudaError_t update_pass_launch(const double* Qin, int64_t ldqin, int q, const double* Qb, int64_t ldqb, double* Qo,
                                int64_t ldqo, int p, int64_t rows, const double* Bt, int ldbt, const double* Rinv_tiles,
-                               int initial, double* Bt_next, double* G, int ldg, double* ws, cudaStream_t s) {
+                               int initial, double* Bt_next, double* G, int ldg, double* ws, cudaStream_t s,
+                               const int* gate) {
   if (rows % 16) return cudaErrorInvalidValue;
   UpdateArgs a{};
   a.Qin = Qin; a.ldqin = ldqin; a.q = q;
@@ -346,6 +350,7 @@ cudaError_t update_pass_launch(const double* Qin, int64_t ldqin, int q, const do
   a.Bt = Bt; a.ldbt = ldbt; a.Rinv = Rinv_tiles;
   a.initial = initial;
   a.ws = ws;
+  a.gate = gate;
   a.qs = up_qs(q);
   const int sr = up_sr(q);
   a.ns = up_stages(q, sr);
@@ -367,7 +372,7 @@ cudaError_t update_pass_launch(const double* Qin, int64_t ldqin, int q, const do
   const int qp = (int)round_up(q, 64);
   const int64_t nel = (int64_t)q * p + (int64_t)p * p;
   int blocks = (int)imin64(ceil_div(nel, 256), 2 * num_sms());
-  update_reduce_kernel<<<blocks < 1 ? 1 : blocks, 256, 0, s>>>(ws, ctas, q, p, qp, Bt_next, q, G, ldg);
+  update_reduce_kernel<<<blocks < 1 ? 1 : blocks, 256, 0, s>>>(ws, ctas, q, p, qp, Bt_next, q, G, ldg, gate);
   return cudaGetLastError();
 }
 
