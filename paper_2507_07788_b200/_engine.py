@@ -216,7 +216,7 @@ class Engine:
                 cx.timer.stop("apply", t0, (src.m_local, self.k))
             cx.launches += 1
 
-    def update_pass(self, q_in, qb, initial, out=None, gate=None):
+    def update_pass(self, q_in, qb, initial, out=None, gate=None, gate_slot=None):
         """Fused block-update pass (cqr_update_pass_to): Bt, G from Q_in and the
         block; in iteration mode the block is first replaced by
         (Q - Q_in Bt) R^-1, in place or written to `out`."""
@@ -231,7 +231,8 @@ class Engine:
                                                 cx.stream),
                    "update_pass")
         if t0 is not None:
-            cx.timer.stop("update_pass", t0, (qb.m_local, q_in.ncols, self.k, 1 if initial else 0))
+            cx.timer.stop("update_pass", t0, (qb.m_local, q_in.ncols, self.k, 1 if initial else 0),
+                          gate=self.stat_all[gate_slot] if gate_slot is not None else None)
         cx.launches += 2
         if cx.world > 1:
             cx.allreduce_(self.Bt)

@@ -492,6 +492,8 @@ def chol_qr_update(q_in, r_in, a_new, cfg=None, ledger=None):
     shifts, attempts, margins, dms = [], [], [], []
     its = 0
     success = True
+    if fused:
+        return _update_pipelined(eng, q_in, r_in, a_new, m, k, p, width, tol, cfg, ledger)
     while True:
         st = eng.factor(_lib.POLICY_UPDATE, m, width, tol=tol, check_tol=True, stop=(its == cfg.max_iter),
                         update_b=True)
@@ -560,6 +562,66 @@ def chol_qr_update(q_in, r_in, a_new, cfg=None, ledger=None):
     q_out = q_in.extended(q)
     b = eng.b_host() if k else np.zeros((0, p))
     r_out = np.block([[r_in, b], [np.zeros((p, k)), eng.r_host()]])
+    return QRResult(q_out, r_out, its, shifts, attempts, success=success, orth_error=st.err,
+                    pivot_margins=margins, decision_margins=dms)
+
+
+def _update_pipelined(eng, q_in, r_in, a_new, m, k, p, width, tol, cfg, ledger):
+    """The iteration of chol_qr_update with the fused update pass, one pass
+    ahead of the host (as rs_chol_qr): pass i+1 (factor, update pass) is
+    enqueued before pass i's status is read, gated on the device by the
+    statuses, and the reference's charges / raises are replayed in order."""
+    handles, outs = [], []
+
+    def enqueue(i):
+        prev = handles[i - 1] if i else None
+        h = eng.factor_async(_lib.POLICY_UPDATE, m, width, tol=tol, check_tol=True, stop=(i == cfg.max_iter),
+                             update_b=True, gate=eng.gate(prev) if i else None, gate_slot=prev)
+        dst = outs[i - 1] if i else None
+        if i < cfg.max_iter:
+            if i == 0:
+                # the first sweep reads the caller's block and writes a fresh Q (no copy)
+                dst = _fresh_like(a_new, p)
+                eng.update_pass(q_in, a_new, initial=False, out=dst, gate=eng.gate(h), gate_slot=h)
+            else:
+                eng.update_pass(q_in, dst, initial=False, gate=eng.gate(h), gate_slot=h)
+        handles.append(h)
+        outs.append(dst)
+
+    enqueue(0)
+    shifts, attempts, margins, dms = [], [], [], []
+    its = 0
+    success = True
+    while True:
+        if its + 1 <= cfg.max_iter:
+            enqueue(its + 1)
+        (st,) = eng.collect([handles[its]])
+        _charge(ledger, "fro_norm", _flops.frobenius_flops(p))
+        if st.code == _lib.CONVERGED:
+            break
+        if st.code == _lib.CAPPED:
+            success = False
+            break
+        _emit_estimate_warning(st)
+        _charge_update(ledger, p, st)
+        _raise_for(st)
+        dms.append(st.plain_margin)
+        attempts.append(st.retries)
+        shifts.extend(st.shifts)
+        margins.append(st.min_pivot_rel)
+        _charge(ledger, "gemm", _flops.gemm_flops(m, k, p))
+        _charge(ledger, "gemm", m * p)
+        _charge(ledger, "trtri", _flops.tri_inverse_flops(p))
+        _charge(ledger, "gemm", _flops.gemm_flops(m, p, p))
+        _charge(ledger, "gemm", _flops.gemm_flops(k, p, p) + k * p)
+        _charge(ledger, "trmm", _flops.trmm_flops(p))
+        _charge(ledger, "gemm", _flops.gemm_flops(m, k, p))
+        _charge(ledger, "gemm", _flops.gemm_flops(m, p, p))
+        _charge(ledger, "gemm", _flops.gemm_flops(p, k, p) + p * p)
+        its += 1
+    q = outs[its - 1] if its else a_new.copy()
+    q_out = q_in.extended(q)
+    r_out = np.block([[r_in, eng.b_host()], [np.zeros((p, k)), eng.r_host()]])
     return QRResult(q_out, r_out, its, shifts, attempts, success=success, orth_error=st.err,
                     pivot_margins=margins, decision_margins=dms)
 
