@@ -572,6 +572,9 @@ def _update_pipelined(eng, q_in, r_in, a_new, m, k, p, width, tol, cfg, ledger):
     enqueued before pass i's status is read, gated on the device by the
     statuses, and the reference's charges / raises are replayed in order."""
     handles, outs = [], []
+    # Q' goes straight into the basis' free capacity when it has some (the
+    # final [q_in, Q] then needs no copy); else into a fresh array
+    tail = q_in._tail_block(p) if q_in._tail_free(p) else None
 
     def enqueue(i):
         prev = handles[i - 1] if i else None
@@ -580,8 +583,8 @@ def _update_pipelined(eng, q_in, r_in, a_new, m, k, p, width, tol, cfg, ledger):
         dst = outs[i - 1] if i else None
         if i < cfg.max_iter:
             if i == 0:
-                # the first sweep reads the caller's block and writes a fresh Q (no copy)
-                dst = _fresh_like(a_new, p)
+                # the first sweep reads the caller's block and writes Q' elsewhere (no copy)
+                dst = tail if tail is not None else _fresh_like(a_new, p)
                 eng.update_pass(q_in, a_new, initial=False, out=dst, gate=eng.gate(h), gate_slot=h)
             else:
                 eng.update_pass(q_in, dst, initial=False, gate=eng.gate(h), gate_slot=h)
@@ -619,8 +622,12 @@ def _update_pipelined(eng, q_in, r_in, a_new, m, k, p, width, tol, cfg, ledger):
         _charge(ledger, "gemm", _flops.gemm_flops(m, p, p))
         _charge(ledger, "gemm", _flops.gemm_flops(p, k, p) + p * p)
         its += 1
-    q = outs[its - 1] if its else a_new.copy()
-    q_out = q_in.extended(q)
+    if its == 0:
+        q_out = q_in.extended(a_new)          # the block itself (copied into the basis)
+    elif tail is not None:
+        q_out = q_in._claim_tail(p)           # already written in place
+    else:
+        q_out = q_in.extended(outs[its - 1])
     r_out = np.block([[r_in, eng.b_host()], [np.zeros((p, k)), eng.r_host()]])
     return QRResult(q_out, r_out, its, shifts, attempts, success=success, orth_error=st.err,
                     pivot_margins=margins, decision_margins=dms)

@@ -95,6 +95,30 @@ class _Storage:
         self.views -= 1
 
 
+class _ColumnBlock:
+    """Columns [c0, c0 + n) of an array's buffer as a kernel operand (QI:
+    column c starts at 4 c doubles, ld = the buffer's capacity).  No ownership:
+    used to let a kernel write straight into free capacity that a later
+    `_claim_tail` turns into columns."""
+
+    def __init__(self, arr, c0, n):
+        self._arr = arr
+        self._c0 = c0
+        self.ncols = n
+        self.space = arr.space
+
+    def ptr(self):
+        return self._arr._buf.data_ptr() + 8 * 4 * self._c0
+
+    @property
+    def ld(self):
+        return self._arr.capacity
+
+    @property
+    def m_local(self):
+        return self._arr.m_local
+
+
 class CudaVectorArray:
     """Tall fp64 array on the local B200, columns-only interface."""
 
@@ -273,6 +297,15 @@ class CudaVectorArray:
         self._gather(other, j0=0, n=other._k, dcol0=self._k)
         self._k = need
         self._st.claimed = max(self._st.claimed, need)
+
+    def _tail_block(self, n):
+        """The n free columns after this array's own (requires _tail_free(n))."""
+        return _ColumnBlock(self, self._k, n)
+
+    def _claim_tail(self, n):
+        """This array plus the n tail columns (already written) as a new array
+        sharing the buffer: extended() without the copy."""
+        return CudaVectorArray(self.space, self._buf, self._k + n, self._st)
 
     def extended(self, other):
         """q_in.copy() + append(other) as a new array (reference

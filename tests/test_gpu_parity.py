@@ -512,3 +512,25 @@ def test_wide_rs_chol_qr_shifts_match_oracle():
     assert P.within10(loo, co.loo_fro(ref.q), k, diverged)
     assert P.within10(rrr, co.rrr_fro(x, ref.q, ref.r), k, diverged)
     assert sum(res.shift_attempts) >= 1   # the shifted attempts ran through the banded path
+
+
+def test_update_into_basis_capacity_is_bitwise_the_copy_path():
+    """chol_qr_update writing Q' straight into the basis' free capacity gives
+    the same bits as the fresh-array + copy path, and leaves the input basis
+    (a view of the same buffer) unchanged."""
+    cq = _cq()
+    rng = np.random.default_rng(21)
+    m, k, p = 20000, 48, 16
+    basis = np.linalg.qr(rng.standard_normal((m, k)))[0]
+    blk = basis @ rng.standard_normal((k, p)) + 1e-6 * rng.standard_normal((m, p))
+    r_in = np.triu(rng.standard_normal((k, k))) + 5 * np.eye(k)
+    plain = cq.CudaVectorArray.from_numpy(basis)
+    roomy = cq.CudaVectorArray.from_numpy(basis, capacity=k + 3 * p)
+    a = cq.CudaVectorArray.from_numpy(blk)
+    r1 = cq.chol_qr_update(plain, r_in, a)
+    r2 = cq.chol_qr_update(roomy, r_in, a)
+    assert r1.iterations == r2.iterations >= 1
+    np.testing.assert_array_equal(r1.r, r2.r)
+    np.testing.assert_array_equal(r1.q.to_numpy(), r2.q.to_numpy())
+    np.testing.assert_array_equal(roomy.to_numpy(), basis)
+    assert roomy.ncols == k and r2.q.ncols == k + p
