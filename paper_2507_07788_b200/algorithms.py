@@ -90,6 +90,7 @@ class QRResult:
     panel_profiles: list | None = None
     pivot_margins: list = field(default_factory=list)
     decision_margins: list = field(default_factory=list)
+    err_history: list = field(default_factory=list)   # ||X - I||_F measured by every pass
 
     @property
     def profile(self):
@@ -350,12 +351,13 @@ def rs_chol_qr(a, cfg=None, ledger=None):
         outs.append(dst)
 
     enqueue(0)
-    shifts, attempts, margins, dms = [], [], [], []
+    shifts, attempts, margins, dms, errs = [], [], [], [], []
     its = 0
     while True:
         if its + 1 <= cfg.max_iter:
             enqueue(its + 1)
         (st,) = eng.collect([handles[its]])
+        errs.append(st.err)
         if its >= 2:
             outs[its - 2] = None   # no longer a source or a result
         _charge(ledger, "fro_norm", _flops.frobenius_flops(n))
@@ -363,7 +365,7 @@ def rs_chol_qr(a, cfg=None, ledger=None):
             break
         if st.code == _lib.CAPPED:
             return QRResult(outs[its - 1] if its else a.copy(), eng.r_host(), its, shifts, attempts,
-                            success=False, orth_error=st.err, pivot_margins=margins, decision_margins=dms)
+                            success=False, orth_error=st.err, pivot_margins=margins, decision_margins=dms, err_history=errs)
         _emit_estimate_warning(st)
         _charge_recompute(ledger, n, st)
         _raise_for(st)
@@ -377,7 +379,7 @@ def rs_chol_qr(a, cfg=None, ledger=None):
         _charge(ledger, "gemm", _flops.gemm_flops(m, n, n))
         its += 1
     return QRResult(outs[its - 1] if its else a.copy(), eng.r_host(), its, shifts, attempts,
-                    success=True, orth_error=st.err, pivot_margins=margins, decision_margins=dms)
+                    success=True, orth_error=st.err, pivot_margins=margins, decision_margins=dms, err_history=errs)
 
 
 def is_chol_qr(a, cfg=None, ledger=None):
@@ -402,16 +404,17 @@ def is_chol_qr(a, cfg=None, ledger=None):
     _charge(ledger, "gemm", _flops.gemm_flops(m, n, n))
     q = None
     sigma0 = None
-    shifts, attempts, margins, dms = [], [], [], []
+    shifts, attempts, margins, dms, errs = [], [], [], [], []
     its = 0
     while True:
         st = eng.factor(_lib.POLICY_PLAIN, m, n, tol=tol, check_tol=True, stop=(its == cfg.max_iter))
+        errs.append(st.err)
         _charge(ledger, "fro_norm", _flops.frobenius_flops(n))
         if st.code == _lib.CONVERGED:
             break
         if st.code == _lib.CAPPED:
             return QRResult(q if q is not None else a.copy(), eng.r_host(), its, shifts, attempts,
-                            success=False, orth_error=st.err, pivot_margins=margins, decision_margins=dms)
+                            success=False, orth_error=st.err, pivot_margins=margins, decision_margins=dms, err_history=errs)
         _charge_plain_attempt(ledger, n)
         dms.append(st.plain_margin)
         err = st.err
@@ -444,7 +447,7 @@ def is_chol_qr(a, cfg=None, ledger=None):
         its += 1
         del err
     return QRResult(q if q is not None else a.copy(), eng.r_host(), its, shifts, attempts,
-                    success=True, orth_error=st.err, pivot_margins=margins, decision_margins=dms)
+                    success=True, orth_error=st.err, pivot_margins=margins, decision_margins=dms, err_history=errs)
 
 
 # ----------------------------------------------------------------------------
@@ -489,7 +492,7 @@ def chol_qr_update(q_in, r_in, a_new, cfg=None, ledger=None):
 
     q = None
     deflated_gram(a_new)
-    shifts, attempts, margins, dms = [], [], [], []
+    shifts, attempts, margins, dms, errs = [], [], [], [], []
     its = 0
     success = True
     if fused:
@@ -497,6 +500,7 @@ def chol_qr_update(q_in, r_in, a_new, cfg=None, ledger=None):
     while True:
         st = eng.factor(_lib.POLICY_UPDATE, m, width, tol=tol, check_tol=True, stop=(its == cfg.max_iter),
                         update_b=True)
+        errs.append(st.err)
         _charge(ledger, "fro_norm", _flops.frobenius_flops(p))
         if st.code == _lib.CONVERGED:
             break
@@ -563,7 +567,7 @@ def chol_qr_update(q_in, r_in, a_new, cfg=None, ledger=None):
     b = eng.b_host() if k else np.zeros((0, p))
     r_out = np.block([[r_in, b], [np.zeros((p, k)), eng.r_host()]])
     return QRResult(q_out, r_out, its, shifts, attempts, success=success, orth_error=st.err,
-                    pivot_margins=margins, decision_margins=dms)
+                    pivot_margins=margins, decision_margins=dms, err_history=errs)
 
 
 def _update_pipelined(eng, q_in, r_in, a_new, m, k, p, width, tol, cfg, ledger):
@@ -592,13 +596,14 @@ def _update_pipelined(eng, q_in, r_in, a_new, m, k, p, width, tol, cfg, ledger):
         outs.append(dst)
 
     enqueue(0)
-    shifts, attempts, margins, dms = [], [], [], []
+    shifts, attempts, margins, dms, errs = [], [], [], [], []
     its = 0
     success = True
     while True:
         if its + 1 <= cfg.max_iter:
             enqueue(its + 1)
         (st,) = eng.collect([handles[its]])
+        errs.append(st.err)
         _charge(ledger, "fro_norm", _flops.frobenius_flops(p))
         if st.code == _lib.CONVERGED:
             break
@@ -630,7 +635,7 @@ def _update_pipelined(eng, q_in, r_in, a_new, m, k, p, width, tol, cfg, ledger):
         q_out = q_in.extended(outs[its - 1])
     r_out = np.block([[r_in, eng.b_host()], [np.zeros((p, k)), eng.r_host()]])
     return QRResult(q_out, r_out, its, shifts, attempts, success=success, orth_error=st.err,
-                    pivot_margins=margins, decision_margins=dms)
+                    pivot_margins=margins, decision_margins=dms, err_history=errs)
 
 
 def _lincomb_device(arr, coeff_dev, k, p):
@@ -665,7 +670,7 @@ def pn_chol_qr(a, r_panels, cfg=None, ledger=None):
     widths = panel_widths(a.ncols, r_panels)
     q = CudaVectorArray.zeros(a.space, 0, capacity=a.ncols)
     r = np.zeros((0, 0))
-    shifts, attempts, profiles, margins, dms = [], [], [], [], []
+    shifts, attempts, profiles, margins, dms, errs = [], [], [], [], [], []
     its = 0
     success = True
     err = None
@@ -685,7 +690,8 @@ def pn_chol_qr(a, r_panels, cfg=None, ledger=None):
         profiles.append(res.profile)
         margins.extend(res.pivot_margins)
         dms.extend(res.decision_margins)
+        errs.extend(res.err_history)
         err = res.orth_error
         success = success and res.success
     return QRResult(q, r, its, shifts, attempts, success=success, orth_error=err,
-                    panel_profiles=profiles, pivot_margins=margins, decision_margins=dms)
+                    panel_profiles=profiles, pivot_margins=margins, decision_margins=dms, err_history=errs)

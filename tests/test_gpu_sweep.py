@@ -1,0 +1,142 @@
+"""Randomised parity sweep: the device path against the oracle on seeded
+matrices of many shapes and condition numbers, with the decision rule of
+tests/parity.py.  GPU only.
+
+The default sweep (CQR_SWEEP unset) is ~50 cases and takes seconds; set
+CQR_SWEEP=5000 for a long run (5000 cases pass, ~1 min)."""
+
+from __future__ import annotations
+
+import math
+import os
+import warnings
+
+import numpy as np
+import pytest
+
+import parity as P
+
+pytestmark = pytest.mark.gpu
+
+N_CASES = int(os.environ.get("CQR_SWEEP", "48"))
+ALGOS = ("rs_chol_qr", "s_chol_qr3", "is_chol_qr", "chol_qr2", "chol_qr_update")
+
+
+def _cases():
+    rng = np.random.default_rng(20250)
+    out = []
+    for i in range(N_CASES):
+        algo = ALGOS[i % len(ALGOS)]
+        k = int(rng.choice([1, 3, 8, 17, 33, 64, 96, 130]))
+        m = int(max(k + 1, rng.choice([5 * k + 3, 1200, 4003])))
+        cond = float(rng.choice([0.0, 2.0, 6.0, 10.0, 14.0]))
+        out.append((i, algo, m, k, cond))
+    return out
+
+
+CASES = _cases()
+
+
+def _matrix(m, k, cond, seed):
+    from paper_2507_07788_b200.matgen import MatrixSpec, generate_host
+
+    return generate_host(MatrixSpec(m, k, cond, seed))[0]
+
+
+def _run_both(algo, x, cq, co):
+    """(ours, ref, our_exc, ref_exc)."""
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        try:
+            if algo in ("rs_chol_qr", "is_chol_qr"):
+                ref = getattr(co, algo)(x, co.default_cfg())
+            else:
+                ref = getattr(co, algo)(x)
+            ref_exc = None
+        except co.OracleBreakdown as exc:
+            ref, ref_exc = None, exc
+        try:
+            mine = getattr(cq, algo)(cq.CudaVectorArray.from_numpy(x))
+            my_exc = None
+        except cq.CholeskyBreakdown as exc:
+            mine, my_exc = None, exc
+    return mine, ref, my_exc, ref_exc
+
+
+@pytest.mark.parametrize("case", CASES, ids=[f"{c[0]}-{c[1]}-{c[2]}x{c[3]}-c{c[4]:g}" for c in CASES])
+def test_sweep_single(case):
+    import paper_2507_07788_b200 as cq
+    from oracle import cholqr_oracle as co
+
+    i, algo, m, k, cond = case
+    if algo == "chol_qr_update":
+        _update_case(i, m, k, cond)
+        return
+    x = _matrix(m, k, cond, i)
+    mine, ref, my_exc, ref_exc = _run_both(algo, x, cq, co)
+    if my_exc is not None or ref_exc is not None:
+        if my_exc is None or ref_exc is None:
+            # only allowed when the deciding pivot sits at the rounding level
+            margin = my_exc.margin if my_exc is not None else getattr(ref_exc, "margin", 0.0)
+            assert not P.robust_margin(margin, k), (margin, my_exc, ref_exc)
+        return
+    np.testing.assert_array_equal(np.tril(mine.r, -1), 0.0)
+    diverged = None
+    if algo in ("rs_chol_qr", "is_chol_qr"):
+        tol = cq.AlgoConfig().effective_tol(k)
+        n = P.compare_iterated(mine, ref, k, tol)
+        if n < max(len(ref.shift_attempts), len(mine.shift_attempts)) or mine.iterations != ref.iterations:
+            diverged = tol
+        assert mine.success == ref.success or diverged is not None
+    if algo in ("chol_qr2", "s_chol_qr3"):
+        # fixed schedules: a pass whose pivots sit at the rounding level (no
+        # breakdown on either side only by chance) leaves the final quality
+        # arbitrary in both runs -- compare it only when every pass was robust
+        margins = list(mine.pivot_margins) + list(getattr(ref, "pivot_margins", []) or [])
+        if not all(P.robust_margin(x, k) for x in margins):
+            return
+    if cond <= 4 and diverged is None:
+        assert np.max(np.abs(mine.r - ref.r)) <= 1e-10 * np.max(np.abs(ref.r))
+    if mine.success and (ref is None or ref.success):
+        loo = cq.loss_of_orthogonality(mine.q, norm="frobenius")
+        rrr = cq.reconstruction_residual(cq.CudaVectorArray.from_numpy(x), mine.q, mine.r, norm="frobenius")
+        assert P.within10(loo, co.loo_fro(ref.q), k, diverged), (loo, co.loo_fro(ref.q))
+        assert P.within10(rrr, co.rrr_fro(x, ref.q, ref.r), k, diverged), (rrr, co.rrr_fro(x, ref.q, ref.r))
+
+
+def _update_case(i, m, k, cond):
+    """A basis of k columns extended by a block of p near-dependent columns."""
+    import paper_2507_07788_b200 as cq
+    from oracle import cholqr_oracle as co
+
+    rng = np.random.default_rng(1000 + i)
+    p = int(min(16, max(1, k // 2)))
+    q_in = np.linalg.qr(rng.standard_normal((m, k)))[0]
+    r_in = np.triu(rng.standard_normal((k, k))) + k * np.eye(k)
+    scale = 10.0 ** (-cond / 2)
+    a_new = q_in @ rng.standard_normal((k, p)) + scale * _matrix(m, p, min(cond, 8.0), i)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        try:
+            ref = co.chol_qr_update(q_in, r_in, a_new, co.default_cfg())
+            ref_exc = None
+        except co.OracleShiftLimit as exc:
+            ref, ref_exc = None, exc
+        try:
+            mine = cq.chol_qr_update(cq.CudaVectorArray.from_numpy(q_in), r_in, cq.CudaVectorArray.from_numpy(a_new))
+            my_exc = None
+        except cq.ShiftAttemptLimitError as exc:
+            mine, my_exc = None, exc
+    if my_exc is not None or ref_exc is not None:
+        assert (my_exc is None) == (ref_exc is None), (my_exc, ref_exc)
+        return
+    np.testing.assert_array_equal(mine.r[:k, :k], r_in)
+    np.testing.assert_array_equal(mine.r[k:, :k], 0.0)
+    tol = cq.AlgoConfig().effective_tol(p)
+    n = P.compare_iterated(mine, ref, p, tol)
+    diverged = tol if (n < max(len(ref.shift_attempts), len(mine.shift_attempts))
+                       or mine.iterations != ref.iterations) else None
+    if mine.success and ref.success:
+        qd = mine.q.to_numpy()
+        loo = float(np.linalg.norm(np.eye(k + p) - qd.T @ qd))
+        assert P.within10(loo, co.loo_fro(ref.q), k + p, diverged), (loo, co.loo_fro(ref.q))
