@@ -140,3 +140,28 @@ def _update_case(i, m, k, cond):
         qd = mine.q.to_numpy()
         loo = float(np.linalg.norm(np.eye(k + p) - qd.T @ qd))
         assert P.within10(loo, co.loo_fro(ref.q), k + p, diverged), (loo, co.loo_fro(ref.q))
+
+
+# Wide widths (the k x k paths for 128 < k <= 256 and the banded L2 path for
+# 256 < k <= 768): CQR_SWEEP_WIDE=N adds N cases (default 6).
+N_WIDE = int(os.environ.get("CQR_SWEEP_WIDE", "6"))
+
+
+def _wide_cases():
+    rng = np.random.default_rng(777)
+    out = []
+    for i in range(N_WIDE):
+        algo = ("rs_chol_qr", "chol_qr2", "s_chol_qr3")[i % 3]
+        k = int(rng.choice([150, 200, 256, 300, 384, 520]))
+        m = int(rng.choice([3 * k + 5, 6000]))
+        cond = float(rng.choice([0.0, 3.0, 8.0, 12.0]))
+        out.append((10000 + i, algo, m, k, cond))
+    return out
+
+
+WIDE = _wide_cases()
+
+
+@pytest.mark.parametrize("case", WIDE, ids=[f"{c[0]}-{c[1]}-{c[2]}x{c[3]}-c{c[4]:g}" for c in WIDE])
+def test_sweep_wide(case):
+    test_sweep_single(case)
