@@ -302,7 +302,8 @@ int cqr_factor(const cqr_factor_config* cfg, int k, const double* G, int ldg, co
     a.Rk1 = x; a.ldr1 = (int)ldr1; x += (size_t)k * ldr1;
     a.W1 = x; x += (size_t)k * (k + 1);
     a.shifts1 = x; x += 1024;
-    a.pub = x;
+    a.pub = x; x += 64;
+    a.part = x;
     a.spec = (cfg->policy == CQR_POLICY_RECOMPUTE && cfg->max_shift_attempts < 1000) ? 1 : 0;
   }
   a.Rk = Rk; a.Rinv = Rinv; a.ldr = ldr;

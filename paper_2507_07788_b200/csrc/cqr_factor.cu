@@ -718,6 +718,71 @@ __device__ double norm_estimate(const double* __restrict__ X, int k, double tol,
   return fro;
 }
 
+// k > 128: X = G (or G - Bt^T Bt), symmetric from the lower triangle, formed in
+// global memory by many CTAs ahead of the single-CTA factorization (one CTA
+// per 32 x 32 tile of the lower triangle; the mirrored half goes through
+// shared memory so both stores are coalesced).  Each tile also leaves its
+// share of ||X - I||_F^2 and the max diagonal of G in a.part.
+constexpr int FP_THREADS = 256;
+
+__global__ void __launch_bounds__(FP_THREADS) factor_prep_kernel(FactorArgs a) {
+  if (a.gate != nullptr && *a.gate != CQR_FACTORED) return;
+  __shared__ double tile[32][33];   // tile[col][row]
+  __shared__ double red[FP_THREADS / 32][2];
+  const int k = a.k;
+  const int b = blockIdx.x;
+  int ti = 0;
+  while ((ti + 1) * (ti + 2) / 2 <= b) ++ti;
+  const int tj = b - ti * (ti + 1) / 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* X = a.X;
+  const bool upd = (a.policy == CQR_POLICY_UPDATE && a.q > 0);
+  double loc = 0.0, dml = -INFINITY;
+  const int r = 32 * ti + lane;
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const int cl = warp + 8 * s, c = 32 * tj + cl;
+    double x = 0.0;
+    if (r < k && c < k && r >= c) {
+      const double gv = a.G[(int64_t)c * a.ldg + r];
+      x = gv;
+      if (upd) {
+        const double* br = a.Bt + (int64_t)r * a.ldbt;
+        const double* bc = a.Bt + (int64_t)c * a.ldbt;
+        double d = 0.0;
+        for (int l = 0; l < a.q; ++l) d += br[l] * bc[l];
+        x = x - d;
+      }
+      X[(int64_t)c * k + r] = x;
+      const double d = x - ((r == c) ? 1.0 : 0.0);
+      loc += ((r == c) ? 1.0 : 2.0) * (d * d);
+      if (r == c) dml = fmax(dml, gv);
+    }
+    tile[cl][lane] = x;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const int rl = warp + 8 * s, rr = 32 * ti + rl, c = 32 * tj + lane;
+    if (rr < k && c < k && rr > c) X[(int64_t)rr * k + c] = tile[lane][rl];
+  }
+  // fixed-order reductions: lanes by xor tree, warps in index order
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    loc += __shfl_xor_sync(0xffffffffu, loc, o);
+    dml = fmax(dml, __shfl_xor_sync(0xffffffffu, dml, o));
+  }
+  if (lane == 0) { red[warp][0] = loc; red[warp][1] = dml; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double e2 = 0.0, dm = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < FP_THREADS / 32; ++w) { e2 += red[w][0]; dm = fmax(dm, red[w][1]); }
+    a.part[2 * b] = e2;
+    a.part[2 * b + 1] = dm;
+  }
+}
+
 __global__ void __launch_bounds__(FK_THREADS, 1) factor_kernel(FactorArgs a) {
   if (a.gate != nullptr && *a.gate != CQR_FACTORED) {
     // gated off (the previous pass did not factor): record it, touch nothing else
@@ -762,52 +827,66 @@ __global__ void __launch_bounds__(FK_THREADS, 1) factor_kernel(FactorArgs a) {
   fmark(0);
   // ---- 1. X = G (or G - Bt^T Bt), symmetric by construction from the lower triangle
   //         (lower triangle read column by column: coalesced)
-  //         and 2. err = ||X - I||_F in the same sweep; loads are batched 16
-  //         per thread before any store (the L2 latency, not bandwidth, bounds
-  //         this phase)
-  const int kk32 = k * k;
-  double loc = 0.0;
-  for (int base = tid; base < kk32; base += 16 * FK_THREADS) {
-    double v[16];
+  //         and 2. err = ||X - I||_F in the same sweep.  k <= 128: here, into
+  //         shared memory; loads are batched 16 per thread before any store
+  //         (the L2 latency, not bandwidth, bounds this phase).  k > 128: by
+  //         factor_prep_kernel ahead of this kernel.
+  if (xs) {
+    const int kk32 = k * k;
+    double loc = 0.0;
+    for (int base = tid; base < kk32; base += 16 * FK_THREADS) {
+      double v[16];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int e = base + j * FK_THREADS;
-      const int r = e % k, c = e / k;
-      v[j] = (e < kk32 && r >= c) ? a.G[(int64_t)c * a.ldg + r] : 0.0;
-    }
+      for (int j = 0; j < 16; ++j) {
+        const int e = base + j * FK_THREADS;
+        const int r = e % k, c = e / k;
+        v[j] = (e < kk32 && r >= c) ? a.G[(int64_t)c * a.ldg + r] : 0.0;
+      }
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int e = base + j * FK_THREADS;
-      const int r = e % k, c = e / k;
-      if (e < kk32 && r >= c) {
-        double x = v[j];
-        if (a.policy == CQR_POLICY_UPDATE && a.q > 0) {
-          const double* br = a.Bt + (int64_t)r * a.ldbt;
-          const double* bc = a.Bt + (int64_t)c * a.ldbt;
-          double d = 0.0;
-          for (int l = 0; l < a.q; ++l) d += br[l] * bc[l];
-          x = x - d;
+      for (int j = 0; j < 16; ++j) {
+        const int e = base + j * FK_THREADS;
+        const int r = e % k, c = e / k;
+        if (e < kk32 && r >= c) {
+          double x = v[j];
+          if (a.policy == CQR_POLICY_UPDATE && a.q > 0) {
+            const double* br = a.Bt + (int64_t)r * a.ldbt;
+            const double* bc = a.Bt + (int64_t)c * a.ldbt;
+            double d = 0.0;
+            for (int l = 0; l < a.q; ++l) d += br[l] * bc[l];
+            x = x - d;
+          }
+          X[(int64_t)c * k + r] = x;
+          X[(int64_t)r * k + c] = x;
+          const double d = x - ((r == c) ? 1.0 : 0.0);
+          loc += ((r == c) ? 1.0 : 2.0) * (d * d);
         }
-        X[(int64_t)c * k + r] = x;
-        X[(int64_t)r * k + c] = x;
-        const double d = x - ((r == c) ? 1.0 : 0.0);
-        loc += ((r == c) ? 1.0 : 2.0) * (d * d);
       }
     }
-  }
-  __syncthreads();
-  const double err = sqrt(block_sum(loc, red));
-  // decision-margin scale: max diag of the undeflated Gram (for updates the
-  // deflated X is itself at rounding level when the block is dependent)
-  double dml = -INFINITY;
-  for (int j = tid; j < k; j += FK_THREADS) dml = fmax(dml, a.G[(int64_t)j * a.ldg + j]);
-  const double dm = block_max(dml, red);
-  if (tid == 0) {
-    fs.err = err;
+    __syncthreads();
+    const double err = sqrt(block_sum(loc, red));
+    // decision-margin scale: max diag of the undeflated Gram (for updates the
+    // deflated X is itself at rounding level when the block is dependent)
+    double dml = -INFINITY;
+    for (int j = tid; j < k; j += FK_THREADS) dml = fmax(dml, a.G[(int64_t)j * a.ldg + j]);
+    const double dm = block_max(dml, red);
+    if (tid == 0) {
+      fs.err = err;
+      fs.diag_max = dm;
+    }
+  } else if (tid == 0) {
+    // X was formed in global memory by factor_prep_kernel; its per-tile
+    // partials are combined here in tile order (fixed, so deterministic)
+    const int nt = (k + 31) / 32, ntiles = nt * (nt + 1) / 2;
+    double e2 = 0.0, dm = -INFINITY;
+    for (int b = 0; b < ntiles; ++b) {
+      e2 += a.part[2 * b];
+      dm = fmax(dm, a.part[2 * b + 1]);
+    }
+    fs.err = sqrt(e2);
     fs.diag_max = dm;
   }
   __syncthreads();
-
+  const double err = fs.err;
   fmark(1);
   // `while not err < tol: if its == max_iter: ...` (algorithms.py:341-343):
   // convergence is tested before the iteration cap.
@@ -1010,7 +1089,8 @@ __global__ void __launch_bounds__(FK_THREADS, 1) factor_kernel(FactorArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// finish: one CTA per 8-column block J, everything in 8x8 blocks with DMMA
+// finish: two CTAs per 8-column block J (one for B/Racc, one for Rinv),
+// everything in 8x8 blocks with DMMA
 //   B(:, J)     += Bt Racc_old(:, J)                      (algorithms.py:445)
 //   Racc(I, J)   = sum_{L=I..J} Rk(I, L) Racc_old(L, J)   (kernels.py:103-114, triu)
 //   Rinv(I, J)   = inv(R_II) (delta_IJ - sum_{L>I} R(I, L) Rinv(L, J)),
@@ -1029,7 +1109,10 @@ __device__ __forceinline__ double frag_b(const double* M, int ldm, int L, int J,
 }
 
 __global__ void __launch_bounds__(FF_WARPS * 32) factor_finish_kernel(FactorArgs a) {
-  // sOld (Racc_old(:, J), first phase) and sX (Rinv(I, J) blocks, second phase) share storage
+  // Two independent CTA roles per 8-column block J, run side by side:
+  //   role 1 (blockIdx >= nblk): B += Bt Racc_old(:, J); Racc(:, J) <- Rk Racc_old(:, J)
+  //   role 0: inverses of the diagonal blocks, Rinv(:, J) by block back substitution
+  // sOld (Racc_old(:, J), role 1) and sX (Rinv(I, J) blocks, role 0) share storage
   __shared__ double sU[256 * 9];
   __shared__ double sInv[32][64];      // inv(R_II), column-major 8x8
   __shared__ double sPart[FF_WARPS][64];
@@ -1037,36 +1120,37 @@ __global__ void __launch_bounds__(FF_WARPS * 32) factor_finish_kernel(FactorArgs
   double (*sX)[64] = reinterpret_cast<double (*)[64]>(sU);   // 32 blocks, column-major 8x8
   if (a.st->code != CQR_FACTORED) return;
   const int k = a.k;
-  const int J = blockIdx.x;
-  const bool prof = (J == (int)gridDim.x - 1 && threadIdx.x == 0);   // the longest column block
+  const int nblk = (k + 7) / 8;
+  const int role = (int)blockIdx.x / nblk;
+  const int J = (int)blockIdx.x - role * nblk;
+  const bool prof = (J == nblk - 1 && threadIdx.x == 0);   // the longest column block
   long long fc0 = prof ? clock64() : 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int ldr = a.ldr;
-  const int KP = (int)round_up(k, 32);
   const double* R = a.Rk;
   const int nrow = 8 * J + 8;          // rows 0 .. 8J+7 of the column block
 
-  // ---- stage Racc_old(:, J) (rows < nrow) and update B with it
-  for (int e = threadIdx.x; e < nrow * 8; e += FF_WARPS * 32) {
-    const int r = e % nrow, cl = e / nrow, c = 8 * J + cl;
-    sOld[r][cl] = (c < k) ? a.Racc[(int64_t)c * ldr + r] : ((r == c) ? 1.0 : 0.0);
-  }
-  __syncthreads();
-  if (a.update_b && a.q > 0) {
-    for (int e = threadIdx.x; e < a.q * 8; e += FF_WARPS * 32) {
-      const int i = e % a.q, cl = e / a.q, c = 8 * J + cl;
-      if (c >= k) continue;
-      double s = 0.0;
-      for (int l = 0; l <= c; ++l) s += a.Bt[(int64_t)l * a.ldbt + i] * sOld[l][cl];
-      a.B[(int64_t)c * a.ldb + i] = a.B[(int64_t)c * a.ldb + i] + s;
+  if (role == 1) {
+    // ---- stage Racc_old(:, J) (rows < nrow) and update B with it
+    for (int e = threadIdx.x; e < nrow * 8; e += FF_WARPS * 32) {
+      const int r = e % nrow, cl = e / nrow, c = 8 * J + cl;
+      sOld[r][cl] = (c < k) ? a.Racc[(int64_t)c * ldr + r] : ((r == c) ? 1.0 : 0.0);
     }
-  }
-  // ---- Racc(I, J) = sum_L Rk(I, L) Racc_old(L, J): warps over I, results kept in registers
-  double accs[4][2];
-  int nmine = 0;
-  if (a.accumulate) {
-    for (int I = warp; I <= J; I += FF_WARPS, ++nmine) {
+    __syncthreads();
+    if (a.update_b && a.q > 0) {
+      for (int e = threadIdx.x; e < a.q * 8; e += FF_WARPS * 32) {
+        const int i = e % a.q, cl = e / a.q, c = 8 * J + cl;
+        if (c >= k) continue;
+        double s = 0.0;
+        for (int l = 0; l <= c; ++l) s += a.Bt[(int64_t)l * a.ldbt + i] * sOld[l][cl];
+        a.B[(int64_t)c * a.ldb + i] = a.B[(int64_t)c * a.ldb + i] + s;
+      }
+    }
+    if (!a.accumulate) return;
+    // ---- Racc(I, J) = sum_L Rk(I, L) Racc_old(L, J): warps over I.  Only this
+    // CTA reads or writes column block J of Racc (its old values are staged)
+    for (int I = warp; I <= J; I += FF_WARPS) {
       double c2[2] = {0.0, 0.0};
       const int ra = 8 * I + g;
       // Rk(I, L) fragments come from L2: load 4 L steps at once so the
@@ -1088,11 +1172,15 @@ __global__ void __launch_bounds__(FF_WARPS * 32) factor_finish_kernel(FactorArgs
           for (int h = 0; h < 2; ++h) dmma(c2, av[j][h], sOld[8 * L + t + 4 * h][g]);
         }
       }
-      accs[nmine][0] = c2[0];
-      accs[nmine][1] = c2[1];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int r = 8 * I + g, c = 8 * J + 2 * t + e;
+        if (c < k && r < k) a.Racc[(int64_t)c * ldr + r] = (r <= c) ? c2[e] : 0.0;
+      }
     }
+    if (prof) g_fprof[13] = (unsigned long long)(clock64() - fc0);
+    return;
   }
-  if (prof) g_fprof[13] = (unsigned long long)(clock64() - fc0);
   // ---- inverses of the diagonal blocks I <= J (warp per block, lanes 0..7 one column each)
   // all 32 lanes: lane = 8 * sub + cl handles block I = warp + 8 (4 i + sub)
   // column cl (four blocks per warp at once); the 8 diagonal reciprocals are
@@ -1127,17 +1215,6 @@ __global__ void __launch_bounds__(FF_WARPS * 32) factor_finish_kernel(FactorArgs
     }
   }
   __syncthreads();
-  // ---- write Racc(:, J) (all reads of Racc_old(:, J) are done: staged in smem)
-  if (a.accumulate) {
-    int n2 = 0;
-    for (int I = warp; I <= J; I += FF_WARPS, ++n2) {
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int r = 8 * I + g, c = 8 * J + 2 * t + e;
-        if (c < k && r < k) a.Racc[(int64_t)c * ldr + r] = (r <= c) ? accs[n2][e] : 0.0;
-      }
-    }
-  }
   // ---- block back substitution for Rinv(:, J); the R(I, L) fragments of the
   // next step are prefetched into registers while the current step runs
   auto load_row = [&](int I, double (&fr)[4][2]) {
@@ -1201,7 +1278,6 @@ __global__ void __launch_bounds__(FF_WARPS * 32) factor_finish_kernel(FactorArgs
     __syncthreads();
   }
   if (prof) g_fprof[15] = (unsigned long long)(clock64() - fc0);
-  (void)KP;
 }
 
 // generic (k > 256) finish: one warp per column, R columns staged through
@@ -1289,8 +1365,10 @@ int factor_profile(unsigned long long* out) {
 
 size_t factor_workspace_bytes(int k) {
   // X (k^2) | W + Ri (k (k+1)) | speculative CTA: Rk1 (k x round_up(k, 32)), W1 (k (k+1)), shifts1 (1024), pub (64)
+  // | prep partials (2 per 32 x 32 tile of the lower triangle)
   const size_t kk = (size_t)k;
-  return (kk * kk + 2 * kk * (kk + 1) + kk * (size_t)round_up(k, 32) + 1024 + 64) * sizeof(double) + 512;
+  const size_t nt = (kk + 31) / 32;
+  return (kk * kk + 2 * kk * (kk + 1) + kk * (size_t)round_up(k, 32) + 1024 + 64 + nt * (nt + 1)) * sizeof(double) + 512;
 }
 
 cudaError_t factor_launch(FactorArgs& a, cudaStream_t stream) {
@@ -1317,12 +1395,16 @@ cudaError_t factor_launch(FactorArgs& a, cudaStream_t stream) {
   }
   static unsigned epoch = 0;
   a.epoch = ++epoch;   // tags the speculative handshake of this launch (no reset launch needed)
+  if (a.k > FK_SMEM_K) {
+    const int nt = (a.k + 31) / 32;
+    factor_prep_kernel<<<nt * (nt + 1) / 2, FP_THREADS, 0, stream>>>(a);
+  }
   factor_kernel<<<a.spec ? 2 : 1, FK_THREADS, smem, stream>>>(a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int blocks = (a.k + 7) / 8;
   if (a.k <= 256) {
-    factor_finish_kernel<<<blocks, FF_WARPS * 32, 0, stream>>>(a);
+    factor_finish_kernel<<<2 * blocks, FF_WARPS * 32, 0, stream>>>(a);   // two roles per column block
   } else {
     factor_finish_wide_kernel<<<(a.k + FW_WARPS - 1) / FW_WARPS, FW_WARPS * 32,
                                 (size_t)(FW_WARPS + 2) * a.k * sizeof(double), stream>>>(a);

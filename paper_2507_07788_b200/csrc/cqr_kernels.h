@@ -84,6 +84,7 @@ struct FactorArgs {
   double fixed_shift;
   int accumulate; int update_b;
   double* X;       // k*k workspace
+  double* part;    // k > 128: per-tile (err^2, max diag G) partials of factor_prep_kernel
   double* W;       // packed-upper workspace (k > smem limit)
   double* Ri;      // packed-upper workspace (k > smem limit)
   double* Rk; double* Rinv; int ldr;   // Rk column-major (ldr); Rinv coefficient tiles
