@@ -407,9 +407,25 @@ __device__ bool chol_banded(double* Wb, int n, int nb, int nbr, int off, double*
 }
 
 __device__ void store_blocked(const double* Wb, int n, int off, double* Rk, int ldr) {
+  // n <= 256; a warp per column pair, all shared loads of the pair before the stores
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int c = warp; c < n; c += FK_NW)
-    for (int i = lane; i <= c; i += 32) Rk[(int64_t)(c + off) * ldr + off + i] = Wb[belem(i, c)];
+  for (int c0 = 2 * warp; c0 < n; c0 += 2 * FK_NW) {
+    double v[2][8];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = c0 + h, i = lane + 32 * u;
+        v[h][u] = (c < n && i <= c) ? Wb[belem(i, c)] : 0.0;
+      }
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = c0 + h, i = lane + 32 * u;
+        if (c < n && i <= c) Rk[(int64_t)(c + off) * ldr + off + i] = v[h][u];
+      }
+  }
 }
 
 // identity padding for rows / columns [n, 8 ceil(n/8)) of a block-packed matrix
@@ -522,9 +538,12 @@ __device__ __forceinline__ void fmark(int slot) {
 
 // One factorization attempt of X + sigma I; on success the factor is in Rk
 // (upper triangle; the caller zeroes the rest).  `smem_w` is the shared work
-// area, `gW` the global fallback for k > FK_BIG_K.  X is symmetric (shared
-// memory for k <= 128, global otherwise).
-__device__ __noinline__ bool chol_attempt(const double* __restrict__ X, int k, double sigma, double* smem_w, double* gW,
+// area, `gW` the global fallback for k > FK_BIG_K.  X is symmetric: Xs in shared
+// memory for k <= 128, else Xg in global memory, read-only for the kernel and
+// read through ld.global.nc (generic loads from one SM run ~4x slower,
+// profiles/r01_single_sm_io.jsonl).
+__device__ __noinline__ bool chol_attempt(const double* __restrict__ Xs, const double* __restrict__ Xg, int k,
+                             double sigma, double* smem_w, double* gW,
                              double* Rk, int ldr, double* rowbuf, FState& fs, int* flag) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   double smin = INFINITY;
@@ -533,7 +552,7 @@ __device__ __noinline__ bool chol_attempt(const double* __restrict__ X, int k, d
     double* Wb = smem_w;
     for (int c = warp; c < k; c += FK_NW)
       for (int i = lane; i <= c; i += 32) {
-        double x = X[c * k + i];
+        double x = Xs[c * k + i];
         if (i == c) x = __dadd_rn(x, sigma);
         Wb[belem(i, c)] = x;
       }
@@ -546,7 +565,7 @@ __device__ __noinline__ bool chol_attempt(const double* __restrict__ X, int k, d
     double* W = gW;   // k x k upper (column-major): X + sigma I, factored in place by bands
     for (int c = warp; c < k; c += FK_NW)
       for (int i = lane; i <= c; i += 32) {
-        double x = X[(int64_t)c * k + i];
+        double x = __ldg(Xg + (int64_t)c * k + i);
         if (i == c) x = __dadd_rn(x, sigma);
         W[(int64_t)c * k + i] = x;
       }
@@ -556,7 +575,7 @@ __device__ __noinline__ bool chol_attempt(const double* __restrict__ X, int k, d
     double* W = gW;
     for (int c = warp; c < k; c += FK_NW)
       for (int i = lane; i <= c; i += 32) {
-        double x = X[(int64_t)c * k + i];
+        double x = __ldg(Xg + (int64_t)c * k + i);
         if (i == c) x = __dadd_rn(x, sigma);
         W[pk(i, c)] = x;
       }
@@ -574,7 +593,7 @@ __device__ __noinline__ bool chol_attempt(const double* __restrict__ X, int k, d
       for (int c = r + lane; c < 8 * nb; c += 32) {
         double x = 0.0;
         if (c < k) {
-          x = X[(int64_t)r * k + c];   // = X(r, c) by symmetry; contiguous in c
+          x = __ldg(Xg + (int64_t)r * k + c);   // = X(r, c) by symmetry; contiguous in c
           if (c == r) x = __dadd_rn(x, sigma);
         }
         Wb[band(r >> 3, c >> 3) + (c & 7) * 8 + (r & 7)] = x;
@@ -583,39 +602,159 @@ __device__ __noinline__ bool chol_attempt(const double* __restrict__ X, int k, d
     ok = chol_banded(Wb, k, nb, 4, 0, rowbuf, smin, fs, band, flag);
     if (ok) {
       // band rows are final rows of R
-      for (int r = warp; r < b; r += FK_NW)
-        for (int c = r + lane; c < k; c += 32) Rk[(int64_t)c * ldr + r] = Wb[band(r >> 3, c >> 3) + (c & 7) * 8 + (r & 7)];
+      // (a warp per column, lanes over the 32 band rows: coalesced)
+      for (int c = warp; c < k; c += FK_NW)
+        if (lane <= c) Rk[(int64_t)c * ldr + lane] = Wb[band(lane >> 3, c >> 3) + (c & 7) * 8 + (lane & 7)];
       __syncthreads();
       fmark(3);
       if (spec_should_stop(fs)) return false;
-      // ---- stage 2: S = X22 - R12^T R12 (block upper, n = k - 32) with DMMA,
-      // fragments of R12 read from Rk (L2); S overwrites the band area
+      // ---- stage 2: S = X22 - R12^T R12 (block upper, n = k - 32) with DMMA.
+      // R12 is read from the band (shared memory; from L2 the re-reads of R12
+      // by every block bound this phase at the SM's L2 bandwidth).  S's block
+      // layout overlays the band for its first `nov` blocks: those are computed
+      // first into registers and stored after a barrier; the rest go straight
+      // to shared memory.
       const int n = k - b;
       double* S = smem_w;
       const int nbs = (n + 7) / 8;
       const int nblk = nbs * (nbs + 1) / 2;
+      const int nov = min(nblk, 4 * nb);          // S blocks inside the band area
       const int g = lane >> 2, t = lane & 3;
-      for (int blk = warp; blk < nblk; blk += FK_NW) {
-        int J = (int)((sqrtf(8.0f * blk + 1.0f) - 1.0f) * 0.5f);
+      auto decode = [&](int blk, int& I, int& J) {
+        J = (int)((sqrtf(8.0f * blk + 1.0f) - 1.0f) * 0.5f);
         while ((J + 1) * (J + 2) / 2 <= blk) ++J;
         while (J * (J + 1) / 2 > blk) --J;
-        const int I = blk - J * (J + 1) / 2;  // I <= J
-        const int ci = b + 8 * I + g, cj = b + 8 * J + g;
-        double acc[2] = {0.0, 0.0};
+        I = blk - J * (J + 1) / 2;  // I <= J
+      };
+      // R12(l, I)^T R12(l, J) for S block (I, J); R12 block column I is band
+      // block column b/8 + I
+      auto sprod = [&](int I, int J, double (&acc)[2]) {
+        const double* pa = Wb + band(0, b / 8 + I) + g * 8 + t;
+        const double* pb = Wb + band(0, b / 8 + J) + g * 8 + t;
+        acc[0] = 0.0; acc[1] = 0.0;
 #pragma unroll
-        for (int l0 = 0; l0 < FK_PANEL; l0 += 4) {
-          const double av = (ci < k) ? Rk[(int64_t)ci * ldr + l0 + t] : 0.0;
-          const double bv = (cj < k) ? Rk[(int64_t)cj * ldr + l0 + t] : 0.0;
-          dmma(acc, av, bv);
+        for (int q4 = 0; q4 < FK_PANEL / 4; ++q4) {
+          const int o = (q4 >> 1) * 64 + 4 * (q4 & 1);   // band block row q4/2, rows 4 (q4 & 1) + t
+          dmma(acc, pa[o], pb[o]);
         }
+      };
+      auto sstore = [&](int I, int J, const double (&v)[2]) {
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int i = 8 * I + g, c = 8 * J + 2 * t + e;  // trailing coordinates
-          if (i <= c && c < n) {
-            double x = X[(int64_t)(b + c) * k + b + i];
-            if (i == c) x = __dadd_rn(x, sigma);
-            S[belem(i, c)] = x - acc[e];
+          const int i = 8 * I + g, c = 8 * J + 2 * t + e;
+          if (i <= c && c < n) S[belem(i, c)] = v[e];
+        }
+      };
+      // X22 (+ sigma on the diagonal), the overlay blocks' share into registers
+      // (all loads in flight at once) and the rest straight into S
+      constexpr int NOV_W = (4 * (FK_BIG_K / 8) + FK_NW - 1) / FK_NW;   // overlay blocks per warp
+      {
+        // a warp per column pair, lanes down the rows: X22 column c (rows <= c)
+        // is contiguous in X; every load of the pair is in flight at once
+        constexpr int RU = (FK_BIG_K - FK_PANEL + 31) / 32;   // row chunks per column (n <= 224)
+        for (int c0 = 2 * warp; c0 < n; c0 += 2 * FK_NW) {
+          double v[2][RU];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c = c0 + h, J = c >> 3, jb = J * (J + 1) / 2;
+            const int i0 = max(0, (nov - jb) * 8);     // rows of blocks outside the overlay
+            const double* src = Xg + (int64_t)(b + c) * k + b;
+#pragma unroll
+            for (int u = 0; u < RU; ++u) {
+              const int i = lane + 32 * u;
+              v[h][u] = (c < n && i >= i0 && i <= c) ? __ldg(src + i) : 0.0;
+            }
           }
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c = c0 + h, J = c >> 3, jb = J * (J + 1) / 2;
+            const int i0 = max(0, (nov - jb) * 8);
+#pragma unroll
+            for (int u = 0; u < RU; ++u) {
+              const int i = lane + 32 * u;
+              if (c < n && i >= i0 && i <= c) S[belem(i, c)] = (i == c) ? __dadd_rn(v[h][u], sigma) : v[h][u];
+            }
+          }
+        }
+      }
+      double keep[NOV_W][2];
+#pragma unroll
+      for (int j = 0; j < NOV_W; ++j) {
+        const int blk = warp + FK_NW * j;
+        int I = 0, J = 0;
+        if (blk < nov) decode(blk, I, J);
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int i = 8 * I + g, c = 8 * J + 2 * t + e;
+          keep[j][e] = (blk < nov && i <= c && c < n) ? __ldg(Xg + (int64_t)(b + c) * k + b + i) : 0.0;
+        }
+      }
+      __syncthreads();   // S holds X22 + sigma I outside the overlay
+#pragma unroll
+      for (int j = 0; j < NOV_W; ++j) {
+        const int blk = warp + FK_NW * j;
+        if (blk < nov) {
+          int I, J;
+          decode(blk, I, J);
+          double acc[2];
+          sprod(I, J, acc);
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            double x = keep[j][e];
+            if (8 * I + g == 8 * J + 2 * t + e) x = __dadd_rn(x, sigma);
+            keep[j][e] = x - acc[e];
+          }
+        }
+      }
+      // two vertically adjacent blocks (I, J), (I + 1, J) per iteration where
+      // the column allows: the B fragment is loaded once for both (3 shared
+      // loads per 2 DMMA) and the two chains overlap
+      for (int blk = nov + 2 * warp; blk < nblk; blk += 2 * FK_NW) {
+        int I, J;
+        decode(blk, I, J);
+        const bool two = blk + 1 < nblk;
+        double acc0[2] = {0.0, 0.0}, acc1[2] = {0.0, 0.0};
+        int I1 = I + 1, J1 = J;
+        if (I == J) { I1 = 0; J1 = J + 1; }   // blk + 1 opens the next column
+        if (I1 <= J1 && J1 == J) {
+          const double* pa0 = Wb + band(0, b / 8 + I) + g * 8 + t;
+          const double* pa1 = Wb + band(0, b / 8 + I1) + g * 8 + t;
+          const double* pb = Wb + band(0, b / 8 + J) + g * 8 + t;
+#pragma unroll
+          for (int q4 = 0; q4 < FK_PANEL / 4; ++q4) {
+            const int o = (q4 >> 1) * 64 + 4 * (q4 & 1);
+            const double bv = pb[o];
+            dmma(acc0, pa0[o], bv);
+            dmma(acc1, pa1[o], bv);
+          }
+        } else {
+          sprod(I, J, acc0);
+          if (two) sprod(I1, J1, acc1);
+        }
+        double v[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int i = 8 * I + g, c = 8 * J + 2 * t + e;
+          v[e] = (i <= c && c < n) ? S[belem(i, c)] - acc0[e] : 0.0;
+        }
+        sstore(I, J, v);
+        if (two) {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int i = 8 * I1 + g, c = 8 * J1 + 2 * t + e;
+            v[e] = (i <= c && c < n) ? S[belem(i, c)] - acc1[e] : 0.0;
+          }
+          sstore(I1, J1, v);
+        }
+      }
+      __syncthreads();   // every read of the band is done
+#pragma unroll
+      for (int j = 0; j < NOV_W; ++j) {
+        const int blk = warp + FK_NW * j;
+        if (blk < nov) {
+          int I, J;
+          decode(blk, I, J);
+          sstore(I, J, keep[j]);
         }
       }
       pad_blocked(S, n);
@@ -639,8 +778,10 @@ __device__ __noinline__ bool chol_attempt(const double* __restrict__ X, int k, d
 // spectral_norm_estimate (kernels.py:126-178) on the full symmetric X.
 // Returns the estimate; sets fs.est_flag (1 stalled, 2 not converged) and
 // fs.code = CQR_ASYMMETRIC on the asymmetry ValueError.
+template <bool GX>
 __device__ double norm_estimate(const double* __restrict__ X, int k, double tol, int max_iter, double* vec,
                                 double* wv, double* red, FState& fs) {
+  auto ldx = [&](int64_t i) { return GX ? __ldg(X + i) : X[i]; };
   const int tid = threadIdx.x;
   const int64_t kk = (int64_t)k * k;
   double loc = 0.0, la = 0.0;
@@ -648,9 +789,9 @@ __device__ double norm_estimate(const double* __restrict__ X, int k, double tol,
   for (int c = tid >> 5; c < k; c += FK_NW)
 #pragma unroll 4
     for (int i = tid & 31; i < k; i += 32) {
-      const double x = X[(int64_t)c * k + i];
+      const double x = ldx((int64_t)c * k + i);
       loc += x * x;
-      const double d = x - X[(int64_t)i * k + c];
+      const double d = x - ldx((int64_t)i * k + c);
       la += d * d;
     }
   const double fro = sqrt(block_sum(loc, red));
@@ -676,7 +817,7 @@ __device__ double norm_estimate(const double* __restrict__ X, int k, double tol,
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           const int i = i0 + r * FK_NW;
-          if (i < k) acc[r] += X[(int64_t)i * k + c] * vc;
+          if (i < k) acc[r] += ldx((int64_t)i * k + c) * vc;
         }
       }
 #pragma unroll
@@ -716,6 +857,13 @@ __device__ double norm_estimate(const double* __restrict__ X, int k, double tol,
   }
   if (tid == 0) { fs.est_flag = 2; g_fprof[8] = max_iter; }
   return fro;
+}
+
+// X in shared memory (k <= 128) or global memory
+__device__ __forceinline__ double norm_estimate_x(const double* Xs, const double* Xg, int k, double tol, int max_iter,
+                                                  double* vec, double* wv, double* red, FState& fs) {
+  return (k <= FK_SMEM_K) ? norm_estimate<false>(Xs, k, tol, max_iter, vec, wv, red, fs)
+                          : norm_estimate<true>(Xg, k, tol, max_iter, vec, wv, red, fs);
 }
 
 // k > 128: X = G (or G - Bt^T Bt), symmetric from the lower triangle, formed in
@@ -801,8 +949,9 @@ __global__ void __launch_bounds__(FK_THREADS, 1) factor_kernel(FactorArgs a) {
   double* wv = vec + kpad;
   // k <= 128: X itself lives in shared memory (k^2 doubles) before the work area
   const bool xs = (k <= FK_SMEM_K);
-  double* X = xs ? wv + kpad : a.X;
-  double* Wsm = xs ? X + (int64_t)k * k : wv + kpad;   // shared work area
+  double* Xs = wv + kpad;                // X in shared memory (k <= 128)
+  const double* Xg = a.X;                // X in global memory (k > 128, formed by factor_prep_kernel)
+  double* Wsm = xs ? Xs + (int64_t)k * k : wv + kpad;   // shared work area
   // speculative CTA 1 (RECOMPUTE): private R, work matrix and shift list; X
   // in global memory (k > 128) is formed identically by both CTAs
   const bool spec1 = a.spec && blockIdx.x == 1;
@@ -855,8 +1004,8 @@ __global__ void __launch_bounds__(FK_THREADS, 1) factor_kernel(FactorArgs a) {
             for (int l = 0; l < a.q; ++l) d += br[l] * bc[l];
             x = x - d;
           }
-          X[(int64_t)c * k + r] = x;
-          X[(int64_t)r * k + c] = x;
+          Xs[(int64_t)c * k + r] = x;
+          Xs[(int64_t)r * k + c] = x;
           const double d = x - ((r == c) ? 1.0 : 0.0);
           loc += ((r == c) ? 1.0 : 2.0) * (d * d);
         }
@@ -906,15 +1055,15 @@ __global__ void __launch_bounds__(FK_THREADS, 1) factor_kernel(FactorArgs a) {
     const double u2 = 2.0 * a.u;
     switch (a.policy) {
       case CQR_POLICY_PLAIN:
-        ok = chol_attempt(X, k, 0.0, Wsm, a.W, a.Rk, a.ldr, rowbuf, fs, &sflag);
+        ok = chol_attempt(Xs, Xg, k, 0.0, Wsm, a.W, a.Rk, a.ldr, rowbuf, fs, &sflag);
         break;
       case CQR_POLICY_FIXED_SHIFT:
         sigma = a.fixed_shift;
         if (tid == 0) { a.shifts[0] = sigma; fs.n_shifts = 1; }
-        ok = chol_attempt(X, k, sigma, Wsm, a.W, a.Rk, a.ldr, rowbuf, fs, &sflag);
+        ok = chol_attempt(Xs, Xg, k, sigma, Wsm, a.W, a.Rk, a.ldr, rowbuf, fs, &sflag);
         break;
       case CQR_POLICY_ESTIMATE: {
-        const double est = norm_estimate(X, k, a.est_tol, a.est_max_iter, vec, wv, red, fs);
+        const double est = norm_estimate_x(Xs, Xg, k, a.est_tol, a.est_max_iter, vec, wv, red, fs);
         __syncthreads();
         if (tid == 0) {
           if (fs.code != CQR_ASYMMETRIC) fs.code = CQR_ESTIMATED;
@@ -925,12 +1074,12 @@ __global__ void __launch_bounds__(FK_THREADS, 1) factor_kernel(FactorArgs a) {
         break;
       }
       case CQR_POLICY_SHIFT_ONCE: {
-        const double est = norm_estimate(X, k, a.est_tol, a.est_max_iter, vec, wv, red, fs);
+        const double est = norm_estimate_x(Xs, Xg, k, a.est_tol, a.est_max_iter, vec, wv, red, fs);
         __syncthreads();
         if (fs.code == CQR_ASYMMETRIC) { done = true; break; }
         sigma = shift_value(a.m_global, a.shift_width, est, a.u);
         if (tid == 0) { fs.est_calls = 1; fs.norm_est = est; a.shifts[0] = sigma; fs.n_shifts = 1; }
-        ok = chol_attempt(X, k, sigma, Wsm, a.W, a.Rk, a.ldr, rowbuf, fs, &sflag);
+        ok = chol_attempt(Xs, Xg, k, sigma, Wsm, a.W, a.Rk, a.ldr, rowbuf, fs, &sflag);
         break;
       }
       case CQR_POLICY_RECOMPUTE: {
@@ -940,10 +1089,10 @@ __global__ void __launch_bounds__(FK_THREADS, 1) factor_kernel(FactorArgs a) {
           if (tid == 0) fs.attempts = 1;
           __syncthreads();
         } else {
-          ok = chol_attempt(X, k, 0.0, Wsm, a.W, a.Rk, a.ldr, rowbuf, fs, &sflag);
+          ok = chol_attempt(Xs, Xg, k, 0.0, Wsm, a.W, a.Rk, a.ldr, rowbuf, fs, &sflag);
           if (ok || a.spec) break;
         }
-        const double est = norm_estimate(X, k, a.est_tol, a.est_max_iter, vec, wv, red, fs);
+        const double est = norm_estimate_x(Xs, Xg, k, a.est_tol, a.est_max_iter, vec, wv, red, fs);
         __syncthreads();
         if (fs.code == CQR_ASYMMETRIC) { done = true; break; }
         if (spec_should_stop(fs)) { done = true; break; }
@@ -959,7 +1108,7 @@ __global__ void __launch_bounds__(FK_THREADS, 1) factor_kernel(FactorArgs a) {
           }
           if (tid == 0) shx[nsh] = sigma;
           ++nsh;
-          ok = chol_attempt(X, k, sigma, Wsm, gWx, Rkx, ldrx, rowbuf, fs, &sflag);
+          ok = chol_attempt(Xs, Xg, k, sigma, Wsm, gWx, Rkx, ldrx, rowbuf, fs, &sflag);
           if (ok) break;
           if (fs.aborted) { done = true; break; }   // speculative CTA: the plain attempt held
           if (tid == 0) fs.escalations += 1;
@@ -972,7 +1121,7 @@ __global__ void __launch_bounds__(FK_THREADS, 1) factor_kernel(FactorArgs a) {
         int retries = 0, nsh = 0;
         sigma = 0.0;
         while (true) {
-          ok = chol_attempt(X, k, sigma, Wsm, a.W, a.Rk, a.ldr, rowbuf, fs, &sflag);
+          ok = chol_attempt(Xs, Xg, k, sigma, Wsm, a.W, a.Rk, a.ldr, rowbuf, fs, &sflag);
           if (ok) break;
           ++retries;
           if (retries > a.max_shift_attempts) {
@@ -981,7 +1130,7 @@ __global__ void __launch_bounds__(FK_THREADS, 1) factor_kernel(FactorArgs a) {
             break;
           }
           if (sigma == 0.0) {
-            const double est = norm_estimate(X, k, a.est_tol, a.est_max_iter, vec, wv, red, fs);
+            const double est = norm_estimate_x(Xs, Xg, k, a.est_tol, a.est_max_iter, vec, wv, red, fs);
             __syncthreads();
             if (fs.code == CQR_ASYMMETRIC) { done = true; break; }
             if (tid == 0) { fs.est_calls += 1; fs.norm_est = est; }
@@ -1052,7 +1201,7 @@ __global__ void __launch_bounds__(FK_THREADS, 1) factor_kernel(FactorArgs a) {
     // ---- 4. TriangularSingularError check, decision margin, zero lower part + padding of Rk
     double tl = -INFINITY, zl = INFINITY;
     for (int j = tid; j < k; j += FK_THREADS) {
-      tl = fmax(tl, __dadd_rn(X[(int64_t)j * k + j], sigma));
+      tl = fmax(tl, __dadd_rn(xs ? Xs[(int64_t)j * k + j] : __ldg(Xg + (int64_t)j * k + j), sigma));
       if (a.Rk[(int64_t)j * a.ldr + j] == 0.0) zl = fmin(zl, (double)j);
     }
     const double top = block_max(tl, red);
@@ -1061,9 +1210,13 @@ __global__ void __launch_bounds__(FK_THREADS, 1) factor_kernel(FactorArgs a) {
       if (zfirst < INFINITY) { fs.code = CQR_TRI_SINGULAR; fs.singular_index = (int)zfirst; }
       fs.min_pivot_rel = fs.min_pivot / top;
     }
+    // k <= 256: only the lower parts of the 8 x 8 diagonal blocks here; the
+    // blocks below them are zeroed by factor_finish_kernel (which never reads them)
     const int KP = (int)round_up(k, 32);
-    for (int c = warp; c < k; c += FK_NW)
-      for (int i = c + 1 + lane; i < KP; i += 32) a.Rk[(int64_t)c * a.ldr + i] = 0.0;
+    for (int c = warp; c < k; c += FK_NW) {
+      const int iend = (k <= 256) ? min(KP, (c | 7) + 1) : KP;
+      for (int i = c + 1 + lane; i < iend; i += 32) a.Rk[(int64_t)c * a.ldr + i] = 0.0;
+    }
   }
 
   __syncthreads();
@@ -1180,6 +1333,14 @@ __global__ void __launch_bounds__(FF_WARPS * 32) factor_finish_kernel(FactorArgs
     }
     if (prof) g_fprof[13] = (unsigned long long)(clock64() - fc0);
     return;
+  }
+  // ---- zero Rk below the diagonal blocks in column block J (rows 8J+8 .. KP)
+  {
+    const int KP = (int)round_up(k, 32);
+    for (int e = threadIdx.x; e < 8 * KP; e += FF_WARPS * 32) {
+      const int cl = e / KP, i = e % KP, c = 8 * J + cl;
+      if (c < k && i >= nrow) a.Rk[(int64_t)c * ldr + i] = 0.0;
+    }
   }
   // ---- inverses of the diagonal blocks I <= J (warp per block, lanes 0..7 one column each)
   // all 32 lanes: lane = 8 * sub + cl handles block I = warp + 8 (4 i + sub)

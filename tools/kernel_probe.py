@@ -105,6 +105,11 @@ def main():
             pol = _lib.POLICY_RECOMPUTE
             ms = timeit(lambda: e2.factor(pol, 10**6, kk), a.reps)
             out[f"factor_k{kk}_ms"] = ms
+            # back to back on the stream (no host sync per call), as inside a pass loop
+            def burst():
+                hs = [e2.factor_async(pol, 10**6, kk) for _ in range(e2.nslots)]
+                e2.collect(hs)
+            out[f"factor_k{kk}_stream_ms"] = timeit(burst, max(1, a.reps // e2.nslots)) / e2.nslots
             import ctypes
             buf = (ctypes.c_ulonglong * 16)()
             e2.cx.lib.cqr_debug_factor_profile(buf)
