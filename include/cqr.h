@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define CQR_ABI_VERSION 6
+#define CQR_ABI_VERSION 7
 
 #define CQR_OK 0
 #define CQR_EINVAL (-1)
@@ -91,6 +91,11 @@ typedef struct cqr_factor_config {
   const int32_t* gate;        /* NULL, or the code field of an earlier pass's status in
                                  device memory: unless it is CQR_FACTORED the launch only
                                  writes code = CQR_SKIPPED (lets a host loop run ahead) */
+  struct cqr_factor_status* status_mirror; /* NULL, or pinned host memory: the kernel also writes the
+                                 status there (and the pass's shifts to shifts_mirror), so
+                                 the host reads it after the launch without a D2H copy  */
+  double* shifts_mirror;      /* pinned host memory, >= max_shift_attempts doubles (with
+                                 status_mirror)                                         */
 } cqr_factor_config;
 
 typedef struct cqr_factor_status {

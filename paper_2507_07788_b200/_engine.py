@@ -168,7 +168,11 @@ class Engine:
             policy=policy, shift_width=width, m_global=m_global, unit_roundoff=cfg.unit_roundoff,
             shift_escalation=cfg.shift_escalation, max_shift_attempts=cfg.max_shift_attempts,
             check_tol=1 if check_tol else 0, tol=tol, stop=1 if stop else 0, accumulate=1,
-            update_b=1 if update_b else 0, est_max_iter=100, est_tol=1e-2, fixed_shift=fixed_shift, gate=gate)
+            update_b=1 if update_b else 0, est_max_iter=100, est_tol=1e-2, fixed_shift=fixed_shift, gate=gate,
+            # the kernel writes the status and shifts straight into this slot's
+            # pinned host buffer (no D2H copy on the stream)
+            status_mirror=self.stat_host_all[slot].data_ptr(),
+            shifts_mirror=self.stat_host_all[slot].data_ptr() + STATUS_BYTES)
         bt = self.Bt.data_ptr() if self.Bt is not None else None
         b = self.B.data_ptr() if self.B is not None else None
         base = self.stat_all[slot].data_ptr()
@@ -181,7 +185,6 @@ class Engine:
             cx.timer.stop("factor", t0, (self.k,),
                           gate=self.stat_all[gate_slot] if gate_slot is not None else None)
         cx.launches += 2
-        self.stat_host_all[slot].copy_(self.stat_all[slot], non_blocking=True)
         ev = torch.cuda.Event()
         ev.record(torch.cuda.current_stream(cx.device))
         self._stat_ev[slot] = ev

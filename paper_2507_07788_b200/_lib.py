@@ -43,6 +43,8 @@ class FactorConfig(ctypes.Structure):
         ("est_tol", ctypes.c_double),
         ("fixed_shift", ctypes.c_double),
         ("gate", ctypes.c_void_p),
+        ("status_mirror", ctypes.c_void_p),
+        ("shifts_mirror", ctypes.c_void_p),
     ]
 
 

@@ -312,6 +312,18 @@ int cqr_factor(const cqr_factor_config* cfg, int k, const double* G, int ldg, co
   a.shifts = shifts;
   a.st = status;
   a.gate = cfg->gate;
+  if (cfg->status_mirror != nullptr) {
+    if (cfg->shifts_mirror == nullptr) return fail(CQR_EINVAL, "cqr_factor: status_mirror needs shifts_mirror");
+    void* d1 = nullptr;
+    void* d2 = nullptr;
+    if (cudaHostGetDevicePointer(&d1, cfg->status_mirror, 0) != cudaSuccess ||
+        cudaHostGetDevicePointer(&d2, cfg->shifts_mirror, 0) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(CQR_EINVAL, "cqr_factor: status_mirror / shifts_mirror must be pinned host memory");
+    }
+    a.stm = static_cast<cqr_factor_status*>(d1);
+    a.shm = static_cast<double*>(d2);
+  }
   return cuda_check(cqr::factor_launch(a, static_cast<cudaStream_t>(stream)), "cqr_factor");
 }
 

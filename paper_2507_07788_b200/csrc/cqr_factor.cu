@@ -934,7 +934,10 @@ __global__ void __launch_bounds__(FP_THREADS) factor_prep_kernel(FactorArgs a) {
 __global__ void __launch_bounds__(FK_THREADS, 1) factor_kernel(FactorArgs a) {
   if (a.gate != nullptr && *a.gate != CQR_FACTORED) {
     // gated off (the previous pass did not factor): record it, touch nothing else
-    if (blockIdx.x == 0 && threadIdx.x == 0) a.st->code = CQR_SKIPPED;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      a.st->code = CQR_SKIPPED;
+      if (a.stm != nullptr) { a.stm->code = CQR_SKIPPED; __threadfence_system(); }
+    }
     return;
   }
   extern __shared__ __align__(16) double fsm[];
@@ -1238,6 +1241,14 @@ __global__ void __launch_bounds__(FK_THREADS, 1) factor_kernel(FactorArgs a) {
     st->singular_index = fs.singular_index;
     st->plain_margin = fs.plain_margin;
     st->diag_max = fs.diag_max;
+    if (a.stm != nullptr) {
+      // host-mapped mirror: the host reads the pass's outcome without a D2H copy
+      // (the shifts were written by this thread)
+      cqr_factor_status* hm = a.stm;
+      *hm = *st;
+      for (int i = 0; i < fs.n_shifts; ++i) a.shm[i] = a.shifts[i];
+      __threadfence_system();
+    }
   }
 }
 

@@ -93,6 +93,7 @@ struct FactorArgs {
   double* shifts;
   cqr_factor_status* st;
   const int* gate;   // nullptr, or: skip the pass unless *gate == CQR_FACTORED
+  cqr_factor_status* stm; double* shm;   // host-mapped mirrors of the status and shifts (or nullptr)
   // speculative shifted branch (RECOMPUTE policy): a second CTA runs the
   // estimate + shifted attempts into private buffers while CTA 0 tries the
   // plain factorization; CTA 0 publishes its outcome in `pub` (epoch-tagged)
