@@ -99,6 +99,7 @@ __device__ __forceinline__ double shift_value(int64_t m, int64_t w, double norm,
 struct FState {
   int code, retries, n_shifts, pivot_index, est_calls, est_flag, escalations, singular_index, attempts;
   double pivot_value, err, norm_est, last_shift, min_pivot_rel, sigma, plain_margin, diag_max, min_pivot;
+  double fro;   // ||X||_F (k > 128: from factor_prep_kernel's partials)
   // speculative CTA: the flag CTA 0 publishes and the value meaning "plain attempt held"
   const volatile unsigned long long* spec_flag;
   unsigned long long spec_done;
@@ -154,6 +155,20 @@ __device__ bool chol_packed(double* W, int n, int off, double* rowbuf, double& s
 // Rows/columns >= n are identity padding (pivots 1, no coupling).
 __device__ __forceinline__ int boff(int I, int J) { return (J * (J + 1) / 2 + I) * 64; }
 __device__ __forceinline__ int belem(int i, int c) { return boff(i >> 3, c >> 3) + (c & 7) * 8 + (i & 7); }
+
+// The two k-steps' A (or B) fragments of an 8x8 block for lane (g, t): rows t and
+// t + 4 of block column g, at p[0] and p[4] for p = block + 8 g + t.  Loading
+// the +4 element first on lanes with (g >> 1) & 1 spreads each half-warp's
+// loads over all 32 banks (g and g + 2 share banks at the same offset), halving
+// the shared-memory wavefronts of every fragment load; the values are then
+// swapped back, so each DMMA sees exactly the operands it saw before.
+__device__ __forceinline__ void frag_pair(const double* p, int g, double& lo, double& hi) {
+  const bool sw = (g >> 1) & 1;
+  const double x = p[sw ? 4 : 0];
+  const double y = p[sw ? 0 : 4];
+  lo = sw ? y : x;
+  hi = sw ? x : y;
+}
 
 // block layouts: the full upper triangle, or a band of the first 4 block rows
 struct LayoutUpper {
@@ -266,8 +281,10 @@ __device__ bool chol_blocked(double* Wb, int n, int nb, int P0, int nbr, int off
         const double* pa = Wb + lay(P, P + 1) + g * 8 + t;
         double* pc = Wb + lay(P + 1, P + 1) + 2 * t * 8 + g;
         double c2[2] = {pc[0], pc[8]};
-        dmma(c2, -pa[0], pa[0]);
-        dmma(c2, -pa[4], pa[4]);
+        double p0, p1;
+        frag_pair(pa, g, p0, p1);
+        dmma(c2, -p0, p0);
+        dmma(c2, -p1, p1);
         pc[0] = c2[0];
         pc[8] = c2[1];
         __syncwarp();
@@ -309,7 +326,10 @@ __device__ bool chol_blocked(double* Wb, int n, int nb, int P0, int nbr, int off
         const double* pb0 = Wb + lay(P, J0) + g * 8 + t;
         double* pc0 = Wb + lay(I0, J0) + 2 * t * 8 + g;
         double c0[2] = {pc0[0], pc0[8]};
-        const double a00 = -pa0[0], a01 = -pa0[4], b00 = pb0[0], b01 = pb0[4];
+        double a00, a01, b00, b01;
+        frag_pair(pa0, g, a00, a01);
+        frag_pair(pb0, g, b00, b01);
+        a00 = -a00; a01 = -a01;
         double c1[2] = {0.0, 0.0}, a10 = 0.0, a11 = 0.0, b10 = 0.0, b11 = 0.0;
         double* pc1 = pc0;
         if (two) {
@@ -317,7 +337,9 @@ __device__ bool chol_blocked(double* Wb, int n, int nb, int P0, int nbr, int off
           const double* pb1 = Wb + lay(P, J1) + g * 8 + t;
           pc1 = Wb + lay(I1, J1) + 2 * t * 8 + g;
           c1[0] = pc1[0]; c1[1] = pc1[8];
-          a10 = -pa1[0]; a11 = -pa1[4]; b10 = pb1[0]; b11 = pb1[4];
+          frag_pair(pa1, g, a10, a11);
+          frag_pair(pb1, g, b10, b11);
+          a10 = -a10; a11 = -a11;
         }
         dmma(c0, a00, b00);
         if (two) dmma(c1, a10, b10);
@@ -373,8 +395,12 @@ __device__ void band_trailing_update(double* Wb, int nb, int P0, int P1, Lay lay
       const double* pb0 = Wb + lay(P, J0) + g * 8 + t;
       const double* pa1 = Wb + lay(P, I1) + g * 8 + t;
       const double* pb1 = Wb + lay(P, J1) + g * 8 + t;
-      const double a00 = -pa0[0], a01 = -pa0[4], b00 = pb0[0], b01 = pb0[4];
-      const double a10 = -pa1[0], a11 = -pa1[4], b10 = pb1[0], b11 = pb1[4];
+      double a00, a01, b00, b01, a10, a11, b10, b11;
+      frag_pair(pa0, g, a00, a01);
+      frag_pair(pb0, g, b00, b01);
+      frag_pair(pa1, g, a10, a11);
+      frag_pair(pb1, g, b10, b11);
+      a00 = -a00; a01 = -a01; a10 = -a10; a11 = -a11;
       dmma(c0, a00, b00);
       dmma(c1, a10, b10);
       dmma(c0, a01, b01);
@@ -507,8 +533,12 @@ __device__ bool chol_bands_global(double* W, int k, double* Wb, double* Rk, int 
           const double* pb0 = Wb + band(P, J0) + g * 8 + t;
           const double* pa1 = Wb + band(P, I1) + g * 8 + t;
           const double* pb1 = Wb + band(P, J1) + g * 8 + t;
-          const double a00 = -pa0[0], a01 = -pa0[4], b00 = pb0[0], b01 = pb0[4];
-          const double a10 = -pa1[0], a11 = -pa1[4], b10 = pb1[0], b11 = pb1[4];
+          double a00, a01, b00, b01, a10, a11, b10, b11;
+          frag_pair(pa0, g, a00, a01);
+          frag_pair(pb0, g, b00, b01);
+          frag_pair(pa1, g, a10, a11);
+          frag_pair(pb1, g, b10, b11);
+          a00 = -a00; a01 = -a01; a10 = -a10; a11 = -a11;
           dmma(c0, a00, b00);
           dmma(c1, a10, b10);
           dmma(c0, a01, b01);
@@ -633,9 +663,12 @@ __device__ __noinline__ bool chol_attempt(const double* __restrict__ Xs, const d
         const double* pb = Wb + band(0, b / 8 + J) + g * 8 + t;
         acc[0] = 0.0; acc[1] = 0.0;
 #pragma unroll
-        for (int q4 = 0; q4 < FK_PANEL / 4; ++q4) {
-          const int o = (q4 >> 1) * 64 + 4 * (q4 & 1);   // band block row q4/2, rows 4 (q4 & 1) + t
-          dmma(acc, pa[o], pb[o]);
+        for (int P = 0; P < FK_PANEL / 8; ++P) {   // band block row P: k-steps rows t, 4 + t
+          double a0, a1, b0, b1;
+          frag_pair(pa + 64 * P, g, a0, a1);
+          frag_pair(pb + 64 * P, g, b0, b1);
+          dmma(acc, a0, b0);
+          dmma(acc, a1, b1);
         }
       };
       auto sstore = [&](int I, int J, const double (&v)[2]) {
@@ -721,11 +754,15 @@ __device__ __noinline__ bool chol_attempt(const double* __restrict__ Xs, const d
           const double* pa1 = Wb + band(0, b / 8 + I1) + g * 8 + t;
           const double* pb = Wb + band(0, b / 8 + J) + g * 8 + t;
 #pragma unroll
-          for (int q4 = 0; q4 < FK_PANEL / 4; ++q4) {
-            const int o = (q4 >> 1) * 64 + 4 * (q4 & 1);
-            const double bv = pb[o];
-            dmma(acc0, pa0[o], bv);
-            dmma(acc1, pa1[o], bv);
+          for (int P = 0; P < FK_PANEL / 8; ++P) {
+            double a0, a1, c0, c1, b0, b1;
+            frag_pair(pa0 + 64 * P, g, a0, a1);
+            frag_pair(pa1 + 64 * P, g, c0, c1);
+            frag_pair(pb + 64 * P, g, b0, b1);
+            dmma(acc0, a0, b0);
+            dmma(acc1, c0, b0);
+            dmma(acc0, a1, b1);
+            dmma(acc1, c1, b1);
           }
         } else {
           sprod(I, J, acc0);
@@ -775,57 +812,111 @@ __device__ __noinline__ bool chol_attempt(const double* __restrict__ Xs, const d
   return ok;
 }
 
+// One X v product row block for the power iteration: rows [i0, i0 + nr) of X
+// (row i at Xr + (i - i0) k), lanes striding the row, butterfly sums -- the
+// same per-row operation order wherever the rows come from.
+template <int MR>
+__device__ __forceinline__ void matvec_rows(const double* Xr, int i0, int nr, int k, const double* vec, double* wv,
+                                            bool global) {
+  const int lane = threadIdx.x & 31;
+  double acc[MR];
+#pragma unroll
+  for (int r = 0; r < MR; ++r) acc[r] = 0.0;
+  for (int c = lane; c < k; c += 32) {
+    const double vc = vec[c];
+#pragma unroll
+    for (int r = 0; r < MR; ++r)
+      if (r < nr) acc[r] += (global ? __ldg(Xr + (int64_t)r * k + c) : Xr[(int64_t)r * k + c]) * vc;
+  }
+#pragma unroll
+  for (int r = 0; r < MR; ++r) {
+    const double sr = warp_sum(acc[r]);
+    if (lane == 0 && r < nr) wv[i0 + r] = sr;
+  }
+}
+
 // spectral_norm_estimate (kernels.py:126-178) on the full symmetric X.
 // Returns the estimate; sets fs.est_flag (1 stalled, 2 not converged) and
 // fs.code = CQR_ASYMMETRIC on the asymmetry ValueError.
+// GX (k > 128, X in global memory): X was formed symmetric by construction
+// (factor_prep_kernel mirrors the lower triangle), so the reference's asymmetry
+// check cannot fire and ||X||_F comes from the prep kernel's partials (fs.fro);
+// each X v streams X through the shared work area `ring` with cp.async.bulk,
+// two row chunks in flight per warp (one SM pulls ~80 B/clk that way against
+// ~30 B/clk with loads, profiles/r01_single_sm_io.jsonl).
 template <bool GX>
 __device__ double norm_estimate(const double* __restrict__ X, int k, double tol, int max_iter, double* vec,
-                                double* wv, double* red, FState& fs) {
-  auto ldx = [&](int64_t i) { return GX ? __ldg(X + i) : X[i]; };
+                                double* wv, double* red, FState& fs, double* ring, int ring_doubles) {
   const int tid = threadIdx.x;
-  const int64_t kk = (int64_t)k * k;
-  double loc = 0.0, la = 0.0;
-  (void)kk;
-  for (int c = tid >> 5; c < k; c += FK_NW)
+  double fro;
+  if (!GX) {
+    double loc = 0.0, la = 0.0;
+    for (int c = tid >> 5; c < k; c += FK_NW)
 #pragma unroll 4
-    for (int i = tid & 31; i < k; i += 32) {
-      const double x = ldx((int64_t)c * k + i);
-      loc += x * x;
-      const double d = x - ldx((int64_t)i * k + c);
-      la += d * d;
+      for (int i = tid & 31; i < k; i += 32) {
+        const double x = X[(int64_t)c * k + i];
+        loc += x * x;
+        const double d = x - X[(int64_t)i * k + c];
+        la += d * d;
+      }
+    fro = sqrt(block_sum(loc, red));
+    const double asym = sqrt(block_sum(la, red));
+    if (fro == 0.0) return 0.0;
+    if (asym > 1e-8 * fro) {
+      if (tid == 0) fs.code = CQR_ASYMMETRIC;
+      return fro;
     }
-  const double fro = sqrt(block_sum(loc, red));
-  const double asym = sqrt(block_sum(la, red));
-  if (fro == 0.0) return 0.0;
-  if (asym > 1e-8 * fro) {
-    if (tid == 0) fs.code = CQR_ASYMMETRIC;
-    return fro;
+  } else {
+    fro = fs.fro;
+    if (fro == 0.0) return 0.0;
   }
   const double v0 = 1.0 / sqrt((double)k);
   for (int i = tid; i < k; i += FK_THREADS) vec[i] = v0;
-  __syncthreads();
   const int warp = tid >> 5, lane = tid & 31;
+  // ring: 2 stages per warp of R rows (k even: rows are whole 16-byte units)
+  constexpr int RMAX = 8;
+  const int R = GX && (k % 2 == 0) ? min(RMAX, ring_doubles / (2 * FK_NW * k)) : 0;
+  __shared__ __align__(8) uint64_t rbar[2 * FK_NW];
+  if (R > 0 && tid == 0) {
+    for (int j = 0; j < 2 * FK_NW; ++j) mbar_init(&rbar[j], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int nch = R > 0 ? (k + R - 1) / R : 0;   // row chunks per product
+  uint32_t uses[2] = {0u, 0u};                    // this warp's stage uses (phase parity)
+  auto issue = [&](int ch, int st) {              // lane 0: chunk ch into this warp's stage st
+    const int r0 = ch * R, nr = min(R, k - r0);
+    double* dst = ring + (int64_t)(2 * warp + st) * R * k;
+    fence_proxy_async_smem();
+    mbar_arrive_expect_tx(&rbar[2 * warp + st], (uint32_t)(nr * k * 8));
+    bulk_g2s(dst, X + (int64_t)r0 * k, (uint32_t)(nr * k * 8), &rbar[2 * warp + st]);
+  };
   bool have_prev = false;
   double prev = 0.0;
-  for (int it = 0; it < max_iter; ++it) {
-    // w = X v: warp w owns rows w, w + 16, ... (4 rows in flight); lanes stride
-    // the row (X symmetric: row i is contiguous), fixed-order butterfly sums
-    for (int i0 = warp; i0 < k; i0 += 4 * FK_NW) {
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      for (int c = lane; c < k; c += 32) {
-        const double vc = vec[c];
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const int i = i0 + r * FK_NW;
-          if (i < k) acc[r] += ldx((int64_t)i * k + c) * vc;
-        }
+  double result = fro;
+  bool finished = false;
+  for (int it = 0; it < max_iter && !finished; ++it) {
+    if (R > 0) {
+      // w = X v, chunk ch = warp + FK_NW q of the rows, stage q & 1 of this warp
+      if (lane == 0) {
+        if (warp < nch) issue(warp, 0);
+        if (warp + FK_NW < nch) issue(warp + FK_NW, 1);
       }
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const double sr = warp_sum(acc[r]);
-        const int i = i0 + r * FK_NW;
-        if (lane == 0 && i < k) wv[i] = sr;
+      __syncthreads();   // vec is ready
+      for (int q = 0; warp + FK_NW * q < nch; ++q) {
+        const int ch = warp + FK_NW * q, st = q & 1;
+        mbar_wait(&rbar[2 * warp + st], uses[st] & 1u);
+        ++uses[st];
+        const int r0 = ch * R, nr = min(R, k - r0);
+        matvec_rows<RMAX>(ring + (int64_t)(2 * warp + st) * R * k, r0, nr, k, vec, wv, false);
+        __syncwarp();
+        if (lane == 0 && ch + 2 * FK_NW < nch) issue(ch + 2 * FK_NW, st);
       }
+    } else {
+      __syncthreads();
+      // warp w owns rows w, w + FK_NW, ... (4 rows in flight)
+      for (int i0 = warp * 4; i0 < k; i0 += 4 * FK_NW)
+        matvec_rows<4>(X + (int64_t)i0 * k, i0, min(4, k - i0), k, vec, wv, GX);
     }
     __syncthreads();
     // ||w||^2 and v.w in one two-value reduction
@@ -844,39 +935,60 @@ __device__ double norm_estimate(const double* __restrict__ X, int k, double tol,
     const double nw = sqrt(nw2);
     if (nw == 0.0) {
       if (tid == 0) fs.est_flag = 1;
-      return fro;
+      result = fro;
+      finished = true;
+      break;
     }
     for (int i = tid; i < k; i += FK_THREADS) vec[i] = wv[i] / nw;
     __syncthreads();   // also: red is rewritten next iteration only after this
     if (have_prev && fabs(lam - prev) <= tol * fabs(lam)) {
       if (tid == 0) g_fprof[8] = it + 1;   // iterations of the last estimate (profiling; one CTA runs it)
-      return fabs(lam);
+      result = fabs(lam);
+      finished = true;
+      break;
     }
     prev = lam;
     have_prev = true;
   }
-  if (tid == 0) { fs.est_flag = 2; g_fprof[8] = max_iter; }
-  return fro;
+  if (!finished) {
+    if (tid == 0) { fs.est_flag = 2; g_fprof[8] = max_iter; }
+    result = fro;
+  }
+  __syncthreads();   // every stage consumed: the barriers can go
+  if (R > 0 && tid == 0)
+    for (int j = 0; j < 2 * FK_NW; ++j) asm volatile("mbarrier.inval.shared.b64 [%0];" ::"r"(smem_u32(&rbar[j])) : "memory");
+  __syncthreads();
+  return result;
 }
 
-// X in shared memory (k <= 128) or global memory
+// X in shared memory (k <= 128) or global memory; `ring` is the shared work area
 __device__ __forceinline__ double norm_estimate_x(const double* Xs, const double* Xg, int k, double tol, int max_iter,
-                                                  double* vec, double* wv, double* red, FState& fs) {
-  return (k <= FK_SMEM_K) ? norm_estimate<false>(Xs, k, tol, max_iter, vec, wv, red, fs)
-                          : norm_estimate<true>(Xg, k, tol, max_iter, vec, wv, red, fs);
+                                                  double* vec, double* wv, double* red, FState& fs, double* ring,
+                                                  int ring_doubles) {
+  return (k <= FK_SMEM_K) ? norm_estimate<false>(Xs, k, tol, max_iter, vec, wv, red, fs, ring, ring_doubles)
+                          : norm_estimate<true>(Xg, k, tol, max_iter, vec, wv, red, fs, ring, ring_doubles);
+}
+
+// doubles of the factor kernel's shared work area (after X for k <= 128)
+__host__ __device__ inline int64_t work_doubles(int k) {
+  auto blocked = [](int n) { const int nb = (n + 7) / 8; return (int64_t)nb * (nb + 1) / 2 * 64; };
+  if (k <= FK_SMEM_K) return blocked(k);
+  if (k <= FK_BIG_K) return (int64_t)FK_PANEL * k > blocked(k - FK_PANEL) ? (int64_t)FK_PANEL * k : blocked(k - FK_PANEL);
+  if (k <= FK_BAND_K) return (int64_t)FK_PANEL * round_up(k, 8);
+  return 0;
 }
 
 // k > 128: X = G (or G - Bt^T Bt), symmetric from the lower triangle, formed in
 // global memory by many CTAs ahead of the single-CTA factorization (one CTA
 // per 32 x 32 tile of the lower triangle; the mirrored half goes through
 // shared memory so both stores are coalesced).  Each tile also leaves its
-// share of ||X - I||_F^2 and the max diagonal of G in a.part.
+// share of ||X - I||_F^2, the max diagonal of G and ||X||_F^2 in a.part.
 constexpr int FP_THREADS = 256;
 
 __global__ void __launch_bounds__(FP_THREADS) factor_prep_kernel(FactorArgs a) {
   if (a.gate != nullptr && *a.gate != CQR_FACTORED) return;
   __shared__ double tile[32][33];   // tile[col][row]
-  __shared__ double red[FP_THREADS / 32][2];
+  __shared__ double red[FP_THREADS / 32][3];
   const int k = a.k;
   const int b = blockIdx.x;
   int ti = 0;
@@ -885,7 +997,7 @@ __global__ void __launch_bounds__(FP_THREADS) factor_prep_kernel(FactorArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* X = a.X;
   const bool upd = (a.policy == CQR_POLICY_UPDATE && a.q > 0);
-  double loc = 0.0, dml = -INFINITY;
+  double loc = 0.0, dml = -INFINITY, f2 = 0.0;
   const int r = 32 * ti + lane;
 #pragma unroll
   for (int s = 0; s < 4; ++s) {
@@ -904,6 +1016,7 @@ __global__ void __launch_bounds__(FP_THREADS) factor_prep_kernel(FactorArgs a) {
       X[(int64_t)c * k + r] = x;
       const double d = x - ((r == c) ? 1.0 : 0.0);
       loc += ((r == c) ? 1.0 : 2.0) * (d * d);
+      f2 += ((r == c) ? 1.0 : 2.0) * (x * x);
       if (r == c) dml = fmax(dml, gv);
     }
     tile[cl][lane] = x;
@@ -918,16 +1031,18 @@ __global__ void __launch_bounds__(FP_THREADS) factor_prep_kernel(FactorArgs a) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     loc += __shfl_xor_sync(0xffffffffu, loc, o);
+    f2 += __shfl_xor_sync(0xffffffffu, f2, o);
     dml = fmax(dml, __shfl_xor_sync(0xffffffffu, dml, o));
   }
-  if (lane == 0) { red[warp][0] = loc; red[warp][1] = dml; }
+  if (lane == 0) { red[warp][0] = loc; red[warp][1] = dml; red[warp][2] = f2; }
   __syncthreads();
   if (threadIdx.x == 0) {
-    double e2 = 0.0, dm = -INFINITY;
+    double e2 = 0.0, dm = -INFINITY, ff = 0.0;
 #pragma unroll
-    for (int w = 0; w < FP_THREADS / 32; ++w) { e2 += red[w][0]; dm = fmax(dm, red[w][1]); }
-    a.part[2 * b] = e2;
-    a.part[2 * b + 1] = dm;
+    for (int w = 0; w < FP_THREADS / 32; ++w) { e2 += red[w][0]; dm = fmax(dm, red[w][1]); ff += red[w][2]; }
+    a.part[3 * b] = e2;
+    a.part[3 * b + 1] = dm;
+    a.part[3 * b + 2] = ff;
   }
 }
 
@@ -955,6 +1070,7 @@ __global__ void __launch_bounds__(FK_THREADS, 1) factor_kernel(FactorArgs a) {
   double* Xs = wv + kpad;                // X in shared memory (k <= 128)
   const double* Xg = a.X;                // X in global memory (k > 128, formed by factor_prep_kernel)
   double* Wsm = xs ? Xs + (int64_t)k * k : wv + kpad;   // shared work area
+  const int wdoubles = work_doubles(k);
   // speculative CTA 1 (RECOMPUTE): private R, work matrix and shift list; X
   // in global memory (k > 128) is formed identically by both CTAs
   const bool spec1 = a.spec && blockIdx.x == 1;
@@ -967,7 +1083,7 @@ __global__ void __launch_bounds__(FK_THREADS, 1) factor_kernel(FactorArgs a) {
     fs.code = CQR_FACTORED; fs.retries = 0; fs.n_shifts = 0; fs.pivot_index = -1; fs.est_calls = 0;
     fs.est_flag = 0; fs.escalations = 0; fs.singular_index = -1;
     fs.pivot_value = 0.0; fs.err = 0.0; fs.norm_est = 0.0; fs.last_shift = 0.0; fs.min_pivot_rel = 0.0;
-    fs.sigma = 0.0; fs.attempts = 0; fs.plain_margin = 0.0; fs.diag_max = 0.0; fs.min_pivot = 0.0;
+    fs.sigma = 0.0; fs.attempts = 0; fs.plain_margin = 0.0; fs.diag_max = 0.0; fs.min_pivot = 0.0; fs.fro = 0.0;
     fs.spec_flag = nullptr; fs.spec_done = 0; fs.aborted = 0;
     if (a.spec && blockIdx.x == 1) {
       fs.spec_flag = reinterpret_cast<const volatile unsigned long long*>(a.pub);
@@ -1029,13 +1145,15 @@ __global__ void __launch_bounds__(FK_THREADS, 1) factor_kernel(FactorArgs a) {
     // X was formed in global memory by factor_prep_kernel; its per-tile
     // partials are combined here in tile order (fixed, so deterministic)
     const int nt = (k + 31) / 32, ntiles = nt * (nt + 1) / 2;
-    double e2 = 0.0, dm = -INFINITY;
+    double e2 = 0.0, dm = -INFINITY, ff = 0.0;
     for (int b = 0; b < ntiles; ++b) {
-      e2 += a.part[2 * b];
-      dm = fmax(dm, a.part[2 * b + 1]);
+      e2 += a.part[3 * b];
+      dm = fmax(dm, a.part[3 * b + 1]);
+      ff += a.part[3 * b + 2];
     }
     fs.err = sqrt(e2);
     fs.diag_max = dm;
+    fs.fro = sqrt(ff);
   }
   __syncthreads();
   const double err = fs.err;
@@ -1066,7 +1184,7 @@ __global__ void __launch_bounds__(FK_THREADS, 1) factor_kernel(FactorArgs a) {
         ok = chol_attempt(Xs, Xg, k, sigma, Wsm, a.W, a.Rk, a.ldr, rowbuf, fs, &sflag);
         break;
       case CQR_POLICY_ESTIMATE: {
-        const double est = norm_estimate_x(Xs, Xg, k, a.est_tol, a.est_max_iter, vec, wv, red, fs);
+        const double est = norm_estimate_x(Xs, Xg, k, a.est_tol, a.est_max_iter, vec, wv, red, fs, Wsm, wdoubles);
         __syncthreads();
         if (tid == 0) {
           if (fs.code != CQR_ASYMMETRIC) fs.code = CQR_ESTIMATED;
@@ -1077,7 +1195,7 @@ __global__ void __launch_bounds__(FK_THREADS, 1) factor_kernel(FactorArgs a) {
         break;
       }
       case CQR_POLICY_SHIFT_ONCE: {
-        const double est = norm_estimate_x(Xs, Xg, k, a.est_tol, a.est_max_iter, vec, wv, red, fs);
+        const double est = norm_estimate_x(Xs, Xg, k, a.est_tol, a.est_max_iter, vec, wv, red, fs, Wsm, wdoubles);
         __syncthreads();
         if (fs.code == CQR_ASYMMETRIC) { done = true; break; }
         sigma = shift_value(a.m_global, a.shift_width, est, a.u);
@@ -1095,7 +1213,7 @@ __global__ void __launch_bounds__(FK_THREADS, 1) factor_kernel(FactorArgs a) {
           ok = chol_attempt(Xs, Xg, k, 0.0, Wsm, a.W, a.Rk, a.ldr, rowbuf, fs, &sflag);
           if (ok || a.spec) break;
         }
-        const double est = norm_estimate_x(Xs, Xg, k, a.est_tol, a.est_max_iter, vec, wv, red, fs);
+        const double est = norm_estimate_x(Xs, Xg, k, a.est_tol, a.est_max_iter, vec, wv, red, fs, Wsm, wdoubles);
         __syncthreads();
         if (fs.code == CQR_ASYMMETRIC) { done = true; break; }
         if (spec_should_stop(fs)) { done = true; break; }
@@ -1133,7 +1251,7 @@ __global__ void __launch_bounds__(FK_THREADS, 1) factor_kernel(FactorArgs a) {
             break;
           }
           if (sigma == 0.0) {
-            const double est = norm_estimate_x(Xs, Xg, k, a.est_tol, a.est_max_iter, vec, wv, red, fs);
+            const double est = norm_estimate_x(Xs, Xg, k, a.est_tol, a.est_max_iter, vec, wv, red, fs, Wsm, wdoubles);
             __syncthreads();
             if (fs.code == CQR_ASYMMETRIC) { done = true; break; }
             if (tid == 0) { fs.est_calls += 1; fs.norm_est = est; }
@@ -1537,25 +1655,19 @@ int factor_profile(unsigned long long* out) {
 
 size_t factor_workspace_bytes(int k) {
   // X (k^2) | W + Ri (k (k+1)) | speculative CTA: Rk1 (k x round_up(k, 32)), W1 (k (k+1)), shifts1 (1024), pub (64)
-  // | prep partials (2 per 32 x 32 tile of the lower triangle)
+  // | prep partials (3 per 32 x 32 tile of the lower triangle)
   const size_t kk = (size_t)k;
   const size_t nt = (kk + 31) / 32;
-  return (kk * kk + 2 * kk * (kk + 1) + kk * (size_t)round_up(k, 32) + 1024 + 64 + nt * (nt + 1)) * sizeof(double) + 512;
+  return (kk * kk + 2 * kk * (kk + 1) + kk * (size_t)round_up(k, 32) + 1024 + 64 + 2 * nt * (nt + 1)) * sizeof(double) + 512;
 }
 
 cudaError_t factor_launch(FactorArgs& a, cudaStream_t stream) {
   if (a.k < 1 || a.k > FK_MAX_K) return cudaErrorInvalidValue;
   const int kpad = (int)round_up(a.k, 8);
   size_t smem = (32 + 3 * (size_t)kpad) * sizeof(double);
-  auto blocked = [](int n) { const int nb = (n + 7) / 8; return (int64_t)nb * (nb + 1) / 2 * 64; };
-  if (a.k <= FK_SMEM_K) {
-    smem += ((size_t)a.k * a.k + blocked(a.k)) * sizeof(double);
-  } else if (a.k <= FK_BIG_K) {
-    const int n = a.k - FK_PANEL;
-    smem += (size_t)std::max<int64_t>((int64_t)FK_PANEL * a.k, blocked(n)) * sizeof(double);
-  } else if (a.k <= FK_BAND_K) {
-    smem += (size_t)FK_PANEL * kpad * sizeof(double);   // one 32-row band
-  }
+  // k <= 128: X, then the block-packed triangle; 128 < k <= 256: the band or the
+  // trailing triangle; k <= 768: one 32-row band (work_doubles)
+  smem += ((a.k <= FK_SMEM_K ? (size_t)a.k * a.k : 0) + (size_t)work_doubles(a.k)) * sizeof(double);
   static bool attr_set = false;
   if (!attr_set) {
     const int mx = 220 * 1024;  // <= 227 KB minus the static shared state
