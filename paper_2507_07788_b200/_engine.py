@@ -249,8 +249,21 @@ class Engine:
         """apply_gram may overwrite its input (fused kernel, or k <= 64)."""
         return self.k <= 64 or self.cx.lib.cqr_apply_gram_inplace_ok(self.k) == 1
 
+    def _to_host(self, t):
+        """A column-major device matrix as a row-major numpy array, through a
+        pooled pinned buffer (a pageable copy costs several times more)."""
+        t = t.contiguous()
+        buf = self.cx.acquire_pinned((t.numel() * 8,))
+        try:
+            view = buf.view(torch.float64)[: t.numel()].view(t.shape)
+            view.copy_(t, non_blocking=True)
+            torch.cuda.current_stream(self.cx.device).synchronize()
+            return view.numpy().T.copy()
+        finally:
+            self.cx.release_pinned(buf)
+
     def r_host(self):
-        return self.Racc[:, : self.k].cpu().numpy().T.copy()
+        return self._to_host(self.Racc[:, : self.k])
 
     def b_host(self):
-        return self.B.cpu().numpy().T.copy()
+        return self._to_host(self.B)

@@ -156,6 +156,19 @@ __device__ bool chol_packed(double* W, int n, int off, double* rowbuf, double& s
 __device__ __forceinline__ int boff(int I, int J) { return (J * (J + 1) / 2 + I) * 64; }
 __device__ __forceinline__ int belem(int i, int c) { return boff(i >> 3, c >> 3) + (c & 7) * 8 + (i & 7); }
 
+// Column J of linear upper-triangle block index blk = J (J + 1) / 2 + I, I <= J:
+// an approximate root from the MUFU reciprocal square root, then an exact
+// integer fix-up (the IEEE sqrtf with its slow-path branch showed up as a hot
+// spot of the block loops under ncu source sampling).
+__device__ __forceinline__ int tri_col(int blk) {
+  const float x = 8.0f * (float)blk + 1.0f;
+  int J = (int)((x * __frsqrt_rn(x) - 1.0f) * 0.5f);
+  J = max(J, 0);
+  while ((J + 1) * (J + 2) / 2 <= blk) ++J;
+  while (J * (J + 1) / 2 > blk) --J;
+  return J;
+}
+
 // The two k-steps' A (or B) fragments of an 8x8 block for lane (g, t): rows t and
 // t + 4 of block column g, at p[0] and p[4] for p = block + 8 g + t.  Loading
 // the +4 element first on lanes with (g >> 1) & 1 spreads each half-warp's
@@ -297,9 +310,7 @@ __device__ bool chol_blocked(double* Wb, int n, int nb, int P0, int nbr, int off
       // two blocks per iteration: all loads first, then the DMMAs (ILP)
       auto decode = [&](int blk, int& I, int& Jb) {
         if (nrows_b == ncb) {
-          int J = (int)((sqrtf(8.0f * blk + 1.0f) - 1.0f) * 0.5f);
-          while ((J + 1) * (J + 2) / 2 <= blk) ++J;
-          while (J * (J + 1) / 2 > blk) --J;
+          int J = tri_col(blk);
           I = P + 1 + (blk - J * (J + 1) / 2);
           Jb = P + 1 + J;
         } else {
@@ -373,9 +384,7 @@ __device__ void band_trailing_update(double* Wb, int nb, int P0, int P1, Lay lay
   const int tn = nb - P1;
   const int nblk = tn * (tn + 1) / 2;
   auto decode = [&](int blk, int& I, int& J) {
-    J = (int)((sqrtf(8.0f * blk + 1.0f) - 1.0f) * 0.5f);
-    while ((J + 1) * (J + 2) / 2 <= blk) ++J;
-    while (J * (J + 1) / 2 > blk) --J;
+    J = tri_col(blk);
     I = P1 + blk - J * (J + 1) / 2;
     J += P1;
   };
@@ -506,9 +515,7 @@ __device__ bool chol_bands_global(double* W, int k, double* Wb, double* Rk, int 
       const int tn = nb - 4;
       const int nblk = tn * (tn + 1) / 2;
       auto decode = [&](int blk, int& I, int& J) {
-        J = (int)((sqrtf(8.0f * blk + 1.0f) - 1.0f) * 0.5f);
-        while ((J + 1) * (J + 2) / 2 <= blk) ++J;
-        while (J * (J + 1) / 2 > blk) --J;
+        J = tri_col(blk);
         I = 4 + blk - J * (J + 1) / 2;
         J += 4;
       };
@@ -651,9 +658,7 @@ __device__ __noinline__ bool chol_attempt(const double* __restrict__ Xs, const d
       const int nov = min(nblk, 4 * nb);          // S blocks inside the band area
       const int g = lane >> 2, t = lane & 3;
       auto decode = [&](int blk, int& I, int& J) {
-        J = (int)((sqrtf(8.0f * blk + 1.0f) - 1.0f) * 0.5f);
-        while ((J + 1) * (J + 2) / 2 <= blk) ++J;
-        while (J * (J + 1) / 2 > blk) --J;
+        J = tri_col(blk);
         I = blk - J * (J + 1) / 2;  // I <= J
       };
       // R12(l, I)^T R12(l, J) for S block (I, J); R12 block column I is band
