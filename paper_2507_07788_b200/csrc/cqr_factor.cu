@@ -377,47 +377,64 @@ __device__ bool chol_blocked(double* Wb, int n, int nb, int P0, int nbr, int off
 // [P0, P1) is final: C(I, J) -= sum_P R(P, I)^T R(P, J) for P1 <= I <= J < nb.
 // Each element sees the same DMMA chain (P ascending, k4 0 then 4) as P1-P0
 // separate rank-8 steps, so the result is bitwise the unbanded one.
+// A warp takes a 2 x 2 group of blocks (I0, I1) x (J0, J1): four independent
+// accumulator chains, and each fragment it loads feeds two DMMAs (5 shared
+// loads per 4 DMMAs with the C fragments, against 9 for blocks taken one or
+// two at a time; those ran at ~45 cycles per DMMA per sub-partition, 3x the
+// pipe's 16).  On diagonal groups the (I1, J0) block lies below the diagonal:
+// it is computed and dropped.
 template <typename Lay>
 __device__ void band_trailing_update(double* Wb, int nb, int P0, int P1, Lay lay) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int tn = nb - P1;
-  const int nblk = tn * (tn + 1) / 2;
-  auto decode = [&](int blk, int& I, int& J) {
-    J = tri_col(blk);
-    I = P1 + blk - J * (J + 1) / 2;
-    J += P1;
-  };
-  // two blocks per iteration: two independent DMMA chains in flight
-  for (int blk = warp; blk < nblk; blk += 2 * FK_NW) {
-    const int blk2 = blk + FK_NW;
-    const bool two = blk2 < nblk;
-    int I0, J0, I1 = 0, J1 = 0;
-    decode(blk, I0, J0);
-    if (two) decode(blk2, I1, J1);
-    double* pc0 = Wb + lay(I0, J0) + 2 * t * 8 + g;
-    double* pc1 = two ? Wb + lay(I1, J1) + 2 * t * 8 + g : pc0;
-    double c0[2] = {pc0[0], pc0[8]};
-    double c1[2] = {pc1[0], pc1[8]};
-    for (int P = P0; P < P1; ++P) {
-      const double* pa0 = Wb + lay(P, I0) + g * 8 + t;
-      const double* pb0 = Wb + lay(P, J0) + g * 8 + t;
-      const double* pa1 = Wb + lay(P, I1) + g * 8 + t;
-      const double* pb1 = Wb + lay(P, J1) + g * 8 + t;
-      double a00, a01, b00, b01, a10, a11, b10, b11;
-      frag_pair(pa0, g, a00, a01);
-      frag_pair(pb0, g, b00, b01);
-      frag_pair(pa1, g, a10, a11);
-      frag_pair(pb1, g, b10, b11);
-      a00 = -a00; a01 = -a01; a10 = -a10; a11 = -a11;
-      dmma(c0, a00, b00);
-      dmma(c1, a10, b10);
-      dmma(c0, a01, b01);
-      dmma(c1, a11, b11);
+  const int G = (tn + 1) >> 1;                 // group rows / columns
+  const int ngroups = G * (G + 1) / 2;
+  for (int gidx = warp; gidx < ngroups; gidx += FK_NW) {
+    const int gj = tri_col(gidx), gi = gidx - gj * (gj + 1) / 2;
+    const int I[2] = {P1 + 2 * gi, P1 + 2 * gi + 1};
+    const int J[2] = {P1 + 2 * gj, P1 + 2 * gj + 1};
+    bool live[2][2];
+    double c[2][2][2];
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+      for (int y = 0; y < 2; ++y) {
+        live[x][y] = I[x] <= J[y] && J[y] < nb;
+        const double* pc = Wb + lay(live[x][y] ? I[x] : P1, live[x][y] ? J[y] : P1) + 2 * t * 8 + g;
+        c[x][y][0] = live[x][y] ? pc[0] : 0.0;
+        c[x][y][1] = live[x][y] ? pc[8] : 0.0;
+      }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {   // bands are at most 4 block rows: unrolled, loads hoisted
+      const int P = P0 + q;
+      if (P >= P1) break;
+      double a[2][2], bb[2][2];
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {
+        const int Ix = I[x] < nb ? I[x] : P1;
+        const int Jx = J[x] < nb ? J[x] : P1;
+        frag_pair(Wb + lay(P, Ix) + g * 8 + t, g, a[x][0], a[x][1]);
+        frag_pair(Wb + lay(P, Jx) + g * 8 + t, g, bb[x][0], bb[x][1]);
+        a[x][0] = -a[x][0];
+        a[x][1] = -a[x][1];
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int x = 0; x < 2; ++x)
+#pragma unroll
+          for (int y = 0; y < 2; ++y) dmma(c[x][y], a[x][h], bb[y][h]);
     }
-    pc0[0] = c0[0];
-    pc0[8] = c0[1];
-    if (two) { pc1[0] = c1[0]; pc1[8] = c1[1]; }
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+      for (int y = 0; y < 2; ++y)
+        if (live[x][y]) {
+          double* pc = Wb + lay(I[x], J[y]) + 2 * t * 8 + g;
+          pc[0] = c[x][y][0];
+          pc[8] = c[x][y][1];
+        }
   }
 }
 
