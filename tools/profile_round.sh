@@ -19,8 +19,8 @@ full gram_k64 gram_pairs_kernel python tools/kernel_probe.py --only gram --m 320
 full trmm_k64 gemm_kernel python tools/kernel_probe.py --only apply --m 32000000 --k 64 --reps 1
 full update_q256 update_pass_kernel python tools/kernel_probe.py --only update --m 8000000 --q 256 --k 16 --reps 1
 full update_q64 update_pass_kernel python tools/kernel_probe.py --only update --m 8000000 --q 64 --k 16 --reps 1
-# the k = 256 factor launch (after the probe's setup call and the k = 64 and k = 128 ones)
-"python" tools/kernel_probe.py --only factor --reps 1 > /dev/null 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:factor_kernel --launch-skip 5 -c 1 \
-      -o gpurun_out/prof/factor_k256 python tools/kernel_probe.py --only factor --reps 1 > gpurun_out/prof/factor_k256.log 2>&1
+# the k = 256 factor launch (the second one: after the probe's warm-up call)
+"python" tools/kernel_probe.py --only factor --fk 256 --reps 1 > /dev/null 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:factor_kernel --launch-skip 1 -c 1 \
+      -o gpurun_out/prof/factor_k256 python tools/kernel_probe.py --only factor --fk 256 --reps 1 > gpurun_out/prof/factor_k256.log 2>&1
 ls -la gpurun_out/prof
