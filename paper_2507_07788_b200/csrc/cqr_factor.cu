@@ -262,8 +262,18 @@ __device__ bool chol_blocked(double* Wb, int n, int nb, int P0, int nbr, int off
   }
   __syncthreads();
   if (*flag) return false;
+  // speculative CTA: thread 0 polls CTA 0's flag once per step without
+  // waiting on it -- the load issued in one step is tested in the next
+  unsigned long long spec_pend = 0;
+  bool spec_have = false;
   for (int P = P0; P < nbr; ++P) {
     const long long c0 = clock64();
+    int spec_abort = 0;
+    if (tid == 0 && fs.spec_flag != nullptr) {
+      if (spec_have && spec_pend == fs.spec_done) { spec_abort = 1; fs.aborted = 1; }
+      spec_pend = *fs.spec_flag;
+      spec_have = true;
+    }
     const double* D = Wb + lay(P, P);
     // ---- (b) panel: R_PJ = R_PP^{-T} W_PJ, one column per thread
     const int ncols = 8 * (nb - 1 - P);
@@ -305,7 +315,7 @@ __device__ bool chol_blocked(double* Wb, int n, int nb, int P0, int nbr, int off
         f = diag_block_warp(Wb + lay(P + 1, P + 1), P + 1, n, off, inv, smin, fs);
         if (lane == 0 && blockIdx.x == 0) atomicAdd(&g_fprof[12], (unsigned long long)(clock64() - cd));
       }
-      if (lane == 0) *flag = f;
+      if (lane == 0) *flag = f | spec_abort;
     } else {
       // two blocks per iteration: all loads first, then the DMMAs (ILP)
       auto decode = [&](int blk, int& I, int& Jb) {
@@ -448,7 +458,6 @@ __device__ bool chol_banded(double* Wb, int n, int nb, int nbr, int off, double*
                             Lay lay, int* flag) {
   for (int P0 = 0; P0 < nbr; P0 += 4) {
     const int P1 = min(nbr, P0 + 4);
-    if (spec_should_stop(fs)) return false;
     if (!chol_blocked(Wb, n, nb, P0, P1, off, inv, smin, fs, lay, flag)) return false;
     if (P1 < nbr) {
       band_trailing_update(Wb, nb, P0, P1, lay);
@@ -662,159 +671,101 @@ __device__ __noinline__ bool chol_attempt(const double* __restrict__ Xs, const d
       __syncthreads();
       fmark(3);
       if (spec_should_stop(fs)) return false;
-      // ---- stage 2: S = X22 - R12^T R12 (block upper, n = k - 32) with DMMA.
-      // R12 is read from the band (shared memory; from L2 the re-reads of R12
-      // by every block bound this phase at the SM's L2 bandwidth).  S's block
-      // layout overlays the band for its first `nov` blocks: those are computed
-      // first into registers and stored after a barrier; the rest go straight
-      // to shared memory.
+      // ---- stage 2: S = X22 + sigma I - R12^T R12 (block upper, n = k - 32) with DMMA.
+      // A warp takes 2 x 2 groups of S blocks (four accumulator chains; each
+      // R12 fragment, read from the band in shared memory, feeds two DMMAs) and
+      // loads its X22 values as C fragments straight from L2 at the start of
+      // the group, so their latency hides under the DMMA chains.  S's block
+      // layout overlays the band for its first block columns: the groups that
+      // touch them (group columns <= GJO) are kept in registers and stored
+      // after a barrier; the others are stored at once.
       const int n = k - b;
       double* S = smem_w;
       const int nbs = (n + 7) / 8;
       const int nblk = nbs * (nbs + 1) / 2;
       const int nov = min(nblk, 4 * nb);          // S blocks inside the band area
       const int g = lane >> 2, t = lane & 3;
-      auto decode = [&](int blk, int& I, int& J) {
-        J = tri_col(blk);
-        I = blk - J * (J + 1) / 2;  // I <= J
-      };
-      // R12(l, I)^T R12(l, J) for S block (I, J); R12 block column I is band
-      // block column b/8 + I
-      auto sprod = [&](int I, int J, double (&acc)[2]) {
-        const double* pa = Wb + band(0, b / 8 + I) + g * 8 + t;
-        const double* pb = Wb + band(0, b / 8 + J) + g * 8 + t;
-        acc[0] = 0.0; acc[1] = 0.0;
+      const int G = (nbs + 1) >> 1;               // group rows / columns
+      const int ngroups = G * (G + 1) / 2;
+      int GJO = -1;                               // last group column that can touch the overlay
+      while (GJO + 1 < G && (2 * (GJO + 1)) * (2 * (GJO + 1) + 1) / 2 < nov) ++GJO;
+      const int nog = (GJO + 1) * (GJO + 2) / 2;  // groups gidx < nog are kept
+      // one group: v[x][y][e] = S values of blocks (2gi + x, 2gj + y), fragment (row g, col 2t + e)
+      auto sgroup = [&](int gidx, double (&v)[2][2][2]) {
+        const int gj = tri_col(gidx), gi = gidx - gj * (gj + 1) / 2;
+        double acc[2][2][2];
+#pragma unroll
+        for (int x = 0; x < 2; ++x)
+#pragma unroll
+          for (int y = 0; y < 2; ++y)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int i = 8 * (2 * gi + x) + g, c = 8 * (2 * gj + y) + 2 * t + e;   // trailing coordinates
+              v[x][y][e] = (i <= c && c < n) ? __ldg(Xg + (int64_t)(b + c) * k + b + i) : 0.0;
+              acc[x][y][e] = 0.0;
+            }
+        const int I0 = min(2 * gi, nbs - 1), I1 = min(2 * gi + 1, nbs - 1);
+        const int J0 = min(2 * gj, nbs - 1), J1 = min(2 * gj + 1, nbs - 1);
+        const int Ic[2] = {I0, I1}, Jc[2] = {J0, J1};
 #pragma unroll
         for (int P = 0; P < FK_PANEL / 8; ++P) {   // band block row P: k-steps rows t, 4 + t
-          double a0, a1, b0, b1;
-          frag_pair(pa + 64 * P, g, a0, a1);
-          frag_pair(pb + 64 * P, g, b0, b1);
-          dmma(acc, a0, b0);
-          dmma(acc, a1, b1);
+          double fa[2][2], fb[2][2];
+#pragma unroll
+          for (int x = 0; x < 2; ++x) {
+            frag_pair(Wb + band(P, b / 8 + Ic[x]) + g * 8 + t, g, fa[x][0], fa[x][1]);
+            frag_pair(Wb + band(P, b / 8 + Jc[x]) + g * 8 + t, g, fb[x][0], fb[x][1]);
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int x = 0; x < 2; ++x)
+#pragma unroll
+              for (int y = 0; y < 2; ++y) dmma(acc[x][y], fa[x][h], fb[y][h]);
         }
-      };
-      auto sstore = [&](int I, int J, const double (&v)[2]) {
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int i = 8 * I + g, c = 8 * J + 2 * t + e;
-          if (i <= c && c < n) S[belem(i, c)] = v[e];
-        }
-      };
-      // X22 (+ sigma on the diagonal), the overlay blocks' share into registers
-      // (all loads in flight at once) and the rest straight into S
-      constexpr int NOV_W = (4 * (FK_BIG_K / 8) + FK_NW - 1) / FK_NW;   // overlay blocks per warp
-      {
-        // a warp per column pair, lanes down the rows: X22 column c (rows <= c)
-        // is contiguous in X; every load of the pair is in flight at once
-        constexpr int RU = (FK_BIG_K - FK_PANEL + 31) / 32;   // row chunks per column (n <= 224)
-        for (int c0 = 2 * warp; c0 < n; c0 += 2 * FK_NW) {
-          double v[2][RU];
+        for (int x = 0; x < 2; ++x)
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int c = c0 + h, J = c >> 3, jb = J * (J + 1) / 2;
-            const int i0 = max(0, (nov - jb) * 8);     // rows of blocks outside the overlay
-            const double* src = Xg + (int64_t)(b + c) * k + b;
+          for (int y = 0; y < 2; ++y)
 #pragma unroll
-            for (int u = 0; u < RU; ++u) {
-              const int i = lane + 32 * u;
-              v[h][u] = (c < n && i >= i0 && i <= c) ? __ldg(src + i) : 0.0;
+            for (int e = 0; e < 2; ++e) {
+              const int i = 8 * (2 * gi + x) + g, c = 8 * (2 * gj + y) + 2 * t + e;
+              double xv = v[x][y][e];
+              if (i == c) xv = __dadd_rn(xv, sigma);
+              v[x][y][e] = xv - acc[x][y][e];
             }
-          }
+      };
+      auto gstore = [&](int gidx, const double (&v)[2][2][2]) {
+        const int gj = tri_col(gidx), gi = gidx - gj * (gj + 1) / 2;
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int c = c0 + h, J = c >> 3, jb = J * (J + 1) / 2;
-            const int i0 = max(0, (nov - jb) * 8);
+        for (int x = 0; x < 2; ++x)
 #pragma unroll
-            for (int u = 0; u < RU; ++u) {
-              const int i = lane + 32 * u;
-              if (c < n && i >= i0 && i <= c) S[belem(i, c)] = (i == c) ? __dadd_rn(v[h][u], sigma) : v[h][u];
+          for (int y = 0; y < 2; ++y)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int i = 8 * (2 * gi + x) + g, c = 8 * (2 * gj + y) + 2 * t + e;
+              if (i <= c && c < n) S[belem(i, c)] = v[x][y][e];
             }
-          }
-        }
+      };
+      // kept groups per warp, bounded at the largest overlay (nov <= 4 (FK_BIG_K / 8))
+      constexpr int NOV_MAX = 4 * (FK_BIG_K / 8);
+      constexpr int GJO_MAX = [] { int j = -1; while ((2 * (j + 1)) * (2 * (j + 1) + 1) / 2 < NOV_MAX) ++j; return j; }();
+      constexpr int KG = ((GJO_MAX + 1) * (GJO_MAX + 2) / 2 + FK_NW - 1) / FK_NW;
+      double keep[KG][2][2][2];
+#pragma unroll
+      for (int j = 0; j < KG; ++j) {
+        const int gidx = warp + FK_NW * j;
+        if (gidx < nog) sgroup(gidx, keep[j]);
       }
-      double keep[NOV_W][2];
-#pragma unroll
-      for (int j = 0; j < NOV_W; ++j) {
-        const int blk = warp + FK_NW * j;
-        int I = 0, J = 0;
-        if (blk < nov) decode(blk, I, J);
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int i = 8 * I + g, c = 8 * J + 2 * t + e;
-          keep[j][e] = (blk < nov && i <= c && c < n) ? __ldg(Xg + (int64_t)(b + c) * k + b + i) : 0.0;
-        }
-      }
-      __syncthreads();   // S holds X22 + sigma I outside the overlay
-#pragma unroll
-      for (int j = 0; j < NOV_W; ++j) {
-        const int blk = warp + FK_NW * j;
-        if (blk < nov) {
-          int I, J;
-          decode(blk, I, J);
-          double acc[2];
-          sprod(I, J, acc);
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            double x = keep[j][e];
-            if (8 * I + g == 8 * J + 2 * t + e) x = __dadd_rn(x, sigma);
-            keep[j][e] = x - acc[e];
-          }
-        }
-      }
-      // two vertically adjacent blocks (I, J), (I + 1, J) per iteration where
-      // the column allows: the B fragment is loaded once for both (3 shared
-      // loads per 2 DMMA) and the two chains overlap
-      for (int blk = nov + 2 * warp; blk < nblk; blk += 2 * FK_NW) {
-        int I, J;
-        decode(blk, I, J);
-        const bool two = blk + 1 < nblk;
-        double acc0[2] = {0.0, 0.0}, acc1[2] = {0.0, 0.0};
-        int I1 = I + 1, J1 = J;
-        if (I == J) { I1 = 0; J1 = J + 1; }   // blk + 1 opens the next column
-        if (I1 <= J1 && J1 == J) {
-          const double* pa0 = Wb + band(0, b / 8 + I) + g * 8 + t;
-          const double* pa1 = Wb + band(0, b / 8 + I1) + g * 8 + t;
-          const double* pb = Wb + band(0, b / 8 + J) + g * 8 + t;
-#pragma unroll
-          for (int P = 0; P < FK_PANEL / 8; ++P) {
-            double a0, a1, c0, c1, b0, b1;
-            frag_pair(pa0 + 64 * P, g, a0, a1);
-            frag_pair(pa1 + 64 * P, g, c0, c1);
-            frag_pair(pb + 64 * P, g, b0, b1);
-            dmma(acc0, a0, b0);
-            dmma(acc1, c0, b0);
-            dmma(acc0, a1, b1);
-            dmma(acc1, c1, b1);
-          }
-        } else {
-          sprod(I, J, acc0);
-          if (two) sprod(I1, J1, acc1);
-        }
-        double v[2];
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int i = 8 * I + g, c = 8 * J + 2 * t + e;
-          v[e] = (i <= c && c < n) ? S[belem(i, c)] - acc0[e] : 0.0;
-        }
-        sstore(I, J, v);
-        if (two) {
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int i = 8 * I1 + g, c = 8 * J1 + 2 * t + e;
-            v[e] = (i <= c && c < n) ? S[belem(i, c)] - acc1[e] : 0.0;
-          }
-          sstore(I1, J1, v);
-        }
+      for (int gidx = nog + warp; gidx < ngroups; gidx += FK_NW) {
+        double v[2][2][2];
+        sgroup(gidx, v);
+        gstore(gidx, v);
       }
       __syncthreads();   // every read of the band is done
 #pragma unroll
-      for (int j = 0; j < NOV_W; ++j) {
-        const int blk = warp + FK_NW * j;
-        if (blk < nov) {
-          int I, J;
-          decode(blk, I, J);
-          sstore(I, J, keep[j]);
-        }
+      for (int j = 0; j < KG; ++j) {
+        const int gidx = warp + FK_NW * j;
+        if (gidx < nog) gstore(gidx, keep[j]);
       }
       pad_blocked(S, n);
       __syncthreads();
