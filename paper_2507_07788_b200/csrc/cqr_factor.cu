@@ -1478,58 +1478,42 @@ __global__ void __launch_bounds__(FF_WARPS * 32) factor_finish_kernel(FactorArgs
     }
   }
   __syncthreads();
-  // ---- block back substitution for Rinv(:, J); the R(I, L) fragments of the
-  // next step are prefetched into registers while the current step runs
-  auto load_row = [&](int I, double (&fr)[4][2]) {
+  if (prof) g_fprof[14] = (unsigned long long)(clock64() - fc0);
+  // ---- R^-1(:, J) by right-looking block back substitution.  Warp w owns the
+  // block rows I' = w + 8 s; acc[s] collects sum_{L > I'} R(I', L) X_L as each
+  // X_L is published (L descending), so step I only waits for X_{I+1}'s term
+  // of row I: one barrier and four dependent DMMAs per step, against two
+  // barriers, a partial-sum reduction and 8x8 products over all L before.
+  // R(I', L) fragments are loaded two steps ahead.
+  double acc[4][2];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) { acc[j][0] = 0.0; acc[j][1] = 0.0; }
+  auto load_col = [&](int L, double (&fr)[4][2]) {   // R(I', L) for this warp's rows I' < L
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const int L = I + 1 + warp + FF_WARPS * j;
+      const int Ip = warp + FF_WARPS * j;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int ra = 8 * I + g, ca = 8 * L + t + 4 * h;
-        fr[j][h] = (I >= 0 && L <= J && ra < k && ca < k) ? R[(int64_t)ca * ldr + ra] : 0.0;
+        const int ra = 8 * Ip + g, ca = 8 * L + t + 4 * h;
+        fr[j][h] = (L >= 0 && Ip < L && ra < k && ca < k) ? R[(int64_t)ca * ldr + ra] : 0.0;
       }
     }
   };
-  if (prof) g_fprof[14] = (unsigned long long)(clock64() - fc0);
-  double cur[4][2], nxt[4][2];
-  load_row(J, cur);
-  for (int I = J; I >= 0; --I) {
-    load_row(I - 1, nxt);
-    // S = sum_{L=I+1..J} R(I, L) X_L, L split over warps
-    double c2[2] = {0.0, 0.0};
+  double (*sM)[64] = sPart;   // the owner warp's M, column-major
+  auto step = [&](int I, const double (&fr)[4][2]) {
+    if (warp == (I & (FF_WARPS - 1))) {
+      // X_I = inv(R_II) (delta_IJ I - S_I)
+      const int sl = I / FF_WARPS;
+      double s0 = acc[0][0], s1 = acc[0][1];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int L = I + 1 + warp + FF_WARPS * j;
-      if (L <= J) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) dmma(c2, cur[j][h], sX[L][g * 8 + t + 4 * h]);
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) { cur[j][0] = nxt[j][0]; cur[j][1] = nxt[j][1]; }
-    sPart[warp][(2 * t) * 8 + g] = c2[0];
-    sPart[warp][(2 * t + 1) * 8 + g] = c2[1];
-    __syncthreads();
-    if (warp == 0) {
-      // M = delta_IJ I - sum_w S_w (fixed order), X_I = inv(R_II) M
-      double m[2];
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int idx = (2 * t + e) * 8 + g;   // (row g, col 2t+e)
-        double sum = 0.0;
-#pragma unroll
-        for (int w = 0; w < FF_WARPS; ++w) sum += sPart[w][idx];
-        m[e] = ((I == J && g == 2 * t + e) ? 1.0 : 0.0) - sum;
-      }
-      __syncwarp();
-      // stage M in sPart[0] (column-major) for the B fragments
-      sPart[0][(2 * t) * 8 + g] = m[0];
-      sPart[0][(2 * t + 1) * 8 + g] = m[1];
+      for (int j = 1; j < 4; ++j)
+        if (sl == j) { s0 = acc[j][0]; s1 = acc[j][1]; }
+      sM[warp][(2 * t) * 8 + g] = ((I == J && g == 2 * t) ? 1.0 : 0.0) - s0;
+      sM[warp][(2 * t + 1) * 8 + g] = ((I == J && g == 2 * t + 1) ? 1.0 : 0.0) - s1;
       __syncwarp();
       double x2[2] = {0.0, 0.0};
 #pragma unroll
-      for (int h = 0; h < 2; ++h) dmma(x2, sInv[I][(t + 4 * h) * 8 + g], sPart[0][g * 8 + t + 4 * h]);
+      for (int h = 0; h < 2; ++h) dmma(x2, sInv[I][(t + 4 * h) * 8 + g], sM[warp][g * 8 + t + 4 * h]);
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int r = 8 * I + g, c = 8 * J + 2 * t + e;
@@ -1538,7 +1522,30 @@ __global__ void __launch_bounds__(FF_WARPS * 32) factor_finish_kernel(FactorArgs
         if (r < k && c < k) a.Rinv[coeff_off(r, c, k)] = v;
       }
     }
-    __syncthreads();
+    __syncthreads();   // X_I is published
+    // X_I's term for every row above it, the highest first (row I - 1 is on
+    // the critical path: its owner computes X_{I-1} next)
+#pragma unroll
+    for (int j = 3; j >= 0; --j) {
+      const int Ip = warp + FF_WARPS * j;
+      if (Ip < I) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) dmma(acc[j], fr[j][h], sX[I][g * 8 + t + 4 * h]);
+      }
+    }
+  };
+  // two fragment sets used alternately, each reloaded right after its step for
+  // the step after next (no register moves that would wait on the loads)
+  double fr0[4][2], fr1[4][2];
+  load_col(J, fr0);
+  load_col(J - 1, fr1);
+  for (int I = J; I >= 0; I -= 2) {
+    step(I, fr0);
+    load_col(I - 2, fr0);
+    if (I >= 1) {
+      step(I - 1, fr1);
+      load_col(I - 3, fr1);
+    }
   }
   if (prof) g_fprof[15] = (unsigned long long)(clock64() - fc0);
 }
