@@ -161,10 +161,11 @@ int cqr_pack_coeffs(const double* src, int ld, int k, int n, double* dst, void* 
  * over X (Q may alias X).  Replaces the lincomb + gramian pair of one
  * iteration (algorithms.py:350,352 / :238,:240 / :211 + :209). */
 size_t cqr_apply_gram_workspace_bytes(int64_t m, int k);
-/* Select the single-kernel fused TRMM + Gram pass for 33 <= k <= 64 and
- * 97 <= k <= 128 (default off: the two-kernel TRMM then Gram path is faster on
- * B200, where these passes are FP64-pipe bound, not HBM bound). */
-void cqr_set_fused(int enable);
+/* Fused TRMM + Gram selection: 2 (default) = the single-kernel pass for
+ * k <= 64 only; 1 = also the two-group kernel for 97 <= k <= 128 (slower on
+ * B200 than TRMM then Gram there: those passes are FP64-pipe bound); 0 = never
+ * fused (TRMM then Gram, for comparisons). */
+void cqr_set_fused(int mode);
 /* Number of kernel launches one cqr_apply_gram call issues for width k. */
 int cqr_apply_gram_launches(int k);
 /* 1 when cqr_apply_gram may run in place (Q == X) for width k. */

@@ -167,7 +167,7 @@ size_t cqr_apply_gram_workspace_bytes(int64_t m, int k) {
   return a;
 }
 
-void cqr_set_fused(int enable) { cqr::set_fused(enable); }
+void cqr_set_fused(int mode) { cqr::set_fused(mode); }
 
 int cqr_apply_gram_launches(int k) { return cqr::apply_gram_fused_supported(k) ? 2 : 3; }
 

@@ -35,12 +35,15 @@ struct FuCfg {
   // KP = 64: a dedicated producer warp issues the X copies; KP = 128 (16
   // compute warps, 128 registers each) keeps the producer inline on thread 0
   static constexpr bool PRODUCER = KP == 64;
-  static constexpr int THREADS = 64 * PAIRS + (PRODUCER ? 32 : 0);
+  // KP = 64: a dedicated storer warp also writes the Q panels back to HBM
+  // (otherwise one lane of Gram warp 0 does, and that warp paces the Gram side)
+  static constexpr bool STORER = KP == 64;
+  static constexpr int THREADS = 64 * PAIRS + (PRODUCER ? 32 : 0) + (STORER ? 32 : 0);
   static constexpr int NKT = KP / CT_K;       // 32-row coefficient k tiles
   static constexpr int NNT = KP / CT_N;       // 64-column coefficient n tiles
   static constexpr int STAGE = FU_BR * KP;    // doubles per panel
   static constexpr int XST = (KP == 64) ? 6 : 2;
-  static constexpr int QB = (KP == 64) ? 3 : 1;
+  static constexpr int QB = (KP == 64) ? 4 : 1;
 };
 
 // coefficient tiles of R^-1 that hold upper-triangle entries (kt*32 < (nt+1)*64), packed in order
@@ -136,7 +139,7 @@ __global__ void __launch_bounds__(FuCfg<KP>::THREADS, 1)
 
   if (tid == 0) {
     for (int s = 0; s < XST; ++s) { mbar_init(&xfull[s], 1); mbar_init(&xempty[s], P); }
-    for (int s = 0; s < QB; ++s) { mbar_init(&qfull[s], 32 * P); mbar_init(&qempty[s], P); }
+    for (int s = 0; s < QB; ++s) { mbar_init(&qfull[s], 32 * P); mbar_init(&qempty[s], P + (C::STORER ? 1 : 0)); }
     mbar_init(rbar, 1);
     fence_mbar_init();
   }
@@ -177,6 +180,41 @@ __global__ void __launch_bounds__(FuCfg<KP>::THREADS, 1)
       return;
     }
   }
+  if constexpr (C::STORER) {
+    if (warp == 2 * P + 1) {
+      // storer warp: Q panel j -> HBM as soon as the TRMM warps filled it; the
+      // slot is released once the bulk engine has read it (one group in flight)
+      if (lane == 0) {
+        int qs = 0, prev = -1;
+        uint32_t qph = 0;
+        for (int64_t j = 0; j < mine; ++j) {
+          mbar_wait(&qfull[qs], qph);
+          const int64_t r0 = (blockIdx.x + j * gridDim.x) * FU_BR;
+          const int nq = (int)imin64(FU_BR, rows - r0) >> 2;
+          const double* src = qbuf + qs * C::STAGE;
+          double* dst = Q + (r0 >> 2) * 4 * ldq;
+          if (ldq == KP && KFULL) {
+            bulk_s2g(dst, src, (uint32_t)nq * KP * 32);
+          } else {
+            for (int q = 0; q < nq; ++q) bulk_s2g(dst + q * 4 * ldq, src + q * 4 * KP, (uint32_t)k * 32);
+          }
+          bulk_commit();
+          if (prev >= 0) {
+            bulk_wait_read<1>();
+            mbar_arrive(&qempty[prev]);
+          }
+          prev = qs;
+          if (++qs == QB) { qs = 0; qph ^= 1; }
+        }
+        if (prev >= 0) {
+          bulk_wait_read<0>();
+          mbar_arrive(&qempty[prev]);
+        }
+        bulk_wait<0>();
+      }
+      return;
+    }
+  }
 
   if (warp < P) {
     // ---------------- TRMM warps
@@ -211,7 +249,11 @@ __global__ void __launch_bounds__(FuCfg<KP>::THREADS, 1)
 #pragma unroll
           for (int c = 0; c < 2; ++c)
 #pragma unroll
-            for (int e = 0; e < 2; ++e) qd[rb * 8 * KP + 4 * (8 * (c ? cB : cA) + 2 * t + e)] = acc[rb][c][e];
+            for (int e0 = 0; e0 < 2; ++e0) {
+              // lanes t >= 2 store e = 1 first: every half-warp then covers all 32 banks
+              const int e = e0 ^ (t >> 1);
+              qd[rb * 8 * KP + 4 * (8 * (c ? cB : cA) + 2 * t + e)] = e ? acc[rb][c][1] : acc[rb][c][0];
+            }
       } else {
 #pragma unroll
         for (int rb = 0; rb < 4; ++rb) {
@@ -239,7 +281,7 @@ __global__ void __launch_bounds__(FuCfg<KP>::THREADS, 1)
     for (int c = 0; c <= NB; ++c) { gacc[c][0] = 0.0; gacc[c][1] = 0.0; }
     int qs = 0;
     uint32_t qph = 0;
-    const bool storer = (pr == 0 && lane == 0);
+    const bool storer = !C::STORER && pr == 0 && lane == 0;
     for (int64_t j = 0; j < mine; ++j) {
       mbar_wait(&qfull[qs], qph);
       if (storer) {
@@ -277,6 +319,182 @@ __global__ void __launch_bounds__(FuCfg<KP>::THREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// K2+K1 for k <= 64, register resident ("transposed TRMM"): each warp owns 8
+// rows of a 64-row panel and computes Q^T = R^-T X^T for them, i.e. the DMMA
+// takes A = R^-T (lane (g,t): R^-1[4ks+t][8j+g], the coefficient tiles as
+// stored) and B = X^T (lane (g,t): X[r0+g][4ks+t], the staged QI panel).  The
+// accumulator of column block j then holds, in lane (g,t),
+//   qt[j][e] = Q[r0 + 2t + e][8j + g],
+// which is exactly the A fragment (and the B fragment) of the Gram DMMA over
+// the 4 rows {r0 + 2t + e : t} -- the k index of a DMMA is a row index here,
+// and a Gram is a sum over rows in any order.  So the Gram of the fresh Q
+// block is accumulated straight from the TRMM accumulators: no Q round trip
+// through shared memory, no hand-over between warp groups.  Each lane's two
+// values are consecutive in the QI layout (rows 2t, 2t+1 of one quad), so Q
+// goes to HBM as one 16-byte store per lane per column block, two fully
+// coalesced 256-byte runs per warp instruction.
+// Per 8 rows a warp issues NB(NB+1) TRMM DMMAs (column block j needs K up to
+// 8j+8) and NB(NB+1) Gram DMMAs (the NB(NB+1)/2 lower blocks, two row quads)
+// from compile-time loops (no predicated-off DMMA); its Gram partial stays
+// in registers (NB(NB+1) doubles per lane) for the whole sweep.
+// Only the X panel and the R^-1 tiles live in shared memory: 88 LDS.64 per
+// 144 DMMAs at k = 64, against ~1.0 LDS + 0.1 STS per DMMA in the two-group
+// kernel above.
+constexpr int RT_ROWS = 64;   // rows per staged panel (8 compute warps x 8 rows)
+
+template <int KP>
+struct RtCfg {
+  static constexpr int NB = KP / 8;
+  static constexpr int NKS = KP / 4;                      // k4 steps of the TRMM
+  static constexpr int NKT = KP > CT_K ? KP / CT_K : 1;   // 32-row coefficient k tiles (one 64-wide n tile)
+  static constexpr int NG = NB * (NB + 1) / 2;            // lower-triangle 8x8 blocks
+  static constexpr int STAGE = RT_ROWS * KP;              // doubles per panel
+  static constexpr int STAGES = KP >= 64 ? 5 : 8;
+  static constexpr int THREADS = 256;                     // 8 compute warps
+};
+template <int KP>
+__host__ __device__ constexpr size_t rt_smem_doubles() {
+  return (size_t)RtCfg<KP>::NKT * CT_TILE + (size_t)RtCfg<KP>::STAGES * RtCfg<KP>::STAGE;
+}
+
+__device__ __forceinline__ void st_global_v2(double* p, double a, double b) {
+  asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
+}
+
+template <int KP, bool KFULL>
+__global__ void __launch_bounds__(RtCfg<KP>::THREADS, 1)
+    apply_gram_rt_kernel(const double* X, int64_t ldx, int k, const double* __restrict__ Rt, double* Q, int64_t ldq,
+                         int64_t rows, double* __restrict__ ws, const int* gate) {
+  if (gate != nullptr && *gate != 0) return;   // gated off
+  using C = RtCfg<KP>;
+  constexpr int NB = C::NB, NKS = C::NKS, ST = C::STAGES;
+  // thread 0 keeps D panels in flight and refills the stage of panel j - LAG
+  // (8 warps, no producer warp: a 9-warp CTA is capped at 168 registers per
+  // thread, and the Gram partial alone takes 144 at k = 64)
+  constexpr int LAG = 2, D = ST - LAG;
+  extern __shared__ __align__(128) double smem[];
+  double* rt_s = smem;                      // R^-1 coefficient tiles
+  double* xst = smem + C::NKT * CT_TILE;    // ST X panels (QI, ldk = KP)
+  __shared__ __align__(8) uint64_t bars[2 * ST + 1];
+  uint64_t* full = bars;
+  uint64_t* empty = bars + ST;
+  uint64_t* rbar = bars + 2 * ST;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t npan = ceil_div(rows, RT_ROWS);
+  const int64_t mine = (npan > blockIdx.x) ? ceil_div(npan - blockIdx.x, gridDim.x) : 0;
+
+  if (tid == 0) {
+    for (int s = 0; s < ST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 8); }
+    mbar_init(rbar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  auto issue = [&](int64_t j, int st) {
+    const int64_t r0 = (blockIdx.x + j * gridDim.x) * RT_ROWS;
+    const int nq = (int)imin64(RT_ROWS, rows - r0) >> 2;
+    double* dst = xst + st * C::STAGE;
+    const double* src = X + (r0 >> 2) * 4 * ldx;
+    mbar_arrive_expect_tx(&full[st], (uint32_t)nq * k * 32);
+    if (ldx == KP && KFULL) {
+      bulk_g2s(dst, src, (uint32_t)nq * KP * 32, &full[st]);
+    } else {
+      for (int q = 0; q < nq; ++q) bulk_g2s(dst + q * 4 * KP, src + q * 4 * ldx, (uint32_t)k * 32, &full[st]);
+    }
+  };
+  if (tid == 0) {
+    mbar_arrive_expect_tx(rbar, C::NKT * CT_TILE * 8);
+    for (int kt = 0; kt < C::NKT; ++kt) bulk_g2s(rt_s + kt * CT_TILE, Rt + (int64_t)kt * CT_TILE, CT_TILE * 8, rbar);
+    for (int j = 0; j < D && j < mine; ++j) issue(j, j);
+  }
+
+  // ---------------- compute warps: 8 rows of every panel each
+  double gacc[C::NG][2];
+#pragma unroll
+  for (int b = 0; b < C::NG; ++b) { gacc[b][0] = 0.0; gacc[b][1] = 0.0; }
+  // A fragments (R^-1[4ks+t][8j+g]) at rp[tile(ks) + 8j*CT_LD + 4(ks%8)]
+  const double* rp = rt_s + g * CT_LD + t;
+  mbar_wait(rbar, 0);
+  int s = 0;
+  uint32_t ph = 0;
+  for (int64_t j = 0; j < mine; ++j) {
+    if (tid == 0 && j + D < mine) {
+      // stage s2 last held panel j - LAG (released by all 8 warps)
+      const int64_t j2 = j + D;
+      const int s2 = (int)(j2 % ST);
+      if (j2 >= ST) mbar_wait(&empty[s2], (uint32_t)((j2 / ST) - 1) & 1);
+      issue(j2, s2);
+    }
+    const int64_t r0 = (blockIdx.x + j * gridDim.x) * RT_ROWS + 8 * warp;
+    const bool valid = r0 < rows;   // rows is a multiple of 16: a row octet is all in or all out
+    mbar_wait(&full[s], ph);
+    double qt[NB][2];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) { qt[b][0] = 0.0; qt[b][1] = 0.0; }
+    if (valid) {
+      // B fragments X[r0+g][4ks+t]: quad 2*warp + g/4 of the panel, conflict-free
+      const double* xp = xst + s * C::STAGE + (2 * warp + (g >> 2)) * 4 * KP + 4 * t + (g & 3);
+      double xb[2];
+      xb[0] = (KFULL || t < k) ? xp[0] : 0.0;
+#pragma unroll
+      for (int ks = 0; ks < NKS; ++ks) {
+        const int cur = ks & 1;
+        if (ks + 1 < NKS) xb[cur ^ 1] = (KFULL || 4 * (ks + 1) + t < k) ? xp[16 * (ks + 1)] : 0.0;
+        // column blocks j >= ks/2 see k4 step ks (R^-1 upper triangular)
+#pragma unroll
+        for (int b = ks / 2; b < NB; ++b) {
+          const double ra = rp[(ks / 8) * CT_TILE + 8 * b * CT_LD + 4 * (ks % 8)];
+          dmma(qt[b], ra, xb[cur]);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);   // the panel is consumed: the producer may refill it
+    if (++s == ST) { s = 0; ph ^= 1; }
+    if (!valid) continue;
+    if (!KFULL) {
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+        if (8 * b + g >= k) { qt[b][0] = 0.0; qt[b][1] = 0.0; }
+    }
+    // Q -> HBM: lane (g,t) holds rows 2t, 2t+1 (one quad, consecutive) of column 8b+g
+    double* qd = Q + ((r0 >> 2) + (t >> 1)) * 4 * ldq + 4 * g + 2 * (t & 1);
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+      if (KFULL || 8 * b + g < k) st_global_v2(qd + 32 * b, qt[b][0], qt[b][1]);
+    // Gram of the block: G(i, c) += sum over the 8 rows, two row quads
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+#pragma unroll
+      for (int i = 0; i < NB; ++i)
+#pragma unroll
+        for (int c = 0; c <= i; ++c) dmma(gacc[i * (i + 1) / 2 + c], qt[i][e], qt[c][e]);
+    }
+  }
+
+  // ---- per-CTA partial (KP x KP column-major, lower triangle): warps in fixed order
+  double* red = smem;
+  __syncthreads();   // every warp is done with the tiles and panels
+  for (int e = tid; e < KP * KP; e += 256) red[e] = 0.0;
+  asm volatile("bar.sync 1, 256;" ::: "memory");
+  for (int w = 0; w < 8; ++w) {
+    if (warp == w) {
+#pragma unroll
+      for (int i = 0; i < NB; ++i)
+#pragma unroll
+        for (int c = 0; c <= i; ++c)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) red[(8 * c + 2 * t + e) * KP + 8 * i + g] += gacc[i * (i + 1) / 2 + c][e];
+    }
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+  }
+  double* out = ws + (int64_t)blockIdx.x * KP * KP;
+  for (int e = tid; e < KP * KP; e += 256) out[e] = red[e];
+}
+
 // fixed-order sum over CTAs of the per-CTA KP x KP partials; lower triangle, mirrored
 __global__ void gram_fused_reduce(const double* __restrict__ ws, int nparts, int KP, int k, double* G, int ldg,
                                   const int* gate) {
@@ -297,26 +515,78 @@ static int fused_kp(int k) {
   if (k > 96 && k <= 128) return 128;
   return 0;   // k <= 32 and 65..96: unfused path
 }
+static int rt_kp(int k) {
+  if (k < 1) return 0;
+  if (k <= 16) return 16;
+  if (k <= 32) return 32;
+  if (k <= 64) return 64;
+  return 0;
+}
 
-// Off by default: on B200 every pass with k >= 64 is bound by the FP64 tensor
-// pipe, not HBM, so saving the second read of Q does not pay; measured
-// (tools/kernel_probe.py): k=64 fused 10.85 ms vs TRMM 5.24 + Gram 4.99 ms at
-// m=32M, k=128 fused 5.89 ms vs 2.21 + 2.10 ms at m=4M.  cqr_set_fused(1)
-// selects it (tests exercise both).
-static int g_fused_enabled = 0;
-void set_fused(int on) { g_fused_enabled = on ? 1 : 0; }
-bool apply_gram_fused_supported(int k) { return g_fused_enabled && k >= 1 && fused_kp(k) != 0; }
+// Fused-pass selection (cqr_set_fused):
+//   2 (default) "auto": the register-resident kernel for k <= 64, the
+//     two-kernel TRMM then Gram path otherwise;
+//   1: every fused kernel (register-resident for k <= 64, the two-group
+//     kernel for 97 <= k <= 128);
+//   0: never fused.
+// The two-group kernel is not the default for 97..128: there every pass is
+// FP64-pipe bound and its split of one SM between two dependent warp groups
+// costs more than the saved read of Q (k=128 fused 5.89 ms vs 2.21 + 2.10 ms
+// at m=4M, tools/fused_probe.py).
+static int g_fused_mode = 2;
+void set_fused(int mode) { g_fused_mode = mode < 0 ? 0 : (mode > 2 ? 2 : mode); }
+static int fused_variant(int k) {   // 0 none, 1 register-resident, 2 two-group
+  if (g_fused_mode == 0 || k < 1) return 0;
+  if (rt_kp(k)) return 1;
+  if (g_fused_mode == 1 && fused_kp(k) == 128) return 2;
+  return 0;
+}
+bool apply_gram_fused_supported(int k) { return fused_variant(k) != 0; }
 
 static int fused_ctas(int64_t rows) {
   int64_t n = ceil_div(rows, FU_BR);
   int64_t c = num_sms();
   return (int)(n < c ? (n < 1 ? 1 : n) : c);
 }
+static int rt_ctas(int64_t rows) {
+  int64_t n = ceil_div(rows, RT_ROWS);
+  int64_t c = num_sms();
+  return (int)(n < c ? (n < 1 ? 1 : n) : c);
+}
 
 size_t apply_gram_fused_ws_bytes(int64_t rows, int k) {
-  const int kp = fused_kp(k);
-  if (!kp) return 0;
-  return (size_t)fused_ctas(rows) * kp * kp * sizeof(double) + 256;
+  switch (fused_variant(k)) {
+    case 1: return (size_t)rt_ctas(rows) * rt_kp(k) * rt_kp(k) * sizeof(double) + 256;
+    case 2: return (size_t)fused_ctas(rows) * fused_kp(k) * fused_kp(k) * sizeof(double) + 256;
+    default: return 0;
+  }
+}
+
+template <int KP>
+static cudaError_t launch_rt(const double* X, int64_t ldx, int k, const double* Rt, double* Q, int64_t ldq,
+                             int64_t rows, double* G, int ldg, double* ws, cudaStream_t s, const int* gate) {
+  static bool attr = false;
+  const size_t smem = rt_smem_doubles<KP>() * sizeof(double);
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(apply_gram_rt_kernel<KP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(apply_gram_rt_kernel<KP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int ctas = rt_ctas(rows);
+  if (k == KP)
+    apply_gram_rt_kernel<KP, true><<<ctas, RtCfg<KP>::THREADS, smem, s>>>(X, ldx, k, Rt, Q, ldq, rows, ws, gate);
+  else
+    apply_gram_rt_kernel<KP, false><<<ctas, RtCfg<KP>::THREADS, smem, s>>>(X, ldx, k, Rt, Q, ldq, rows, ws, gate);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const int64_t nel = (int64_t)k * k;
+  int blocks = (int)imin64(ceil_div(nel, 256), 2 * num_sms());
+  gram_fused_reduce<<<blocks < 1 ? 1 : blocks, 256, 0, s>>>(ws, ctas, KP, k, G, ldg, gate);
+  return cudaGetLastError();
 }
 
 template <int KP>
@@ -350,11 +620,16 @@ cudaError_t apply_gram_fused_launch(const double* X, int64_t ldx, int k, const d
                                     int64_t ldq, int64_t rows, double* G, int ldg, double* ws, size_t ws_bytes,
                                     cudaStream_t stream, const int* gate) {
   (void)ws_bytes;
-  switch (fused_kp(k)) {
-    case 64: return launch_fused<64>(X, ldx, k, Rinv_tiles, Q, ldq, rows, G, ldg, ws, stream, gate);
-    case 128: return launch_fused<128>(X, ldx, k, Rinv_tiles, Q, ldq, rows, G, ldg, ws, stream, gate);
-    default: return cudaErrorNotSupported;
+  if (fused_variant(k) == 1) {
+    switch (rt_kp(k)) {
+      case 16: return launch_rt<16>(X, ldx, k, Rinv_tiles, Q, ldq, rows, G, ldg, ws, stream, gate);
+      case 32: return launch_rt<32>(X, ldx, k, Rinv_tiles, Q, ldq, rows, G, ldg, ws, stream, gate);
+      case 64: return launch_rt<64>(X, ldx, k, Rinv_tiles, Q, ldq, rows, G, ldg, ws, stream, gate);
+      default: return cudaErrorNotSupported;
+    }
   }
+  if (fused_variant(k) == 2) return launch_fused<128>(X, ldx, k, Rinv_tiles, Q, ldq, rows, G, ldg, ws, stream, gate);
+  return cudaErrorNotSupported;
 }
 
 }  // namespace cqr

@@ -61,7 +61,7 @@ cudaError_t apply_gram_fused_launch(const double* X, int64_t ldx, int k, const d
                                     cudaStream_t stream, const int* gate = nullptr);
 size_t apply_gram_fused_ws_bytes(int64_t rows, int k);
 bool apply_gram_fused_supported(int k);
-void set_fused(int on);
+void set_fused(int mode);
 
 // ------------------------------------------------------------- fused update pass (K3)
 bool update_pass_supported(int q, int p);

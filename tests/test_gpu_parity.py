@@ -399,7 +399,7 @@ def test_apply_gram_matches_separate_ops(m, k, inplace, fused):
     try:
         _apply_gram_case(cq, _lib, Engine, m, k, inplace)
     finally:
-        ctx().lib.cqr_set_fused(0)
+        ctx().lib.cqr_set_fused(2)   # back to the default (auto)
 
 
 def _apply_gram_case(cq, _lib, Engine, m, k, inplace):

@@ -1,4 +1,5 @@
-"""Fused vs two-kernel TRMM + Gram at one shape: python tools/fused_probe.py --m M --k K"""
+"""Fused vs two-kernel TRMM + Gram at one shape: python tools/fused_probe.py --m M --k K
+(cqr_set_fused modes: 0 = TRMM then Gram, 2 = default, 1 = every fused kernel)"""
 import argparse, json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -21,7 +22,7 @@ eng.gram(x)
 assert eng.factor(_lib.POLICY_PLAIN, a.m, a.k).code == _lib.FACTORED
 out = {"m": a.m, "k": a.k}
 for fused in (0, 1, 0, 1):
-    ctx().lib.cqr_set_fused(fused)
+    ctx().lib.cqr_set_fused(fused)   # 1: every fused kernel (k <= 64: the default one)
     eng.apply(x, q, with_gram=True)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -31,5 +32,5 @@ for fused in (0, 1, 0, 1):
     e1.record()
     torch.cuda.synchronize()
     out.setdefault("fused_ms" if fused else "unfused_ms", []).append(round(e0.elapsed_time(e1) / a.reps, 3))
-ctx().lib.cqr_set_fused(0)
+ctx().lib.cqr_set_fused(2)
 print(json.dumps(out))
