@@ -129,9 +129,10 @@ size_t cqr_gram_workspace_bytes(int64_t m, int ka, int kb, int self);
 int cqr_gram(const double* X, int64_t ldx, int64_t m, int k, double* G, int ldg, void* ws, size_t ws_bytes,
              void* stream);
 
-/* Select the self-Gram schedule: 1 (default) = block-row pairs over full-row
- * panels (k <= 256), 0 = 64x64 tile items. */
-void cqr_set_gram_pairs(int enable);
+/* Select the self-Gram schedule: 1 (default) = register-resident row sweep for
+ * k = 64, m >= 2^21 and block-row pairs over full-row panels for k <= 256; 2 = block-row
+ * pairs for every k <= 256; 0 = 64x64 tile items. */
+void cqr_set_gram_pairs(int mode);
 
 /* Cross Gram G = A^T B (ka x kb).  Replaces gramian(other) (varray.py:154-155). */
 int cqr_cross_gram(const double* A, int64_t lda, int ka, const double* B, int64_t ldb, int kb, int64_t m, double* G,

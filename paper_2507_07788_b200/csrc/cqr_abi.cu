@@ -41,8 +41,11 @@ int cqr_abi_version(void) { return CQR_ABI_VERSION; }
 
 const char* cqr_last_error(void) { return g_last_error.c_str(); }
 
-static int g_gram_pairs = 1;   // block-row-pair self-Gram kernel (k <= 256)
-void cqr_set_gram_pairs(int enable) { g_gram_pairs = enable ? 1 : 0; }
+// self-Gram kernel choice: 1 (default) = register-resident row sweep for
+// k = 64 and m >= 2M, block-row pairs for k <= 256; 2 = block-row pairs up to 256;
+// 0 = the generic tiled kernel
+static int g_gram_pairs = 1;
+void cqr_set_gram_pairs(int mode) { g_gram_pairs = mode < 0 ? 0 : (mode > 2 ? 2 : mode); }
 
 size_t cqr_gram_workspace_bytes(int64_t m, int ka, int kb, int self) {
   if (ka <= 0 || kb <= 0) return 256;
@@ -51,6 +54,10 @@ size_t cqr_gram_workspace_bytes(int64_t m, int ka, int kb, int self) {
   if (self && cqr::gram_pairs_supported(ka)) {
     const size_t b2 = cqr::gram_pairs_ws_bytes(cqr::round_up(m, 16), ka);
     if (b2 > b) b = b2;
+  }
+  if (self && cqr::gram_rt_supported(ka, cqr::round_up(m, 16))) {
+    const size_t b3 = cqr::gram_rt_ws_bytes(cqr::round_up(m, 16), ka);
+    if (b3 > b) b = b3;
   }
   return b;
 }
@@ -66,6 +73,13 @@ static int gram_common(const double* A, int64_t lda, int ka, const double* B, in
   }
   if (ka == 0 || kb == 0) return CQR_OK;
   if (G == nullptr || ldg < ka) return fail(CQR_EINVAL, std::string(who) + ": bad output G / ldg");
+  if (self && g_gram_pairs == 1 && cqr::gram_rt_supported(ka, cqr::round_up(m, 16))) {
+    if (ws == nullptr || ws_bytes < cqr::gram_rt_ws_bytes(cqr::round_up(m, 16), ka))
+      return fail(CQR_EINVAL, std::string(who) + ": workspace too small");
+    return cuda_check(cqr::gram_rt_launch(A, lda, ka, cqr::round_up(m, 16), G, ldg, static_cast<double*>(ws),
+                                          static_cast<cudaStream_t>(stream), gate),
+                      who);
+  }
   if (self && g_gram_pairs && cqr::gram_pairs_supported(ka)) {
     if (ws == nullptr || ws_bytes < cqr::gram_pairs_ws_bytes(cqr::round_up(m, 16), ka))
       return fail(CQR_EINVAL, std::string(who) + ": workspace too small");

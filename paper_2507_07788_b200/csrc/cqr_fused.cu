@@ -362,7 +362,11 @@ __device__ __forceinline__ void st_global_v2(double* p, double a, double b) {
   asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
 }
 
-template <int KP, bool KFULL>
+// TRMM = false: the same sweep as a plain self Gram of X (k <= 64): the
+// fragments of the Gram DMMA are loaded straight from the staged panel (lane
+// (g,t): X[r0 + t + 4e][8b + g], conflict-free), 16 LDS.64 per 72 DMMAs, and
+// the warp's 36-block partial stays in registers.
+template <int KP, bool KFULL, bool TRMM>
 __global__ void __launch_bounds__(RtCfg<KP>::THREADS, 1)
     apply_gram_rt_kernel(const double* X, int64_t ldx, int k, const double* __restrict__ Rt, double* Q, int64_t ldq,
                          int64_t rows, double* __restrict__ ws, const int* gate) {
@@ -406,8 +410,11 @@ __global__ void __launch_bounds__(RtCfg<KP>::THREADS, 1)
     }
   };
   if (tid == 0) {
-    mbar_arrive_expect_tx(rbar, C::NKT * CT_TILE * 8);
-    for (int kt = 0; kt < C::NKT; ++kt) bulk_g2s(rt_s + kt * CT_TILE, Rt + (int64_t)kt * CT_TILE, CT_TILE * 8, rbar);
+    if (TRMM) {
+      mbar_arrive_expect_tx(rbar, C::NKT * CT_TILE * 8);
+      for (int kt = 0; kt < C::NKT; ++kt)
+        bulk_g2s(rt_s + kt * CT_TILE, Rt + (int64_t)kt * CT_TILE, CT_TILE * 8, rbar);
+    }
     for (int j = 0; j < D && j < mine; ++j) issue(j, j);
   }
 
@@ -417,7 +424,7 @@ __global__ void __launch_bounds__(RtCfg<KP>::THREADS, 1)
   for (int b = 0; b < C::NG; ++b) { gacc[b][0] = 0.0; gacc[b][1] = 0.0; }
   // A fragments (R^-1[4ks+t][8j+g]) at rp[tile(ks) + 8j*CT_LD + 4(ks%8)]
   const double* rp = rt_s + g * CT_LD + t;
-  mbar_wait(rbar, 0);
+  if (TRMM) mbar_wait(rbar, 0);
   int s = 0;
   uint32_t ph = 0;
   for (int64_t j = 0; j < mine; ++j) {
@@ -434,7 +441,15 @@ __global__ void __launch_bounds__(RtCfg<KP>::THREADS, 1)
     double qt[NB][2];
 #pragma unroll
     for (int b = 0; b < NB; ++b) { qt[b][0] = 0.0; qt[b][1] = 0.0; }
-    if (valid) {
+    if (!TRMM && valid) {
+      // Gram operands straight from the panel: rows r0 + t + 4e (quad 2*warp + e), column 8b + g
+      const double* xp = xst + s * C::STAGE + 2 * warp * 4 * KP + 4 * g + t;
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int b = 0; b < NB; ++b) qt[b][e] = (KFULL || 8 * b + g < k) ? xp[e * 4 * KP + 32 * b] : 0.0;
+    }
+    if (TRMM && valid) {
       // B fragments X[r0+g][4ks+t]: quad 2*warp + g/4 of the panel, conflict-free
       const double* xp = xst + s * C::STAGE + (2 * warp + (g >> 2)) * 4 * KP + 4 * t + (g & 3);
       double xb[2];
@@ -455,16 +470,18 @@ __global__ void __launch_bounds__(RtCfg<KP>::THREADS, 1)
     if (lane == 0) mbar_arrive(&empty[s]);   // the panel is consumed: the producer may refill it
     if (++s == ST) { s = 0; ph ^= 1; }
     if (!valid) continue;
-    if (!KFULL) {
+    if (TRMM && !KFULL) {
 #pragma unroll
       for (int b = 0; b < NB; ++b)
         if (8 * b + g >= k) { qt[b][0] = 0.0; qt[b][1] = 0.0; }
     }
     // Q -> HBM: lane (g,t) holds rows 2t, 2t+1 (one quad, consecutive) of column 8b+g
-    double* qd = Q + ((r0 >> 2) + (t >> 1)) * 4 * ldq + 4 * g + 2 * (t & 1);
+    if (TRMM) {
+      double* qd = Q + ((r0 >> 2) + (t >> 1)) * 4 * ldq + 4 * g + 2 * (t & 1);
 #pragma unroll
-    for (int b = 0; b < NB; ++b)
-      if (KFULL || 8 * b + g < k) st_global_v2(qd + 32 * b, qt[b][0], qt[b][1]);
+      for (int b = 0; b < NB; ++b)
+        if (KFULL || 8 * b + g < k) st_global_v2(qd + 32 * b, qt[b][0], qt[b][1]);
+    }
     // Gram of the block: G(i, c) += sum over the 8 rows, two row quads
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
@@ -562,25 +579,26 @@ size_t apply_gram_fused_ws_bytes(int64_t rows, int k) {
   }
 }
 
-template <int KP>
+template <int KP, bool TRMM>
 static cudaError_t launch_rt(const double* X, int64_t ldx, int k, const double* Rt, double* Q, int64_t ldq,
                              int64_t rows, double* G, int ldg, double* ws, cudaStream_t s, const int* gate) {
   static bool attr = false;
   const size_t smem = rt_smem_doubles<KP>() * sizeof(double);
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(apply_gram_rt_kernel<KP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(apply_gram_rt_kernel<KP, true, TRMM>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(apply_gram_rt_kernel<KP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      e = cudaFuncSetAttribute(apply_gram_rt_kernel<KP, false, TRMM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int ctas = rt_ctas(rows);
   if (k == KP)
-    apply_gram_rt_kernel<KP, true><<<ctas, RtCfg<KP>::THREADS, smem, s>>>(X, ldx, k, Rt, Q, ldq, rows, ws, gate);
+    apply_gram_rt_kernel<KP, true, TRMM><<<ctas, RtCfg<KP>::THREADS, smem, s>>>(X, ldx, k, Rt, Q, ldq, rows, ws, gate);
   else
-    apply_gram_rt_kernel<KP, false><<<ctas, RtCfg<KP>::THREADS, smem, s>>>(X, ldx, k, Rt, Q, ldq, rows, ws, gate);
+    apply_gram_rt_kernel<KP, false, TRMM><<<ctas, RtCfg<KP>::THREADS, smem, s>>>(X, ldx, k, Rt, Q, ldq, rows, ws,
+                                                                                gate);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int64_t nel = (int64_t)k * k;
@@ -622,14 +640,34 @@ cudaError_t apply_gram_fused_launch(const double* X, int64_t ldx, int k, const d
   (void)ws_bytes;
   if (fused_variant(k) == 1) {
     switch (rt_kp(k)) {
-      case 16: return launch_rt<16>(X, ldx, k, Rinv_tiles, Q, ldq, rows, G, ldg, ws, stream, gate);
-      case 32: return launch_rt<32>(X, ldx, k, Rinv_tiles, Q, ldq, rows, G, ldg, ws, stream, gate);
-      case 64: return launch_rt<64>(X, ldx, k, Rinv_tiles, Q, ldq, rows, G, ldg, ws, stream, gate);
+      case 16: return launch_rt<16, true>(X, ldx, k, Rinv_tiles, Q, ldq, rows, G, ldg, ws, stream, gate);
+      case 32: return launch_rt<32, true>(X, ldx, k, Rinv_tiles, Q, ldq, rows, G, ldg, ws, stream, gate);
+      case 64: return launch_rt<64, true>(X, ldx, k, Rinv_tiles, Q, ldq, rows, G, ldg, ws, stream, gate);
       default: return cudaErrorNotSupported;
     }
   }
   if (fused_variant(k) == 2) return launch_fused<128>(X, ldx, k, Rinv_tiles, Q, ldq, rows, G, ldg, ws, stream, gate);
   return cudaErrorNotSupported;
+}
+
+// ---- plain self Gram for k = 64 (K1): the register-resident sweep without the TRMM.
+// Used for full 64-wide panels only: measured (tools/gram_probe.py) 4.27 ms vs
+// 4.59 ms for the block-row pairs at m = 32M, k = 64, but slower for narrower
+// or ragged widths, where the pass is HBM bound and the pairs kernel's
+// dedicated producer warp streams better (k = 32: 0.48 vs 0.35 ms at 8M;
+// k = 50: 1.50 vs 1.23 ms), and for short sweeps (m = 200k: 0.071 vs 0.058 ms).
+bool gram_rt_supported(int k, int64_t rows) { return k == 64 && rows >= (int64_t(1) << 21); }
+size_t gram_rt_ws_bytes(int64_t rows, int k) {
+  return gram_rt_supported(k, rows) ? (size_t)rt_ctas(rows) * rt_kp(k) * rt_kp(k) * sizeof(double) + 256 : 0;
+}
+cudaError_t gram_rt_launch(const double* X, int64_t ldx, int k, int64_t rows, double* G, int ldg, double* ws,
+                           cudaStream_t stream, const int* gate) {
+  switch (rt_kp(k)) {
+    case 16: return launch_rt<16, false>(X, ldx, k, nullptr, nullptr, 0, rows, G, ldg, ws, stream, gate);
+    case 32: return launch_rt<32, false>(X, ldx, k, nullptr, nullptr, 0, rows, G, ldg, ws, stream, gate);
+    case 64: return launch_rt<64, false>(X, ldx, k, nullptr, nullptr, 0, rows, G, ldg, ws, stream, gate);
+    default: return cudaErrorNotSupported;
+  }
 }
 
 }  // namespace cqr

@@ -62,6 +62,11 @@ cudaError_t apply_gram_fused_launch(const double* X, int64_t ldx, int k, const d
 size_t apply_gram_fused_ws_bytes(int64_t rows, int k);
 bool apply_gram_fused_supported(int k);
 void set_fused(int mode);
+// self Gram for k = 64, register-resident row sweep (cqr_fused.cu)
+bool gram_rt_supported(int k, int64_t rows);
+size_t gram_rt_ws_bytes(int64_t rows, int k);
+cudaError_t gram_rt_launch(const double* X, int64_t ldx, int k, int64_t rows, double* G, int ldg, double* ws,
+                           cudaStream_t stream, const int* gate);
 
 // ------------------------------------------------------------- fused update pass (K3)
 bool update_pass_supported(int q, int p);

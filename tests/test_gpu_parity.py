@@ -216,6 +216,29 @@ def test_gramian_symmetric_and_accurate(m, k):
     assert np.max(np.abs(g - ref)) <= 1e-13 * np.max(np.abs(ref)) * max(1, math.log2(m))
 
 
+@pytest.mark.parametrize("m,k", [(7, 1), (300, 10), (1000, 16), (4099, 17), (5000, 33), (20000, 50), (70001, 64),
+                                 (2_097_155, 64)])
+@pytest.mark.parametrize("cap", [0, 5])
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_gram_schedules_k_le_64(m, k, cap, mode):
+    """Every self-Gram schedule (cqr_set_gram_pairs: 1 = the register-resident
+    row sweep for k <= 64, 2 = block-row pairs, 0 = tiles) on ragged widths,
+    with and without spare column capacity (ldk != k)."""
+    cq = _cq()
+    from paper_2507_07788_b200._device import ctx
+
+    x = np.random.default_rng(m + k + cap).normal(size=(m, k))
+    a = cq.CudaVectorArray.from_numpy(x, capacity=k + cap if cap else None)
+    ctx().lib.cqr_set_gram_pairs(mode)
+    try:
+        g = a.gramian()
+    finally:
+        ctx().lib.cqr_set_gram_pairs(1)
+    np.testing.assert_array_equal(g, g.T)
+    ref = x.T @ x
+    assert np.max(np.abs(g - ref)) <= 1e-13 * np.max(np.abs(ref)) * max(1, math.log2(m))
+
+
 @pytest.mark.parametrize("m,ka,kb", [(30, 4, 2), (5000, 100, 16), (3001, 496, 16)])
 def test_cross_gramian(m, ka, kb):
     cq = _cq()
