@@ -38,19 +38,26 @@ FP64_PEAK_SRC = "measured DMMA.8x8x4 microbenchmark (profiles/r01_fp64_peak.json
 # the bench's exact per-launch shape (tools/profile_round.sh); per config: the
 # captures summed, and the (rows, cols) they were taken at.
 NCU_SUMMARY = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_ncu_summary.json")
-TRAFFIC_CAPTURES = {3: (("trmm_k256.ncu-rep", "gram_k256.ncu-rep"), (2_000_000, 256))}
+TRAFFIC_CAPTURES = {
+    3: (("trmm_k256.ncu-rep", "gram_k256.ncu-rep"), (2_000_000, 256)),
+    # config 5's pass is one fused launch; captured at 32M rows (the 128M-row
+    # launch is 4x the same streaming sweep), scaled per row
+    5: (("fused_k64.ncu-rep",), (32_000_000, 64)),
+}
 
 
 def _traffic(config, rows, cols):
-    """Measured bytes per launch (read + write) or None when no capture matches."""
+    """Measured DRAM bytes per launch (read + write) of the dominant pass, or
+    None when no capture matches (same width; rows scaled for streaming sweeps
+    captured at a smaller row count)."""
     caps, shape = TRAFFIC_CAPTURES.get(config, ((), None))
-    if not caps or shape != (rows, cols) or not os.path.exists(NCU_SUMMARY):
+    if not caps or shape[1] != cols or rows <= 0 or not os.path.exists(NCU_SUMMARY):
         return None
     with open(NCU_SUMMARY) as fh:
         by = {d["capture"]: d for d in json.load(fh)}
     if not all(c in by for c in caps):
         return None
-    return sum(by[c]["dram_read_bytes"] + by[c]["dram_write_bytes"] for c in caps)
+    return sum(by[c]["dram_read_bytes"] + by[c]["dram_write_bytes"] for c in caps) * rows / shape[0]
 
 
 def _args():
@@ -363,7 +370,8 @@ def run_ours():
                          "unit": "TFLOP/s", "frac": tfs / FP64_PEAK_TFS,
                          "traffic": _traffic(ARGS.config, lm[0] if lm else 0, k),
                          "traffic_note": "DRAM bytes per launch, ncu --set full (profiles/r01_ncu_summary.json); "
-                                         "algorithmic: read X + write Q + read Q = 3 m k 8 B",
+                                         "algorithmic: read X + write Q (+ read Q again where TRMM and Gram "
+                                         "are separate launches, k > 64) = 2-3 m k 8 B",
                          "peak_source": FP64_PEAK_SRC, "kernel_share_of_step": step_share,
                          "flops_model": "TRMM k(k+1) + SYRK k(k+1) flops per row"},
             "kernels": kernel_summary,
