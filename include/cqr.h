@@ -219,6 +219,9 @@ size_t cqr_factor_workspace_bytes(int k);
 /* Diagnostics: globaltimer stamps (ns) of the phases of the last cqr_factor
  * launch (HOST array of 16; synchronous). */
 int cqr_debug_factor_profile(unsigned long long* out16);
+/* Diagnostics: 1 (default) = the update pass stages narrow sub-panels with one
+ * TMA tensor copy each; 0 = per-row-quad bulk copies only (comparisons). */
+void cqr_debug_update_tma(int on);
 int cqr_factor(const cqr_factor_config* cfg, int k, const double* G, int ldg, const double* Bt, int ldbt, int q,
                double* Rk, double* Rinv, int ldr, double* Racc, double* B, int ldb, double* shifts,
                cqr_factor_status* status, void* ws, size_t ws_bytes, void* stream);

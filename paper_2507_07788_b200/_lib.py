@@ -103,6 +103,7 @@ SIGNATURES = {
                                    _P, _P]),
     "cqr_factor_workspace_bytes": (_SZ, [_I]),
     "cqr_debug_factor_profile": (_I, [ctypes.POINTER(ctypes.c_ulonglong)]),
+    "cqr_debug_update_tma": (None, [_I]),
     "cqr_factor": (_I, [ctypes.POINTER(FactorConfig), _I, _P, _I, _P, _I, _I, _P, _P, _I, _P, _P, _I, _P, _P,
                         _P, _SZ, _P]),
 }

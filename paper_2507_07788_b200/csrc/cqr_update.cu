@@ -25,6 +25,9 @@
 // over through mbarriers; the projection group syncs on a named barrier.
 // Per-CTA partials [Bt'(q_pad x 16) | G'(16 x 16)] are written once per CTA
 // and summed by a fixed-order reduce kernel.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "cqr_common.cuh"
 #include "cqr_kernels.h"
 
@@ -43,7 +46,18 @@ __host__ __device__ constexpr int up_fixed(int SR) {   // doubles before the rin
   return UP_PB * CT_LD + 8 * SR * UP_PB + SR * UP_PB + UP_YS * SR * UP_PB;
 }
 
-struct UpdateArgs {
+// A sub-panel of a QI array with column capacity ldk is SR/4 runs of 4q
+// doubles, 32*ldk bytes apart.  As separate cp.async.bulk copies these are
+// small (512 B per row quad at q = 16) and a copy costs ~110 cycles of issue on
+// one SM (profiles/r01_bulk_pieces.jsonl: 512-B pieces stream at 1.4 TB/s,
+// 8 KB pieces at 6.5 TB/s), so narrow passes stage through a 3-D TMA tensor
+// map instead -- dims {4 (row in quad), ldk, quads}, box {4, qs, SR/4}: ONE
+// cp.async.bulk.tensor per sub-panel, landing exactly in the padded stage
+// layout (columns past the capacity and quads past the end are zero-filled).
+struct alignas(64) UpdateArgs {
+  CUtensorMap tm_qin;                     // valid when use_tm_qin
+  CUtensorMap tm_qb;                      // valid when use_tm_qb
+  int use_tm_qin, use_tm_qb;
   const double* Qin; int64_t ldqin; int q;
   const double* Qb; int64_t ldqb; int p;  // block read by the pass
   double* Qo; int64_t ldqo;               // where Q' goes (iteration mode; may be Qb)
@@ -70,7 +84,7 @@ static size_t update_smem_bytes(int q, int sr) {
 }
 
 template <int NQ, int SR>
-__global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(UpdateArgs a) {
+__global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(const __grid_constant__ UpdateArgs a) {
   if (a.gate != nullptr && *a.gate != 0) return;   // gated off
   constexpr int RB = SR / 8;        // 8-row blocks per sub-panel
   constexpr int Q4 = SR / 4;        // quads (k4 steps of the cross Gram) per sub-panel
@@ -109,11 +123,20 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(UpdateArgs a
     const int nq = (int)imin64(SR, a.rows - r0) >> 2;
     double* dq = stg + st * STG;
     double* db = dq + SR * qs;
-    mbar_arrive_expect_tx(&full[st], (uint32_t)nq * (q + p) * 32);
+    // a tensor copy always delivers the whole box (zero-filled out of bounds)
+    const uint32_t bq = a.use_tm_qin ? (uint32_t)(SR / 4) * qs * 32 : (uint32_t)nq * q * 32;
+    const uint32_t bb = a.use_tm_qb ? (uint32_t)(SR / 4) * UP_PB * 32 : (uint32_t)nq * p * 32;
+    mbar_arrive_expect_tx(&full[st], bq + bb);
     const double* sq = a.Qin + (r0 >> 2) * 4 * a.ldqin;
     const double* sb = a.Qb + (r0 >> 2) * 4 * a.ldqb;
-    for (int qq = 0; qq < nq; ++qq) bulk_g2s(dq + qq * 4 * qs, sq + qq * 4 * a.ldqin, (uint32_t)q * 32, &full[st]);
-    if (a.ldqb == UP_PB && p == UP_PB) {
+    if (a.use_tm_qin) {
+      tma_load_3d(dq, &a.tm_qin, 0, 0, (int)(r0 >> 2), &full[st]);
+    } else {
+      for (int qq = 0; qq < nq; ++qq) bulk_g2s(dq + qq * 4 * qs, sq + qq * 4 * a.ldqin, (uint32_t)q * 32, &full[st]);
+    }
+    if (a.use_tm_qb) {
+      tma_load_3d(db, &a.tm_qb, 0, 0, (int)(r0 >> 2), &full[st]);
+    } else if (a.ldqb == UP_PB && p == UP_PB) {
       bulk_g2s(db, sb, (uint32_t)nq * UP_PB * 32, &full[st]);
     } else {
       for (int qq = 0; qq < nq; ++qq) bulk_g2s(db + qq * 4 * UP_PB, sb + qq * 4 * a.ldqb, (uint32_t)p * 32, &full[st]);
@@ -126,8 +149,26 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(UpdateArgs a
   uint32_t ph = 0, yph = 0;
   if (warp < 8) {
     // ================= projection group
+    // Bases up to 64 columns ("narrow", 32-row sub-panels): warp wa owns the
+    // output block (rows 8(wa/2).., columns 8(wa%2)..) of proj = Q_in Bt over
+    // the FULL width, its Bt column block in registers, so there are no
+    // per-warp partials to reduce through shared memory: t = Q - proj goes
+    // straight from the accumulators to the t buffer (one barrier per
+    // sub-panel instead of two, 1 KB of t stores instead of 8 x 4 KB of
+    // partials plus their 8-way sum).  Wider bases split the width over the
+    // warps (Bt rows in registers) and sum the 8 partials in a fixed order.
+    constexpr bool NARROW = NQ == 1 && SR == 32;
     const int wa = warp;
-    double btr[NQ][2][2];   // Bt(64c + 8wa + 4h + t, 8nb + g)
+    double btn[NARROW ? 16 * NQ : 1];   // narrow: Bt(4ks + t, 8(wa%2) + g)
+    if constexpr (NARROW) {
+#pragma unroll
+      for (int ks = 0; ks < 16 * NQ; ++ks) {
+        const int kk = 4 * ks + t, n = 8 * (wa & 1) + g;
+        btn[ks] = (!init && kk < q && n < p) ? a.Bt[(int64_t)n * a.ldbt + kk] : 0.0;
+      }
+    }
+    double btr[NARROW ? 1 : NQ][2][2];   // Bt(64c + 8wa + 4h + t, 8nb + g)
+    if constexpr (!NARROW) {
 #pragma unroll
     for (int c = 0; c < NQ; ++c)
 #pragma unroll
@@ -137,6 +178,7 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(UpdateArgs a
           const int kk = 64 * c + 8 * wa + 4 * h + t, n = 8 * nb + g;
           btr[c][h][nb] = (!init && kk < q && n < p) ? a.Bt[(int64_t)n * a.ldbt + kk] : 0.0;
         }
+    }
     for (int64_t j = 0; j < mine; ++j) {
       const int64_t r0 = (blockIdx.x + j * gridDim.x) * SR;
       const int nrows = (int)imin64(SR, a.rows - r0);
@@ -150,7 +192,28 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(UpdateArgs a
         double* Qz = stg + s * STG + nrows * qs;
         for (int e = tid; e < (SR - nrows) * qs; e += 256) Qz[e] = 0.0;
       }
-      if (!init) {
+      if (NARROW && !init) {
+        const int rbw = wa >> 1, nbw = wa & 1;
+        // A fragments Q_in(row 8 rbw + g, column 4 ks + t): conflict-free (qs = 4 mod 8)
+        const double* xa = Qs + (2 * rbw + (g >> 2)) * 4 * qs + (g & 3) + 4 * t;
+        double acc[4][2] = {};   // k4 steps round-robin over four accumulator chains
+#pragma unroll
+        for (int ks = 0; ks < 16; ++ks) {
+          if (4 * ks < q) {   // warp-uniform
+            const double av = (4 * ks + t < q) ? xa[16 * ks] : 0.0;
+            dmma(acc[ks & 3], av, btn[ks]);
+          }
+        }
+        const int row = 8 * rbw + g;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int col = 8 * nbw + 2 * t + e;
+          const int off = (row >> 2) * 4 * UP_PB + 4 * col + (row & 3);
+          tq[off] = (col < p && row < nrows) ? Ys[off] - ((acc[0][e] + acc[1][e]) + (acc[2][e] + acc[3][e])) : 0.0;
+        }
+        asm volatile("bar.sync 2, 256;" ::: "memory");
+      }
+      if (!NARROW && !init) {
         double pr[RB][2][2];
 #pragma unroll
         for (int rb = 0; rb < RB; ++rb)
@@ -190,6 +253,8 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(UpdateArgs a
           tq[e] = (col < p && row < nrows) ? Ys[e] - sum : 0.0;
         }
         asm volatile("bar.sync 2, 256;" ::: "memory");
+      }
+      if (!init) {
         if (j >= UP_YS) mbar_wait(&yempty[ys], yph ^ 1);
         if (wa < 2 * RB) {
           // Q' block (rb, nb) = t(rows 8rb.., :) R^-1(:, cols 8nb..); R^-1 upper: K < 8(nb+1)
@@ -315,6 +380,36 @@ static int update_ctas(int64_t rows) {
   return (int)(n < c ? (n < 1 ? 1 : n) : c);
 }
 
+// ---- 3-D tensor maps of QI arrays (driver entry point through the runtime: no libcuda link)
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &qr) == cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+static int g_update_tma = 1;   // cqr_debug_update_tma: 0 = per-quad bulk copies only (comparisons)
+void set_update_tma(int on) { g_update_tma = on ? 1 : 0; }
+
+// box {4, boxc, sr/4} over a QI array (rows multiple of 16, column capacity ld)
+static bool encode_qi_map(CUtensorMap* tm, const double* base, int64_t ld, int64_t rows, int boxc, int sr) {
+  auto enc = tensor_map_encoder();
+  if (!g_update_tma || enc == nullptr || boxc > 256 || ((uintptr_t)base & 15) != 0) return false;
+  const cuuint64_t dims[3] = {4, (cuuint64_t)ld, (cuuint64_t)(rows / 4)};
+  const cuuint64_t strides[2] = {32, (cuuint64_t)ld * 32};
+  const cuuint32_t box[3] = {4, (cuuint32_t)boxc, (cuuint32_t)(sr / 4)};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool update_pass_supported(int q, int p) {
   return q >= 1 && q <= UP_MAXQ && p >= 1 && p <= UP_PB && up_stages(q, up_sr(q)) >= 2;
 }
@@ -353,6 +448,9 @@ cudaError_t update_pass_launch(const double* Qin, int64_t ldqin, int q, const do
   a.gate = gate;
   a.qs = up_qs(q);
   const int sr = up_sr(q);
+  // one tensor copy per sub-panel where the per-quad runs would be small
+  a.use_tm_qin = (q * 32 < 8192) && encode_qi_map(&a.tm_qin, Qin, ldqin, rows, a.qs, sr) ? 1 : 0;
+  a.use_tm_qb = !(ldqb == UP_PB && p == UP_PB) && encode_qi_map(&a.tm_qb, Qb, ldqb, rows, UP_PB, sr) ? 1 : 0;
   a.ns = up_stages(q, sr);
   const size_t smem = update_smem_bytes(q, sr);
   const int ctas = update_ctas(rows);

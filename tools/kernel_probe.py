@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--shifted", action="store_true", help="factor a rank-deficient Gram (shift path)")
     ap.add_argument("--q", type=int, default=256, help="basis width for --only update")
     ap.add_argument("--fk", default="64,128,256", help="widths for --only factor")
+    ap.add_argument("--tma", type=int, default=1, help="update: TMA tensor staging of narrow sub-panels (0/1)")
+    ap.add_argument("--cap", type=int, default=0, help="update: column capacity of the basis (config 4's chain: 512)")
     a = ap.parse_args()
     import paper_2507_07788_b200 as cq
     from paper_2507_07788_b200 import _lib
@@ -36,7 +38,10 @@ def main():
     from paper_2507_07788_b200.workloads import device_gaussian
 
     if a.only == "update":
-        q_in = device_gaussian(cq.CudaVectorArray.zeros(cq.VectorSpace(m), a.q), 2)
+        from paper_2507_07788_b200._device import ctx
+
+        ctx().lib.cqr_debug_update_tma(a.tma)
+        q_in = device_gaussian(cq.CudaVectorArray.zeros(cq.VectorSpace(m), a.q, capacity=a.cap or None), 2)
         qb = device_gaussian(cq.CudaVectorArray.zeros(cq.VectorSpace(m), k), 3)
         eng = Engine(k, cq.AlgoConfig(), q=a.q)
         g = torch.randn((k, k), dtype=torch.float64, device="cuda")
