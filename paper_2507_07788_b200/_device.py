@@ -39,6 +39,7 @@ class DeviceContext:
         self._ws = torch.empty(0, dtype=torch.uint8, device=self.device)
         self._ws2 = torch.empty(0, dtype=torch.uint8, device=self.device)
         self._pinned = {}   # shape -> free pinned host buffers (status slots; cudaHostAlloc is slow)
+        self.engine_pool = {}   # (k, q, status capacity) -> [(Engine buffers, release event)]
         self.launches = 0   # libcqr kernel launches issued (bench bookkeeping)
         self.timer = None   # optional KernelTimer (bench): CUDA events per libcqr call
 

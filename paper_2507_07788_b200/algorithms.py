@@ -196,6 +196,7 @@ def chol_qr(a, cfg=None, ledger=None):
     h = eng.factor_async(_lib.POLICY_PLAIN, m, n)
     q = _fresh_like(a, n)
     eng.apply(a, q, with_gram=False)
+    eng.r_prefetch()
     (st,) = eng.collect([h])
     _charge(ledger, "gemm", _flops.gemm_flops(m, n, n))
     _charge_plain_attempt(ledger, n)
@@ -228,6 +229,7 @@ def chol_qr2(a, cfg=None, ledger=None):
     eng.apply(a, q, with_gram=True)
     h2 = eng.factor_async(_lib.POLICY_PLAIN, m, n)
     _apply_last(eng, q)
+    eng.r_prefetch()
     st1, st2 = eng.collect([h1, h2])
     margins = []
     for i, st in enumerate((st1, st2)):
@@ -285,6 +287,7 @@ def s_chol_qr3(a, cfg=None, ledger=None):
     q = _apply_gram_into(eng, q, fresh_ok=False)
     hs.append(eng.factor_async(_lib.POLICY_PLAIN, m, n))
     _apply_last(eng, q)
+    eng.r_prefetch()
     sts = eng.collect(hs)
 
     st = sts[0]

@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--m", type=int, default=2_000_000)
     ap.add_argument("--k", type=int, default=256)
     ap.add_argument("--cond", type=float, default=15.0)
+    ap.add_argument("--algo", default="rs_chol_qr")
     a = ap.parse_args()
     space = cq.VectorSpace(a.m)
 
@@ -29,23 +30,21 @@ def main():
         return cq.CudaVectorArray.from_device_colmajor(space, x_full.T)
 
     x = device_svd_matrix(from_global, a.m, a.k, a.cond, 20250, u_from="cholqr2")
+    algo = getattr(cq, a.algo)
     for _ in range(3):
-        cq.rs_chol_qr(x)
+        algo(x)
     torch.cuda.synchronize()
     from torch.profiler import ProfilerActivity, profile
 
     with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
-        cq.rs_chol_qr(x)
-        torch.cuda.synchronize()
-        cq.rs_chol_qr(x)
+        for _ in range(4):
+            algo(x)
         torch.cuda.synchronize()
     ev = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
     ev.sort(key=lambda e: e.time_range.start)
-    # second call only: after the largest gap (the host sync between calls)
-    starts = [e.time_range.start for e in ev]
-    gaps = [(starts[i + 1] - ev[i].time_range.end, i) for i in range(len(ev) - 1)]
-    cut = max(gaps)[1] + 1
-    ev = ev[cut:]
+    # calls 2-4 (back to back, as in bench.py's timed loop)
+    n_per = len(ev) // 4
+    ev = ev[n_per:]
     busy = sum(e.time_range.end - e.time_range.start for e in ev)
     span = ev[-1].time_range.end - ev[0].time_range.start
     gl = []
