@@ -19,7 +19,7 @@
 // loops (no predicated-off DMMA occupies the tensor pipe).  The groups hand
 // panels over through mbarriers only (no CTA-wide barrier in the sweep).
 // Thread 0 issues the bulk copies.  Per-CTA partial triangles are summed in a
-// fixed warp order, then over CTAs by gram_fused_reduce in a fixed order.
+// fixed warp order, then over CTAs by gram_partials_reduce in a fixed order.
 #include "cqr_common.cuh"
 #include "cqr_kernels.h"
 #include "cqr_pairs.cuh"
@@ -512,21 +512,6 @@ __global__ void __launch_bounds__(RtCfg<KP>::THREADS, 1)
   for (int e = tid; e < KP * KP; e += 256) out[e] = red[e];
 }
 
-// fixed-order sum over CTAs of the per-CTA KP x KP partials; lower triangle, mirrored
-__global__ void gram_fused_reduce(const double* __restrict__ ws, int nparts, int KP, int k, double* G, int ldg,
-                                  const int* gate) {
-  if (gate != nullptr && *gate != 0) return;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)k * k;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int r = (int)(e % k), c = (int)(e / k);
-    if (r < c) continue;
-    double s = 0.0;
-    for (int p = 0; p < nparts; ++p) s += ws[(int64_t)p * KP * KP + c * KP + r];
-    G[(int64_t)c * ldg + r] = s;
-    G[(int64_t)r * ldg + c] = s;
-  }
-}
-
 static int fused_kp(int k) {
   if (k > 32 && k <= 64) return 64;
   if (k > 96 && k <= 128) return 128;
@@ -601,9 +586,7 @@ static cudaError_t launch_rt(const double* X, int64_t ldx, int k, const double* 
                                                                                 gate);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  const int64_t nel = (int64_t)k * k;
-  int blocks = (int)imin64(ceil_div(nel, 256), 2 * num_sms());
-  gram_fused_reduce<<<blocks < 1 ? 1 : blocks, 256, 0, s>>>(ws, ctas, KP, k, G, ldg, gate);
+  gram_partials_reduce<<<gram_partials_reduce_blocks(k), 32 * PR_WARPS, 0, s>>>(ws, ctas, KP, k, G, ldg, gate);
   return cudaGetLastError();
 }
 
@@ -628,9 +611,7 @@ static cudaError_t launch_fused(const double* X, int64_t ldx, int k, const doubl
     apply_gram_fused_kernel<KP, false><<<ctas, FuCfg<KP>::THREADS, smem, s>>>(X, ldx, k, Rt, Q, ldq, rows, ws, gate);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  const int64_t nel = (int64_t)k * k;
-  int blocks = (int)imin64(ceil_div(nel, 256), 2 * num_sms());
-  gram_fused_reduce<<<blocks < 1 ? 1 : blocks, 256, 0, s>>>(ws, ctas, KP, k, G, ldg, gate);
+  gram_partials_reduce<<<gram_partials_reduce_blocks(k), 32 * PR_WARPS, 0, s>>>(ws, ctas, KP, k, G, ldg, gate);
   return cudaGetLastError();
 }
 

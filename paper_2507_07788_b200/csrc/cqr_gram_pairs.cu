@@ -149,20 +149,6 @@ __global__ void __launch_bounds__(GPCfg<KP>::THREADS, 1) gram_pairs_kernel(const
   }
 }
 
-__global__ void gram_pairs_reduce(const double* __restrict__ ws, int nparts, int KP, int k, double* G, int ldg,
-                                  const int* gate) {
-  if (gate != nullptr && *gate != 0) return;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)k * k;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int r = (int)(e % k), c = (int)(e / k);
-    if (r < c) continue;
-    double s = 0.0;
-    for (int p = 0; p < nparts; ++p) s += ws[(int64_t)p * KP * KP + (int64_t)c * KP + r];
-    G[(int64_t)c * ldg + r] = s;
-    G[(int64_t)r * ldg + c] = s;
-  }
-}
-
 static int gp_kp(int k) {
   if (k <= 16) return 16;
   if (k <= 32) return 32;
@@ -207,9 +193,8 @@ static cudaError_t launch_gp(const double* X, int64_t ldx, int k, int64_t rows, 
   gram_pairs_kernel<KP><<<items * nsplit, GPCfg<KP>::THREADS, smem, s>>>(X, ldx, k, rows, nsplit, ws, gate);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  const int64_t nel = (int64_t)k * k;
-  int blocks = (int)imin64(ceil_div(nel, 256), 4 * num_sms());
-  gram_pairs_reduce<<<blocks < 1 ? 1 : blocks, 256, 0, s>>>(ws, items * nsplit, KP, k, G, ldg, gate);
+  gram_partials_reduce<<<gram_partials_reduce_blocks(k), 32 * PR_WARPS, 0, s>>>(ws, items * nsplit, KP, k, G, ldg,
+                                                                                gate);
   return cudaGetLastError();
 }
 
