@@ -243,9 +243,18 @@ def run_ours():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # plumbing check of the N > 1 path on a one-GPU box (tests only): every rank
+    # on cuda:0 with gloo's host-staged allreduce; no kernel waits on another rank
+    one_gpu_check = os.environ.get("CQR_BENCH_ONE_GPU_RANKS") == "1"
+    if one_gpu_check:
+        local = 0
+        os.environ["LOCAL_RANK"] = "0"
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu_check:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2507_07788_b200 as cq
     from paper_2507_07788_b200 import _device
     from paper_2507_07788_b200.workloads import device_gaussian, device_svd_matrix

@@ -169,3 +169,24 @@ def test_sharded_update_chain(sharded):
     floor = 10 * U * math.sqrt(two["r"].shape[0])
     assert two["loo"] <= 10 * max(one["loo"], floor)
     assert two["rrr"] <= 10 * max(one["rrr"], floor)
+
+
+@pytest.mark.parametrize("config,rows", [(3, 400_000), (4, 200_000)])
+def test_bench_two_ranks_plumbing(config, rows, tmp_path):
+    """bench.py's N > 1 path (torchrun, row sharding, max-over-ranks timing,
+    e2e, the update chain) end to end with two ranks on cuda:0 and gloo
+    (CQR_BENCH_ONE_GPU_RANKS): one JSON line from rank 0 with n_gpus = 2."""
+    import json
+    import subprocess
+
+    env = dict(os.environ, CQR_BENCH_ONE_GPU_RANKS="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--config", str(config), "--steps", "2", "--warmup", "1", "--rows", str(rows), "--no-cpu"]
+    out = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["e2e"]["value"] > 0
+    assert line["config"]["rows"] == rows
