@@ -621,9 +621,12 @@ __device__ __noinline__ bool chol_attempt(const double* __restrict__ Xs, const d
       }
     pad_blocked(Wb, k);
     __syncthreads();
+    fmark(2);
     const int nb = (k + 7) >> 3;
     ok = chol_banded(Wb, k, nb, nb, 0, rowbuf, smin, fs, LayoutUpper(), flag);
+    fmark(3);
     if (ok) store_blocked(Wb, k, 0, Rk, ldr);
+    fmark(4);
   } else if (k > FK_BIG_K && k <= FK_BAND_K) {
     double* W = gW;   // k x k upper (column-major): X + sigma I, factored in place by bands
     for (int c = warp; c < k; c += FK_NW)

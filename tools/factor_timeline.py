@@ -33,4 +33,9 @@ rows = []
 for i, e in enumerate(ev[:12]):
     gap = e.time_range.start - ev[i - 1].time_range.end if i else 0.0
     rows.append((e.name[:40], round(e.time_range.end - e.time_range.start, 1), round(gap, 1)))
-print(json.dumps({"k": k, "policy": a.policy, "first_kernels_us_gap": rows}, indent=0))
+import ctypes
+buf = (ctypes.c_ulonglong * 16)()
+eng.cx.lib.cqr_debug_factor_profile(buf)
+phases = [round((buf[i] - buf[0]) / 1e3, 2) if buf[i] >= buf[0] else None for i in range(7)]
+print(json.dumps({"k": k, "policy": a.policy, "phases_us(last call: 0 start,1 X formed,2 copied in,3 factored,"
+                  "4 stored,6 end)": phases, "first_kernels_us_gap": rows[:4]}))
