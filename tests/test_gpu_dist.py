@@ -188,5 +188,7 @@ def test_bench_two_ranks_plumbing(config, rows, tmp_path):
     lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1, out.stdout[-2000:]
     line = json.loads(lines[0])
-    assert line["n_gpus"] == 2 and line["value"] > 0 and line["e2e"]["value"] > 0
+    assert line["n_gpus"] == 2 and line["value"] > 0
+    if config != 4:   # the update chain reports no e2e
+        assert line["e2e"]["value"] > 0
     assert line["config"]["rows"] == rows
