@@ -425,7 +425,19 @@ def test_apply_gram_matches_separate_ops(m, k, inplace, fused):
         ctx().lib.cqr_set_fused(2)   # back to the default (auto)
 
 
-def _apply_gram_case(cq, _lib, Engine, m, k, inplace):
+@pytest.mark.parametrize("m,k", [(4100, 17), (70001, 50), (90000, 64), (3001, 128)])
+@pytest.mark.parametrize("inplace", [False, True])
+def test_apply_gram_with_spare_capacity(m, k, inplace):
+    """cqr_apply_gram on arrays whose column capacity exceeds k (ld != k: the
+    per-quad staging paths of the fused and TRMM kernels)."""
+    cq = _cq()
+    from paper_2507_07788_b200 import _lib
+    from paper_2507_07788_b200._engine import Engine
+
+    _apply_gram_case(cq, _lib, Engine, m, k, inplace, cap=k + 7)
+
+
+def _apply_gram_case(cq, _lib, Engine, m, k, inplace, cap=None):
     rng = np.random.default_rng(m + k)
     x = rng.normal(size=(m, k))
     g = rng.normal(size=(k, k))
@@ -435,10 +447,10 @@ def _apply_gram_case(cq, _lib, Engine, m, k, inplace):
     eng.G.copy_(torch.from_numpy(spd))
     st = eng.factor(_lib.POLICY_PLAIN, m, k)
     assert st.code == _lib.FACTORED
-    a = cq.CudaVectorArray.from_numpy(x)
+    a = cq.CudaVectorArray.from_numpy(x, capacity=cap)
     if inplace and not eng.in_place_gram_ok():
         pytest.skip("in place needs the fused kernel or k <= 64")
-    dst = a if inplace else cq.CudaVectorArray.zeros(a.space, k)
+    dst = a if inplace else cq.CudaVectorArray.zeros(a.space, k, capacity=cap)
     eng.apply(a, dst, with_gram=True)
     g_dev = eng.G.cpu().numpy()
     r = eng.Rk[:, :k].cpu().numpy().T
