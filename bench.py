@@ -453,7 +453,7 @@ def run_ours():
                        "passes": passes, "shift_attempts": attempts,
                        "parallelism": f"row-sharded dp{world}",
                        "l2": "inputs larger than L2 (%.1f GB)" % (m * k * 8 / 1e9)},
-            "roofline": {"bound": "fp64", "kernel": dom, "achieved": tfs, "peak": FP64_PEAK_TFS,
+            "roofline": {"bound": "tensor", "pipe": "FP64 DMMA.8x8x4 (tensor pipe)", "kernel": dom, "achieved": tfs, "peak": FP64_PEAK_TFS,
                          "unit": "TFLOP/s", "frac": tfs / FP64_PEAK_TFS,
                          "traffic": _traffic(ARGS.config, lm[0] if lm else 0, k),
                          "traffic_note": "DRAM bytes per launch, ncu --set full (profiles/r01_ncu_summary.json); "
@@ -560,7 +560,7 @@ def run_update_chain(cq, cx, cfg, m, world, rank, local):
             "config": {"workload": cfg["workload"], "rows": m, "cols": 512, "block": p, "blocks": nblk,
                        "parallelism": f"row-sharded dp{world}", "timed": "sum of update-call event times",
                        "per_block": passes[:3] + ["..."] + passes[-2:], "final_loo_fro": loo},
-            "roofline": {"bound": "fp64", "kernel": "update_pass", "achieved": tfs, "peak": FP64_PEAK_TFS,
+            "roofline": {"bound": "tensor", "pipe": "FP64 DMMA.8x8x4 (tensor pipe)", "kernel": "update_pass", "achieved": tfs, "peak": FP64_PEAK_TFS,
                          "unit": "TFLOP/s", "frac": tfs / FP64_PEAK_TFS, "traffic": None,
                          "peak_source": FP64_PEAK_SRC,
                          "flops_model": "2 m q p (projection) + 2 m q p (cross Gram) + 2 m p (p+1) per pass"},
