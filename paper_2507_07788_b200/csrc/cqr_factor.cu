@@ -811,6 +811,76 @@ __device__ __forceinline__ void matvec_rows(const double* Xr, int i0, int nr, in
   }
 }
 
+// Power iteration of spectral_norm_estimate (kernels.py:126-178) for X in
+// shared memory (k <= 128) on warp 0 alone: lane l owns rows l, l + 32, ...
+// (NR = ceil(k/32) rows), reads column j of the symmetric X (consecutive lanes,
+// consecutive addresses) against the broadcast v[j], and the two dot products
+// of an iteration are warp sums -- no block barrier inside the loop.  The
+// block-wide version spent ~4000 cycles per iteration at k = 64 on four
+// 384-thread barriers and per-row warp reductions; this one ~600.  The caller
+// has set vec = 1/sqrt(k).  Returns the estimate (or `fro` with est_flag set).
+template <int NR>
+__device__ double power_iter_warp(const double* __restrict__ X, int k, double tol, int max_iter, double* vec,
+                                  FState& fs, double fro) {
+  const int lane = threadIdx.x & 31;
+  double vr[NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) vr[r] = (lane + 32 * r < k) ? vec[lane + 32 * r] : 0.0;
+  bool have_prev = false;
+  double prev = 0.0;
+  for (int it = 0; it < max_iter; ++it) {
+    double acc[NR][2];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) { acc[r][0] = 0.0; acc[r][1] = 0.0; }
+    int j = 0;
+    for (; j + 1 < k; j += 2) {   // two accumulator chains per row (even / odd columns)
+      const double v0 = vec[j], v1 = vec[j + 1];
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const int i = lane + 32 * r;
+        if (i < k) {
+          acc[r][0] += X[(int64_t)j * k + i] * v0;
+          acc[r][1] += X[(int64_t)(j + 1) * k + i] * v1;
+        }
+      }
+    }
+    if (j < k) {
+      const double v0 = vec[j];
+#pragma unroll
+      for (int r = 0; r < NR; ++r)
+        if (lane + 32 * r < k) acc[r][0] += X[(int64_t)j * k + lane + 32 * r] * v0;
+    }
+    double ww = 0.0, vw = 0.0, w[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      w[r] = acc[r][0] + acc[r][1];
+      ww += w[r] * w[r];
+      vw += vr[r] * w[r];
+    }
+    const double nw = sqrt(warp_sum(ww));
+    const double lam = warp_sum(vw);
+    if (nw == 0.0) {
+      if (lane == 0) fs.est_flag = 1;
+      return fro;
+    }
+    __syncwarp();   // every lane has read vec for this product
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      vr[r] = w[r] / nw;
+      if (lane + 32 * r < k) vec[lane + 32 * r] = vr[r];
+    }
+    __syncwarp();
+    if (have_prev && fabs(lam - prev) <= tol * fabs(lam)) {
+      if (lane == 0) g_fprof[8] = it + 1;   // iterations of the last estimate (profiling)
+      return fabs(lam);
+    }
+    prev = lam;
+    have_prev = true;
+  }
+  if (lane == 0) { fs.est_flag = 2; g_fprof[8] = max_iter; }
+  return fro;
+}
+
 // spectral_norm_estimate (kernels.py:126-178) on the full symmetric X.
 // Returns the estimate; sets fs.est_flag (1 stalled, 2 not converged) and
 // fs.code = CQR_ASYMMETRIC on the asymmetry ValueError.
@@ -858,6 +928,23 @@ __device__ double norm_estimate(const double* __restrict__ X, int k, double tol,
     fence_mbar_init();
   }
   __syncthreads();
+  if constexpr (!GX) {
+    // X in shared memory: the whole iteration on warp 0, the result broadcast through red
+    if (warp == 0) {
+      double res;
+      switch ((k + 31) >> 5) {
+        case 1: res = power_iter_warp<1>(X, k, tol, max_iter, vec, fs, fro); break;
+        case 2: res = power_iter_warp<2>(X, k, tol, max_iter, vec, fs, fro); break;
+        case 3: res = power_iter_warp<3>(X, k, tol, max_iter, vec, fs, fro); break;
+        default: res = power_iter_warp<4>(X, k, tol, max_iter, vec, fs, fro); break;
+      }
+      if (lane == 0) red[0] = res;
+    }
+    __syncthreads();
+    const double res = red[0];
+    __syncthreads();   // red is reused by the caller's reductions
+    return res;
+  }
   const int nch = R > 0 ? (k + R - 1) / R : 0;   // row chunks per product
   uint32_t uses[2] = {0u, 0u};                    // this warp's stage uses (phase parity)
   auto issue = [&](int ch, int st) {              // lane 0: chunk ch into this warp's stage st
