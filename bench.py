@@ -22,6 +22,10 @@ k(k+1) per row for the symmetric Gram) / mean launch time, against the FP64
 peak measured on this pool's B200s (profiles/r01_fp64_peak.json, DMMA).
 cpu_baseline: the CPU oracle (NumPy restatement of the reference, `oracle/`)
 on a bounded row sample of the same construction, all host cores.
+
+CQR_BENCH_ONE_GPU_RANKS=1 (tests only): under torchrun every rank runs on
+cuda:0 with gloo instead of NCCL, to exercise the N > 1 code path on a
+one-GPU box; its timings mean nothing.
 """
 
 from __future__ import annotations
