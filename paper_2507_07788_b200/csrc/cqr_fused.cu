@@ -586,7 +586,7 @@ static cudaError_t launch_rt(const double* X, int64_t ldx, int k, const double* 
                                                                                 gate);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  gram_partials_reduce<<<gram_partials_reduce_blocks(k), 32 * PR_WARPS, 0, s>>>(ws, ctas, KP, k, G, ldg, gate);
+  gram_partials_reduce<<<gram_partials_reduce_blocks(k), 256, 0, s>>>(ws, ctas, KP, k, G, ldg, gate);
   return cudaGetLastError();
 }
 
@@ -611,7 +611,7 @@ static cudaError_t launch_fused(const double* X, int64_t ldx, int k, const doubl
     apply_gram_fused_kernel<KP, false><<<ctas, FuCfg<KP>::THREADS, smem, s>>>(X, ldx, k, Rt, Q, ldq, rows, ws, gate);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  gram_partials_reduce<<<gram_partials_reduce_blocks(k), 32 * PR_WARPS, 0, s>>>(ws, ctas, KP, k, G, ldg, gate);
+  gram_partials_reduce<<<gram_partials_reduce_blocks(k), 256, 0, s>>>(ws, ctas, KP, k, G, ldg, gate);
   return cudaGetLastError();
 }
 

@@ -124,38 +124,34 @@ struct PairDispatch<NB, NB / 2> {
 };
 
 // Fixed-order sum of the per-CTA KP x KP partial triangles into G (k x k,
-// lower triangle mirrored).  A block owns 32 consecutive column-major
-// elements (coalesced across the lanes); its 8 warps split the partials
-// (warp w sums p = w, w + 8, ... in order), then the 8 warp sums are added in
-// warp order.  With one thread per element summing all ~148 partials in a
-// chain, the k = 64 reduce was latency bound at 30-50 us (one warp per SM,
-// profiles/r01_launches_config5.csv); here every warp has ~19 independent loads.
-constexpr int PR_WARPS = 8;
-static __global__ void __launch_bounds__(32 * PR_WARPS) gram_partials_reduce(const double* __restrict__ ws, int nparts, int KP,
-                                                                      int k, double* G, int ldg, const int* gate) {
+// lower triangle mirrored): one thread per element adds the partials in CTA
+// order, p = 0, 1, 2, ... (the order every earlier version used, so results
+// are bitwise unchanged).  The partials are loaded in batches of 32 before the
+// adds: the first version issued one load per add and was latency bound at
+// 30-50 us per call at k = 64 (profiles/r01_launches_config5.csv).
+constexpr int PR_BATCH = 32;
+static __global__ void __launch_bounds__(256) gram_partials_reduce(const double* __restrict__ ws, int nparts, int KP,
+                                                                   int k, double* G, int ldg, const int* gate) {
   if (gate != nullptr && *gate != 0) return;
-  __shared__ double part[PR_WARPS][32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t e = (int64_t)blockIdx.x * 32 + lane;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)k * k) return;
   const int r = (int)(e % k), c = (int)(e / k);
-  const bool live = e < (int64_t)k * k && r >= c;
+  if (r < c) return;
+  const double* src = ws + (int64_t)c * KP + r;
+  const int64_t ps = (int64_t)KP * KP;
   double s = 0.0;
-  if (live) {
-    const double* src = ws + (int64_t)c * KP + r;
-    const int64_t ps = (int64_t)KP * KP;
-#pragma unroll 4
-    for (int p = warp; p < nparts; p += PR_WARPS) s += src[p * ps];
-  }
-  part[warp][lane] = s;
-  __syncthreads();
-  if (warp == 0 && live) {
-    double t = part[0][lane];
+  int p = 0;
+  for (; p + PR_BATCH <= nparts; p += PR_BATCH) {
+    double v[PR_BATCH];
 #pragma unroll
-    for (int w = 1; w < PR_WARPS; ++w) t += part[w][lane];
-    G[(int64_t)c * ldg + r] = t;
-    G[(int64_t)r * ldg + c] = t;
+    for (int j = 0; j < PR_BATCH; ++j) v[j] = src[(p + j) * ps];
+#pragma unroll
+    for (int j = 0; j < PR_BATCH; ++j) s += v[j];
   }
+  for (; p < nparts; ++p) s += src[p * ps];
+  G[(int64_t)c * ldg + r] = s;
+  G[(int64_t)r * ldg + c] = s;
 }
-inline int gram_partials_reduce_blocks(int k) { return (int)((int64_t)k * k + 31) / 32; }
+inline int gram_partials_reduce_blocks(int k) { return (int)(((int64_t)k * k + 255) / 256); }
 
 }  // namespace cqr

@@ -351,44 +351,37 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(const __grid
 }
 
 // fixed-order sum over CTAs; Bt' (q x p, ld ldbt) and G (p x p, lower mirrored, ld ldg).
-// A block owns 32 consecutive output elements; its 8 warps split the partials
-// (warp w: p = w, w + 8, ...) and the warp sums are added in warp order (one
-// thread summing all ~148 partials in a chain was latency bound).
-__global__ void __launch_bounds__(256) update_reduce_kernel(const double* __restrict__ ws, int nparts, int q, int p,
-                                                            int qp, double* Bt, int ldbt, double* G, int ldg,
-                                                            const int* gate) {
+// One thread per element adds the partials in CTA order (bitwise the order of
+// every earlier version), loading them in batches of 32 ahead of the adds.
+__global__ void update_reduce_kernel(const double* __restrict__ ws, int nparts, int q, int p, int qp,
+                                     double* Bt, int ldbt, double* G, int ldg, const int* gate) {
   if (gate != nullptr && *gate != 0) return;
-  __shared__ double part[8][32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int ld = qp + UP_PB;
   const int64_t nbt = (int64_t)q * p, ng = (int64_t)p * p;
-  const int64_t e = (int64_t)blockIdx.x * 32 + lane;
-  int r = 0, c = 0;
-  int64_t off = 0;
-  bool live = e < nbt + ng;
-  if (live) {
+  const int64_t ps = (int64_t)ld * UP_PB;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nbt + ng;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int r, c;
+    int64_t off;
     if (e < nbt) { r = (int)(e % q); c = (int)(e / q); off = (int64_t)c * ld + r; }
     else {
       const int64_t f = e - nbt;
       r = (int)(f % p); c = (int)(f / p);
-      live = r >= c;
+      if (r < c) continue;
       off = (int64_t)c * ld + qp + r;
     }
-  }
-  double s = 0.0;
-  if (live) {
-    const int64_t ps = (int64_t)ld * UP_PB;
-#pragma unroll 4
-    for (int i = warp; i < nparts; i += 8) s += ws[i * ps + off];
-  }
-  part[warp][lane] = s;
-  __syncthreads();
-  if (warp == 0 && live) {
-    double t = part[0][lane];
+    double s = 0.0;
+    int i = 0;
+    for (; i + 32 <= nparts; i += 32) {
+      double v[32];
 #pragma unroll
-    for (int w = 1; w < 8; ++w) t += part[w][lane];
-    if (e < nbt) Bt[(int64_t)c * ldbt + r] = t;
-    else { G[(int64_t)c * ldg + r] = t; G[(int64_t)r * ldg + c] = t; }
+      for (int j = 0; j < 32; ++j) v[j] = ws[(i + j) * ps + off];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) s += v[j];
+    }
+    for (; i < nparts; ++i) s += ws[i * ps + off];
+    if (e < nbt) Bt[(int64_t)c * ldbt + r] = s;
+    else { G[(int64_t)c * ldg + r] = s; G[(int64_t)r * ldg + c] = s; }
   }
 }
 
@@ -487,7 +480,7 @@ cudaError_t update_pass_launch(const double* Qin, int64_t ldqin, int q, const do
   if (e != cudaSuccess) return e;
   const int qp = (int)round_up(q, 64);
   const int64_t nel = (int64_t)q * p + (int64_t)p * p;
-  update_reduce_kernel<<<(int)ceil_div(nel, 32), 256, 0, s>>>(ws, ctas, q, p, qp, Bt_next, q, G, ldg, gate);
+  update_reduce_kernel<<<(int)ceil_div(nel, 256), 256, 0, s>>>(ws, ctas, q, p, qp, Bt_next, q, G, ldg, gate);
   return cudaGetLastError();
 }
 
