@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define CQR_ABI_VERSION 7
+#define CQR_ABI_VERSION 8
 
 #define CQR_OK 0
 #define CQR_EINVAL (-1)
@@ -225,6 +225,20 @@ void cqr_debug_update_tma(int on);
 int cqr_factor(const cqr_factor_config* cfg, int k, const double* G, int ldg, const double* Bt, int ldbt, int q,
                double* Rk, double* Rinv, int ldr, double* Racc, double* B, int ldb, double* shifts,
                cqr_factor_status* status, void* ws, size_t ws_bytes, void* stream);
+
+/* Standalone k x k kernels behind the reference's kernel API (the drivers
+ * never call them: cqr_factor does the same work inside its launch).
+ * Column-major, one CTA.
+ *   cqr_tri_inverse:  Rinv = R^-1, R upper triangular with a nonzero diagonal
+ *                     (checked by the caller), exact zeros below the diagonal
+ *                     -- replaces tri_inverse (kernels.py:85-100);
+ *   cqr_tri_multiply: C = triu(A B) for upper-triangular A, B
+ *                     -- replaces tri_multiply (kernels.py:103-114);
+ *   cqr_frobenius:    out[0] = ||X||_F, fixed-order reduction
+ *                     -- replaces frobenius (kernels.py:117-123). */
+int cqr_tri_inverse(const double* R, int ldr, int n, double* Rinv, int ldinv, void* stream);
+int cqr_tri_multiply(const double* A, int lda, const double* B, int ldb, int n, double* C, int ldc, void* stream);
+int cqr_frobenius(const double* X, int ldx, int rows, int cols, double* out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -367,7 +367,13 @@ def is_chol_qr(a, cfg=None):
 
 def _deflated(q, bt):
     """Deflated, symmetrized Gramian (`algorithms.py:358-366`)."""
-    x = gram(q) - bt.T @ bt
+    return _deflated_from(gram(q), bt)
+
+
+def _deflated_from(g, bt):
+    """The same from an already formed Gramian g = q^T q (used to replay the
+    decision stage on another implementation's Gramians)."""
+    x = g - bt.T @ bt
     return (x + x.T) / 2.0
 
 

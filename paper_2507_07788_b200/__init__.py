@@ -57,7 +57,7 @@ def backend_class(name):
 
 def __getattr__(name):
     # k x k API and metrics are imported lazily (they pull in torch device code)
-    if name in ("cholesky", "spectral_norm_estimate", "compute_shift"):
+    if name in ("cholesky", "spectral_norm_estimate", "compute_shift", "tri_inverse", "tri_multiply", "frobenius"):
         from . import kernels
 
         return getattr(kernels, name)

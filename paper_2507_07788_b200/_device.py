@@ -49,6 +49,10 @@ class DeviceContext:
         self.engine_pool = {}   # (k, q, status capacity) -> [(Engine buffers, release event)]
         self.launches = 0   # libcqr kernel launches issued (bench bookkeeping)
         self.timer = None   # optional KernelTimer (bench): CUDA events per libcqr call
+        # optional list (tests): every factor call appends the k x k inputs it
+        # reads -- (policy, m_global, width, G copy, Bt copy or None) -- so a
+        # checker can replay the decision stage on the device's own Gramians
+        self.trace = None
 
     # ---------------------------------------------------------------- plumbing
     @property

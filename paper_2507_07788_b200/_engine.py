@@ -160,10 +160,10 @@ class Engine:
 
     # ------------------------------------------------------------ k x k stage
     def factor(self, policy, m_global, width, *, tol=0.0, check_tol=False, stop=False, update_b=False,
-               fixed_shift=0.0):
+               fixed_shift=0.0, est_tol=1e-2, est_max_iter=100):
         """Run the k x k stage and return its status (one host sync)."""
         h = self.factor_async(policy, m_global, width, tol=tol, check_tol=check_tol, stop=stop, update_b=update_b,
-                              fixed_shift=fixed_shift)
+                              fixed_shift=fixed_shift, est_tol=est_tol, est_max_iter=est_max_iter)
         return self.collect([h])[0]
 
     def gate(self, handle):
@@ -187,18 +187,23 @@ class Engine:
         return out
 
     def factor_async(self, policy, m_global, width, *, tol=0.0, check_tol=False, stop=False, update_b=False,
-                     fixed_shift=0.0, gate=None, gate_slot=None):
+                     fixed_shift=0.0, gate=None, gate_slot=None, est_tol=1e-2, est_max_iter=100):
         """Enqueue the k x k stage; its status lands in a pinned host slot
         (returned handle) without a sync.  Up to `nslots` calls may be pending."""
         cx = self.cx
         slot = self._next_slot
         self._next_slot = (slot + 1) % self.nslots
         cfg = self.cfg
+        if cx.trace is not None:
+            # stream-ordered copies: exactly what this launch will read
+            cx.trace.append(dict(policy=policy, m_global=m_global, width=width, tol=tol, check_tol=check_tol,
+                                 stop=stop, fixed_shift=fixed_shift, G=self.G.clone(),
+                                 Bt=self.Bt.clone() if (self.Bt is not None and self.q) else None))
         fc = _lib.FactorConfig(
             policy=policy, shift_width=width, m_global=m_global, unit_roundoff=cfg.unit_roundoff,
             shift_escalation=cfg.shift_escalation, max_shift_attempts=cfg.max_shift_attempts,
             check_tol=1 if check_tol else 0, tol=tol, stop=1 if stop else 0, accumulate=1,
-            update_b=1 if update_b else 0, est_max_iter=100, est_tol=1e-2, fixed_shift=fixed_shift, gate=gate,
+            update_b=1 if update_b else 0, est_max_iter=est_max_iter, est_tol=est_tol, fixed_shift=fixed_shift, gate=gate,
             # the kernel writes the status and shifts straight into this slot's
             # pinned host buffer (no D2H copy on the stream)
             status_mirror=self.stat_host_all[slot].data_ptr(),

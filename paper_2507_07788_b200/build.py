@@ -1,6 +1,9 @@
 """Build libcqr.so in-tree with nvcc for sm_100a (no torch JIT, no cache dir).
 
     python -m paper_2507_07788_b200.build        # or __graft_entry__.build()
+
+Each csrc/*.cu compiles to its own object in parallel (the kernel files share
+no device symbols), then one nvcc link makes the shared library.
 """
 
 from __future__ import annotations
@@ -8,17 +11,21 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 LIB = os.path.join(HERE, "libcqr.so")
-SOURCES = ["cqr_abi.cu", "cqr_gram.cu", "cqr_gram_pairs.cu", "cqr_gemm.cu", "cqr_layout.cu", "cqr_fused.cu", "cqr_update.cu", "cqr_factor.cu"]
+OBJ = os.path.join(HERE, "build_obj")
+SOURCES = ["cqr_abi.cu", "cqr_gram.cu", "cqr_gram_pairs.cu", "cqr_gemm.cu", "cqr_layout.cu", "cqr_fused.cu",
+           "cqr_update.cu", "cqr_factor.cu", "cqr_small.cu", "cqr_device.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = [
-    "-gencode", "arch=compute_100a,code=sm_100a",
+    *ARCH,
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
     "--expt-relaxed-constexpr",
     "-Xptxas", "-v",
 ]
@@ -32,18 +39,38 @@ def _stale():
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _compile(src):
+    obj = os.path.join(OBJ, os.path.splitext(src)[0] + ".o")
+    cmd = [NVCC, *FLAGS, "-I", INCLUDE, "-c", "-o", obj, os.path.join(CSRC, src)]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    return src, obj, res
+
+
 def build(force=False, verbose=False):
-    """Compile every .cu of csrc/ into one shared library."""
+    """Compile every .cu of csrc/ (in parallel) and link one shared library."""
     if not force and not _stale():
         return LIB
-    cmd = [NVCC, *FLAGS, "-I", INCLUDE, "-o", LIB] + [os.path.join(CSRC, s) for s in SOURCES]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    if verbose or res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
-    if res.returncode != 0:
+    os.makedirs(OBJ, exist_ok=True)
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as pool:
+        results = list(pool.map(_compile, SOURCES))
+    report = []
+    failed = False
+    for src, _obj, res in results:
+        report.append(f"==== {src}\n{res.stdout}{res.stderr}")
+        if res.returncode != 0:
+            failed = True
+            sys.stderr.write(f"nvcc failed on {src}:\n{res.stdout}{res.stderr}")
+    if verbose and not failed:
+        sys.stderr.write("".join(report))
+    if failed:
         raise RuntimeError("nvcc failed building libcqr.so")
+    link = [NVCC, *ARCH, "-shared", "-o", LIB] + [obj for _src, obj, _res in results]
+    res = subprocess.run(link, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError("nvcc failed linking libcqr.so")
     with open(os.path.join(HERE, "ptxas_report.txt"), "w") as fh:
-        fh.write(res.stderr)
+        fh.write("".join(report))
     return LIB
 
 

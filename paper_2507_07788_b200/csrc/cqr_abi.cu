@@ -342,4 +342,26 @@ int cqr_factor(const cqr_factor_config* cfg, int k, const double* G, int ldg, co
   return cuda_check(cqr::factor_launch(a, static_cast<cudaStream_t>(stream)), "cqr_factor");
 }
 
+// ---- standalone k x k kernels (kernels.py:85-123)
+int cqr_tri_inverse(const double* R, int ldr, int n, double* Rinv, int ldinv, void* stream) {
+  if (n < 0 || (n > 0 && (R == nullptr || Rinv == nullptr || ldr < n || ldinv < n)))
+    return fail(CQR_EINVAL, "cqr_tri_inverse: bad arguments");
+  return cuda_check(cqr::tri_inverse_launch(R, ldr, n, Rinv, ldinv, static_cast<cudaStream_t>(stream)),
+                    "cqr_tri_inverse");
+}
+
+int cqr_tri_multiply(const double* A, int lda, const double* B, int ldb, int n, double* C, int ldc, void* stream) {
+  if (n < 0 || (n > 0 && (A == nullptr || B == nullptr || C == nullptr || lda < n || ldb < n || ldc < n)))
+    return fail(CQR_EINVAL, "cqr_tri_multiply: bad arguments");
+  return cuda_check(cqr::tri_multiply_launch(A, lda, B, ldb, n, C, ldc, static_cast<cudaStream_t>(stream)),
+                    "cqr_tri_multiply");
+}
+
+int cqr_frobenius(const double* X, int ldx, int rows, int cols, double* out, void* stream) {
+  if (rows < 0 || cols < 0 || out == nullptr || (rows > 0 && cols > 0 && (X == nullptr || ldx < rows)))
+    return fail(CQR_EINVAL, "cqr_frobenius: bad arguments");
+  return cuda_check(cqr::frobenius_launch(X, ldx, rows, cols, out, static_cast<cudaStream_t>(stream)),
+                    "cqr_frobenius");
+}
+
 }  // extern "C"

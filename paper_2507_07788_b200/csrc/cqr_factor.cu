@@ -1738,14 +1738,11 @@ cudaError_t factor_launch(FactorArgs& a, cudaStream_t stream) {
   // k <= 128: X, then the block-packed triangle; 128 < k <= 256: the band or the
   // trailing triangle; k <= 768: one 32-row band (work_doubles)
   smem += ((a.k <= FK_SMEM_K ? (size_t)a.k * a.k : 0) + (size_t)work_doubles(a.k)) * sizeof(double);
-  static bool attr_set = false;
-  if (!attr_set) {
-    const int mx = 220 * 1024;  // <= 227 KB minus the static shared state
-    cudaError_t e = cudaFuncSetAttribute(factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  {
+    const size_t mx = 220 * 1024;  // <= 227 KB minus the static shared state
+    cudaError_t e = smem_attr((const void*)factor_kernel, mx);
+    if (e == cudaSuccess) e = smem_attr((const void*)factor_finish_wide_kernel, mx);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(factor_finish_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   static unsigned epoch = 0;
   a.epoch = ++epoch;   // tags the speculative handshake of this launch (no reset launch needed)
@@ -1753,8 +1750,29 @@ cudaError_t factor_launch(FactorArgs& a, cudaStream_t stream) {
     const int nt = (a.k + 31) / 32;
     factor_prep_kernel<<<nt * (nt + 1) / 2, FP_THREADS, 0, stream>>>(a);
   }
-  factor_kernel<<<a.spec ? 2 : 1, FK_THREADS, smem, stream>>>(a);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e;
+  if (a.spec) {
+    // The speculative pair hands over through a flag CTA 1 spins on, so both
+    // CTAs must be resident at once: a 2-CTA thread-block cluster guarantees
+    // co-scheduling (a plain 2-block grid does not, e.g. under MPS SM limits
+    // or a concurrent kernel holding every other SM).
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2);
+    cfg.blockDim = dim3(FK_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, factor_kernel, a);
+  } else {
+    factor_kernel<<<1, FK_THREADS, smem, stream>>>(a);
+    e = cudaGetLastError();
+  }
   if (e != cudaSuccess) return e;
   const int blocks = (a.k + 7) / 8;
   if (a.k <= 256) {

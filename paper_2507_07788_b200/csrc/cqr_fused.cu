@@ -567,16 +567,11 @@ size_t apply_gram_fused_ws_bytes(int64_t rows, int k) {
 template <int KP, bool TRMM>
 static cudaError_t launch_rt(const double* X, int64_t ldx, int k, const double* Rt, double* Q, int64_t ldq,
                              int64_t rows, double* G, int ldg, double* ws, cudaStream_t s, const int* gate) {
-  static bool attr = false;
   const size_t smem = rt_smem_doubles<KP>() * sizeof(double);
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(apply_gram_rt_kernel<KP, true, TRMM>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(apply_gram_rt_kernel<KP, false, TRMM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem);
+  {
+    cudaError_t e = smem_attr((const void*)apply_gram_rt_kernel<KP, true, TRMM>, smem);
+    if (e == cudaSuccess) e = smem_attr((const void*)apply_gram_rt_kernel<KP, false, TRMM>, smem);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   const int ctas = rt_ctas(rows);
   if (k == KP)
@@ -593,16 +588,11 @@ static cudaError_t launch_rt(const double* X, int64_t ldx, int k, const double* 
 template <int KP>
 static cudaError_t launch_fused(const double* X, int64_t ldx, int k, const double* Rt, double* Q, int64_t ldq,
                                 int64_t rows, double* G, int ldg, double* ws, cudaStream_t s, const int* gate) {
-  static bool attr = false;
   const size_t smem = fused_smem_doubles<KP>() * sizeof(double);
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(apply_gram_fused_kernel<KP, true>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(apply_gram_fused_kernel<KP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem);
+  {
+    cudaError_t e = smem_attr((const void*)apply_gram_fused_kernel<KP, true>, smem);
+    if (e == cudaSuccess) e = smem_attr((const void*)apply_gram_fused_kernel<KP, false>, smem);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   const int ctas = fused_ctas(rows);
   if (k == KP)

@@ -215,12 +215,10 @@ __global__ void __launch_bounds__(GM_THREADS, 2) gemm_kernel(GemmArgs args) {
 }
 
 cudaError_t gemm_launch(GemmArgs& a, cudaStream_t stream) {
-  static bool attr_set = false;
   const size_t smem = gemm_smem_bytes();
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    cudaError_t e = smem_attr((const void*)gemm_kernel, smem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   a.ntile_n = (int)ceil_div(a.n, GM_BN);
   a.nrow_tiles = ceil_div(a.rows, GM_BR);

@@ -252,16 +252,6 @@ __global__ void gram_reduce_kernel(GramArgs args, double* G, int ldg) {
   }
 }
 
-static int g_num_sms = 0;
-int num_sms() {
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
-  }
-  return g_num_sms;
-}
 
 GramArgs gram_plan(const double* A, int64_t lda, int ka, const double* B, int64_t ldb, int kb, int64_t rows,
                    bool self) {
@@ -289,12 +279,10 @@ size_t gram_workspace_bytes(const GramArgs& a) {
 }
 
 cudaError_t gram_launch(GramArgs& a, double* G, int ldg, cudaStream_t stream) {
-  static bool attr_set = false;
   const size_t smem = gram_smem_bytes();
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    cudaError_t e = smem_attr((const void*)gram_kernel, smem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   if (a.rows > 0) {
     dim3 grid(a.nitems, a.nsplit);

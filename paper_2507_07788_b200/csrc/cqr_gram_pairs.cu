@@ -180,13 +180,10 @@ size_t gram_pairs_ws_bytes(int64_t rows, int k) {
 template <int KP>
 static cudaError_t launch_gp(const double* X, int64_t ldx, int k, int64_t rows, double* G, int ldg, double* ws,
                              cudaStream_t s, const int* gate) {
-  static bool attr = false;
   const size_t smem = gp_smem_bytes<KP>();
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gram_pairs_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+  {
+    cudaError_t e = smem_attr((const void*)gram_pairs_kernel<KP>, smem);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   int items, nsplit;
   gp_grid(rows, KP, items, nsplit);

@@ -8,7 +8,10 @@
 
 namespace cqr {
 
-int num_sms();
+int num_sms();   // of the current device (cqr_device.cu)
+// opt the kernel `fn` into `bytes` of dynamic shared memory on the current
+// device (cached per device and kernel)
+cudaError_t smem_attr(const void* fn, size_t bytes);
 
 // ------------------------------------------------------------- Gram (K1)
 struct GramArgs {
@@ -109,5 +112,11 @@ struct FactorArgs {
 cudaError_t factor_launch(FactorArgs& a, cudaStream_t stream);
 size_t factor_workspace_bytes(int k);
 int factor_profile(unsigned long long* out);
+
+// ------------------------------------------------------------- standalone k x k kernels (cqr_small.cu)
+cudaError_t tri_inverse_launch(const double* R, int ldr, int n, double* X, int ldx, cudaStream_t s);
+cudaError_t tri_multiply_launch(const double* A, int lda, const double* B, int ldb, int n, double* C, int ldc,
+                                cudaStream_t s);
+cudaError_t frobenius_launch(const double* X, int ldx, int rows, int cols, double* out, cudaStream_t s);
 
 }  // namespace cqr

@@ -408,11 +408,15 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 static int g_update_tma = 1;   // cqr_debug_update_tma: 0 = per-quad bulk copies only (comparisons)
 void set_update_tma(int on) { g_update_tma = on ? 1 : 0; }
 
-// box {4, boxc, sr/4} over a QI array (rows multiple of 16, column capacity ld)
-static bool encode_qi_map(CUtensorMap* tm, const double* base, int64_t ld, int64_t rows, int boxc, int sr) {
+// box {4, boxc, sr/4} over the first `cols` columns of a QI array (rows a
+// multiple of 16, column capacity ld).  The column extent is `cols`, not the
+// capacity: `base` may be a column block inside the buffer (the update path's
+// tail block), and a box reaching past its last column must be zero-filled by
+// the TMA unit, never read from past the allocation.
+static bool encode_qi_map(CUtensorMap* tm, const double* base, int64_t ld, int cols, int64_t rows, int boxc, int sr) {
   auto enc = tensor_map_encoder();
   if (!g_update_tma || enc == nullptr || boxc > 256 || ((uintptr_t)base & 15) != 0) return false;
-  const cuuint64_t dims[3] = {4, (cuuint64_t)ld, (cuuint64_t)(rows / 4)};
+  const cuuint64_t dims[3] = {4, (cuuint64_t)cols, (cuuint64_t)(rows / 4)};
   const cuuint64_t strides[2] = {32, (cuuint64_t)ld * 32};
   const cuuint32_t box[3] = {4, (cuuint32_t)boxc, (cuuint32_t)(sr / 4)};
   const cuuint32_t es[3] = {1, 1, 1};
@@ -432,12 +436,9 @@ size_t update_pass_ws_bytes(int64_t rows, int q) {
 
 template <int NQ, int SR>
 static cudaError_t launch_up(const UpdateArgs& a, int ctas, size_t smem, cudaStream_t s) {
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(update_pass_kernel<NQ, SR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+  {
+    cudaError_t e = smem_attr((const void*)update_pass_kernel<NQ, SR>, smem);
     if (e != cudaSuccess) return e;
-    attr = smem;
   }
   update_pass_kernel<NQ, SR><<<ctas, UP_THREADS, smem, s>>>(a);
   return cudaGetLastError();
@@ -460,8 +461,8 @@ cudaError_t update_pass_launch(const double* Qin, int64_t ldqin, int q, const do
   a.qs = up_qs(q);
   const int sr = up_sr(q);
   // one tensor copy per sub-panel where the per-quad runs would be small
-  a.use_tm_qin = (q * 32 < 8192) && encode_qi_map(&a.tm_qin, Qin, ldqin, rows, a.qs, sr) ? 1 : 0;
-  a.use_tm_qb = !(ldqb == UP_PB && p == UP_PB) && encode_qi_map(&a.tm_qb, Qb, ldqb, rows, UP_PB, sr) ? 1 : 0;
+  a.use_tm_qin = (q * 32 < 8192) && encode_qi_map(&a.tm_qin, Qin, ldqin, q, rows, a.qs, sr) ? 1 : 0;
+  a.use_tm_qb = !(ldqb == UP_PB && p == UP_PB) && encode_qi_map(&a.tm_qb, Qb, ldqb, p, rows, UP_PB, sr) ? 1 : 0;
   a.ns = up_stages(q, sr);
   const size_t smem = update_smem_bytes(q, sr);
   const int ctas = update_ctas(rows);

@@ -18,7 +18,7 @@ import warnings
 import numpy as np
 import pytest
 
-from conftest import Golden, algo_cfg
+from conftest import Golden, algo_cfg, oracle_cfg
 import parity as P
 
 pytestmark = pytest.mark.gpu
@@ -69,40 +69,57 @@ def _oracle_single(case, blk):
             return None, exc
 
 
+ITERATED = ("rs_chol_qr", "is_chol_qr")
+
+# Update cases whose deflated Gramian is exactly singular in exact arithmetic,
+# so its computed value (and the plain attempt's branch) is rounding noise:
+# an incoming column that duplicates a basis column (reference
+# tests/test_update_panel.py:66-78).
+UPDATE_ROUNDING = {"upd_duplicate"}
+
+
 @pytest.mark.parametrize("case", SINGLE, ids=[c["name"] for c in SINGLE])
 def test_single_input_golden(case):
-    """Device run vs the oracle on the same box (decision rule of
-    tests/parity.py) and vs the reference's golden quality numbers."""
+    """Device run vs the oracle on the same box and vs the reference's golden
+    record, decision by decision (tests/parity.py): every pass's branch, its
+    shift attempts (exact) and shifts (1e-6), and the stop decision; then R
+    (1e-10, well-conditioned) and LOO_F / RRR_F within 10x."""
     cq = _cq()
     blk = G.input(case)
     k = blk.shape[1]
     a = cq.CudaVectorArray.from_numpy(blk)
     ref, ref_exc = _oracle_single(case, blk)
-    try:
-        res, exc = _run(case, a), None
-    except cq.CholeskyBreakdown as e:
-        res, exc = None, e
-    if ref_exc is not None or exc is not None:
-        # both must break down unless the deciding pivot was rounding noise
-        if ref_exc is None or exc is None:
-            m = exc.margin if exc is not None else getattr(ref_exc, "margin", 0.0)
-            assert not P.robust_margin(m, k), (m, ref_exc, exc)
+    res, trace = P.traced(_run, case, a)
+    exc = res if isinstance(res, cq.CholeskyBreakdown) else None
+    if isinstance(res, Exception) and exc is None:
+        raise res
+    if exc is not None:
+        res = None
+    if ref_exc is not None or exc is not None or "exception" in case:
+        # both break down (the pivot index itself is rounding-determined at
+        # these condition numbers), or the deciding pivot is rounding-level
+        P.compare_single(res, exc, ref, ref_exc, k)
+        if exc is None and trace:
+            # the device succeeded where the reference broke down: the oracle's own
+            # Cholesky on the device's Gramian agrees with the device
+            _replay_single(trace, res, k)
         return
-    assert res.success == ref.success
     np.testing.assert_array_equal(np.tril(res.r, -1), 0.0)
     diverged_tol = None
-    if case["algo"] in ("rs_chol_qr", "is_chol_qr"):
+    if case["algo"] in ITERATED:
         tol = algo_cfg(case).effective_tol(k)
-        n = P.compare_iterated(res, ref, k, tol)
-        if n < max(len(ref.shift_attempts), len(res.shift_attempts)) or res.iterations != ref.iterations:
-            diverged_tol = tol
-        if n == len(ref.shift_attempts) == len(res.shift_attempts) and res.iterations == case["iterations"]:
-            assert res.shift_attempts == case["attempts"]
-            np.testing.assert_allclose(res.shifts_applied, case["shifts"], rtol=1e-6)
+        cmp = P.compare_iterated(res, ref, k, tol)
+        gcmp = P.compare_iterated(res, P.Record(case), k, tol)
+        if not (cmp.full and gcmp.full):
+            diverged_tol = tol     # a rounding-level divergence (compare_iterated checked it)
+        if case["algo"] == "rs_chol_qr":
+            rep = P.replay_iterated(trace, res, oracle_cfg(case), "rs")
+            assert rep.passes == res.iterations, rep
     else:
         assert res.iterations == case["iterations"]
         assert len(res.shifts_applied) == len(case["shifts"])
         np.testing.assert_allclose(res.shifts_applied, case["shifts"], rtol=1e-6)
+        np.testing.assert_allclose(res.shifts_applied, ref.shifts_applied, rtol=1e-6)
     x = _cond(case)
     if x is not None and x <= 4:
         r_ref = G.r(case)
@@ -112,6 +129,59 @@ def test_single_input_golden(case):
         rrr = cq.reconstruction_residual(a, res.q, res.r, norm="frobenius")
         assert P.within10(loo, case["loo"], k, diverged_tol), (loo, case["loo"])
         assert P.within10(rrr, case["rrr"], k, diverged_tol), (rrr, case["rrr"])
+
+
+def _replay_single(trace, res, k):
+    """Fixed schedules: the oracle's plain Cholesky on each pass's device
+    Gramian takes the device's branch (or its pivot there is rounding-level)."""
+    from oracle import cholqr_oracle as co
+
+    for e in trace:
+        if e["policy"] != 0:   # POLICY_PLAIN passes only
+            continue
+        g, _ = P._device_x(e)
+        rk, dm, _ = co._attempt(g)
+        assert rk is not None or P.fragile_margin(dm, k), dm
+
+
+# Shifted iterations of the 47 golden rs/is cases the device trajectory must
+# reproduce exactly (same attempts, shifts to 1e-6).  The rest sit behind a
+# rounding-level decision where the device and the reference's BLAS parted
+# (listed by the test); the replay compares those passes on the device's own
+# Gramians instead.
+GOLDEN_TRAJECTORY_SHIFTED_FLOOR = 38   # measured: 38 of 42 (the 4 others behind rounding-level decisions)
+
+
+def test_golden_shifted_iterations_compared():
+    """Across the golden iterated cases: the reference took 42 shifted
+    iterations.  The device trajectory is compared with the reference's record
+    decision by decision (tests/parity.py); where a rounding-level decision
+    parted them, the replay compares every remaining device pass against the
+    oracle's decision stage on the device's own Gramian."""
+    cq = _cq()
+    shifted = total = replayed = rep_shifted = 0
+    parted = []
+    for case in SINGLE:
+        if case["algo"] not in ITERATED or "exception" in case:
+            continue
+        blk = G.input(case)
+        k = blk.shape[1]
+        res, trace = P.traced(_run, case, cq.CudaVectorArray.from_numpy(blk))
+        assert not isinstance(res, Exception), (case["name"], res)
+        cmp = P.compare_iterated(res, P.Record(case), k, algo_cfg(case).effective_tol(k))
+        shifted += cmp.shifted
+        total += sum(1 for x in case["attempts"] if x > 0)
+        if not cmp.full:
+            parted.append((case["name"], cmp.reason))
+        if case["algo"] == "rs_chol_qr":
+            rep = P.replay_iterated(trace, res, oracle_cfg(case), "rs")
+            assert rep.passes == res.iterations, (case["name"], rep)
+            replayed += rep.passes
+            rep_shifted += rep.shifted
+    print(f"golden trajectories: {shifted} of {total} shifted iterations compared; parted at rounding-level "
+          f"decisions: {parted}; replay: {replayed} passes ({rep_shifted} shifted) on the device Gramians")
+    assert total == 42
+    assert shifted >= GOLDEN_TRAJECTORY_SHIFTED_FLOOR
 
 
 @pytest.mark.parametrize("case", UPDATE, ids=[c["name"] for c in UPDATE])
@@ -132,22 +202,34 @@ def test_update_golden(case):
             else:
                 assert info.value.last_shift == pytest.approx(case["last_shift"], rel=1e-6)
             return
-        res = cq.chol_qr_update(q_in, r_in, a_new, algo_cfg(case))
+        res, trace = P.traced(cq.chol_qr_update, q_in, r_in, a_new, algo_cfg(case))
         from oracle import cholqr_oracle as co
 
         ref = co.chol_qr_update(qin, r_in, G.arrays[case["name"] + "__in"],
                                 co.default_cfg(**case.get("cfg", {})))
+    assert not isinstance(res, Exception), res
     assert res.success == ref.success == case["success"]
     p = a_new.ncols
     tol = algo_cfg(case).effective_tol(p)
-    n = P.compare_iterated(res, ref, p, tol)
-    diverged_tol = tol if (n < max(len(ref.shift_attempts), len(res.shift_attempts))
-                           or res.iterations != ref.iterations) else None
+    cmp = P.compare_iterated(res, ref, p, tol)
+    gcmp = P.compare_iterated(res, P.Record(case), p, tol)
+    rep = P.replay_iterated(trace, res, oracle_cfg(case), "update")
+    assert rep.passes == res.iterations, rep
+    if case["name"] in UPDATE_ROUNDING:
+        # the deflated Gramian is rounding noise: the trajectory may part from
+        # the reference's at that rounding-level branch (compare_iterated checked
+        # the margin); the replay above reproduced the device's own branch
+        pass
+    else:
+        assert cmp.full and gcmp.full, (cmp, gcmp)
+        assert res.shift_attempts == case["attempts"]
+        np.testing.assert_allclose(res.shifts_applied, case["shifts"], rtol=1e-6)
     k = qin.shape[1]
     np.testing.assert_array_equal(res.r[k:, :k], 0.0)
     np.testing.assert_array_equal(res.r[:k, :k], r_in)
     if case["success"]:
         loo = cq.loss_of_orthogonality(res.q, norm="frobenius")
+        diverged_tol = None if (cmp.full and gcmp.full) else tol
         assert P.within10(loo, case["loo"], res.q.ncols, diverged_tol), (loo, case["loo"])
 
 
@@ -538,15 +620,14 @@ def test_wide_rs_chol_qr_shifts_match_oracle():
         warnings.simplefilter("ignore")
         ref = co.rs_chol_qr(x, co.default_cfg())
     tol = cq.AlgoConfig().effective_tol(k)
-    n = P.compare_iterated(res, ref, k, tol)
-    diverged = tol if (n < max(len(ref.shift_attempts), len(res.shift_attempts))
-                       or res.iterations != ref.iterations) else None
+    cmp = P.compare_iterated(res, ref, k, tol)
+    assert cmp.full, cmp
+    assert cmp.shifted == sum(1 for a in ref.shift_attempts if a) >= 1   # shifted passes through the banded path
     assert res.success == ref.success
     loo = cq.loss_of_orthogonality(res.q, norm="frobenius")
     rrr = cq.reconstruction_residual(cq.CudaVectorArray.from_numpy(x), res.q, res.r, norm="frobenius")
-    assert P.within10(loo, co.loo_fro(ref.q), k, diverged)
-    assert P.within10(rrr, co.rrr_fro(x, ref.q, ref.r), k, diverged)
-    assert sum(res.shift_attempts) >= 1   # the shifted attempts ran through the banded path
+    assert P.within10(loo, co.loo_fro(ref.q), k)
+    assert P.within10(rrr, co.rrr_fro(x, ref.q, ref.r), k)
 
 
 def test_update_into_basis_capacity_is_bitwise_the_copy_path():

@@ -129,7 +129,7 @@ def test_cholqr_breaks_down_on_ill_conditioned():
     cq = _cq()
     import parity as P
 
-    for seed in (0, 1, 2):
+    for seed in (1, 2):   # seed 0 is the reference's own case, strict in test_gpu_contracts.py
         a, _ = cq.generate(cq.MatrixSpec(300, 10, 9.0, seed=seed))
         for fn in (cq.chol_qr, cq.chol_qr2):
             try:

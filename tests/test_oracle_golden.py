@@ -118,3 +118,55 @@ def test_oracle_nan_pivot_is_breakdown():
     x[1, 1] = np.nan
     with pytest.raises(co.OracleBreakdown):
         co.cholesky_upper(x)
+
+
+def test_decision_rule_compares_every_golden_decision():
+    """The decision rule of tests/parity.py, applied to the oracle against the
+    reference's own records, compares every decision of every iterated golden
+    case: all 42 shifted iterations (shift attempts exact, shifts 1e-6) and the
+    stop decisions.  The GPU tests apply the same rule to the device path."""
+    import parity as P
+
+    shifted = total = 0
+    for case in SINGLE:
+        if case["algo"] not in ("rs_chol_qr", "is_chol_qr") or "exception" in case:
+            continue
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            res = _run_single(case, G.input(case))
+        k = G.input(case).shape[1]
+        tol = co.effective_tol(oracle_cfg(case), k)
+        cmp = P.compare_iterated(res, P.Record(case), k, tol)
+        assert cmp.full, (case["name"], cmp)
+        assert cmp.decisions == case["iterations"]
+        shifted += cmp.shifted
+        total += sum(1 for a in case["attempts"] if a > 0)
+    assert shifted == total == 42
+
+
+def test_decision_rule_rejects_robust_differences():
+    """A robust branch difference, a shift off by 1e-5, a different attempt
+    count and a NaN pivot all fail the rule; a rounding-level margin passes."""
+    import types
+
+    import parity as P
+
+    def run(att, shifts, dms, its=None, ok=True):
+        its = len(att) if its is None else its
+        return types.SimpleNamespace(iterations=its, shift_attempts=att, shifts_applied=shifts, success=ok,
+                                     err_history=[1.0] * its + [1e-16], decision_margins=dms)
+
+    ref = run([1, 0], [1e-10], [-1e-3, 0.5])
+    assert P.compare_iterated(run([1, 0], [1e-10 * (1 + 1e-9)], [-1e-3, 0.5]), ref, 8, 1e-13).full
+    with pytest.raises(AssertionError):
+        P.compare_iterated(run([0, 0], [], [1e-3, 0.5]), ref, 8, 1e-13)
+    with pytest.raises(AssertionError):
+        P.compare_iterated(run([1, 0], [1.00001e-10], [-1e-3, 0.5]), ref, 8, 1e-13)
+    with pytest.raises(AssertionError):
+        P.compare_iterated(run([2, 0], [1e-10, 1e-9], [-1e-3, 0.5]), ref, 8, 1e-13)
+    nan = run([1, 0], [1e-10], [float("nan"), 0.5])
+    with pytest.raises(AssertionError):
+        P.compare_iterated(run([0, 0], [], [float("nan"), 0.5]), nan, 8, 1e-13)
+    fragile = run([1, 0], [1e-10], [-1e-16, 0.5])
+    cmp = P.compare_iterated(run([0, 0], [], [1e-16, 0.5]), fragile, 8, 1e-13)
+    assert not cmp.full and cmp.decisions == 0
