@@ -96,8 +96,10 @@ CFG = {
             cond=12.0, cpu_rows=200_000),
     2: dict(workload="chol_qr2 4000000x128 N(0,1) (BASELINE config 2)", m=4_000_000, k=128, algo="chol_qr2",
             cond=None, cpu_rows=1_000_000),
+    # cpu_rows: the bounded CPU sample; 1M rows of config 3 take the same 5
+    # passes [1, 1, 1, 0, 0] as the 2M-row workload (200k rows take 4)
     3: dict(workload="rs_chol_qr 2000000x256 kappa=1e15 (BASELINE config 3)", m=2_000_000, k=256,
-            algo="rs_chol_qr", cond=15.0, cpu_rows=200_000),
+            algo="rs_chol_qr", cond=15.0, cpu_rows=1_000_000),
     4: dict(workload="chol_qr_update chain 8000000 x (16 + 31 x 16), A_j = Q_prev C_j + 1e-8 G_j "
                      "(BASELINE config 4)", m=8_000_000, k=512, p=16, blocks=31, algo="chol_qr_update",
             cond=None, cpu_rows=200_000),

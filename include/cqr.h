@@ -240,6 +240,28 @@ int cqr_tri_inverse(const double* R, int ldr, int n, double* Rinv, int ldinv, vo
 int cqr_tri_multiply(const double* A, int lda, const double* B, int ldb, int n, double* C, int ldc, void* stream);
 int cqr_frobenius(const double* X, int ldx, int rows, int cols, double* out, void* stream);
 
+/* Deterministic cross-rank sum of a row-sharded partial (the Gram, or the
+ * packed [Bt | G] of an update pass): parts holds the nparts per-rank
+ * partials of n doubles back to back (as ncclAllGather leaves them), out[e] =
+ * parts[0][e] + parts[1][e] + ... in rank order.  Every rank computes the same
+ * bits whatever algorithm the collective used, and bit-symmetric partials sum
+ * to a bit-symmetric matrix (the reference's run-to-run
+ * determinism, tests/test_algorithms.py:107-113). */
+int cqr_sum_ranks(const double* parts, int nparts, int64_t n, double* out, void* stream);
+
+/* Streaming reconstruction residual (K5), k <= 64: one sweep over the rows of
+ * Q and A (both QI, m rows) that forms D = A - Q R in registers -- never as a
+ * tall array -- and returns DtD = D^T D (k x k, ldd; bit-symmetric) and
+ * asq[0] = ||A||_F^2, both summed over CTAs in a fixed order.  R (k x k upper
+ * triangular) in coefficient tiles (cqr_pack_coeffs).  Replaces
+ * reconstruction_residual's a.copy() / q.lincomb(r) / axpy / diff.gramian()
+ * (metrics.py:53-71), which needs two extra m x k arrays.  Local rows only:
+ * under row sharding the caller sums DtD and asq over ranks. */
+int cqr_resid_gram_supported(int k);
+size_t cqr_resid_gram_workspace_bytes(int64_t m, int k);
+int cqr_resid_gram(const double* Q, int64_t ldq, const double* A, int64_t lda, int64_t m, int k, const double* R_tiles,
+                   double* DtD, int ldd, double* asq, void* ws, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -86,11 +86,14 @@ class DeviceContext:
 
         return row_range(m, self.rank, self.world)
 
-    def allreduce_(self, t, symmetric=False):
-        """Sum a small device tensor over ranks (NCCL); no-op on one rank."""
-        from .dist import allreduce_gram_
+    def reduce_ranks_(self, t):
+        """Sum a small device tensor over ranks in a fixed order (all-gather +
+        in-order device sum, dist.reduce_ranks_); no-op on one rank."""
+        if self.world == 1:
+            return t
+        from .dist import reduce_ranks_
 
-        return allreduce_gram_(t, symmetric=symmetric)
+        return reduce_ranks_(t)
 
     def allgather_rows(self, local, m):
         """Concatenate per-rank row blocks (host numpy, m_local x k) to m x k."""

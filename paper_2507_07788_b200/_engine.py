@@ -27,14 +27,6 @@ def _gram_ws(m_local, ka, kb, self_):
     return cx.workspace(cx.lib.cqr_gram_workspace_bytes(m_local, ka, kb, 1 if self_ else 0))
 
 
-def _symmetrize_(g):
-    """Mirror the lower triangle (exact), keeping the Gram bit-symmetric after
-    a cross-rank reduction whose per-element order may differ."""
-    low = torch.tril(g)
-    g.copy_(low + torch.tril(g, -1).T)
-    return g
-
-
 def gram_device(arr, out=None):
     """G = X^T X (allreduced, bit-symmetric) as a k x k device tensor."""
     cx = ctx()
@@ -48,8 +40,7 @@ def gram_device(arr, out=None):
     if t0 is not None:
         cx.timer.stop("gram", t0, (arr.m_local, k))
     cx.launches += 2
-    if cx.world > 1:
-        cx.allreduce_(g, symmetric=True)
+    cx.reduce_ranks_(g)
     return g
 
 
@@ -69,7 +60,7 @@ def cross_gram_device(left, right, out=None):
         _lib.check(cx.lib.cqr_cross_gram(left.ptr(), left.ld, ka, right.ptr(), right.ld, kb, left.m_local,
                                          g.data_ptr(), ka, ws.data_ptr(), ws.numel(), cx.stream), "cross_gram")
         cx.launches += 2
-        cx.allreduce_(g)
+        cx.reduce_ranks_(g)
     else:
         g.zero_()
     return g
@@ -117,7 +108,7 @@ class Engine:
             bufs, ev = free.pop()
             torch.cuda.current_stream(cx.device).wait_event(ev)   # released on another stream
             (self.G, self.Rk, self.Rinv, self.Racc, self._racc0, self.stat_all, self.stat_host_all, self.fws,
-             self.B, self.Bt) = bufs
+             self.B, self.Bt, self._xch) = bufs
             self.Racc.copy_(self._racc0)
             if q:
                 self.B.zero_()
@@ -125,7 +116,10 @@ class Engine:
         else:
             dev = cx.device
             self.ldr = max(round_up(k, 32), 32)
-            self.G = torch.empty((k, k), dtype=torch.float64, device=dev)
+            # the exchange buffer of one pass: [Bt (q x p) | G (p x p)] for updates,
+            # G alone otherwise -- one cross-rank reduction per pass
+            self._xch = torch.empty(k * q + k * k, dtype=torch.float64, device=dev)
+            self.G = self._xch[k * q:].view(k, k)
             self.Rk = torch.zeros((k, self.ldr), dtype=torch.float64, device=dev)
             self.Rinv = torch.zeros(max(cx.lib.cqr_coeff_doubles(k, k), 1), dtype=torch.float64, device=dev)  # tiles
             self._racc0 = torch.eye(k, self.ldr, dtype=torch.float64, device=dev)   # [I | 0]
@@ -136,7 +130,8 @@ class Engine:
             self.fws = torch.empty(cx.lib.cqr_factor_workspace_bytes(k), dtype=torch.uint8, device=dev)
             if q:
                 self.B = torch.zeros((k, q), dtype=torch.float64, device=dev)     # (p, q): column-major q x p
-                self.Bt = torch.zeros((k, q), dtype=torch.float64, device=dev)
+                self.Bt = self._xch[: k * q].view(k, q)
+                self.Bt.zero_()
             else:
                 self.B = self.Bt = None
         self.ldr = self.Rk.shape[1]
@@ -152,7 +147,7 @@ class Engine:
             free = self.cx.engine_pool.setdefault(self._key, [])
             if len(free) < 2:
                 free.append(((self.G, self.Rk, self.Rinv, self.Racc, self._racc0, self.stat_all, self.stat_host_all,
-                              self.fws, self.B, self.Bt), ev))
+                              self.fws, self.B, self.Bt, self._xch), ev))
             else:
                 self.cx.release_pinned(self.stat_host_all)
         except Exception:   # interpreter shutdown
@@ -244,8 +239,7 @@ class Engine:
             if t0 is not None:
                 cx.timer.stop("apply_gram", t0, (src.m_local, self.k),
                               gate=self.stat_all[gate_slot] if gate_slot is not None else None)
-            if cx.world > 1:
-                cx.allreduce_(self.G)
+            cx.reduce_ranks_(self.G)
         else:
             assert gate is None, "gated TRMM without Gram is not needed by any schedule"
             _lib.check(cx.lib.cqr_lincomb(src.ptr(), src.ld, src.m_local, self.k, self.Rinv.data_ptr(),
@@ -272,9 +266,8 @@ class Engine:
             cx.timer.stop("update_pass", t0, (qb.m_local, q_in.ncols, self.k, 1 if initial else 0),
                           gate=self.stat_all[gate_slot] if gate_slot is not None else None)
         cx.launches += 2
-        if cx.world > 1:
-            cx.allreduce_(self.Bt)
-            cx.allreduce_(self.G, symmetric=True)
+        # one collective per pass: Bt and G are adjacent in one buffer
+        cx.reduce_ranks_(self._xch)
 
     def in_place_ok(self):
         """TRMM may overwrite its input (one 64-wide column tile per row tile)."""

@@ -364,4 +364,32 @@ int cqr_frobenius(const double* X, int ldx, int rows, int cols, double* out, voi
                     "cqr_frobenius");
 }
 
+int cqr_sum_ranks(const double* parts, int nparts, int64_t n, double* out, void* stream) {
+  if (nparts < 1 || n < 0 || (n > 0 && (parts == nullptr || out == nullptr)))
+    return fail(CQR_EINVAL, "cqr_sum_ranks: bad arguments");
+  return cuda_check(cqr::sum_ranks_launch(parts, nparts, n, out, static_cast<cudaStream_t>(stream)), "cqr_sum_ranks");
+}
+
+// ---- K5 streaming residual (metrics.py:53-71)
+int cqr_resid_gram_supported(int k) { return cqr::resid_gram_supported(k) ? 1 : 0; }
+
+size_t cqr_resid_gram_workspace_bytes(int64_t m, int k) { return cqr::resid_gram_ws_bytes(cqr::round_up(m, 16), k); }
+
+int cqr_resid_gram(const double* Q, int64_t ldq, const double* A, int64_t lda, int64_t m, int k, const double* R_tiles,
+                   double* DtD, int ldd, double* asq, void* ws, size_t ws_bytes, void* stream) {
+  int rc = check_tall(Q, ldq, m, k, "cqr_resid_gram");
+  if (rc) return rc;
+  rc = check_tall(A, lda, m, k, "cqr_resid_gram");
+  if (rc) return rc;
+  if (!cqr::resid_gram_supported(k)) return fail(CQR_EINVAL, "cqr_resid_gram: k must be in [1, 64]");
+  if (R_tiles == nullptr || DtD == nullptr || asq == nullptr || ldd < k)
+    return fail(CQR_EINVAL, "cqr_resid_gram: bad R / DtD / asq");
+  const int64_t rows = cqr::round_up(m, 16);
+  if (ws == nullptr || ws_bytes < cqr::resid_gram_ws_bytes(rows, k))
+    return fail(CQR_EINVAL, "cqr_resid_gram: workspace too small");
+  return cuda_check(cqr::resid_gram_launch(Q, ldq, A, lda, k, R_tiles, rows, DtD, ldd, asq, static_cast<double*>(ws),
+                                           static_cast<cudaStream_t>(stream)),
+                    "cqr_resid_gram");
+}
+
 }  // extern "C"

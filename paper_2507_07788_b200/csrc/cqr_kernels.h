@@ -118,5 +118,13 @@ cudaError_t tri_inverse_launch(const double* R, int ldr, int n, double* X, int l
 cudaError_t tri_multiply_launch(const double* A, int lda, const double* B, int ldb, int n, double* C, int ldc,
                                 cudaStream_t s);
 cudaError_t frobenius_launch(const double* X, int ldx, int rows, int cols, double* out, cudaStream_t s);
+cudaError_t sum_ranks_launch(const double* parts, int nparts, int64_t n, double* out, cudaStream_t s);
+
+// ------------------------------------------------------------- streaming quality measures (K5, cqr_metrics.cu)
+bool resid_gram_supported(int k);
+size_t resid_gram_ws_bytes(int64_t rows, int k);
+cudaError_t resid_gram_launch(const double* Q, int64_t ldq, const double* A, int64_t lda, int k,
+                              const double* R_tiles, int64_t rows, double* DtD, int ldd, double* asq, double* ws,
+                              cudaStream_t s);
 
 }  // namespace cqr

@@ -66,6 +66,26 @@ __global__ void __launch_bounds__(SM_THREADS) frobenius_kernel(const double* __r
   if (threadIdx.x == 0) out[0] = sqrt(part[0]);
 }
 
+// out[e] = ((parts[0][e] + parts[1][e]) + parts[2][e]) + ... : the per-rank
+// partial sums of a row-sharded Gram added in rank order, so every rank gets
+// bitwise the same matrix whatever the collective's internal algorithm, and
+// bit-symmetric partials give a bit-symmetric sum (the two mirror elements
+// see the same operands in the same order).
+__global__ void sum_ranks_kernel(const double* __restrict__ parts, int nparts, int64_t n, double* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    double s = parts[e];
+    for (int r = 1; r < nparts; ++r) s += parts[(int64_t)r * n + e];
+    out[e] = s;
+  }
+}
+
+cudaError_t sum_ranks_launch(const double* parts, int nparts, int64_t n, double* out, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const int blocks = (int)imin64(ceil_div(n, SM_THREADS), 4 * num_sms());
+  sum_ranks_kernel<<<blocks, SM_THREADS, 0, s>>>(parts, nparts, n, out);
+  return cudaGetLastError();
+}
+
 cudaError_t tri_inverse_launch(const double* R, int ldr, int n, double* X, int ldx, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   tri_inverse_kernel<<<(int)ceil_div(n, SM_THREADS), SM_THREADS, 0, s>>>(R, ldr, n, X, ldx);

@@ -3,7 +3,8 @@
 The GPU box gives one device per call, so the N > 1 data path is exercised
 here with the product's own sharding helpers (`paper_2507_07788_b200.dist`):
 each rank owns rows [r m / P, (r+1) m / P), forms its local Gram (NumPy
-stands in for the K1 kernel), the Grams are summed with `allreduce_gram_`,
+stands in for the K1 kernel), the Grams are summed with `reduce_ranks_`
+(all-gather + in-order sum: deterministic and bit-symmetric),
 and every rank runs the k x k stage of the oracle on the reduced matrix with
 the GLOBAL m in the shift rule.  The sharded run must reproduce the
 single-process oracle's decisions and factor, and both ranks must hold
@@ -22,7 +23,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2507_07788_b200.dist import allreduce_gram_, row_range
+from paper_2507_07788_b200.dist import reduce_ranks_, row_range
 
 
 def _free_port():
@@ -42,8 +43,9 @@ def _sharded_rs(x, rank, world):
     cfg = co.default_cfg()
 
     def gram(qloc):
-        g = torch.from_numpy(qloc.T @ qloc)
-        allreduce_gram_(g)
+        g = qloc.T @ qloc
+        g = torch.from_numpy((g + g.T) / 2.0)   # bit-symmetric local partial, as the Gram kernels write it
+        reduce_ranks_(g)
         return g.numpy()
 
     g = gram(q)
@@ -75,6 +77,13 @@ def _worker(rank, world, port, x, out):
         with warnings.catch_warnings():
             warnings.simplefilter("ignore")
             q, r, attempts, shifts, grams = _sharded_rs(x, rank, world)
+            q2, r2, _, shifts2, grams2 = _sharded_rs(x, rank, world)
+        # run-to-run determinism at world size > 1 (reference test_algorithms.py:107-113)
+        np.testing.assert_array_equal(r, r2)
+        np.testing.assert_array_equal(q, q2)
+        assert shifts == shifts2
+        for g in grams:
+            np.testing.assert_array_equal(g, g.T)   # bit-symmetric after the cross-rank sum
         # bit-identical Grams and decisions on every rank
         allg = [None] * world
         dist.all_gather_object(allg, (attempts, shifts, [gg.tobytes() for gg in grams]))
@@ -128,3 +137,52 @@ def test_sharded_rs_chol_qr_matches_single_process(cond):
         assert np.max(np.abs(r - ref.r)) <= 1e-10 * np.max(np.abs(ref.r))
     assert co.loo_fro(q) <= 10 * max(co.loo_fro(ref.q), 1e-14)
     assert co.rrr_fro(x, q, r) <= 10 * max(co.rrr_fro(x, ref.q, ref.r), 1e-15)
+
+
+def _reduce_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(100 + rank)
+        g = rng.standard_normal((33, 33)) * 10.0 ** rng.integers(-8, 8, size=(33, 33))
+        g = (g + g.T) / 2.0
+        bt = rng.standard_normal((5, 33))
+        flat = torch.from_numpy(np.concatenate([bt.ravel(), g.ravel()]))
+        reduce_ranks_(flat)
+        allv = [None] * world
+        dist.all_gather_object(allv, flat.numpy().tobytes())
+        assert all(v == allv[0] for v in allv)
+        if rank == 0:
+            out.put(flat.numpy().copy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_reduce_ranks_is_in_rank_order_and_bit_symmetric(world):
+    """The packed [Bt | G] partials summed over 2 and 3 ranks: every rank holds
+    the same bits, equal to ((p0 + p1) + p2) in rank order, and the G part is
+    bit-symmetric (a ring allreduce at world >= 3 may not be)."""
+    ctx = mp.get_context("spawn")
+    out = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_reduce_worker, args=(r, world, port, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = out.get(timeout=120)
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    parts = []
+    for r in range(world):
+        rng = np.random.default_rng(100 + r)
+        g = rng.standard_normal((33, 33)) * 10.0 ** rng.integers(-8, 8, size=(33, 33))
+        g = (g + g.T) / 2.0
+        bt = rng.standard_normal((5, 33))
+        parts.append(np.concatenate([bt.ravel(), g.ravel()]))
+    want = parts[0].copy()
+    for p_ in parts[1:]:
+        want = want + p_
+    np.testing.assert_array_equal(got, want)
+    gsum = got[5 * 33:].reshape(33, 33)
+    np.testing.assert_array_equal(gsum, gsum.T)

@@ -101,6 +101,7 @@ def _worker(rank, port, out_dir):
         for name, build in _cases().items():
             out[name] = _run(cq, name, build())
         out["update"] = _run_update(cq)
+        out["again"] = _run(cq, "rs_kappa15_k128", _cases()["rs_kappa15_k128"]())
         out["rows"] = ctx().row_range(24_002)
         np.save(os.path.join(out_dir, f"rank{rank}.npy"), np.array(out, dtype=object), allow_pickle=True)
     finally:
@@ -128,6 +129,16 @@ def test_ranks_agree_bitwise(sharded):
         assert a[name]["attempts"] == b[name]["attempts"], name
         if "shifts" in a[name]:
             assert a[name]["shifts"] == b[name]["shifts"], name
+
+
+def test_sharded_runs_are_deterministic(sharded):
+    """Two sharded runs of the same input give bitwise the same R and shifts:
+    the cross-rank sum is an all-gather plus an in-order device sum, so the
+    collective's algorithm cannot change a bit (reference
+    tests/test_algorithms.py:107-113)."""
+    for rank in sharded:
+        assert np.array_equal(rank["again"]["r"], rank["rs_kappa15_k128"]["r"])
+        assert rank["again"]["shifts"] == rank["rs_kappa15_k128"]["shifts"]
 
 
 def _rel(a, b):

@@ -55,11 +55,16 @@ def _run_both(algo, x, cq, co):
             ref_exc = None
         except co.OracleBreakdown as exc:
             ref, ref_exc = None, exc
-        try:
-            mine = getattr(cq, algo)(cq.CudaVectorArray.from_numpy(x))
-            my_exc = None
-        except cq.CholeskyBreakdown as exc:
-            mine, my_exc = None, exc
+        mine, trace = P.traced(getattr(cq, algo), cq.CudaVectorArray.from_numpy(x))
+        my_exc = None
+        if isinstance(mine, cq.CholeskyBreakdown):
+            mine, my_exc = None, mine
+        elif isinstance(mine, Exception):
+            raise mine
+    if algo == "rs_chol_qr" and mine is not None:
+        # every pass's decision against the oracle's decision stage on the device's own Gramian
+        rep = P.replay_iterated(trace, mine, co.default_cfg(), "rs")
+        assert rep.passes == mine.iterations, rep
     return mine, ref, my_exc, ref_exc
 
 
@@ -120,11 +125,16 @@ def _update_case(i, m, k, cond):
             ref_exc = None
         except co.OracleShiftLimit as exc:
             ref, ref_exc = None, exc
-        try:
-            mine = cq.chol_qr_update(cq.CudaVectorArray.from_numpy(q_in), r_in, cq.CudaVectorArray.from_numpy(a_new))
-            my_exc = None
-        except cq.ShiftAttemptLimitError as exc:
-            mine, my_exc = None, exc
+        mine, trace = P.traced(cq.chol_qr_update, cq.CudaVectorArray.from_numpy(q_in), r_in,
+                               cq.CudaVectorArray.from_numpy(a_new))
+        my_exc = None
+        if isinstance(mine, cq.ShiftAttemptLimitError):
+            mine, my_exc = None, mine
+        elif isinstance(mine, Exception):
+            raise mine
+    if mine is not None:
+        rep = P.replay_iterated(trace, mine, co.default_cfg(), "update")
+        assert rep.passes == mine.iterations, rep
     if my_exc is not None or ref_exc is not None:
         assert (my_exc is None) == (ref_exc is None), (my_exc, ref_exc)
         return
