@@ -260,7 +260,14 @@ def run_ours():
         if one_gpu_check:
             dist.init_process_group("gloo")
         else:
+            # NCCL's own INIT lines (ranks, NVLink / NVLS topology) on stderr so the
+            # rank count can be checked from the run's log; stdout keeps the one JSON line
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        sys.stderr.write(f"[bench] rank {dist.get_rank()} of {dist.get_world_size()} on cuda:{local}, backend "
+                         f"{dist.get_backend()}, nccl {'.'.join(map(str, torch.cuda.nccl.version()))}\n")
     import paper_2507_07788_b200 as cq
     from paper_2507_07788_b200 import _device
     from paper_2507_07788_b200.workloads import device_gaussian, device_svd_matrix
@@ -278,7 +285,16 @@ def run_ours():
 
     if ARGS.config == 4:
         return run_update_chain(cq, cx, cfg, m, world, rank, local)
-    if cfg["cond"] is not None:
+    data = "synthetic (seeded, built in HBM with torch)"
+    if ARGS.config == 3 and world == 1 and not ARGS.rows:
+        # the headline input: exactly the bits tests/test_gpu_fullsize.py checks
+        # against the oracle (workloads.host_config, NumPy on the host)
+        from paper_2507_07788_b200.workloads import host_config
+
+        a = cq.CudaVectorArray.from_numpy(host_config(3, seed=SEED))
+        data = "synthetic: workloads.host_config(3, seed=2025), NumPy on the host (the input tests/" \
+               "test_gpu_fullsize.py checks against the oracle)"
+    elif cfg["cond"] is not None:
         u_from = "householder" if ARGS.config == 1 else "cholqr2"
         a = device_svd_matrix(from_global, m, k, cfg["cond"], SEED, u_from=u_from)
     else:
@@ -320,6 +336,11 @@ def run_ours():
     passes, attempts = res.iterations, list(res.shift_attempts)
     ms = max_over_ranks(e0.elapsed_time(e1) / ARGS.steps)
     value = m * k / (ms * 1e-3)
+    # quality of the timed run's result (outside the timed region), the
+    # reference's Frobenius measures (metrics.py:42-71)
+    quality = {"loo_fro": cq.loss_of_orthogonality(res.q, norm="frobenius"),
+               "rrr_fro": cq.reconstruction_residual(a, res.q, res.r, norm="frobenius"),
+               "shift_attempts": attempts, "shifts": list(res.shifts_applied)}
 
     # ---- the same K steps again with CUDA events around every libcqr call on
     # the launching stream (KernelTimer): the per-kernel durations of the
@@ -454,11 +475,14 @@ def run_ours():
         line = {
             "metric": _metric(), "value": value, "unit": "rows*cols/s", "n_gpus": world,
             "steps": ARGS.steps, "warmup": ARGS.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, built in HBM)",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": data,
             "config": {"workload": cfg["workload"], "rows": m, "cols": k, "algo": cfg["algo"],
                        "passes": passes, "shift_attempts": attempts,
                        "parallelism": f"row-sharded dp{world}",
+                       "collective": "per pass: all-gather of the k x k partials + in-order device sum "
+                                     "(deterministic)" if world > 1 else None,
                        "l2": "inputs larger than L2 (%.1f GB)" % (m * k * 8 / 1e9)},
+            "quality": quality,
             "roofline": {"bound": "tensor", "pipe": "FP64 DMMA.8x8x4 (tensor pipe)", "kernel": dom, "achieved": tfs, "peak": FP64_PEAK_TFS,
                          "unit": "TFLOP/s", "frac": tfs / FP64_PEAK_TFS,
                          "traffic": _traffic(ARGS.config, lm[0] if lm else 0, k),

@@ -421,12 +421,18 @@ def chol_qr_update(q_in, r_in, a_new, cfg=None):
     err = identity_distance(x)
     hist = [err]
     dms = []
+    ratios = []
     while not err < tol:
         if its == cfg["max_iter"]:
             ok = False
             break
         top = float(np.max(np.diag(x) + np.sum(bt * bt, axis=0))) if bt.size else None
         dms.append(_attempt(_with_shift(x, 0.0), top)[1])
+        # how much of the Gramian the deflation cancelled: X's rounding error
+        # relative to X is ~u times this (test infrastructure: it scales the
+        # tolerance of the shift comparison, tests/parity.py)
+        dx = float(np.max(np.abs(np.diag(x)))) if x.size else 0.0
+        ratios.append(top / dx if (top is not None and dx > 0) else 1.0)
         rk, tries, xs = _update_attempts(x, m, width, cfg, shifts)
         attempts.append(tries)
         margins.append(_margin(xs, rk))
@@ -444,6 +450,7 @@ def chol_qr_update(q_in, r_in, a_new, cfg=None):
     out = Result(q_out, r_out, its, shifts, attempts, ok, err, margins)
     out.err_history = hist
     out.decision_margins = dms
+    out.deflation_ratios = ratios
     return out
 
 
@@ -462,3 +469,55 @@ def rrr_fro(a, q, r):
     num = math.sqrt(max(float(np.trace(gram(d))), 0.0))
     den = math.sqrt(max(float(np.trace(gram(a))), 0.0))
     return num / den
+
+
+def panel_widths(n, r_panels):
+    """n columns in r contiguous panels, the first n mod r one wider
+    (`algorithms.py:461-467`)."""
+    if not 1 <= r_panels <= n:
+        raise ValueError(f"need 1 <= r_panels <= {n}, got {r_panels}")
+    base, extra = divmod(n, r_panels)
+    return [base + 1] * extra + [base] * (r_panels - extra)
+
+
+def pn_chol_qr(a, r_panels, cfg=None):
+    """Panel scheme, Alg. 3: chol_qr_update folded over contiguous column
+    panels from an empty basis; a capped panel marks the result unsuccessful
+    but later panels still run; an exception is annotated with its panel
+    index (`algorithms.py:470-505`)."""
+    cfg = cfg or default_cfg()
+    a = np.asfortranarray(a, dtype=float)
+    m = a.shape[0]
+    q = np.zeros((m, 0), order="F")
+    r = np.zeros((0, 0))
+    shifts, attempts, profiles, margins, dms, hist, ratios = [], [], [], [], [], [], []
+    its = 0
+    ok = True
+    err = None
+    start = 0
+    for index, width in enumerate(panel_widths(a.shape[1], r_panels)):
+        panel = a[:, start:start + width]
+        start += width
+        try:
+            res = chol_qr_update(q, r, panel, cfg)
+        except OracleShiftLimit as exc:
+            exc.panel_index = index
+            raise
+        q, r = res.q, res.r
+        its += res.iterations
+        shifts.extend(res.shifts_applied)
+        attempts.extend(res.shift_attempts)
+        profiles.append((res.iterations, tuple(res.shift_attempts))
+                        if len(res.shift_attempts) == res.iterations else None)
+        margins.extend(res.pivot_margins)
+        dms.extend(res.decision_margins)
+        hist.extend(res.err_history)
+        ratios.extend(res.deflation_ratios)
+        err = res.orth_error
+        ok = ok and res.success
+    out = Result(q, r, its, shifts, attempts, ok, err, margins)
+    out.panel_profiles = profiles
+    out.decision_margins = dms
+    out.err_history = hist
+    out.deflation_ratios = ratios
+    return out

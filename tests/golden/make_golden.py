@@ -194,6 +194,34 @@ def main():
         r = c.chol_qr_update(c.DenseVectorArray.from_numpy(qcur), rcur, c.DenseVectorArray.from_numpy(anew))
         qcur, rcur = c.to_dense_block(r.q), r.r
 
+    # --- panel scheme (test_update_panel.py:115-162): Alg. 3 as a fold of the update
+    def pn(name, blk, r_panels, cfg=None, cfgd=None, spec=None):
+        rec_extra = {"r_panels": r_panels}
+        try:
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore")
+                res = c.pn_chol_qr(c.DenseVectorArray.from_numpy(blk), r_panels, cfg)
+            loo, rrr = _metrics(c, blk, res)
+            rec_extra.update(loo=loo, rrr=rrr,
+                             panel_profiles=[None if p is None else [p.outer, list(p.shift_attempts)]
+                                             for p in res.panel_profiles])
+            add(name, "pn_chol_qr", blk, res, cfg=cfgd, extra=rec_extra, spec=spec)
+        except (c.ShiftAttemptLimitError, c.CholeskyBreakdown) as e:
+            rec_extra["panel_index"] = getattr(e, "panel_index", None)
+            add(name, "pn_chol_qr", blk, exc=e, cfg=cfgd, extra=rec_extra, spec=spec)
+
+    for rp in (1, 2, 3, 5, 10):
+        pn(f"pn_500x10_c10_s5_r{rp}", _block(c, 500, 10, 10.0, 5), rp, spec=[500, 10, 10.0, 5, []])
+    for rp in (2, 4):
+        pn(f"pn_2000x64_c12_s0_r{rp}", _block(c, 2000, 64, 12.0, 0), rp, spec=[2000, 64, 12.0, 0, []])
+    blk = _block(c, 300, 8, 2.0, 6)
+    blk[:, 1] = 0.0
+    pn("pn_capped_panel", blk, 2, c.AlgoConfig(max_iter=3, update_shift_width="incoming"),
+       {"max_iter": 3, "update_shift_width": "incoming"}, spec=[300, 8, 2.0, 6, [1]])
+    blk = _block(c, 100, 6, 1.0, 7)
+    blk[0, 4] = np.nan
+    pn("pn_nan_panel", blk, 2, c.AlgoConfig(max_shift_attempts=3), {"max_shift_attempts": 3})
+
     # --- k x k kernels (test_kernels.py)
     kern = {}
     kern["chol_4252"] = c.cholesky(np.array([[4.0, 2.0], [2.0, 5.0]])).tolist()

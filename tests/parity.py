@@ -29,6 +29,21 @@ in at least one run:
 * a convergence decision: ||X - I||_F within [tol/100, 100 tol] in either run
   (after a pass it is itself ~kappa^2 u rounding noise of the previous Q).
 
+Two refinements, both measured on the golden panel cases:
+
+* the shifts of an update pass are compared within max(1e-6, 100 u r), r =
+  max diag G / max |diag X| of the deflated Gramian X = G - Bt^T Bt (from the
+  oracle): the deflation cancels r-fold, so X -- and the norm estimate and
+  shift taken from it -- carries a relative rounding error of ~u r in any
+  implementation (pn_2000x64_c12_s0_r4, panel 4: r ~ 1e10, the two shifts
+  differ by 3.7e-6);
+* the number of x10 escalations after a failed shifted attempt may differ:
+  an escalation only happens when the shift sits below the Gramian's own
+  rounding-level negative eigenvalue (the 2u clamp of an empty basis), and
+  how many decades that noise spans is itself rounding (pn_500x10_c10_s5_r1:
+  19 escalations on the device, 21 in the reference).  The first shift must
+  still agree and every later one must be the x10 ladder above it.
+
 Any other difference fails the test.  The compare functions return a record
 with how many decisions were compared, so each test can assert its count.
 """
@@ -112,15 +127,31 @@ def compare_iterated(mine, ref, k, tol):
             assert fragile_margin(dm_m, k) or fragile_margin(dm_r, k), (
                 f"breakdown decision differs at pass {i}", mine.shift_attempts, ref.shift_attempts, dm_m, dm_r)
             return Compared(dec, shifted, stops, False, f"branch at pass {i} (margins {dm_m} / {dm_r})")
-        assert a_m == a_r, (f"shift attempts differ at pass {i}", mine.shift_attempts, ref.shift_attempts)
+        ratio = _at(getattr(ref, "deflation_ratios", None), i) or 1.0
+        rtol = max(1e-6, 100 * U * ratio)
+        if a_m != a_r:
+            # both broke down; the escalation count differs: allowed only as a
+            # rounding-level ladder (module docstring)
+            assert max(a_m, a_r) >= 2, (f"shift attempts differ at pass {i}", mine.shift_attempts,
+                                        ref.shift_attempts)
+            np.testing.assert_allclose(shifts_m[pm], shifts_r[pr], rtol=rtol, err_msg=f"first shift of pass {i}")
+            for sh, a in ((shifts_m[pm:pm + a_m], a_m), (shifts_r[pr:pr + a_r], a_r)):
+                for s0, s1 in zip(sh[:-1], sh[1:]):
+                    assert s1 == pytest_approx_ratio(s0, s1), (f"pass {i}: not a x10 ladder", sh)
+            return Compared(dec, shifted, stops, False, f"escalations at pass {i} ({a_m} / {a_r})")
         if a_m:
-            np.testing.assert_allclose(shifts_m[pm:pm + a_m], shifts_r[pr:pr + a_r], rtol=1e-6,
+            np.testing.assert_allclose(shifts_m[pm:pm + a_m], shifts_r[pr:pr + a_r], rtol=rtol,
                                        err_msg=f"shifts of pass {i}")
             shifted += 1
         pm += a_m
         pr += a_r
         dec += 1
         i += 1
+
+
+def pytest_approx_ratio(s0, s1, esc=10.0):
+    """s1 when s1 / s0 is the escalation factor to 1e-12, else None."""
+    return s1 if abs(s1 / s0 - esc) <= 1e-12 * esc else None
 
 
 def compare_single(res_m, exc_m, res_r, exc_r, k):
@@ -292,3 +323,29 @@ def traced(fn, *args, **kw):
     finally:
         tr, cx.trace = cx.trace, None
     return res, tr
+
+
+def split_panels(res, tols):
+    """Per-panel views of a pn_chol_qr result (algorithms.py:470-505), in the
+    shape compare_iterated reads: panel i took outer_i passes (its profile),
+    its slice of shift_attempts / shifts / decision margins, and outer_i + 1
+    ||X - I||_F values; it converged when the last one is below tols[i]."""
+    import types
+
+    out = []
+    pa = ps = pe = pd = 0
+    for prof, tol in zip(res.panel_profiles, tols):
+        outer = prof[0] if isinstance(prof, tuple) else prof.outer
+        att = list(res.shift_attempts[pa:pa + outer])
+        nsh = sum(att)
+        errs = list(res.err_history[pe:pe + outer + 1])
+        out.append(types.SimpleNamespace(
+            iterations=outer, shift_attempts=att, shifts_applied=list(res.shifts_applied[ps:ps + nsh]),
+            success=bool(errs and errs[-1] < tol), err_history=errs,
+            decision_margins=list(res.decision_margins[pd:pd + outer]),
+            deflation_ratios=list(getattr(res, "deflation_ratios", [])[pd:pd + outer])))
+        pa += outer
+        ps += nsh
+        pe += outer + 1
+        pd += outer
+    return out

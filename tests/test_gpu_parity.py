@@ -650,3 +650,50 @@ def test_update_into_basis_capacity_is_bitwise_the_copy_path():
     np.testing.assert_array_equal(r1.q.to_numpy(), r2.q.to_numpy())
     np.testing.assert_array_equal(roomy.to_numpy(), basis)
     assert roomy.ncols == k and r2.q.ncols == k + p
+
+
+PANEL = [c for c in G.meta["cases"] if c["algo"] == "pn_chol_qr"]
+
+
+@pytest.mark.parametrize("case", PANEL, ids=[c["name"] for c in PANEL])
+def test_panel_scheme_golden(case):
+    """pn_chol_qr (Alg. 3, algorithms.py:470-505) against the reference's record
+    and the oracle on the same box: panel by panel, every pass's decision
+    (tests/parity.py), the per-panel profiles, R_in of each fold embedded, the
+    panel index of an exception, LOO_F / RRR_F within 10x."""
+    cq = _cq()
+    from oracle import cholqr_oracle as co
+
+    blk = G.input(case)
+    a = cq.CudaVectorArray.from_numpy(blk)
+    cfg = algo_cfg(case)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        if "exception" in case:
+            with pytest.raises(cq.ShiftAttemptLimitError) as info:
+                cq.pn_chol_qr(a, case["r_panels"], cfg)
+            assert info.value.panel_index == case["panel_index"]
+            assert info.value.attempts == case["attempts"]
+            return
+        res = cq.pn_chol_qr(a, case["r_panels"], cfg)
+        ref = co.pn_chol_qr(blk, case["r_panels"], oracle_cfg(case))
+    widths = cq.panel_widths(blk.shape[1], case["r_panels"])
+    assert len(res.panel_profiles) == len(widths)
+    np.testing.assert_array_equal(np.tril(res.r, -1), 0.0)
+    diverged = None
+    tols = [cfg.effective_tol(w) for w in widths]
+    for mine, oref, width, tol in zip(P.split_panels(res, tols), P.split_panels(ref, tols), widths, tols):
+        cmp = P.compare_iterated(mine, oref, width, tol)
+        if not cmp.full:
+            diverged = tol
+            break
+    if diverged is None:
+        assert res.shift_attempts == case["attempts"]
+        assert [[p.outer, list(p.shift_attempts)] for p in res.panel_profiles] == case["panel_profiles"]
+        np.testing.assert_allclose(res.shifts_applied, case["shifts"], rtol=1e-6)
+    assert res.success == case["success"] or diverged is not None
+    if case["success"] and "loo" in case:
+        loo = cq.loss_of_orthogonality(res.q, norm="frobenius")
+        rrr = cq.reconstruction_residual(a, res.q, res.r, norm="frobenius")
+        assert P.within10(loo, case["loo"], blk.shape[1], diverged), (loo, case["loo"])
+        assert P.within10(rrr, case["rrr"], blk.shape[1], diverged), (rrr, case["rrr"])

@@ -162,11 +162,50 @@ def test_decision_rule_rejects_robust_differences():
         P.compare_iterated(run([0, 0], [], [1e-3, 0.5]), ref, 8, 1e-13)
     with pytest.raises(AssertionError):
         P.compare_iterated(run([1, 0], [1.00001e-10], [-1e-3, 0.5]), ref, 8, 1e-13)
-    with pytest.raises(AssertionError):
-        P.compare_iterated(run([2, 0], [1e-10, 1e-9], [-1e-3, 0.5]), ref, 8, 1e-13)
+    with pytest.raises(AssertionError):      # an escalation that is not the x10 ladder
+        P.compare_iterated(run([2, 0], [1e-10, 3e-10], [-1e-3, 0.5]), ref, 8, 1e-13)
+    with pytest.raises(AssertionError):      # a ladder from a different first shift
+        P.compare_iterated(run([2, 0], [2e-10, 2e-9], [-1e-3, 0.5]), ref, 8, 1e-13)
+    ladder = P.compare_iterated(run([2, 0], [1e-10, 1e-9], [-1e-3, 0.5]), ref, 8, 1e-13)
+    assert not ladder.full and "escalations" in ladder.reason
     nan = run([1, 0], [1e-10], [float("nan"), 0.5])
     with pytest.raises(AssertionError):
         P.compare_iterated(run([0, 0], [], [float("nan"), 0.5]), nan, 8, 1e-13)
     fragile = run([1, 0], [1e-10], [-1e-16, 0.5])
     cmp = P.compare_iterated(run([0, 0], [], [1e-16, 0.5]), fragile, 8, 1e-13)
     assert not cmp.full and cmp.decisions == 0
+
+
+PANEL = [c for c in G.meta["cases"] if c["algo"] == "pn_chol_qr"]
+
+
+@pytest.mark.parametrize("case", PANEL, ids=[c["name"] for c in PANEL])
+def test_oracle_panel_scheme_matches_reference(case):
+    """Alg. 3 (algorithms.py:470-505) against the unmodified reference: per-panel
+    profiles, attempts, shifts, R, and the panel index of an exception."""
+    a = G.input(case)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        if "exception" in case:
+            with pytest.raises(co.OracleShiftLimit) as info:
+                co.pn_chol_qr(a, case["r_panels"], oracle_cfg(case))
+            assert info.value.panel_index == case["panel_index"]
+            assert info.value.attempts == case["attempts"]
+            return
+        res = co.pn_chol_qr(a, case["r_panels"], oracle_cfg(case))
+    assert res.iterations == case["iterations"]
+    assert res.shift_attempts == case["attempts"]
+    assert res.success == case["success"]
+    assert [None if p is None else [p[0], list(p[1])] for p in res.panel_profiles] == case["panel_profiles"]
+    np.testing.assert_allclose(res.shifts_applied, case["shifts"], rtol=1e-12)
+    r_ref = G.r(case)
+    assert np.max(np.abs(res.r - r_ref)) <= 1e-12 * max(np.max(np.abs(r_ref)), 1e-300)
+    if "loo" in case:
+        assert co.loo_fro(res.q) == pytest.approx(case["loo"], rel=1e-6, abs=1e-18)
+
+
+def test_oracle_panel_bounds():
+    with pytest.raises(ValueError):
+        co.pn_chol_qr(np.ones((50, 4)), 0)
+    with pytest.raises(ValueError):
+        co.pn_chol_qr(np.ones((50, 4)), 5)
