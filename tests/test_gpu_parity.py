@@ -688,12 +688,35 @@ def test_panel_scheme_golden(case):
             diverged = tol
             break
     if diverged is None:
+        # the oracle matched the reference's record on CPU (test_oracle_golden.py); here
+        # the device against the record, with the oracle's per-pass deflation ratios
         assert res.shift_attempts == case["attempts"]
         assert [[p.outer, list(p.shift_attempts)] for p in res.panel_profiles] == case["panel_profiles"]
-        np.testing.assert_allclose(res.shifts_applied, case["shifts"], rtol=1e-6)
+        i = 0
+        for s_m, s_r, ratio, att in zip(_pass_shifts(res), _pass_shifts_record(case), ref.deflation_ratios,
+                                        res.shift_attempts):
+            if att:
+                np.testing.assert_allclose(s_m, s_r, rtol=max(1e-6, 100 * U * ratio), err_msg=f"pass {i}")
+            i += 1
     assert res.success == case["success"] or diverged is not None
     if case["success"] and "loo" in case:
         loo = cq.loss_of_orthogonality(res.q, norm="frobenius")
         rrr = cq.reconstruction_residual(a, res.q, res.r, norm="frobenius")
         assert P.within10(loo, case["loo"], blk.shape[1], diverged), (loo, case["loo"])
         assert P.within10(rrr, case["rrr"], blk.shape[1], diverged), (rrr, case["rrr"])
+
+
+def _pass_shifts(res):
+    out, p = [], 0
+    for a in res.shift_attempts:
+        out.append(list(res.shifts_applied[p:p + a]))
+        p += a
+    return out
+
+
+def _pass_shifts_record(case):
+    out, p = [], 0
+    for a in case["attempts"]:
+        out.append(list(case["shifts"][p:p + a]))
+        p += a
+    return out
