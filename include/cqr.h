@@ -249,6 +249,13 @@ int cqr_frobenius(const double* X, int ldx, int rows, int cols, double* out, voi
  * determinism, tests/test_algorithms.py:107-113). */
 int cqr_sum_ranks(const double* parts, int nparts, int64_t n, double* out, void* stream);
 
+/* host_pinned[0:n] = src[0:n] (device), written by a kernel through the
+ * pinned buffer's mapped alias instead of a copy-engine transfer: the small
+ * results of a call (R, the status records) leave the GPU without queueing
+ * behind a large cudaMemcpy another stream has in flight.  Asynchronous on
+ * `stream`; the host reads after synchronizing with it. */
+int cqr_store_to_host(const double* src, int64_t n, double* host_pinned, void* stream);
+
 /* Streaming reconstruction residual (K5), k <= 64: one sweep over the rows of
  * Q and A (both QI, m rows) that forms D = A - Q R in registers -- never as a
  * tall array -- and returns DtD = D^T D (k x k, ldd; bit-symmetric) and

@@ -277,6 +277,15 @@ class Engine:
         """apply_gram may overwrite its input (fused kernel, or k <= 64)."""
         return self.k <= 64 or self.cx.lib.cqr_apply_gram_inplace_ok(self.k) == 1
 
+    def _store_host(self, t, buf):
+        """Enqueue t (contiguous device fp64) -> the pinned buffer `buf` as a
+        kernel's mapped stores (cqr_store_to_host), not a copy-engine
+        transfer: it must not queue behind a caller's bulk D2H copy of Q on
+        another stream (the streamed e2e loader)."""
+        _lib.check(self.cx.lib.cqr_store_to_host(t.data_ptr(), t.numel(), buf.data_ptr(), self.cx.stream),
+                   "store_to_host")
+        self.cx.launches += 1
+
     def _to_host(self, t):
         """A column-major device matrix as a row-major numpy array, through a
         pooled pinned buffer (a pageable copy costs several times more)."""
@@ -284,14 +293,14 @@ class Engine:
         buf = self.cx.acquire_pinned((t.numel() * 8,))
         try:
             view = buf.view(torch.float64)[: t.numel()].view(t.shape)
-            view.copy_(t, non_blocking=True)
+            self._store_host(t, buf)
             torch.cuda.current_stream(self.cx.device).synchronize()
             return view.numpy().T.copy()
         finally:
             self.cx.release_pinned(buf)
 
     def r_prefetch(self):
-        """Enqueue the D2H copy of R now (after the last launch of a fixed
+        """Enqueue the download of R now (after the last launch of a fixed
         schedule), so it runs right behind the last kernel while the host reads
         the statuses; r_host() then only waits for it."""
         t = self.Racc[:, : self.k]
@@ -299,7 +308,7 @@ class Engine:
             t = t.contiguous()
         buf = self.cx.acquire_pinned((t.numel() * 8,))
         view = buf.view(torch.float64)[: t.numel()].view(t.shape)
-        view.copy_(t, non_blocking=True)
+        self._store_host(t, buf)
         ev = torch.cuda.Event()
         ev.record(torch.cuda.current_stream(self.cx.device))
         self._r_pending = (buf, view, ev)

@@ -108,6 +108,7 @@ SIGNATURES = {
     "cqr_tri_multiply": (_I, [_P, _I, _P, _I, _I, _P, _I, _P]),
     "cqr_frobenius": (_I, [_P, _I, _I, _I, _P, _P]),
     "cqr_sum_ranks": (_I, [_P, _I, _I64, _P, _P]),
+    "cqr_store_to_host": (_I, [_P, _I64, _P, _P]),
     "cqr_resid_gram_supported": (_I, [_I]),
     "cqr_resid_gram_workspace_bytes": (_SZ, [_I64, _I]),
     "cqr_resid_gram": (_I, [_P, _I64, _P, _I64, _I64, _I, _P, _P, _I, _P, _P, _SZ, _P]),

@@ -392,4 +392,17 @@ int cqr_resid_gram(const double* Q, int64_t ldq, const double* A, int64_t lda, i
                     "cqr_resid_gram");
 }
 
+int cqr_store_to_host(const double* src, int64_t n, double* host_pinned, void* stream) {
+  if (n < 0 || (n > 0 && (src == nullptr || host_pinned == nullptr)))
+    return fail(CQR_EINVAL, "cqr_store_to_host: bad arguments");
+  if (n == 0) return CQR_OK;
+  void* d = nullptr;
+  if (cudaHostGetDevicePointer(&d, host_pinned, 0) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(CQR_EINVAL, "cqr_store_to_host: destination must be pinned (mapped) host memory");
+  }
+  return cuda_check(cqr::store_mapped_launch(src, n, static_cast<double*>(d), static_cast<cudaStream_t>(stream)),
+                    "cqr_store_to_host");
+}
+
 }  // extern "C"

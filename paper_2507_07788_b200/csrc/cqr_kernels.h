@@ -119,6 +119,7 @@ cudaError_t tri_multiply_launch(const double* A, int lda, const double* B, int l
                                 cudaStream_t s);
 cudaError_t frobenius_launch(const double* X, int ldx, int rows, int cols, double* out, cudaStream_t s);
 cudaError_t sum_ranks_launch(const double* parts, int nparts, int64_t n, double* out, cudaStream_t s);
+cudaError_t store_mapped_launch(const double* src, int64_t n, double* dst_dev_alias, cudaStream_t s);
 
 // ------------------------------------------------------------- streaming quality measures (K5, cqr_metrics.cu)
 bool resid_gram_supported(int k);

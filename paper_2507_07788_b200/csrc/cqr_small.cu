@@ -86,6 +86,23 @@ cudaError_t sum_ranks_launch(const double* parts, int nparts, int64_t n, double*
   return cudaGetLastError();
 }
 
+// dst (mapped pinned host memory, seen through its device alias) = src, n
+// doubles, written by the SMs as posted PCIe stores: a small result leaves the
+// GPU without a copy-engine transfer, so it does not queue behind a large
+// cudaMemcpy a caller runs on another stream (the e2e loader's D2H of Q).
+__global__ void store_mapped_kernel(const double* __restrict__ src, int64_t n, double* dst) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    dst[e] = src[e];
+  __threadfence_system();
+}
+
+cudaError_t store_mapped_launch(const double* src, int64_t n, double* dst_dev_alias, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const int blocks = (int)imin64(ceil_div(n, SM_THREADS), 64);
+  store_mapped_kernel<<<blocks, SM_THREADS, 0, s>>>(src, n, dst_dev_alias);
+  return cudaGetLastError();
+}
+
 cudaError_t tri_inverse_launch(const double* R, int ldr, int n, double* X, int ldx, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   tri_inverse_kernel<<<(int)ceil_div(n, SM_THREADS), SM_THREADS, 0, s>>>(R, ldr, n, X, ldx);
