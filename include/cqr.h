@@ -222,6 +222,9 @@ int cqr_debug_factor_profile(unsigned long long* out16);
 /* Diagnostics: 1 (default) = the update pass stages narrow sub-panels with one
  * TMA tensor copy each; 0 = per-row-quad bulk copies only (comparisons). */
 void cqr_debug_update_tma(int on);
+/* Diagnostics: 1 = the blocked Cholesky in bands of 32 pivots with a rank-32
+ * update between bands; 0 (default) = one lookahead chain over all block steps. */
+int cqr_debug_factor_banded(int on);
 int cqr_factor(const cqr_factor_config* cfg, int k, const double* G, int ldg, const double* Bt, int ldbt, int q,
                double* Rk, double* Rinv, int ldr, double* Racc, double* B, int ldb, double* shifts,
                cqr_factor_status* status, void* ws, size_t ws_bytes, void* stream);

@@ -270,6 +270,7 @@ int cqr_update_pass(const double* Qin, int64_t ldqin, int q, double* Q, int64_t 
 
 int cqr_debug_factor_profile(unsigned long long* out16) { return cqr::factor_profile(out16); }
 void cqr_debug_update_tma(int on) { cqr::set_update_tma(on); }
+int cqr_debug_factor_banded(int on) { return cqr::factor_set_banded(on); }
 
 size_t cqr_factor_workspace_bytes(int k) { return k > 0 ? cqr::factor_workspace_bytes(k) : 256; }
 

@@ -52,6 +52,9 @@ __host__ __device__ __forceinline__ int64_t pk(int i, int c) { return (int64_t)c
 // phase timestamps of the last factor launch (globaltimer ns), for profiling;
 // slots 9..12 accumulate SM cycles of the blocked-Cholesky step phases
 __device__ unsigned long long g_fprof[16];
+// 1: bands of 4 block rows with a rank-32 update between bands; 0: one
+// lookahead chain over every block step (cqr_debug_factor_banded)
+__device__ int g_banded = 1;
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -266,6 +269,8 @@ __device__ bool chol_blocked(double* Wb, int n, int nb, int P0, int nbr, int off
   // waiting on it -- the load issued in one step is tested in the next
   unsigned long long spec_pend = 0;
   bool spec_have = false;
+  constexpr int NWKR = FK_NW - 1;                    // worker warps 1.. (panel solve)
+  constexpr int NWK = FK_NW - FK_NW / 4;             // of which the trailing-update warps (warp % 4 != 0)
   for (int P = P0; P < nbr; ++P) {
     const long long c0 = clock64();
     int spec_abort = 0;
@@ -275,10 +280,12 @@ __device__ bool chol_blocked(double* Wb, int n, int nb, int P0, int nbr, int off
       spec_have = true;
     }
     const double* D = Wb + lay(P, P);
-    // ---- (b) panel: R_PJ = R_PP^{-T} W_PJ, one column per thread
-    const int ncols = 8 * (nb - 1 - P);
     const double* iv = inv + 8 * P;
-    for (int col = tid; col < ncols; col += FK_THREADS) {
+    const int ncb = nb - 1 - P;                      // block columns right of the diagonal
+    const int nrows_b = nbr - 1 - P;                 // band rows below P
+    const bool ahead = nrows_b > 0;                  // warp 0 runs the lookahead chain
+    // panel row P: R_PJ = R_PP^{-T} W_PJ, one column per thread (8-long chain)
+    auto solve_col = [&](int col) {
       double* blk = Wb + lay(P, P + 1 + (col >> 3)) + (col & 7) * 8;   // column (col & 7), rows 0..7
       double y[8];
 #pragma unroll
@@ -290,17 +297,16 @@ __device__ bool chol_blocked(double* Wb, int n, int nb, int P0, int nbr, int off
       }
 #pragma unroll
       for (int jj = 0; jj < 8; ++jj) blk[jj] = y[jj];
-    }
-    __syncthreads();
-    const long long c1 = clock64();
-    // ---- (c) trailing rank-8 update: blocks (I, J), P < I < nbr, I <= J < nb
-    const int ncb = nb - 1 - P;
-    const int nrows_b = nbr - 1 - P;
-    const int nblk = (nrows_b == ncb) ? ncb * (ncb + 1) / 2 : nrows_b * ncb - nrows_b * (nrows_b - 1) / 2;
+    };
     int f = 0;
     if (warp == 0) {
-      if (nrows_b > 0) {
-        // block (P+1, P+1) (index 0 in both enumerations), then factor it
+      // ---- the critical chain of the step, alone on warp 0:
+      // solve block (P, P+1) -> rank-8 update of (P+1, P+1) -> factor it
+      if (ahead) {
+        if (lane < 8) solve_col(lane);
+        __syncwarp();
+        // (P, P+1) is final: release it to the workers' updates of block row P+1
+        asm volatile("bar.arrive 2, %0;" ::"n"(FK_THREADS) : "memory");
         const double* pa = Wb + lay(P, P + 1) + g * 8 + t;
         double* pc = Wb + lay(P + 1, P + 1) + 2 * t * 8 + g;
         double c2[2] = {pc[0], pc[8]};
@@ -317,7 +323,15 @@ __device__ bool chol_blocked(double* Wb, int n, int nb, int P0, int nbr, int off
       }
       if (lane == 0) *flag = f | spec_abort;
     } else {
-      // two blocks per iteration: all loads first, then the DMMAs (ILP)
+      // ---- workers: the rest of panel row P, then the trailing update
+      const int first = ahead ? 8 : 0;               // warp 0 solves block (P, P+1)
+      for (int col = first + (tid - 32); col < 8 * ncb; col += 32 * NWKR) solve_col(col);
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * NWKR) : "memory");   // panel row P final (but (P, P+1))
+      const long long c1 = clock64();
+      if (tid == 32 && blockIdx.x == 0) g_fprof[9] += (unsigned long long)(c1 - c0);
+      if (ahead) asm volatile("bar.sync 2, %0;" ::"n"(FK_THREADS) : "memory");   // (P, P+1) from warp 0
+      // trailing rank-8 update of blocks (I, J), P < I < nbr, I <= J < nb, but (P+1, P+1)
+      const int nblk = (nrows_b == ncb) ? ncb * (ncb + 1) / 2 : nrows_b * ncb - nrows_b * (nrows_b - 1) / 2;
       auto decode = [&](int blk, int& I, int& Jb) {
         if (nrows_b == ncb) {
           int J = tri_col(blk);
@@ -331,11 +345,10 @@ __device__ bool chol_blocked(double* Wb, int n, int nb, int P0, int nbr, int off
           Jb = I + rem;
         }
       };
-      // Workers: the 12 warps outside warp 0's SM sub-partition (warp % 4 != 0);
-      // warps 4, 8, 12 stay idle so their DMMAs do not contend for the FP64 pipe
-      // with warp 0's dependent pivot chain (it runs 2-3x slower otherwise).
-      // blk 0 is warp 0's.
-      constexpr int NWK = FK_NW - FK_NW / 4;
+      // the 9 warps outside warp 0's SM sub-partition (warp % 4 != 0); warps 4
+      // and 8 stay out so their DMMAs do not share warp 0's FP64 pipe (its
+      // dependent pivot chain runs 2-3x slower otherwise).  blk 0 = (P+1, P+1)
+      // is warp 0's.
       const int wk = warp - 1 - (warp >> 2);
       for (int blk = ((warp & 3) ? 1 + wk : nblk); blk < nblk; blk += 2 * NWK) {
         const int blk2 = blk + NWK;
@@ -346,38 +359,34 @@ __device__ bool chol_blocked(double* Wb, int n, int nb, int P0, int nbr, int off
         const double* pa0 = Wb + lay(P, I0) + g * 8 + t;
         const double* pb0 = Wb + lay(P, J0) + g * 8 + t;
         double* pc0 = Wb + lay(I0, J0) + 2 * t * 8 + g;
-        double c0[2] = {pc0[0], pc0[8]};
+        double c0r[2] = {pc0[0], pc0[8]};
         double a00, a01, b00, b01;
         frag_pair(pa0, g, a00, a01);
         frag_pair(pb0, g, b00, b01);
         a00 = -a00; a01 = -a01;
-        double c1[2] = {0.0, 0.0}, a10 = 0.0, a11 = 0.0, b10 = 0.0, b11 = 0.0;
+        double c1r[2] = {0.0, 0.0}, a10 = 0.0, a11 = 0.0, b10 = 0.0, b11 = 0.0;
         double* pc1 = pc0;
         if (two) {
           const double* pa1 = Wb + lay(P, I1) + g * 8 + t;
           const double* pb1 = Wb + lay(P, J1) + g * 8 + t;
           pc1 = Wb + lay(I1, J1) + 2 * t * 8 + g;
-          c1[0] = pc1[0]; c1[1] = pc1[8];
+          c1r[0] = pc1[0]; c1r[1] = pc1[8];
           frag_pair(pa1, g, a10, a11);
           frag_pair(pb1, g, b10, b11);
           a10 = -a10; a11 = -a11;
         }
-        dmma(c0, a00, b00);
-        if (two) dmma(c1, a10, b10);
-        dmma(c0, a01, b01);
-        if (two) dmma(c1, a11, b11);
-        pc0[0] = c0[0];
-        pc0[8] = c0[1];
-        if (two) { pc1[0] = c1[0]; pc1[8] = c1[1]; }
+        dmma(c0r, a00, b00);
+        if (two) dmma(c1r, a10, b10);
+        dmma(c0r, a01, b01);
+        if (two) dmma(c1r, a11, b11);
+        pc0[0] = c0r[0];
+        pc0[8] = c0r[1];
+        if (two) { pc1[0] = c1r[0]; pc1[8] = c1r[1]; }
       }
+      if (tid == 32 && blockIdx.x == 0) g_fprof[10] += (unsigned long long)(clock64() - c1);
     }
     __syncthreads();
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-      const long long c2 = clock64();
-      g_fprof[9] += (unsigned long long)(c1 - c0);
-      g_fprof[10] += (unsigned long long)(c2 - c1);
-      g_fprof[11] += 1;
-    }
+    if (threadIdx.x == 0 && blockIdx.x == 0) g_fprof[11] += 1;
     if (*flag) return false;
   }
   return true;
@@ -623,7 +632,8 @@ __device__ __noinline__ bool chol_attempt(const double* __restrict__ Xs, const d
     __syncthreads();
     fmark(2);
     const int nb = (k + 7) >> 3;
-    ok = chol_banded(Wb, k, nb, nb, 0, rowbuf, smin, fs, LayoutUpper(), flag);
+    ok = g_banded ? chol_banded(Wb, k, nb, nb, 0, rowbuf, smin, fs, LayoutUpper(), flag)
+                  : chol_blocked(Wb, k, nb, 0, nb, 0, rowbuf, smin, fs, LayoutUpper(), flag);
     fmark(3);
     if (ok) store_blocked(Wb, k, 0, Rk, ldr);
     fmark(4);
@@ -773,7 +783,8 @@ __device__ __noinline__ bool chol_attempt(const double* __restrict__ Xs, const d
       pad_blocked(S, n);
       __syncthreads();
       fmark(4);
-      ok = chol_banded(S, n, nbs, nbs, b, rowbuf, smin, fs, LayoutUpper(), flag);
+      ok = g_banded ? chol_banded(S, n, nbs, nbs, b, rowbuf, smin, fs, LayoutUpper(), flag)
+                    : chol_blocked(S, n, nbs, 0, nbs, b, rowbuf, smin, fs, LayoutUpper(), flag);
       fmark(5);
       if (ok) store_blocked(S, n, b, Rk, ldr);
     }
@@ -1162,7 +1173,63 @@ __global__ void __launch_bounds__(FK_THREADS, 1) factor_kernel(FactorArgs a) {
   //         shared memory; loads are batched 16 per thread before any store
   //         (the L2 latency, not bandwidth, bounds this phase).  k > 128: by
   //         factor_prep_kernel ahead of this kernel.
-  if (xs) {
+  if (xs && a.policy == CQR_POLICY_UPDATE && a.q > 0 && a.bt_stage) {
+    // deflated X = G - Bt^T Bt (algorithms.py:358-366).  Bt (q x k) is staged
+    // in the work area first (one coalesced sweep, latency overlapped across
+    // all threads; column stride q + 1 against bank conflicts), then each
+    // thread forms its elements' q-long dot products from shared memory with
+    // eight accumulator chains, added in a fixed order.  One thread per element
+    // streaming the chain from L2 took ~20 us at q = 256 (~40 at 496).
+    const int q = a.q, ldb = q + 1;
+    double* bts = Wsm + wdoubles;   // the launch sized shared memory for it (a.bt_stage)
+    for (int base = tid; base < k * q; base += 8 * FK_THREADS) {
+      double v[8];   // all loads of the batch in flight before any store
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = base + u * FK_THREADS;
+        v[u] = (e < k * q) ? a.Bt[(int64_t)(e / q) * a.ldbt + e % q] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = base + u * FK_THREADS;
+        if (e < k * q) bts[(e / q) * ldb + e % q] = v[u];
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < k * k; e += FK_THREADS) {
+      const int r = e % k, c = e / k;
+      if (r < c) continue;
+      const double* br = bts + r * ldb;
+      const double* bc = bts + c * ldb;
+      double d[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      int l = 0;
+      for (; l + 8 <= q; l += 8) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) d[u] = fma(br[l + u], bc[l + u], d[u]);
+      }
+      for (; l < q; ++l) d[0] = fma(br[l], bc[l], d[0]);
+      const double dd = ((d[0] + d[1]) + (d[2] + d[3])) + ((d[4] + d[5]) + (d[6] + d[7]));
+      const double x = a.G[(int64_t)c * a.ldg + r] - dd;
+      Xs[(int64_t)c * k + r] = x;
+      Xs[(int64_t)r * k + c] = x;
+    }
+    __syncthreads();
+    double loc = 0.0;
+    for (int e = tid; e < k * k; e += FK_THREADS) {
+      const int r = e % k, c = e / k;
+      if (r < c) continue;
+      const double dd = Xs[(int64_t)c * k + r] - ((r == c) ? 1.0 : 0.0);
+      loc += ((r == c) ? 1.0 : 2.0) * (dd * dd);
+    }
+    const double err = sqrt(block_sum(loc, red));
+    double dml = -INFINITY;
+    for (int j = tid; j < k; j += FK_THREADS) dml = fmax(dml, a.G[(int64_t)j * a.ldg + j]);
+    const double dm = block_max(dml, red);
+    if (tid == 0) {
+      fs.err = err;
+      fs.diag_max = dm;
+    }
+  } else if (xs) {
     const int kk32 = k * k;
     double loc = 0.0;
     for (int base = tid; base < kk32; base += 16 * FK_THREADS) {
@@ -1719,6 +1786,11 @@ __global__ void __launch_bounds__(FW_WARPS * 32) factor_finish_wide_kernel(Facto
     for (int i = c + 1 + lane; i < KP; i += 32) out[(i / CT_K) * CT_TILE + i % CT_K] = 0.0;
 }
 
+int factor_set_banded(int on) {
+  const int v = on ? 1 : 0;
+  return cudaMemcpyToSymbol(g_banded, &v, sizeof(int)) == cudaSuccess ? 0 : -1;
+}
+
 int factor_profile(unsigned long long* out) {
   return cudaMemcpyFromSymbol(out, g_fprof, sizeof(g_fprof)) == cudaSuccess ? 0 : -1;
 }
@@ -1738,6 +1810,12 @@ cudaError_t factor_launch(FactorArgs& a, cudaStream_t stream) {
   // k <= 128: X, then the block-packed triangle; 128 < k <= 256: the band or the
   // trailing triangle; k <= 768: one 32-row band (work_doubles)
   smem += ((a.k <= FK_SMEM_K ? (size_t)a.k * a.k : 0) + (size_t)work_doubles(a.k)) * sizeof(double);
+  // update policy, k <= 128: room to stage Bt (q x k, column stride q + 1) for the deflation
+  a.bt_stage = 0;
+  if (a.policy == CQR_POLICY_UPDATE && a.q > 0 && a.k <= FK_SMEM_K) {
+    const size_t extra = (size_t)a.k * (a.q + 1) * sizeof(double);
+    if (smem + extra <= 220 * 1024) { smem += extra; a.bt_stage = 1; }
+  }
   {
     const size_t mx = 220 * 1024;  // <= 227 KB minus the static shared state
     cudaError_t e = smem_attr((const void*)factor_kernel, mx);

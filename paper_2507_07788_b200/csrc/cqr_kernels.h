@@ -107,11 +107,13 @@ struct FactorArgs {
   // estimate + shifted attempts into private buffers while CTA 0 tries the
   // plain factorization; CTA 0 publishes its outcome in `pub` (epoch-tagged)
   int spec; unsigned epoch;
+  int bt_stage;    // update policy: Bt staged in shared memory after the work area
   double* Rk1; int ldr1; double* W1; double* shifts1; double* pub;
 };
 cudaError_t factor_launch(FactorArgs& a, cudaStream_t stream);
 size_t factor_workspace_bytes(int k);
 int factor_profile(unsigned long long* out);
+int factor_set_banded(int on);
 
 // ------------------------------------------------------------- standalone k x k kernels (cqr_small.cu)
 cudaError_t tri_inverse_launch(const double* R, int ldr, int n, double* X, int ldx, cudaStream_t s);
