@@ -665,15 +665,21 @@ __device__ __noinline__ bool chol_attempt(const double* __restrict__ Xs, const d
     const int nb = (k + 7) >> 3;
     double* Wb = smem_w;
     const LayoutBand4 band;
-    for (int r = warp; r < b; r += FK_NW)
-      for (int c = r + lane; c < 8 * nb; c += 32) {
-        double x = 0.0;
-        if (c < k) {
-          x = __ldg(Xg + (int64_t)r * k + c);   // = X(r, c) by symmetry; contiguous in c
-          if (c == r) x = __dadd_rn(x, sigma);
-        }
-        Wb[band(r >> 3, c >> 3) + (c & 7) * 8 + (r & 7)] = x;
+    // (8 nb <= 256 columns: one batch of 8 loads per lane and row, all in
+    // flight before the stores)
+    for (int r = warp; r < b; r += FK_NW) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = r + lane + 32 * u;
+        v[u] = (c < 8 * nb && c < k) ? __ldg(Xg + (int64_t)r * k + c) : 0.0;   // = X(r, c) by symmetry
       }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = r + lane + 32 * u;
+        if (c < 8 * nb) Wb[band(r >> 3, c >> 3) + (c & 7) * 8 + (r & 7)] = (c == r) ? __dadd_rn(v[u], sigma) : v[u];
+      }
+    }
     __syncthreads();
     ok = chol_banded(Wb, k, nb, 4, 0, rowbuf, smin, fs, band, flag);
     if (ok) {
