@@ -83,7 +83,10 @@ static size_t update_smem_bytes(int q, int sr) {
   return ((size_t)up_fixed(sr) + (size_t)up_stages(q, sr) * up_stage(q, sr)) * 8;
 }
 
-template <int NQ, int SR>
+// PART: the last 64-column block is partial (q % 64 != 0, NQ >= 2): its work
+// is split by k4 step (projection) and by output block (cross Gram) so that it
+// spreads over the four SM sub-partitions and the part past q is skipped.
+template <int NQ, int SR, bool PART>
 __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(const __grid_constant__ UpdateArgs a) {
   if (a.gate != nullptr && *a.gate != 0) return;   // gated off
   constexpr int RB = SR / 8;        // 8-row blocks per sub-panel
@@ -167,7 +170,17 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(const __grid
         btn[ks] = (!init && kk < q && n < p) ? a.Bt[(int64_t)n * a.ldbt + kk] : 0.0;
       }
     }
-    double btr[NARROW ? 1 : NQ][2][2];   // Bt(64c + 8wa + 4h + t, 8nb + g)
+    // Bt(kc(c, h) + t, 8nb + g).  Full 64-column blocks: warp wa owns the 8
+    // columns [64c + 8wa, +8).  The last block (only q - 64(NQ-1) columns
+    // valid) is split by k4 step instead: warp wa takes steps s + 4j + 8h
+    // (s = wa % 4 = its SM sub-partition, j = wa / 4), so the valid steps of a
+    // partial block land evenly on the four sub-partitions, and the steps past
+    // q are skipped whole (warp-uniform), not multiplied by zero.
+    const int kap = (wa & 3) + 4 * (wa >> 2);
+    auto kcol = [&](int c, int h) {
+      return (PART && c == NQ - 1) ? 64 * c + 4 * (kap + 8 * h) : 64 * c + 8 * wa + 4 * h;
+    };
+    double btr[NARROW ? 1 : NQ][2][2];
     if constexpr (!NARROW) {
 #pragma unroll
     for (int c = 0; c < NQ; ++c)
@@ -175,7 +188,7 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(const __grid
       for (int h = 0; h < 2; ++h)
 #pragma unroll
         for (int nb = 0; nb < 2; ++nb) {
-          const int kk = 64 * c + 8 * wa + 4 * h + t, n = 8 * nb + g;
+          const int kk = kcol(c, h) + t, n = 8 * nb + g;
           btr[c][h][nb] = (!init && kk < q && n < p) ? a.Bt[(int64_t)n * a.ldbt + kk] : 0.0;
         }
     }
@@ -224,7 +237,8 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(const __grid
         for (int c = 0; c < NQ; ++c)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const int kc = 64 * c + 8 * wa + 4 * h;   // + t
+            const int kc = kcol(c, h);                // + t
+            if (PART && c == NQ - 1 && kc >= q) continue;   // a whole k4 step past q: skipped (warp-uniform)
             const bool kv = kc + t < q;               // columns >= q of the stage are stale
             double av[RB];
 #pragma unroll
@@ -300,6 +314,12 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(const __grid
       for (int n = 0; n < 2; ++n) { ct[c][n][0] = 0.0; ct[c][n][1] = 0.0; }
     double gq[2] = {0.0, 0.0};
     const int bi = (wb == 0) ? 0 : 1, bj = (wb == 2) ? 1 : 0;
+    // Full blocks c < NQ - 1: warp wb owns the Bt' rows [64c + 8wb, +8) (both
+    // 8-column halves of p).  The last block is split by output 8 x 8 block
+    // instead: chain i = wb + 8 h2 is block (rows 64(NQ-1) + 8(i / 2), columns
+    // 8(i % 2)), kept in ct[NQ-1][h2]; the chains of a partial block spread
+    // over the sub-partitions and the blocks past q are skipped whole.
+    const int cl0 = 64 * (NQ - 1);
     for (int64_t j = 0; j < mine; ++j) {
       mbar_wait(&yfull[ys], yph);
       const double* Qs = stg + s * STG;
@@ -309,11 +329,21 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(const __grid
       for (int ks = 0; ks < Q4; ++ks) {
         const double b0 = yd[ks * 64 + 4 * g + t], b1 = yd[ks * 64 + 32 + 4 * g + t];
 #pragma unroll
-        for (int c = 0; c < NQ; ++c) {
-          const bool v = 64 * c + 8 * wb + g < q;
+        for (int c = 0; c < (PART ? NQ - 1 : NQ); ++c) {
+          const bool v = PART || 64 * c + 8 * wb + g < q;
           const double av = v ? xa[ks * 4 * qs + 256 * c] : 0.0;
           dmma(ct[c][0], av, b0);
           dmma(ct[c][1], av, b1);
+        }
+        if (PART) {
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const int i = wb + 8 * h2, ob = i >> 1;
+            if (cl0 + 8 * ob >= q) continue;             // warp-uniform: block past q
+            const bool v = cl0 + 8 * ob + g < q;
+            const double av = v ? Qs[4 * (cl0 + 8 * ob + g) + t + ks * 4 * qs] : 0.0;
+            dmma(ct[NQ - 1][h2], av, (i & 1) ? b1 : b0);
+          }
         }
       }
       if (wb < 3) {
@@ -338,11 +368,19 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(const __grid
     const int ld = qp + UP_PB;
     double* out = a.ws + (int64_t)blockIdx.x * ld * UP_PB;
 #pragma unroll
-    for (int c = 0; c < NQ; ++c)
+    for (int c = 0; c < (PART ? NQ - 1 : NQ); ++c)
 #pragma unroll
       for (int n = 0; n < 2; ++n)
 #pragma unroll
         for (int e = 0; e < 2; ++e) out[(int64_t)(8 * n + 2 * t + e) * ld + 64 * c + 8 * wb + g] = ct[c][n][e];
+    if (PART) {
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int i = wb + 8 * h2, ob = i >> 1, n = i & 1;   // chains past q hold zeros (never accumulated)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) out[(int64_t)(8 * n + 2 * t + e) * ld + cl0 + 8 * ob + g] = ct[NQ - 1][h2][e];
+      }
+    }
     if (wb < 3) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) out[(int64_t)(8 * bj + 2 * t + e) * ld + qp + 8 * bi + g] = gq[e];
@@ -436,11 +474,15 @@ size_t update_pass_ws_bytes(int64_t rows, int q) {
 
 template <int NQ, int SR>
 static cudaError_t launch_up(const UpdateArgs& a, int ctas, size_t smem, cudaStream_t s) {
-  {
-    cudaError_t e = smem_attr((const void*)update_pass_kernel<NQ, SR>, smem);
-    if (e != cudaSuccess) return e;
-  }
-  update_pass_kernel<NQ, SR><<<ctas, UP_THREADS, smem, s>>>(a);
+  const bool part = NQ >= 2 && (a.q % 64) != 0;
+  const void* fn = part ? (const void*)update_pass_kernel<NQ, SR, (NQ >= 2)>
+                        : (const void*)update_pass_kernel<NQ, SR, false>;
+  cudaError_t e = smem_attr(fn, smem);
+  if (e != cudaSuccess) return e;
+  if (part)
+    update_pass_kernel<NQ, SR, (NQ >= 2)><<<ctas, UP_THREADS, smem, s>>>(a);
+  else
+    update_pass_kernel<NQ, SR, false><<<ctas, UP_THREADS, smem, s>>>(a);
   return cudaGetLastError();
 }
 
