@@ -42,8 +42,9 @@ constexpr int UP_MAXNS = 8;               // TMA ring stages (at most)
 // SR = rows per sub-panel (16 or 32): 32 halves the per-row cost of the
 // projection group's barriers and reduction, used where the stage still
 // leaves room for a deep ring (narrow bases).
-__host__ __device__ constexpr int up_fixed(int SR) {   // doubles before the ring
-  return UP_PB * CT_LD + 8 * SR * UP_PB + SR * UP_PB + UP_YS * SR * UP_PB;
+// (the narrow path -- bases up to 64 columns -- has no projection partials)
+__host__ __device__ constexpr int up_fixed(int SR, bool narrow = false) {   // doubles before the ring
+  return UP_PB * CT_LD + (narrow ? 0 : 8 * SR * UP_PB) + SR * UP_PB + UP_YS * SR * UP_PB;
 }
 
 // A sub-panel of a QI array with column capacity ldk is SR/4 runs of 4q
@@ -72,15 +73,19 @@ struct alignas(64) UpdateArgs {
 };
 
 static int up_qs(int q) { return (int)round_up(q, 8) + 4; }
-static int up_sr(int q) { return q <= 192 ? 32 : 16; }
+// 64-row sub-panels for bases up to 64 columns: the narrow pass is bound by the
+// per-sub-panel chain (projection -> t -> R^-1 -> hand-over), so twice the rows
+// per chain halve its cost per row (q = 16 at 8M rows: 1.45 -> see DESIGN)
+static int up_sr(int q) { return q <= 64 ? 64 : (q <= 192 ? 32 : 16); }
+static bool up_narrow(int q) { return q <= 64; }
 static int up_stage(int q, int sr) { return sr * up_qs(q) + sr * UP_PB; }
 static int up_stages(int q, int sr) {
-  const int64_t avail = 227 * 1024 - 512 - (int64_t)up_fixed(sr) * 8;
+  const int64_t avail = 227 * 1024 - 512 - (int64_t)up_fixed(sr, up_narrow(q)) * 8;
   int64_t ns = avail / ((int64_t)up_stage(q, sr) * 8);
   return (int)(ns > UP_MAXNS ? UP_MAXNS : ns);
 }
 static size_t update_smem_bytes(int q, int sr) {
-  return ((size_t)up_fixed(sr) + (size_t)up_stages(q, sr) * up_stage(q, sr)) * 8;
+  return ((size_t)up_fixed(sr, up_narrow(q)) + (size_t)up_stages(q, sr) * up_stage(q, sr)) * 8;
 }
 
 // PART: the last 64-column block is partial (q % 64 != 0, NQ >= 2): its work
@@ -95,9 +100,10 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(const __grid
   extern __shared__ __align__(128) double smem[];
   const int q = a.q, p = a.p, qs = a.qs, ns = a.ns;
   const int STG = SR * qs + SR * UP_PB;
+  constexpr bool NARROW = NQ == 1 && SR >= 32;   // bases up to 64 columns
   double* ris = smem;                      // R^-1 as [n][k] (ld 36)
-  double* red = ris + UP_PB * CT_LD;       // 8 projection partials (QI, SR x 16)
-  double* tq = red + 8 * TE;               // t = Q - proj (QI, SR x 16)
+  double* red = ris + UP_PB * CT_LD;       // 8 projection partials (QI, SR x 16); none on the narrow path
+  double* tq = red + (NARROW ? 0 : 8 * TE);   // t = Q - proj (QI, SR x 16)
   double* yring = tq + TE;                 // UP_YS x Q' (QI, SR x 16)
   double* stg = yring + UP_YS * TE;        // ns x [Q_in sub-panel (Q4 quads x qs x 4) | block (Q4 quads x 16 x 4)]
   __shared__ __align__(8) uint64_t full[UP_MAXNS], empty[UP_MAXNS], yfull[UP_YS], yempty[UP_YS];
@@ -160,7 +166,6 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(const __grid
     // sub-panel instead of two, 1 KB of t stores instead of 8 x 4 KB of
     // partials plus their 8-way sum).  Wider bases split the width over the
     // warps (Bt rows in registers) and sum the 8 partials in a fixed order.
-    constexpr bool NARROW = NQ == 1 && SR == 32;
     const int wa = warp;
     double btn[NARROW ? 16 * NQ : 1];   // narrow: Bt(4ks + t, 8(wa%2) + g)
     if constexpr (NARROW) {
@@ -206,23 +211,33 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(const __grid
         for (int e = tid; e < (SR - nrows) * qs; e += 256) Qz[e] = 0.0;
       }
       if (NARROW && !init) {
-        const int rbw = wa >> 1, nbw = wa & 1;
-        // A fragments Q_in(row 8 rbw + g, column 4 ks + t): conflict-free (qs = 4 mod 8)
-        const double* xa = Qs + (2 * rbw + (g >> 2)) * 4 * qs + (g & 3) + 4 * t;
-        double acc[4][2] = {};   // k4 steps round-robin over four accumulator chains
+        // warp wa owns the output blocks (row block (wa / 2) + 4u, column block wa % 2), u < NU
+        constexpr int NU = NARROW ? RB / 4 : 1;
+        const int nbw = wa & 1;
+        double acc[NU][4][2] = {};   // k4 steps round-robin over four accumulator chains per block
 #pragma unroll
         for (int ks = 0; ks < 16; ++ks) {
           if (4 * ks < q) {   // warp-uniform
-            const double av = (4 * ks + t < q) ? xa[16 * ks] : 0.0;
-            dmma(acc[ks & 3], av, btn[ks]);
+#pragma unroll
+            for (int u = 0; u < NU; ++u) {
+              // A fragments Q_in(row 8 rbw + g, column 4 ks + t): conflict-free (qs = 4 mod 8)
+              const int rbw = (wa >> 1) + 4 * u;
+              const double* xa = Qs + (2 * rbw + (g >> 2)) * 4 * qs + (g & 3) + 4 * t;
+              const double av = (4 * ks + t < q) ? xa[16 * ks] : 0.0;
+              dmma(acc[u][ks & 3], av, btn[ks]);
+            }
           }
         }
-        const int row = 8 * rbw + g;
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int col = 8 * nbw + 2 * t + e;
-          const int off = (row >> 2) * 4 * UP_PB + 4 * col + (row & 3);
-          tq[off] = (col < p && row < nrows) ? Ys[off] - ((acc[0][e] + acc[1][e]) + (acc[2][e] + acc[3][e])) : 0.0;
+        for (int u = 0; u < NU; ++u) {
+          const int row = 8 * ((wa >> 1) + 4 * u) + g;
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int col = 8 * nbw + 2 * t + e;
+            const int off = (row >> 2) * 4 * UP_PB + 4 * col + (row & 3);
+            tq[off] = (col < p && row < nrows)
+                          ? Ys[off] - ((acc[u][0][e] + acc[u][1][e]) + (acc[u][2][e] + acc[u][3][e])) : 0.0;
+          }
         }
         asm volatile("bar.sync 2, 256;" ::: "memory");
       }
@@ -270,9 +285,9 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(const __grid
       }
       if (!init) {
         if (j >= UP_YS) mbar_wait(&yempty[ys], yph ^ 1);
-        if (wa < 2 * RB) {
+        for (int qb = wa; qb < 2 * RB; qb += 8) {
           // Q' block (rb, nb) = t(rows 8rb.., :) R^-1(:, cols 8nb..); R^-1 upper: K < 8(nb+1)
-          const int rb = wa >> 1, nb = wa & 1;
+          const int rb = qb >> 1, nb = qb & 1;
           const int r = 8 * rb + g;
           const double* tp = tq + (r >> 2) * 4 * UP_PB + (r & 3) + 4 * t;
           const double* rp = ris + (8 * nb + g) * CT_LD + t;
@@ -510,7 +525,7 @@ cudaError_t update_pass_launch(const double* Qin, int64_t ldqin, int q, const do
   const int ctas = update_ctas(rows);
   cudaError_t e;
   switch ((q + 63) / 64) {
-    case 1: e = launch_up<1, 32>(a, ctas, smem, s); break;
+    case 1: e = launch_up<1, 64>(a, ctas, smem, s); break;
     case 2: e = launch_up<2, 32>(a, ctas, smem, s); break;
     case 3: e = (sr == 32) ? launch_up<3, 32>(a, ctas, smem, s) : launch_up<3, 16>(a, ctas, smem, s); break;
     case 4: e = launch_up<4, 16>(a, ctas, smem, s); break;
