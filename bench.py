@@ -174,7 +174,9 @@ def run_reference():
     else:
         x = host_config(ARGS.config, m=rows, seed=SEED)
         fn = {"s_chol_qr3": co.s_chol_qr3, "chol_qr2": co.chol_qr2, "rs_chol_qr": co.rs_chol_qr}[cfg["algo"]]
-        for _ in range(ARGS.warmup):
+        # NumPy / OpenBLAS need one warm-up call (thread pool, page faults); more
+        # would only lengthen the run (each call is a bounded ~10-20 s sample)
+        for _ in range(min(ARGS.warmup, 1)):
             fn(x)
         t0 = time.perf_counter()
         for _ in range(ARGS.steps):
