@@ -42,9 +42,10 @@ constexpr int UP_MAXNS = 8;               // TMA ring stages (at most)
 // SR = rows per sub-panel (16 or 32): 32 halves the per-row cost of the
 // projection group's barriers and reduction, used where the stage still
 // leaves room for a deep ring (narrow bases).
-// (the narrow path -- bases up to 64 columns -- has no projection partials)
-__host__ __device__ constexpr int up_fixed(int SR, bool narrow = false) {   // doubles before the ring
-  return UP_PB * CT_LD + (narrow ? 0 : 8 * SR * UP_PB) + SR * UP_PB + UP_YS * SR * UP_PB;
+// (the narrow path -- bases up to 64 columns -- has no projection partials;
+// the two-team path has two t buffers)
+__host__ __device__ constexpr int up_fixed(int SR, bool narrow = false, bool teams = false) {   // doubles before the ring
+  return UP_PB * CT_LD + (narrow ? 0 : 8 * SR * UP_PB) + (teams ? 2 : 1) * SR * UP_PB + UP_YS * SR * UP_PB;
 }
 
 // A sub-panel of a QI array with column capacity ldk is SR/4 runs of 4q
@@ -79,19 +80,32 @@ static int up_qs(int q) { return (int)round_up(q, 8) + 4; }
 static int up_sr(int q) { return q <= 64 ? 64 : (q <= 192 ? 32 : 16); }
 static bool up_narrow(int q) { return q <= 64; }
 static int up_stage(int q, int sr) { return sr * up_qs(q) + sr * UP_PB; }
-static int up_stages(int q, int sr) {
-  const int64_t avail = 227 * 1024 - 512 - (int64_t)up_fixed(sr, up_narrow(q)) * 8;
+static int up_stages_with(int q, int sr, bool teams) {
+  const int64_t avail = 227 * 1024 - 512 - (int64_t)up_fixed(sr, up_narrow(q), teams) * 8;
   int64_t ns = avail / ((int64_t)up_stage(q, sr) * 8);
-  return (int)(ns > UP_MAXNS ? UP_MAXNS : ns);
+  if (ns > UP_MAXNS) ns = UP_MAXNS;
+  // Two projection teams take alternate sub-panels, so each must see every
+  // phase of the stages it waits on: an even stage count keeps each stage with
+  // one team (with an odd count a team would skip a phase of a stage and read
+  // it a phase early through the parity wait).
+  if (teams) ns &= ~int64_t(1);
+  return (int)ns;
 }
+// Two projection teams where they fit with four stages (65 <= q <= 144 at 32-row
+// sub-panels): with two stages the teams starve (q = 160: 3.63 -> 4.58 ms).
+static bool up_teams_q(int q, int sr) {
+  const int nq = (q + 63) / 64;
+  return sr == 32 && (nq == 2 || nq == 3) && up_stages_with(q, sr, true) >= 4;
+}
+static int up_stages(int q, int sr) { return up_stages_with(q, sr, up_teams_q(q, sr)); }
 static size_t update_smem_bytes(int q, int sr) {
-  return ((size_t)up_fixed(sr, up_narrow(q)) + (size_t)up_stages(q, sr) * up_stage(q, sr)) * 8;
+  return ((size_t)up_fixed(sr, up_narrow(q), up_teams_q(q, sr)) + (size_t)up_stages(q, sr) * up_stage(q, sr)) * 8;
 }
 
 // PART: the last 64-column block is partial (q % 64 != 0, NQ >= 2): its work
 // is split by k4 step (projection) and by output block (cross Gram) so that it
 // spreads over the four SM sub-partitions and the part past q is skipped.
-template <int NQ, int SR, bool PART>
+template <int NQ, int SR, bool PART, bool TEAMS>
 __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(const __grid_constant__ UpdateArgs a) {
   if (a.gate != nullptr && *a.gate != 0) return;   // gated off
   constexpr int RB = SR / 8;        // 8-row blocks per sub-panel
@@ -101,10 +115,13 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(const __grid
   const int q = a.q, p = a.p, qs = a.qs, ns = a.ns;
   const int STG = SR * qs + SR * UP_PB;
   constexpr bool NARROW = NQ == 1 && SR >= 32;   // bases up to 64 columns
+  // 65 <= q <= 192: two independent projection teams of 4 warps take alternate
+  // sub-panels, so one team's reduction / R^-1 / hand-over overlaps the other
+  // team's DMMAs (one team of 8 left the cross-Gram warps waiting on Q')
   double* ris = smem;                      // R^-1 as [n][k] (ld 36)
   double* red = ris + UP_PB * CT_LD;       // 8 projection partials (QI, SR x 16); none on the narrow path
-  double* tq = red + (NARROW ? 0 : 8 * TE);   // t = Q - proj (QI, SR x 16)
-  double* yring = tq + TE;                 // UP_YS x Q' (QI, SR x 16)
+  double* tq = red + (NARROW ? 0 : 8 * TE);   // t = Q - proj (QI, SR x 16), one per team
+  double* yring = tq + (TEAMS ? 2 : 1) * TE;  // UP_YS x Q' (QI, SR x 16)
   double* stg = yring + UP_YS * TE;        // ns x [Q_in sub-panel (Q4 quads x qs x 4) | block (Q4 quads x 16 x 4)]
   __shared__ __align__(8) uint64_t full[UP_MAXNS], empty[UP_MAXNS], yfull[UP_YS], yempty[UP_YS];
 
@@ -116,7 +133,7 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(const __grid
 
   if (tid == 0) {
     for (int s = 0; s < ns; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 8); }
-    for (int s = 0; s < UP_YS; ++s) { mbar_init(&yfull[s], 256); mbar_init(&yempty[s], 8); }
+    for (int s = 0; s < UP_YS; ++s) { mbar_init(&yfull[s], TEAMS ? 128 : 256); mbar_init(&yempty[s], 8); }
     fence_mbar_init();
   }
   if (!init) {
@@ -156,7 +173,111 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(const __grid
 
   int s = 0, ys = 0;
   uint32_t ph = 0, yph = 0;
-  if (warp < 8) {
+  if (TEAMS && warp < 8) {
+    // ================= projection group, two teams of 4 warps (alternate sub-panels)
+    const int team = warp >> 2, wt = warp & 3, tt = tid & 127;
+    // warp wt of a team owns the 16 columns [64c + 16wt, +16) of every full block
+    // (k4 steps h = 0..3); a partial last block is split by k4 step, step wt + 4h,
+    // so its valid steps land evenly on the four sub-partitions.
+    auto kcolt = [&](int c, int h) {
+      return (PART && c == NQ - 1) ? 64 * c + 4 * (wt + 4 * h) : 64 * c + 16 * wt + 4 * h;
+    };
+    double btt[NQ][4][2];
+#pragma unroll
+    for (int c = 0; c < NQ; ++c)
+#pragma unroll
+      for (int h = 0; h < 4; ++h)
+#pragma unroll
+        for (int nb = 0; nb < 2; ++nb) {
+          const int kk = kcolt(c, h) + t, n = 8 * nb + g;
+          btt[c][h][nb] = (!init && kk < q && n < p) ? a.Bt[(int64_t)n * a.ldbt + kk] : 0.0;
+        }
+    double* tqt = tq + team * TE;
+    const int bar = 2 + team;
+    for (int64_t j = team; j < mine; j += 2) {
+      const int sj = (int)(j % ns), ysj = (int)(j % UP_YS);
+      const uint32_t phj = (uint32_t)((j / ns) & 1), yphj = (uint32_t)((j / UP_YS) & 1);
+      const int64_t r0 = (blockIdx.x + j * gridDim.x) * SR;
+      const int nrows = (int)imin64(SR, a.rows - r0);
+      mbar_wait(&full[sj], phj);
+      const double* Qs = stg + sj * STG;
+      const double* Ys = Qs + SR * qs;
+      double* yd = yring + ysj * TE;
+      if (nrows < SR) {
+        double* Qz = stg + sj * STG + nrows * qs;
+        for (int e = tt; e < (SR - nrows) * qs; e += 128) Qz[e] = 0.0;
+      }
+      if (!init) {
+        double pr[RB][2][2];
+#pragma unroll
+        for (int rb = 0; rb < RB; ++rb)
+#pragma unroll
+          for (int nb = 0; nb < 2; ++nb) { pr[rb][nb][0] = 0.0; pr[rb][nb][1] = 0.0; }
+        const double* xa = Qs + (g >> 2) * 4 * qs + (g & 3) + 4 * t;   // row g, column t
+#pragma unroll
+        for (int c = 0; c < NQ; ++c)
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            const int kc = kcolt(c, h);
+            if (PART && c == NQ - 1 && kc >= q) continue;   // warp-uniform
+            const bool kv = kc + t < q;
+            double av[RB];
+#pragma unroll
+            for (int rb = 0; rb < RB; ++rb) av[rb] = kv ? xa[4 * kc + rb * 8 * qs] : 0.0;
+#pragma unroll
+            for (int rb = 0; rb < RB; ++rb) {
+              dmma(pr[rb][0], av[rb], btt[c][h][0]);
+              dmma(pr[rb][1], av[rb], btt[c][h][1]);
+            }
+          }
+#pragma unroll
+        for (int rb = 0; rb < RB; ++rb)
+#pragma unroll
+          for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+              red[warp * TE + (2 * rb + (g >> 2)) * 4 * UP_PB + 4 * (8 * nb + 2 * t + e) + (g & 3)] = pr[rb][nb][e];
+        asm volatile("bar.sync %0, 128;" ::"r"(bar) : "memory");
+        for (int e = tt; e < TE; e += 128) {
+          const int row = 4 * (e >> 6) + (e & 3), col = (e >> 2) & 15;
+          double sum = 0.0;
+#pragma unroll
+          for (int w = 0; w < 4; ++w) sum += red[(4 * team + w) * TE + e];
+          tqt[e] = (col < p && row < nrows) ? Ys[e] - sum : 0.0;
+        }
+        asm volatile("bar.sync %0, 128;" ::"r"(bar) : "memory");
+        if (j >= UP_YS) mbar_wait(&yempty[ysj], yphj ^ 1);
+        for (int qb = wt; qb < 2 * RB; qb += 4) {
+          const int rb = qb >> 1, nb = qb & 1;
+          const int r = 8 * rb + g;
+          const double* tp = tqt + (r >> 2) * 4 * UP_PB + (r & 3) + 4 * t;
+          const double* rp = ris + (8 * nb + g) * CT_LD + t;
+          double c2[2] = {0.0, 0.0};
+          if (nb == 0) {
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) dmma(c2, tp[16 * ks], rp[4 * ks]);
+          } else {
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) dmma(c2, tp[16 * ks], rp[4 * ks]);
+          }
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int cc = 8 * nb + 2 * t + e;
+            const bool v = cc < p;
+            yd[(r >> 2) * 4 * UP_PB + 4 * cc + (r & 3)] = v ? c2[e] : 0.0;
+            if (v && r < nrows) a.Qo[((r0 + r) >> 2) * 4 * a.ldqo + 4 * cc + (r & 3)] = c2[e];
+          }
+        }
+      } else {
+        if (j >= UP_YS) mbar_wait(&yempty[ysj], yphj ^ 1);
+        for (int e = tt; e < TE; e += 128) {
+          const int row = 4 * (e >> 6) + (e & 3), col = (e >> 2) & 15;
+          yd[e] = (col < p && row < nrows) ? Ys[e] : 0.0;
+        }
+      }
+      mbar_arrive(&yfull[ysj]);   // every thread of the team: its own stores are released
+    }
+  } else if (warp < 8) {
     // ================= projection group
     // Bases up to 64 columns ("narrow", 32-row sub-panels): warp wa owns the
     // output block (rows 8(wa/2).., columns 8(wa%2)..) of proj = Q_in Bt over
@@ -487,18 +608,26 @@ size_t update_pass_ws_bytes(int64_t rows, int q) {
   return (size_t)update_ctas(rows) * (qp + UP_PB) * UP_PB * sizeof(double) + 256;
 }
 
-template <int NQ, int SR>
-static cudaError_t launch_up(const UpdateArgs& a, int ctas, size_t smem, cudaStream_t s) {
+template <int NQ, int SR, bool TEAMS>
+static cudaError_t launch_up_t(const UpdateArgs& a, int ctas, size_t smem, cudaStream_t s) {
   const bool part = NQ >= 2 && (a.q % 64) != 0;
-  const void* fn = part ? (const void*)update_pass_kernel<NQ, SR, (NQ >= 2)>
-                        : (const void*)update_pass_kernel<NQ, SR, false>;
+  const void* fn = part ? (const void*)update_pass_kernel<NQ, SR, (NQ >= 2), TEAMS>
+                        : (const void*)update_pass_kernel<NQ, SR, false, TEAMS>;
   cudaError_t e = smem_attr(fn, smem);
   if (e != cudaSuccess) return e;
   if (part)
-    update_pass_kernel<NQ, SR, (NQ >= 2)><<<ctas, UP_THREADS, smem, s>>>(a);
+    update_pass_kernel<NQ, SR, (NQ >= 2), TEAMS><<<ctas, UP_THREADS, smem, s>>>(a);
   else
-    update_pass_kernel<NQ, SR, false><<<ctas, UP_THREADS, smem, s>>>(a);
+    update_pass_kernel<NQ, SR, false, TEAMS><<<ctas, UP_THREADS, smem, s>>>(a);
   return cudaGetLastError();
+}
+
+template <int NQ, int SR>
+static cudaError_t launch_up(const UpdateArgs& a, int ctas, size_t smem, cudaStream_t s) {
+  if constexpr (SR == 32 && (NQ == 2 || NQ == 3)) {
+    if (up_teams_q(a.q, SR)) return launch_up_t<NQ, SR, true>(a, ctas, smem, s);
+  }
+  return launch_up_t<NQ, SR, false>(a, ctas, smem, s);
 }
 
 cudaError_t update_pass_launch(const double* Qin, int64_t ldqin, int q, const double* Qb, int64_t ldqb, double* Qo,
