@@ -453,6 +453,18 @@ def run_ours():
         streamed()
         barrier()
         e2e_ms = max_over_ranks((time.perf_counter() - t0) / n_str * 1e3)
+        # the PCIe floor of this run: one H2D of the input and one D2H of Q at
+        # once, through the same pinned buffers (the e2e step moves both)
+        qdev_probe = torch.empty_like(dev_in[1])
+        torch.cuda.synchronize()
+        p0 = time.perf_counter()
+        with torch.cuda.stream(s_in):
+            dev_in[0].copy_(host, non_blocking=True)
+        with torch.cuda.stream(s_out):
+            qhost.copy_(qdev_probe, non_blocking=True)
+        torch.cuda.synchronize()
+        floor_ms = (time.perf_counter() - p0) * 1e3
+        del qdev_probe
         h2d = (hi - lo) * k * 8
         e2e = {"value": m * k / (e2e_ms * 1e-3), "unit": "rows*cols/s", "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": (h2d + k * k * 8) * world,
@@ -460,7 +472,10 @@ def run_ours():
                "schedule": f"{n_str} calls streamed: H2D of call i+1 and D2H of call i-1 overlap call i "
                            "(copy streams); ms_per_step = total / calls",
                "serial": {"value": m * k / (ser_ms * 1e-3), "ms_per_step": ser_ms,
-                          "schedule": "one call at a time: H2D, run, D2H, synchronize"}}
+                          "schedule": "one call at a time: H2D, run, D2H, synchronize"},
+               "pcie_floor_ms_per_step": floor_ms,
+               "pcie_floor_note": "one H2D of the input concurrent with one D2H of Q through the same pinned "
+                                  "buffers, measured in this run: the bound of a streamed call"}
 
     # ---- CPU baseline (rank 0, N = 1 only)
     cpu = None
