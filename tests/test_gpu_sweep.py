@@ -19,6 +19,9 @@ import parity as P
 pytestmark = pytest.mark.gpu
 
 N_CASES = int(os.environ.get("CQR_SWEEP", "48"))
+# decision tallies over the sweep (printed by test_zz_sweep_summary)
+STATS = {"cases": 0, "decisions": 0, "shifted": 0, "parted_rounding": 0, "replayed": 0, "replayed_shifted": 0,
+         "replay_rounding": 0, "both_raised": 0}
 ALGOS = ("rs_chol_qr", "s_chol_qr3", "is_chol_qr", "chol_qr2", "chol_qr_update")
 
 
@@ -65,6 +68,9 @@ def _run_both(algo, x, cq, co):
         # every pass's decision against the oracle's decision stage on the device's own Gramian
         rep = P.replay_iterated(trace, mine, co.default_cfg(), "rs")
         assert rep.passes == mine.iterations, rep
+        STATS["replayed"] += rep.passes
+        STATS["replayed_shifted"] += rep.shifted
+        STATS["replay_rounding"] += rep.fragile
     return mine, ref, my_exc, ref_exc
 
 
@@ -74,6 +80,7 @@ def test_sweep_single(case):
     from oracle import cholqr_oracle as co
 
     i, algo, m, k, cond = case
+    STATS["cases"] += 1
     if algo == "chol_qr_update":
         _update_case(i, m, k, cond)
         return
@@ -81,15 +88,21 @@ def test_sweep_single(case):
     mine, ref, my_exc, ref_exc = _run_both(algo, x, cq, co)
     if my_exc is not None or ref_exc is not None:
         # both raise, or the deciding pivot sits at the rounding level
-        P.compare_single(mine, my_exc, ref, ref_exc, k)
+        if P.compare_single(mine, my_exc, ref, ref_exc, k):
+            STATS["both_raised"] += 1
+        else:
+            STATS["parted_rounding"] += 1
         return
     np.testing.assert_array_equal(np.tril(mine.r, -1), 0.0)
     diverged = None
     if algo in ("rs_chol_qr", "is_chol_qr"):
         tol = cq.AlgoConfig().effective_tol(k)
         cmp = P.compare_iterated(mine, ref, k, tol)
+        STATS["decisions"] += cmp.decisions
+        STATS["shifted"] += cmp.shifted
         if not cmp.full:
             diverged = tol
+            STATS["parted_rounding"] += 1
         assert mine.success == ref.success or diverged is not None
     if algo in ("chol_qr2", "s_chol_qr3"):
         # fixed schedules: a pass whose pivots sit at the rounding level (no
@@ -135,6 +148,9 @@ def _update_case(i, m, k, cond):
     if mine is not None:
         rep = P.replay_iterated(trace, mine, co.default_cfg(), "update")
         assert rep.passes == mine.iterations, rep
+        STATS["replayed"] += rep.passes
+        STATS["replayed_shifted"] += rep.shifted
+        STATS["replay_rounding"] += rep.fragile
     if my_exc is not None or ref_exc is not None:
         assert (my_exc is None) == (ref_exc is None), (my_exc, ref_exc)
         return
@@ -142,6 +158,9 @@ def _update_case(i, m, k, cond):
     np.testing.assert_array_equal(mine.r[k:, :k], 0.0)
     tol = cq.AlgoConfig().effective_tol(p)
     cmp = P.compare_iterated(mine, ref, p, tol)
+    STATS["decisions"] += cmp.decisions
+    STATS["shifted"] += cmp.shifted
+    STATS["parted_rounding"] += 0 if cmp.full else 1
     diverged = None if cmp.full else tol
     if mine.success and ref.success:
         qd = mine.q.to_numpy()
@@ -172,3 +191,18 @@ WIDE = _wide_cases()
 @pytest.mark.parametrize("case", WIDE, ids=[f"{c[0]}-{c[1]}-{c[2]}x{c[3]}-c{c[4]:g}" for c in WIDE])
 def test_sweep_wide(case):
     test_sweep_single(case)
+
+
+def test_zz_sweep_summary():
+    """Tallies of the sweep above (runs last in this file): decisions compared
+    along the trajectories, trajectories that parted at a rounding-level
+    decision, and passes replayed on the device's own Gramians."""
+    print("sweep decision tallies:", STATS)
+    out = os.environ.get("CQR_SWEEP_STATS")
+    if out:
+        import json
+
+        with open(out, "w") as fh:
+            json.dump(STATS, fh)
+    if STATS["cases"]:
+        assert STATS["replayed"] > 0
