@@ -71,14 +71,27 @@ def cross_gram_host(left, right):
     return g.cpu().numpy().T.copy()
 
 
+# cqr_factor_status as a NumPy record (include/cqr.h; offsets checked against
+# the ctypes struct in tests/test_abi_cpu.py)
+_STATUS_DTYPE = np.dtype({
+    "names": [n for n, _ in _lib.FactorStatus._fields_],
+    "formats": [np.int32 if t is ctypes.c_int32 else np.float64 for _, t in _lib.FactorStatus._fields_],
+    "offsets": [getattr(_lib.FactorStatus, n).offset for n, _ in _lib.FactorStatus._fields_],
+    "itemsize": ctypes.sizeof(_lib.FactorStatus)})
+
+
 class PassStatus:
     """Host copy of one cqr_factor_status plus the shifts it appended."""
 
-    def __init__(self, raw, shifts):
-        st = _lib.FactorStatus.from_buffer_copy(raw[: ctypes.sizeof(_lib.FactorStatus)])
-        for name, _ in _lib.FactorStatus._fields_:
-            setattr(self, name, getattr(st, name))
-        self.shifts = [float(s) for s in shifts[: max(st.n_shifts, 0)]]
+    __slots__ = tuple(n for n, _ in _lib.FactorStatus._fields_) + ("shifts",)
+
+    def __init__(self, raw):
+        """raw: the slot's pinned bytes (uint8 NumPy view): status record, then shifts."""
+        rec = raw[:_STATUS_DTYPE.itemsize].view(_STATUS_DTYPE)[0].item()
+        for name, v in zip(_STATUS_DTYPE.names, rec):
+            object.__setattr__(self, name, v)
+        n = max(self.n_shifts, 0)
+        self.shifts = raw[STATUS_BYTES:STATUS_BYTES + 8 * n].view(np.float64).tolist()
 
 
 class Engine:
@@ -103,12 +116,16 @@ class Engine:
         # seven allocations and three fill kernels (short calls, config 1, are
         # host bound between calls).  Kernels never write the zero padding of
         # Rk / Rinv, so only Racc (and the update blocks) need resetting.
+        # the stream this run enqueues on (a call runs on one stream; torch's
+        # current_stream() costs ~8 us of host time per query)
+        self._stream = torch.cuda.current_stream(cx.device)
         free = cx.engine_pool.get(self._key)
-        if free:
+        reused = bool(free)
+        if reused:
             bufs, ev = free.pop()
-            torch.cuda.current_stream(cx.device).wait_event(ev)   # released on another stream
+            self._stream.wait_event(ev)   # released on another stream
             (self.G, self.Rk, self.Rinv, self.Racc, self._racc0, self.stat_all, self.stat_host_all, self.fws,
-             self.B, self.Bt, self._xch) = bufs
+             self.B, self.Bt, self._xch, self._fcfg, self._slot_ev) = bufs
             self.Racc.copy_(self._racc0)
             if q:
                 self.B.zero_()
@@ -136,6 +153,21 @@ class Engine:
                 self.B = self.Bt = None
         self.ldr = self.Rk.shape[1]
         self.stat, self.stat_host = self.stat_all[0], self.stat_host_all[0]
+        self._stat_np = self.stat_host_all.numpy()   # (nslots, bytes) view of the pinned slots
+        # per-slot launch config (static fields set once; the kernel writes the status
+        # and shifts straight into the slot's pinned host buffer, no D2H copy) and
+        # per-slot completion events, reused across the run's factor calls
+        # (kept with the pooled buffers: the pinned slots they point at go with them)
+        if not reused:
+            self._fcfg = []
+            for slot in range(self.nslots):
+                hp = self.stat_host_all[slot].data_ptr()
+                self._fcfg.append(_lib.FactorConfig(accumulate=1, status_mirror=hp, shifts_mirror=hp + STATUS_BYTES))
+            self._slot_ev = [torch.cuda.Event() for _ in range(self.nslots)]
+        for fc in self._fcfg:
+            fc.unit_roundoff = cfg.unit_roundoff
+            fc.shift_escalation = cfg.shift_escalation
+            fc.max_shift_attempts = cfg.max_shift_attempts
 
     def __del__(self):
         try:
@@ -143,11 +175,11 @@ class Engine:
                 self._r_pending[2].synchronize()
                 self.cx.release_pinned(self._r_pending[0])
             ev = torch.cuda.Event()
-            ev.record(torch.cuda.current_stream(self.cx.device))
+            ev.record(self._stream)
             free = self.cx.engine_pool.setdefault(self._key, [])
             if len(free) < 2:
                 free.append(((self.G, self.Rk, self.Rinv, self.Racc, self._racc0, self.stat_all, self.stat_host_all,
-                              self.fws, self.B, self.Bt, self._xch), ev))
+                              self.fws, self.B, self.Bt, self._xch, self._fcfg, self._slot_ev), ev))
             else:
                 self.cx.release_pinned(self.stat_host_all)
         except Exception:   # interpreter shutdown
@@ -172,14 +204,11 @@ class Engine:
         for h in handles:
             ev = self._stat_ev[h]
             if ev is None:
-                torch.cuda.current_stream(self.cx.device).synchronize()
+                self._stream.synchronize()
             else:
                 ev.synchronize()
-        out = []
-        for h in handles:
-            raw = self.stat_host_all[h].numpy()
-            out.append(PassStatus(raw.tobytes(), raw[STATUS_BYTES:].view(np.float64)))
-        return out
+        stat = self._stat_np
+        return [PassStatus(stat[h].copy()) for h in handles]
 
     def factor_async(self, policy, m_global, width, *, tol=0.0, check_tol=False, stop=False, update_b=False,
                      fixed_shift=0.0, gate=None, gate_slot=None, est_tol=1e-2, est_max_iter=100):
@@ -194,15 +223,18 @@ class Engine:
             cx.trace.append(dict(policy=policy, m_global=m_global, width=width, tol=tol, check_tol=check_tol,
                                  stop=stop, fixed_shift=fixed_shift, G=self.G.clone(),
                                  Bt=self.Bt.clone() if (self.Bt is not None and self.q) else None))
-        fc = _lib.FactorConfig(
-            policy=policy, shift_width=width, m_global=m_global, unit_roundoff=cfg.unit_roundoff,
-            shift_escalation=cfg.shift_escalation, max_shift_attempts=cfg.max_shift_attempts,
-            check_tol=1 if check_tol else 0, tol=tol, stop=1 if stop else 0, accumulate=1,
-            update_b=1 if update_b else 0, est_max_iter=est_max_iter, est_tol=est_tol, fixed_shift=fixed_shift, gate=gate,
-            # the kernel writes the status and shifts straight into this slot's
-            # pinned host buffer (no D2H copy on the stream)
-            status_mirror=self.stat_host_all[slot].data_ptr(),
-            shifts_mirror=self.stat_host_all[slot].data_ptr() + STATUS_BYTES)
+        fc = self._fcfg[slot]
+        fc.policy = policy
+        fc.shift_width = width
+        fc.m_global = m_global
+        fc.check_tol = 1 if check_tol else 0
+        fc.tol = tol
+        fc.stop = 1 if stop else 0
+        fc.update_b = 1 if update_b else 0
+        fc.est_max_iter = est_max_iter
+        fc.est_tol = est_tol
+        fc.fixed_shift = fixed_shift
+        fc.gate = gate
         bt = self.Bt.data_ptr() if self.Bt is not None else None
         b = self.B.data_ptr() if self.B is not None else None
         base = self.stat_all[slot].data_ptr()
@@ -215,8 +247,8 @@ class Engine:
             cx.timer.stop("factor", t0, (self.k,),
                           gate=self.stat_all[gate_slot] if gate_slot is not None else None)
         cx.launches += 2
-        ev = torch.cuda.Event()
-        ev.record(torch.cuda.current_stream(cx.device))
+        ev = self._slot_ev[slot]
+        ev.record(self._stream)
         self._stat_ev[slot] = ev
         return slot
 
@@ -294,7 +326,7 @@ class Engine:
         try:
             view = buf.view(torch.float64)[: t.numel()].view(t.shape)
             self._store_host(t, buf)
-            torch.cuda.current_stream(self.cx.device).synchronize()
+            self._stream.synchronize()
             return view.numpy().T.copy()
         finally:
             self.cx.release_pinned(buf)
@@ -310,7 +342,7 @@ class Engine:
         view = buf.view(torch.float64)[: t.numel()].view(t.shape)
         self._store_host(t, buf)
         ev = torch.cuda.Event()
-        ev.record(torch.cuda.current_stream(self.cx.device))
+        ev.record(self._stream)
         self._r_pending = (buf, view, ev)
 
     def r_host(self):
