@@ -222,9 +222,15 @@ int cqr_debug_factor_profile(unsigned long long* out16);
 /* Diagnostics: 1 (default) = the update pass stages narrow sub-panels with one
  * TMA tensor copy each; 0 = per-row-quad bulk copies only (comparisons). */
 void cqr_debug_update_tma(int on);
-/* Diagnostics: 1 = the blocked Cholesky in bands of 32 pivots with a rank-32
- * update between bands; 0 (default) = one lookahead chain over all block steps. */
+/* Diagnostics: 1 (default) = the blocked Cholesky in bands of 32 pivots with a
+ * rank-32 update between bands; 0 = one lookahead chain over all block steps. */
 int cqr_debug_factor_banded(int on);
+/* 1 (default): 128 < k <= 256 factors on a thread-block cluster of ceil(k/32)
+   CTAs, one 32-row band each; 0: the single-CTA path (for A/B comparisons). */
+int cqr_debug_factor_cluster(int on);
+/* Diagnostics: globaltimer stamps (ns) of the band-cluster path's last attempt,
+ * [band][event] (HOST array of 64; synchronous). */
+int cqr_debug_factor_cluster_profile(unsigned long long* out64);
 int cqr_factor(const cqr_factor_config* cfg, int k, const double* G, int ldg, const double* Bt, int ldbt, int q,
                double* Rk, double* Rinv, int ldr, double* Racc, double* B, int ldb, double* shifts,
                cqr_factor_status* status, void* ws, size_t ws_bytes, void* stream);

@@ -272,6 +272,10 @@ int cqr_debug_factor_profile(unsigned long long* out16) { return cqr::factor_pro
 void cqr_debug_update_tma(int on) { cqr::set_update_tma(on); }
 int cqr_debug_factor_banded(int on) { return cqr::factor_set_banded(on); }
 
+int cqr_debug_factor_cluster(int on) { return cqr::factor_set_cluster(on); }
+
+int cqr_debug_factor_cluster_profile(unsigned long long* out64) { return cqr::factor_cluster_profile(out64); }
+
 size_t cqr_factor_workspace_bytes(int k) { return k > 0 ? cqr::factor_workspace_bytes(k) : 256; }
 
 int cqr_factor(const cqr_factor_config* cfg, int k, const double* G, int ldg, const double* Bt, int ldbt, int q,

@@ -109,11 +109,14 @@ struct FactorArgs {
   int spec; unsigned epoch;
   int bt_stage;    // update policy: Bt staged in shared memory after the work area
   double* Rk1; int ldr1; double* W1; double* shifts1; double* pub;
+  int ncl;         // CTAs per attempt group (band-cluster path, 128 < k <= 256), else 1
 };
 cudaError_t factor_launch(FactorArgs& a, cudaStream_t stream);
 size_t factor_workspace_bytes(int k);
 int factor_profile(unsigned long long* out);
 int factor_set_banded(int on);
+int factor_set_cluster(int on);
+int factor_cluster_profile(unsigned long long* out64);
 
 // ------------------------------------------------------------- standalone k x k kernels (cqr_small.cu)
 cudaError_t tri_inverse_launch(const double* R, int ldr, int n, double* X, int ldx, cudaStream_t s);

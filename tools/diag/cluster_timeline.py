@@ -1,0 +1,51 @@
+"""Per-band timeline of the band-cluster factor (group 0, last attempt):
+globaltimer stamps per band relative to band 0's start (us), plus the
+single-CTA phase counters of band 0 (per-step cycles) and the power
+iteration count of the last estimate."""
+import ctypes
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+import torch  # noqa: E402
+
+import paper_2507_07788_b200 as cq  # noqa: E402
+from paper_2507_07788_b200._device import ctx  # noqa: E402
+from paper_2507_07788_b200._engine import Engine  # noqa: E402
+from tools.diag.cluster_ab import POL, gramian  # noqa: E402
+
+EV = ["start", "loaded", "upstream_in", "updated", "factored", "published", "agreed"]
+
+
+def timeline(k, policy, kind):
+    cx = ctx()
+    cx.lib.cqr_debug_factor_cluster(1)
+    eng = Engine(k, cq.AlgoConfig())
+    g = torch.from_numpy(gramian(k, kind, 1)).to(cx.device)
+    for _ in range(3):
+        eng.G.copy_(g)
+        st = eng.factor(POL[policy], 10 ** 6, k)
+    buf = (ctypes.c_ulonglong * 64)()
+    cx.lib.cqr_debug_factor_cluster_profile(buf)
+    fp = (ctypes.c_ulonglong * 16)()
+    cx.lib.cqr_debug_factor_profile(fp)
+    C = (k + 31) // 32
+    t0 = buf[0]
+    bands = []
+    for r in range(C):
+        row = {}
+        for e, name in enumerate(EV):
+            v = buf[8 * r + e]
+            row[name] = round((v - t0) / 1e3, 2) if v >= t0 and v - t0 < 10 ** 7 else None
+        bands.append(row)
+    steps = max(int(fp[11]), 1)
+    print(json.dumps({"k": k, "policy": policy, "kind": kind, "code": st.code, "est_iters": int(fp[8]),
+                      "band0_steps": int(fp[11]), "panel_cyc": fp[9] // steps, "update_cyc": fp[10] // steps,
+                      "diag_cyc": fp[12] // steps, "bands": bands}), flush=True)
+
+
+if __name__ == "__main__":
+    for k, pol, kind in ((256, "plain", "spd"), (256, "shift_once", "illcond"), (192, "plain", "spd"),
+                         (160, "plain", "spd")):
+        timeline(k, pol, kind)
