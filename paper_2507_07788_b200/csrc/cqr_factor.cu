@@ -47,8 +47,7 @@ constexpr int FK_SMEM_K = 128;   // whole packed triangle in shared memory
 constexpr int FK_BIG_K = 256;    // panel + shared trailing matrix
 constexpr int FK_MAX_K = 2048;
 // FactorArgs.pub (64 doubles): [0] group 0's outcome flag, [1..3] its plain
-// margin / pivot; the band flags of the two groups; group 1's status record
-constexpr int PUB_BFLAGS = 8;    // 2 x 8 band flags (u64)
+// margin / pivot; group 1's status record
 constexpr int PUB_ST1 = 24;      // cqr_factor_status of the speculative group (96 bytes)
 
 __host__ __device__ __forceinline__ int64_t pk(int i, int c) { return (int64_t)c * (c + 1) / 2 + i; }
@@ -116,12 +115,11 @@ struct FState {
   unsigned long long spec_done;
   int aborted;
   // band-cluster path (csize > 1): this CTA's rank = its 32-row band, the
-  // group's band flags (global, epoch-tagged), the attempt sequence number
+  // attempt sequence number (uniform over the cluster)
   int crank, csize;
   unsigned seq;
-  unsigned long long* bflags;
-  unsigned long long tag0;
   double* crec;   // [2][8][4] attempt records, written into every CTA of the cluster
+  unsigned* crows;   // [8] block rows published by each earlier band (seq * 16 + rows; + 15: failed)
 };
 
 __device__ __forceinline__ void cmark(const FState& fs, int slot) {
@@ -143,13 +141,25 @@ __device__ __forceinline__ void dsmem_st(double* p, int cta, double v) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(p)), "r"(cta));
   asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(ra), "d"(v) : "memory");
 }
-__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+// generic address of `p` in CTA `cta`'s shared memory window (ld / st.shared::cluster operand)
+__device__ __forceinline__ uint32_t dsmem_addr(const void* p, int cta) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(p)), "r"(cta));
+  return ra;
+}
+__device__ __forceinline__ double dsmem_ld(uint32_t ra) {
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra) : "memory");
   return v;
 }
-__device__ __forceinline__ void st_release_gpu(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+// release store of a u32 into CTA `cta`'s copy of the shared variable at `p`
+__device__ __forceinline__ void dsmem_st_release(unsigned* p, int cta, unsigned v) {
+  asm volatile("st.release.cluster.shared::cluster.u32 [%0], %1;" ::"r"(dsmem_addr(p, cta)), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_cluster(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.cluster.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
 }
 
 // Speculative CTA only: has CTA 0's plain attempt already succeeded?  Polled at
@@ -339,9 +349,15 @@ __device__ int diag_block_warp(double* D, int P, int n, int off, double* inv, do
 //       with two DMMA.8x8x4 each -- warp 0 takes block (P+1, P+1) first and
 //       then factors it (lookahead), the other warps take the rest.
 // Two block barriers per 8 pivots.
-template <typename Lay>
+// the per-step hook of chol_blocked: called by every thread once block row P
+// is final (after the step's barrier); the band-cluster path publishes the row
+struct NoRowHook {
+  __device__ __forceinline__ void operator()(int) const {}
+};
+
+template <typename Lay, typename Hook = NoRowHook>
 __device__ bool chol_blocked(double* Wb, int n, int nb, int P0, int nbr, int off, double* inv, double& smin,
-                             FState& fs, Lay lay, int* flag) {
+                             FState& fs, Lay lay, int* flag, Hook hook = Hook()) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   if (warp == 0) {
@@ -482,6 +498,7 @@ __device__ bool chol_blocked(double* Wb, int n, int nb, int P0, int nbr, int off
     __syncthreads();
     if (threadIdx.x == 0 && blockIdx.x == 0) g_fprof[11] += 1;
     if (*flag) return false;
+    hook(P);
   }
   return true;
 }
@@ -554,12 +571,12 @@ __device__ void band_trailing_update(double* Wb, int nb, int P0, int P1, Lay lay
 // rest of the matrix gets one rank-32 update per band (4x fewer barriers and
 // 4x more DMMA per block load than rank-8 steps over the whole matrix).
 // `nbr` limits the factorization to block rows [0, nbr).
-template <typename Lay>
+template <typename Lay, typename Hook = NoRowHook>
 __device__ bool chol_banded(double* Wb, int n, int nb, int nbr, int off, double* inv, double& smin, FState& fs,
-                            Lay lay, int* flag) {
+                            Lay lay, int* flag, Hook hook = Hook()) {
   for (int P0 = 0; P0 < nbr; P0 += 4) {
     const int P1 = min(nbr, P0 + 4);
-    if (!chol_blocked(Wb, n, nb, P0, P1, off, inv, smin, fs, lay, flag)) return false;
+    if (!chol_blocked(Wb, n, nb, P0, P1, off, inv, smin, fs, lay, flag, hook)) return false;
     if (P1 < nbr) {
       band_trailing_update(Wb, nb, P0, P1, lay);
       __syncthreads();
@@ -723,6 +740,26 @@ __device__ __forceinline__ void fmark(int slot) {
 // A cluster guarantees the C CTAs are co-resident, so waiting on a lower
 // band's flag always terminates (a band never waits on a higher one).
 constexpr int FC_LD = 36;   // staged band: column stride (conflict-free DMMA fragment loads)
+constexpr int FC_LD8 = 12;  // one staged block row (8 rows): column stride, conflict-free fragment loads
+
+// chol_blocked hook of the band-cluster path: block row P of this band is
+// final -> count it in every later band's row counter for this band
+struct BandRowHook {
+  unsigned* crows;
+  int r, C;
+  unsigned seq;
+  __device__ __forceinline__ void operator()(int P) const {
+    // the next band takes every block row as it finishes; the later bands read
+    // the band only once it is complete (their DSMEM reads would otherwise
+    // compete with this band's own shared-memory traffic)
+    if (threadIdx.x == FK_THREADS - 32) {   // a worker warp: warp 0 runs the pivot chain
+      const unsigned v = seq * 16u + (unsigned)(P + 1);
+      if (r + 1 < C) dsmem_st_release(crows + r, r + 1, v);
+      if (P == 3)
+        for (int d = r + 2; d < C; ++d) dsmem_st_release(crows + r, d, v);
+    }
+  }
+};
 enum { BAND_OK = 1, BAND_BREAKDOWN = 2, BAND_ABORT = 3, BAND_UPSTREAM = 4 };
 
 __host__ __device__ inline int64_t cluster_work_doubles(int k) {
@@ -741,11 +778,10 @@ __device__ bool chol_attempt_band_cluster(const double* __restrict__ Xg, int k, 
   const int nbr = min(4, nb);
   const int nrow = min(32, n);
   double* Wb = smem_w;                   // the band, LayoutBand4
-  double* stg = smem_w + 256 * nb;       // rows of an earlier band: stg[c * FC_LD + p] = R(32b + p, r0 + c)
+  double* stg = smem_w + 256 * nb;       // one block row of an earlier band: stg[c * FC_LD8 + ii]
   const LayoutBand4 band;
   __shared__ int s_state;
   const unsigned seq = fs.seq + 1;       // uniform over the cluster (every CTA runs every attempt)
-  const unsigned long long tag = fs.tag0 | ((unsigned long long)seq << 4);
   cmark(fs, 0);
 
   // ---- 1. the band of X + sigma I (X symmetric: X(r0 + i, r0 + c) = Xg[(r0 + i) k + r0 + c])
@@ -767,63 +803,71 @@ __device__ bool chol_attempt_band_cluster(const double* __restrict__ Xg, int k, 
   __syncthreads();
   cmark(fs, 1);
 
-  // ---- 2. the updates of the earlier bands, in band order
+  // ---- 2. the updates of the earlier bands, block row by block row as they
+  // are published: rows 8P .. 8P + 7 of band b are read straight from band b's
+  // shared memory (DSMEM) and applied as a rank-8 update, while band b goes on
+  // with its next pivots; only its last block row's hand-over is serial
   int state = BAND_OK;
-  for (int b = 0; b < r; ++b) {
-    if (tid == 0) {
-      unsigned long long f;
-      do { f = ld_acquire_gpu(fs.bflags + b); } while ((f >> 4) != (tag >> 4));
-      s_state = (int)(f & 15);
-    }
-    __syncthreads();
-    if (s_state != BAND_OK) { state = BAND_UPSTREAM; break; }
-    if (b == r - 1) cmark(fs, 2);
-    {
-      // a warp per column, lanes over the band's 32 rows (one 256-byte run); all loads first
-      constexpr int NC = (256 + FK_NW - 1) / FK_NW;
-      double v[NC];
-#pragma unroll
-      for (int u = 0; u < NC; ++u) {
-        const int c = warp + FK_NW * u;
-        v[u] = (c < n) ? __ldcg(Rk + (int64_t)(r0 + c) * ldr + 32 * b + lane) : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < NC; ++u) {
-        const int c = warp + FK_NW * u;
-        if (c < 8 * nb) stg[c * FC_LD + lane] = v[u];
-      }
-    }
-    __syncthreads();
-    // C(I, J) -= sum_P A(P, I)^T B(P, J) over the band's blocks I <= J: a warp
-    // takes a 2 x 2 group (four accumulator chains, each fragment feeds two DMMAs)
-    const int G = (nb + 1) >> 1;
-    const int ngr = G + (nbr > 2 ? G - 1 : 0);
-    for (int gidx = warp; gidx < ngr; gidx += FK_NW) {
-      const int gi = gidx < G ? 0 : 1;
-      const int gj = gidx < G ? gidx : gidx - G + 1;
-      const int I[2] = {2 * gi, 2 * gi + 1}, J[2] = {2 * gj, 2 * gj + 1};
-      bool live[2][2];
-      double c[2][2][2];
-#pragma unroll
-      for (int x = 0; x < 2; ++x)
-#pragma unroll
-        for (int y = 0; y < 2; ++y) {
-          live[x][y] = I[x] < nbr && I[x] <= J[y] && J[y] < nb;
-          const double* pc = Wb + band(live[x][y] ? I[x] : 0, live[x][y] ? J[y] : 0) + 2 * t * 8 + g;
-          cfrag_load(pc, t, c[x][y]);
-          if (!live[x][y]) { c[x][y][0] = 0.0; c[x][y][1] = 0.0; }
+  for (int b = 0; b < r && state == BAND_OK; ++b) {
+    const int offc = r0 - 32 * b;                      // this band's column 0 among band b's columns
+    const uint32_t rbase = dsmem_addr(smem_w, b);      // band b's work area (same offset in every CTA)
+    for (int P = 0; P < 4; ++P) {
+      if (tid == 0) {
+        const unsigned want = seq * 16u + (unsigned)(b == r - 1 ? P + 1 : 4);
+        while (true) {
+          const unsigned v = ld_acquire_cluster(fs.crows + b);
+          if ((v >> 4) != seq) continue;              // an earlier attempt's count
+          if ((v & 15u) == 15u) { s_state = BAND_UPSTREAM; break; }
+          if (v >= want) { s_state = BAND_OK; break; }
         }
-      const int ci[2] = {min(I[0], nb - 1), min(I[1], nb - 1)};
-      const int cj[2] = {min(J[0], nb - 1), min(J[1], nb - 1)};
+      }
+      __syncthreads();
+      if (s_state != BAND_OK) { state = BAND_UPSTREAM; break; }
+      if (b == r - 1 && P == 3) cmark(fs, 2);
+      {
+        // stg[c * FC_LD8 + ii] = R(32b + 8P + ii, r0 + c): lanes over 4 columns x 8 rows (64 contiguous doubles)
+        constexpr int NE = (64 * 32 + FK_THREADS - 1) / FK_THREADS;
+        double v[NE];
 #pragma unroll
-      for (int P = 0; P < 4; ++P) {
+        for (int u = 0; u < NE; ++u) {
+          const int e = tid + FK_THREADS * u, c = e >> 3, ii = e & 7, cp = offc + c;
+          v[u] = (c < n) ? dsmem_ld(rbase + 8u * (uint32_t)(band(P, cp >> 3) + (cp & 7) * 8 + ii)) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < NE; ++u) {
+          const int e = tid + FK_THREADS * u, c = e >> 3, ii = e & 7;
+          if (c < 8 * nb) stg[c * FC_LD8 + ii] = v[u];
+        }
+      }
+      __syncthreads();
+      // C(I, J) -= A(P, I)^T B(P, J) over the band's blocks I <= J: a warp
+      // takes a 2 x 2 group (four accumulator chains, each fragment feeds two DMMAs)
+      const int G = (nb + 1) >> 1;
+      const int ngr = G + (nbr > 2 ? G - 1 : 0);
+      for (int gidx = warp; gidx < ngr; gidx += FK_NW) {
+        const int gi = gidx < G ? 0 : 1;
+        const int gj = gidx < G ? gidx : gidx - G + 1;
+        const int I[2] = {2 * gi, 2 * gi + 1}, J[2] = {2 * gj, 2 * gj + 1};
+        bool live[2][2];
+        double c[2][2][2];
+#pragma unroll
+        for (int x = 0; x < 2; ++x)
+#pragma unroll
+          for (int y = 0; y < 2; ++y) {
+            live[x][y] = I[x] < nbr && I[x] <= J[y] && J[y] < nb;
+            const double* pc = Wb + band(live[x][y] ? I[x] : 0, live[x][y] ? J[y] : 0) + 2 * t * 8 + g;
+            cfrag_load(pc, t, c[x][y]);
+            if (!live[x][y]) { c[x][y][0] = 0.0; c[x][y][1] = 0.0; }
+          }
+        const int ci[2] = {min(I[0], nb - 1), min(I[1], nb - 1)};
+        const int cj[2] = {min(J[0], nb - 1), min(J[1], nb - 1)};
         double a[2][2], bb[2][2];
 #pragma unroll
         for (int x = 0; x < 2; ++x)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            a[x][h] = -stg[(8 * ci[x] + g) * FC_LD + 8 * P + 4 * h + t];
-            bb[x][h] = stg[(8 * cj[x] + g) * FC_LD + 8 * P + 4 * h + t];
+            a[x][h] = -stg[(8 * ci[x] + g) * FC_LD8 + 4 * h + t];
+            bb[x][h] = stg[(8 * cj[x] + g) * FC_LD8 + 4 * h + t];
           }
 #pragma unroll
         for (int h = 0; h < 2; ++h)
@@ -831,36 +875,33 @@ __device__ bool chol_attempt_band_cluster(const double* __restrict__ Xg, int k, 
           for (int x = 0; x < 2; ++x)
 #pragma unroll
             for (int y = 0; y < 2; ++y) dmma(c[x][y], a[x][h], bb[y][h]);
+#pragma unroll
+        for (int x = 0; x < 2; ++x)
+#pragma unroll
+          for (int y = 0; y < 2; ++y)
+            if (live[x][y]) cfrag_store(Wb + band(I[x], J[y]) + 2 * t * 8 + g, t, c[x][y]);
       }
-#pragma unroll
-      for (int x = 0; x < 2; ++x)
-#pragma unroll
-        for (int y = 0; y < 2; ++y)
-          if (live[x][y]) {
-            cfrag_store(Wb + band(I[x], J[y]) + 2 * t * 8 + g, t, c[x][y]);
-          }
+      __syncthreads();
     }
-    __syncthreads();
   }
 
-  // ---- 3. the band's own 32 pivots
+  // ---- 3. the band's own 32 pivots; each finished block row is published to
+  // the later bands (their row counters, DSMEM release stores) by a worker
+  // thread, so warp 0's pivot chain never waits on it
   cmark(fs, 3);
   if (state == BAND_OK) {
-    if (!chol_banded(Wb, n, nb, nbr, r0, inv, smin, fs, LayoutBand4(), flag))
+    if (!chol_banded(Wb, n, nb, nbr, r0, inv, smin, fs, band, flag, BandRowHook{fs.crows, r, C, seq}))
       state = fs.aborted ? BAND_ABORT : BAND_BREAKDOWN;
   }
+  if (state != BAND_OK && threadIdx.x == FK_THREADS - 32)
+    for (int d = r + 1; d < C; ++d) dsmem_st_release(fs.crows + r, d, seq * 16u + 15u);
 
-  // ---- 4. rows r0 .. r0 + nrow - 1 of R, then the band's flag
+  // ---- 4. rows r0 .. r0 + nrow - 1 of R (the later bands read them from shared memory)
   cmark(fs, 4);
   if (state == BAND_OK) {
     for (int c = warp; c < n; c += FK_NW)
       if (lane < nrow && lane <= c)
         Rk[(int64_t)(r0 + c) * ldr + r0 + lane] = Wb[band(lane >> 3, c >> 3) + (c & 7) * 8 + (lane & 7)];
-  }
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    st_release_gpu(fs.bflags + r, tag | (unsigned long long)state);
   }
   cmark(fs, 5);
 
@@ -1533,6 +1574,7 @@ __global__ void __launch_bounds__(FK_THREADS, 1) factor_kernel(FactorArgs a) {
   const int group = (int)blockIdx.x / C, crank = (int)blockIdx.x - group * C;
   const int wdoubles = C > 1 ? (int)cluster_work_doubles(k) : (int)work_doubles(k);
   __shared__ double crec[2 * 8 * 4];
+  __shared__ unsigned crows[8];
   // speculative group 1 (RECOMPUTE): private R, work matrix and shift list; X
   // in global memory (k > 128) is formed identically by both groups
   const bool spec1 = a.spec && group == 1;
@@ -1552,10 +1594,12 @@ __global__ void __launch_bounds__(FK_THREADS, 1) factor_kernel(FactorArgs a) {
       fs.spec_done = (0xC9F0A5ull << 40) | ((unsigned long long)a.epoch << 2) | 1ull;
     }
     fs.crank = crank; fs.csize = C; fs.seq = 0;
-    fs.bflags = reinterpret_cast<unsigned long long*>(a.pub + PUB_BFLAGS + 8 * group);
-    fs.tag0 = (0xB4ull << 56) | ((unsigned long long)a.epoch << 24);
     fs.crec = crec;
+    fs.crows = crows;
   }
+  if (tid < 8) crows[tid] = 0u;
+  // every CTA's row counters are zero before any band can publish into them
+  if (C > 1) cluster_sync_all();
 
   if (tid == 0 && blockIdx.x == 0) { g_fprof[9] = 0; g_fprof[10] = 0; g_fprof[11] = 0; g_fprof[12] = 0; }
   fmark(0);
@@ -1663,19 +1707,32 @@ __global__ void __launch_bounds__(FK_THREADS, 1) factor_kernel(FactorArgs a) {
       fs.err = err;
       fs.diag_max = dm;
     }
-  } else if (tid == 0) {
+  } else {
     // X was formed in global memory by factor_prep_kernel; its per-tile
-    // partials are combined here in tile order (fixed, so deterministic)
+    // partials are combined here in tile order (fixed, so deterministic).  The
+    // partials are loaded by all threads at once (one thread walking them took
+    // ~2.7 us of dependent L2 round trips at k = 256), then summed by thread 0.
     const int nt = (k + 31) / 32, ntiles = nt * (nt + 1) / 2;
+    double* pp = rowbuf;   // rowbuf | vec | wv: 3 kpad doubles, free here
+    const int chunk = kpad;  // tiles per pass (3 doubles each)
     double e2 = 0.0, dm = -INFINITY, ff = 0.0;
-    for (int b = 0; b < ntiles; ++b) {
-      e2 += a.part[3 * b];
-      dm = fmax(dm, a.part[3 * b + 1]);
-      ff += a.part[3 * b + 2];
+    for (int b0 = 0; b0 < ntiles; b0 += chunk) {
+      const int nb = min(chunk, ntiles - b0);
+      for (int e = tid; e < 3 * nb; e += FK_THREADS) pp[e] = a.part[3 * b0 + e];
+      __syncthreads();
+      if (tid == 0)
+        for (int b = 0; b < nb; ++b) {
+          e2 += pp[3 * b];
+          dm = fmax(dm, pp[3 * b + 1]);
+          ff += pp[3 * b + 2];
+        }
+      __syncthreads();
     }
-    fs.err = sqrt(e2);
-    fs.diag_max = dm;
-    fs.fro = sqrt(ff);
+    if (tid == 0) {
+      fs.err = sqrt(e2);
+      fs.diag_max = dm;
+      fs.fro = sqrt(ff);
+    }
   }
   __syncthreads();
   const double err = fs.err;
@@ -1847,29 +1904,29 @@ __global__ void __launch_bounds__(FK_THREADS, 1) factor_kernel(FactorArgs a) {
   __syncthreads();
   fmark(6);
   if (tid == 0) {
-    cqr_factor_status* st = spec1 ? reinterpret_cast<cqr_factor_status*>(a.pub + PUB_ST1) : a.st;
-    st->code = fs.code;
-    st->retries = fs.retries;
-    st->n_shifts = fs.n_shifts;
-    st->pivot_index = fs.pivot_index;
-    st->pivot_value = fs.pivot_value;
-    st->err = fs.err;
-    st->norm_est = fs.norm_est;
-    st->last_shift = fs.last_shift;
-    st->min_pivot_rel = fs.min_pivot_rel;
-    st->est_calls = fs.est_calls;
-    st->est_flag = fs.est_flag;
-    st->escalations = fs.escalations;
-    st->singular_index = fs.singular_index;
-    st->plain_margin = fs.plain_margin;
-    st->diag_max = fs.diag_max;
+    cqr_factor_status rec{};
+    rec.code = fs.code;
+    rec.retries = fs.retries;
+    rec.n_shifts = fs.n_shifts;
+    rec.pivot_index = fs.pivot_index;
+    rec.pivot_value = fs.pivot_value;
+    rec.err = fs.err;
+    rec.norm_est = fs.norm_est;
+    rec.last_shift = fs.last_shift;
+    rec.min_pivot_rel = fs.min_pivot_rel;
+    rec.est_calls = fs.est_calls;
+    rec.est_flag = fs.est_flag;
+    rec.escalations = fs.escalations;
+    rec.singular_index = fs.singular_index;
+    rec.plain_margin = fs.plain_margin;
+    rec.diag_max = fs.diag_max;
+    *(spec1 ? reinterpret_cast<cqr_factor_status*>(a.pub + PUB_ST1) : a.st) = rec;
     if (!spec1 && a.stm != nullptr) {
-      // host-mapped mirror: the host reads the pass's outcome without a D2H copy
-      // (the shifts were written by this thread)
-      cqr_factor_status* hm = a.stm;
-      *hm = *st;
+      // host-mapped mirror: the host reads the pass's outcome without a D2H copy.
+      // No system fence: kernel completion and the host's event wait order these
+      // stores before the host's read (as for cqr_store_to_host)
+      *a.stm = rec;
       for (int i = 0; i < fs.n_shifts; ++i) a.shm[i] = a.shifts[i];
-      __threadfence_system();
     }
   }
 }
@@ -1893,10 +1950,9 @@ __device__ void spec_merge_status(const FactorArgs& a) {
   if (s.pivot_index < 0) { s.pivot_value = a.pub[2]; s.pivot_index = (int)a.pub[3]; }
   *a.st = s;
   for (int i = 0; i < s.n_shifts; ++i) a.shifts[i] = a.shifts1[i];
-  if (a.stm != nullptr) {
+  if (a.stm != nullptr) {   // (kernel completion orders these before the host's read)
     *a.stm = s;
     for (int i = 0; i < s.n_shifts; ++i) a.shm[i] = a.shifts1[i];
-    __threadfence_system();
   }
 }
 

@@ -40,9 +40,13 @@ def timeline(k, policy, kind):
             row[name] = round((v - t0) / 1e3, 2) if v >= t0 and v - t0 < 10 ** 7 else None
         bands.append(row)
     steps = max(int(fp[11]), 1)
+    # kernel-level phases (rank 0 of group 0): start, X/err done, attempt start (band 0), status write
+    kphase = {"xerr_us": round((fp[1] - fp[0]) / 1e3, 2), "to_attempt_us": round((buf[0] - fp[0]) / 1e3, 2),
+              "attempt_us": round((buf[8 * 0 + 6] - buf[0]) / 1e3, 2),
+              "tail_us": round((fp[6] - buf[6]) / 1e3, 2) if fp[6] > buf[6] else None}
     print(json.dumps({"k": k, "policy": policy, "kind": kind, "code": st.code, "est_iters": int(fp[8]),
                       "band0_steps": int(fp[11]), "panel_cyc": fp[9] // steps, "update_cyc": fp[10] // steps,
-                      "diag_cyc": fp[12] // steps, "bands": bands}), flush=True)
+                      "diag_cyc": fp[12] // steps, "kphase": kphase, "bands": bands}), flush=True)
 
 
 if __name__ == "__main__":
