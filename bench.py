@@ -409,7 +409,7 @@ def run_ours():
         s_in, s_out = torch.cuda.Stream(cx.device), torch.cuda.Stream(cx.device)
         dev_in = [torch.empty((k, hi - lo), dtype=torch.float64, device=cx.device) for _ in range(2)]
         ev_in = [torch.cuda.Event() for _ in range(2)]
-        n_str = max(10, ARGS.steps)   # a loader's stream of calls: fill and drain amortised over >= 10
+        n_str = max(20, ARGS.steps)   # a loader's stream of calls: fill and drain amortised over >= 20
 
         def streamed():
             held = []             # (result, Q staging, copy-out event) of calls still copying out

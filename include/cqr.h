@@ -231,6 +231,10 @@ int cqr_debug_factor_cluster(int on);
 /* Diagnostics: globaltimer stamps (ns) of the band-cluster path's last attempt,
  * [band][event] (HOST array of 64; synchronous). */
 int cqr_debug_factor_cluster_profile(unsigned long long* out64);
+/* Diagnostics: out32 == NULL selects the CTA (blockIdx, -1 = off) whose first
+ * four blocked-Cholesky steps record clock64 stamps; else copies the [4][8]
+ * stamps to the HOST array out32 (synchronous). */
+int cqr_debug_factor_step_profile(int cta, long long* out32);
 int cqr_factor(const cqr_factor_config* cfg, int k, const double* G, int ldg, const double* Bt, int ldbt, int q,
                double* Rk, double* Rinv, int ldr, double* Racc, double* B, int ldb, double* shifts,
                cqr_factor_status* status, void* ws, size_t ws_bytes, void* stream);

@@ -107,6 +107,7 @@ SIGNATURES = {
     "cqr_debug_factor_banded": (_I, [_I]),
     "cqr_debug_factor_cluster": (_I, [_I]),
     "cqr_debug_factor_cluster_profile": (_I, [ctypes.POINTER(ctypes.c_ulonglong)]),
+    "cqr_debug_factor_step_profile": (_I, [_I, ctypes.c_void_p]),
     "cqr_tri_inverse": (_I, [_P, _I, _I, _P, _I, _P]),
     "cqr_tri_multiply": (_I, [_P, _I, _P, _I, _I, _P, _I, _P]),
     "cqr_frobenius": (_I, [_P, _I, _I, _I, _P, _P]),

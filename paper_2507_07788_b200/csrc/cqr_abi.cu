@@ -276,6 +276,8 @@ int cqr_debug_factor_cluster(int on) { return cqr::factor_set_cluster(on); }
 
 int cqr_debug_factor_cluster_profile(unsigned long long* out64) { return cqr::factor_cluster_profile(out64); }
 
+int cqr_debug_factor_step_profile(int cta, long long* out32) { return cqr::factor_step_profile(cta, out32); }
+
 size_t cqr_factor_workspace_bytes(int k) { return k > 0 ? cqr::factor_workspace_bytes(k) : 256; }
 
 int cqr_factor(const cqr_factor_config* cfg, int k, const double* G, int ldg, const double* Bt, int ldbt, int q,

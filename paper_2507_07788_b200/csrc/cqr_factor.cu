@@ -62,6 +62,11 @@ __device__ int g_banded = 1;
 // [band][0 start, 1 band loaded, 2 last upstream band received, 3 updates
 //  applied, 4 band factored, 5 published, 6 outcome agreed]
 __device__ unsigned long long g_cprof[8][8];
+// per-step clock64 stamps of chol_blocked in the last band of the cluster
+// (diagnostics): [step][0 start, 1 warp 0 solved, 2 warp 0 updated, 3 diag
+// done, 4 workers' panel done, 5 workers' update done, 6 step barrier passed]
+__device__ long long g_sprof[4][8];
+__device__ int g_sprof_cta = -1;
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -307,30 +312,45 @@ __device__ int diag_block_warp(double* D, int P, int n, int off, double* inv, do
     for (int c = 0; c < 8; ++c)
 #pragma unroll
       for (int i = 0; i <= c; ++i) a[pk8(i, c)] = D[c * 8 + i];
+    // all 8 pivots run unconditionally (no early exit to serialise the
+    // schedule); the first failing pivot is recorded with predicated moves and
+    // everything computed after it is discarded
+    int bj = -1;
+    double bv = 0.0, sm = smin;
+    double rr[8];
 #pragma unroll
     for (int jj = 0; jj < 8; ++jj) {
       const int j = 8 * P + jj;
       const double sj = a[pk8(jj, jj)];
-      if (j < n) {
-        if (!(sj > 0.0)) {
-          fs.pivot_index = j + off;
-          fs.pivot_value = sj;
-          bad = 1;
-          break;
-        }
-        smin = fmin(smin, sj);
-      }
+      const bool live = j < n;
+      if (live && !(sj > 0.0) && bj < 0) { bj = j; bv = sj; }
+      if (live && bj < 0) sm = fmin(sm, sj);
       const double r = rsqrt(sj);
+      rr[jj] = r;
+      // the next pivot's chain first (scale (jj, jj+1), update (jj+1, jj+1)),
+      // then the rest of the step: the same operations in the same order per
+      // element, listed so that the schedule starts the dependent chain early
+      if (jj + 1 < 8) {
+        a[pk8(jj, jj + 1)] *= r;
+        a[pk8(jj + 1, jj + 1)] -= a[pk8(jj, jj + 1)] * a[pk8(jj, jj + 1)];
+      }
       a[pk8(jj, jj)] = sj * r;
-      inv[j] = r;
 #pragma unroll
-      for (int c = jj + 1; c < 8; ++c) a[pk8(jj, c)] *= r;
+      for (int c = jj + 2; c < 8; ++c) a[pk8(jj, c)] *= r;
 #pragma unroll
       for (int c = jj + 1; c < 8; ++c)
 #pragma unroll
-        for (int i = jj + 1; i <= c; ++i) a[pk8(i, c)] -= a[pk8(jj, i)] * a[pk8(jj, c)];
+        for (int i = jj + 1; i <= c; ++i)
+          if (!(i == jj + 1 && c == jj + 1)) a[pk8(i, c)] -= a[pk8(jj, i)] * a[pk8(jj, c)];
     }
-    if (!bad) {
+    if (bj >= 0) {
+      fs.pivot_index = bj + off;
+      fs.pivot_value = bv;
+      bad = 1;
+    } else {
+      smin = sm;
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) inv[8 * P + jj] = rr[jj];
 #pragma unroll
       for (int c = 0; c < 8; ++c)
 #pragma unroll
@@ -372,8 +392,10 @@ __device__ bool chol_blocked(double* Wb, int n, int nb, int P0, int nbr, int off
   bool spec_have = false;
   constexpr int NWKR = FK_NW - 1;                    // worker warps 1.. (panel solve)
   constexpr int NWK = FK_NW - FK_NW / 4;             // of which the trailing-update warps (warp % 4 != 0)
+  const bool sp = (int)blockIdx.x == g_sprof_cta && P0 == 0;
   for (int P = P0; P < nbr; ++P) {
     const long long c0 = clock64();
+    if (sp && tid == 0 && P < 4) g_sprof[P][0] = c0;
     int spec_abort = 0;
     if (tid == 0 && fs.spec_flag != nullptr) {
       if (spec_have && spec_pend == fs.spec_done) { spec_abort = 1; fs.aborted = 1; }
@@ -393,16 +415,22 @@ __device__ bool chol_blocked(double* Wb, int n, int nb, int P0, int nbr, int off
     auto solve_col = [&](int col) {
       double* blk = Wb + lay(P, P + 1 + (col >> 3)) + (col & 7) * 8;   // column (col & 7), rows 0..7
       const int rot = (lane >> 1) & 7;
-      double b[8], y[8];
+      double y[8], dl[28], ivr[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) b[q] = blk[(q + rot) & 7];
-      rot_right8(b, rot);   // b[jj] = row jj
+      for (int q = 0; q < 8; ++q) y[q] = blk[(q + rot) & 7];
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) ivr[jj] = iv[jj];
+#pragma unroll
+      for (int jj = 1, e = 0; jj < 8; ++jj)
+#pragma unroll
+        for (int l = 0; l < jj; ++l, ++e) dl[e] = D[jj * 8 + l];
+      rot_right8(y, rot);   // y[jj] = row jj
+      // right-looking order (per element the same subtractions, ascending l)
 #pragma unroll
       for (int jj = 0; jj < 8; ++jj) {
-        double v = b[jj];
+        y[jj] *= ivr[jj];
 #pragma unroll
-        for (int l = 0; l < jj; ++l) v -= D[jj * 8 + l] * y[l];
-        y[jj] = v * iv[jj];
+        for (int l2 = jj + 1; l2 < 8; ++l2) y[l2] -= dl[l2 * (l2 - 1) / 2 + jj] * y[jj];
       }
       rot_left8(y, rot);    // y[q] = row (q + rot) & 7
 #pragma unroll
@@ -413,10 +441,33 @@ __device__ bool chol_blocked(double* Wb, int n, int nb, int P0, int nbr, int off
       // ---- the critical chain of the step, alone on warp 0:
       // solve block (P, P+1) -> rank-8 update of (P+1, P+1) -> factor it
       if (ahead) {
-        if (lane < 8) solve_col(lane);
+        if (lane < 8) {
+          // block (P, P+1) on 8 lanes: row order (at most 4-way conflicts for 8 lanes,
+          // cheaper than the rotation selects on the critical chain)
+          double* blk = Wb + lay(P, P + 1) + lane * 8;
+          double v[8], dl[28], ivr[8];
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) { v[jj] = blk[jj]; ivr[jj] = iv[jj]; }
+#pragma unroll
+          for (int jj = 1, e = 0; jj < 8; ++jj)
+#pragma unroll
+            for (int l = 0; l < jj; ++l, ++e) dl[e] = D[jj * 8 + l];
+          // right-looking: row jj's value is final once y[0..jj-1] are out; each
+          // element still subtracts its terms in ascending l (the same rounding
+          // as the row-by-row form), but the chain is 2 dependent ops per row
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) {
+            v[jj] *= ivr[jj];
+#pragma unroll
+            for (int l2 = jj + 1; l2 < 8; ++l2) v[l2] -= dl[l2 * (l2 - 1) / 2 + jj] * v[jj];
+          }
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) blk[jj] = v[jj];
+        }
         __syncwarp();
         // (P, P+1) is final: release it to the workers' updates of block row P+1
         asm volatile("bar.arrive 2, %0;" ::"n"(FK_THREADS) : "memory");
+        if (sp && lane == 0 && P < 4) g_sprof[P][1] = clock64();
         const double* pa = Wb + lay(P, P + 1) + g * 8 + t;
         double* pc = Wb + lay(P + 1, P + 1) + 2 * t * 8 + g;
         double c2[2];
@@ -428,17 +479,23 @@ __device__ bool chol_blocked(double* Wb, int n, int nb, int P0, int nbr, int off
         cfrag_store(pc, t, c2);
         __syncwarp();
         const long long cd = clock64();
+        if (sp && lane == 0 && P < 4) g_sprof[P][2] = cd;
         f = diag_block_warp(Wb + lay(P + 1, P + 1), P + 1, n, off, inv, smin, fs);
+        if (sp && lane == 0 && P < 4) g_sprof[P][3] = clock64();
         if (lane == 0 && blockIdx.x == 0) atomicAdd(&g_fprof[12], (unsigned long long)(clock64() - cd));
       }
       if (lane == 0) *flag = f | spec_abort;
     } else {
       // ---- workers: the rest of panel row P, then the trailing update
+      // (the 9 warps outside warp 0's SM sub-partition: warps 4 and 8 would take
+      // its issue slots while it runs the diagonal chain)
       const int first = ahead ? 8 : 0;               // warp 0 solves block (P, P+1)
-      for (int col = first + (tid - 32); col < 8 * ncb; col += 32 * NWKR) solve_col(col);
+      if (warp & 3)
+        for (int col = first + 32 * (warp - 1 - (warp >> 2)) + lane; col < 8 * ncb; col += 32 * NWK) solve_col(col);
       asm volatile("bar.sync 1, %0;" ::"n"(32 * NWKR) : "memory");   // panel row P final (but (P, P+1))
       const long long c1 = clock64();
       if (tid == 32 && blockIdx.x == 0) g_fprof[9] += (unsigned long long)(c1 - c0);
+      if (sp && tid == 32 && P < 4) g_sprof[P][4] = c1;
       if (ahead) asm volatile("bar.sync 2, %0;" ::"n"(FK_THREADS) : "memory");   // (P, P+1) from warp 0
       // trailing rank-8 update of blocks (I, J), P < I < nbr, I <= J < nb, but (P+1, P+1)
       const int nblk = (nrows_b == ncb) ? ncb * (ncb + 1) / 2 : nrows_b * ncb - nrows_b * (nrows_b - 1) / 2;
@@ -494,8 +551,10 @@ __device__ bool chol_blocked(double* Wb, int n, int nb, int P0, int nbr, int off
         if (two) cfrag_store(pc1, t, c1r);
       }
       if (tid == 32 && blockIdx.x == 0) g_fprof[10] += (unsigned long long)(clock64() - c1);
+      if (sp && tid == 32 && P < 4) g_sprof[P][5] = clock64();
     }
     __syncthreads();
+    if (sp && tid == 0 && P < 4) g_sprof[P][6] = clock64();
     if (threadIdx.x == 0 && blockIdx.x == 0) g_fprof[11] += 1;
     if (*flag) return false;
     hook(P);
@@ -2269,6 +2328,12 @@ int factor_set_banded(int on) {
 
 int factor_cluster_profile(unsigned long long* out) {
   return cudaMemcpyFromSymbol(out, g_cprof, sizeof(g_cprof)) == cudaSuccess ? 0 : -1;
+}
+
+// diagnostics: per-step stamps of CTA `cta` (-1: off); out = [4][8] stamps
+int factor_step_profile(int cta, long long* out) {
+  if (out != nullptr) return cudaMemcpyFromSymbol(out, g_sprof, sizeof(g_sprof)) == cudaSuccess ? 0 : -1;
+  return cudaMemcpyToSymbol(g_sprof_cta, &cta, sizeof(int)) == cudaSuccess ? 0 : -1;
 }
 
 int factor_profile(unsigned long long* out) {

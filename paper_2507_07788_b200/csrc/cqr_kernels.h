@@ -117,6 +117,7 @@ int factor_profile(unsigned long long* out);
 int factor_set_banded(int on);
 int factor_set_cluster(int on);
 int factor_cluster_profile(unsigned long long* out64);
+int factor_step_profile(int cta, long long* out32);
 
 // ------------------------------------------------------------- standalone k x k kernels (cqr_small.cu)
 cudaError_t tri_inverse_launch(const double* R, int ldr, int n, double* X, int ldx, cudaStream_t s);

@@ -49,7 +49,33 @@ def timeline(k, policy, kind):
                       "diag_cyc": fp[12] // steps, "kphase": kphase, "bands": bands}), flush=True)
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and len(sys.argv) == 1:
     for k, pol, kind in ((256, "plain", "spd"), (256, "shift_once", "illcond"), (192, "plain", "spd"),
                          (160, "plain", "spd")):
         timeline(k, pol, kind)
+
+
+def steps(k, policy, kind, cta):
+    """clock64 stamps of the first 4 blocked steps of CTA `cta` (cycles from each step's start)."""
+    cx = ctx()
+    cx.lib.cqr_debug_factor_cluster(1)
+    cx.lib.cqr_debug_factor_step_profile(cta, None)
+    eng = Engine(k, cq.AlgoConfig())
+    g = torch.from_numpy(gramian(k, kind, 1)).to(cx.device)
+    for _ in range(3):
+        eng.G.copy_(g)
+        eng.factor(POL[policy], 10 ** 6, k)
+    out = (ctypes.c_longlong * 32)()
+    cx.lib.cqr_debug_factor_step_profile(cta, ctypes.cast(out, ctypes.c_void_p))
+    cx.lib.cqr_debug_factor_step_profile(-1, None)
+    names = ["start", "w0_solved", "w0_updated", "w0_diag", "wk_panel", "wk_update", "barrier", "diag_load"]
+    for P in range(4):
+        row = [out[8 * P + i] for i in range(8)]
+        rec = {n: row[i] - row[0] for i, n in enumerate(names[:7])}
+        rec["diag_load"] = row[7]
+        print(json.dumps({"k": k, "cta": cta, "step": P, **rec}))
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "steps":
+    for cta in (0, 4, 7):
+        steps(256, "plain", "spd", cta)
