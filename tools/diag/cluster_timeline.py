@@ -46,7 +46,8 @@ def timeline(k, policy, kind):
               "tail_us": round((fp[6] - buf[6]) / 1e3, 2) if fp[6] > buf[6] else None}
     print(json.dumps({"k": k, "policy": policy, "kind": kind, "code": st.code, "est_iters": int(fp[8]),
                       "band0_steps": int(fp[11]), "panel_cyc": fp[9] // steps, "update_cyc": fp[10] // steps,
-                      "diag_cyc": fp[12] // steps, "kphase": kphase, "bands": bands}), flush=True)
+                      "diag_cyc": fp[12] // steps, "finish_cyc": {"racc": fp[13], "inv_diag": fp[14], "rinv": fp[15]},
+                      "kphase": kphase, "bands": bands}), flush=True)
 
 
 if __name__ == "__main__" and len(sys.argv) == 1:
