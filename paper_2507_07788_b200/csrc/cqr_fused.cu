@@ -581,7 +581,7 @@ static cudaError_t launch_rt(const double* X, int64_t ldx, int k, const double* 
                                                                                 gate);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  gram_partials_reduce<<<gram_partials_reduce_blocks(k), 256, 0, s>>>(ws, ctas, KP, k, G, ldg, gate);
+  gram_partials_reduce<<<gram_partials_reduce_blocks(k), PR_THREADS, 0, s>>>(ws, ctas, KP, k, G, ldg, gate);
   return cudaGetLastError();
 }
 
@@ -601,7 +601,7 @@ static cudaError_t launch_fused(const double* X, int64_t ldx, int k, const doubl
     apply_gram_fused_kernel<KP, false><<<ctas, FuCfg<KP>::THREADS, smem, s>>>(X, ldx, k, Rt, Q, ldq, rows, ws, gate);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  gram_partials_reduce<<<gram_partials_reduce_blocks(k), 256, 0, s>>>(ws, ctas, KP, k, G, ldg, gate);
+  gram_partials_reduce<<<gram_partials_reduce_blocks(k), PR_THREADS, 0, s>>>(ws, ctas, KP, k, G, ldg, gate);
   return cudaGetLastError();
 }
 

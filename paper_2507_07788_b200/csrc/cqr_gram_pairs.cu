@@ -190,7 +190,7 @@ static cudaError_t launch_gp(const double* X, int64_t ldx, int k, int64_t rows, 
   gram_pairs_kernel<KP><<<items * nsplit, GPCfg<KP>::THREADS, smem, s>>>(X, ldx, k, rows, nsplit, ws, gate);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  gram_partials_reduce<<<gram_partials_reduce_blocks(k), 256, 0, s>>>(ws, items * nsplit, KP, k, G, ldg,
+  gram_partials_reduce<<<gram_partials_reduce_blocks(k), PR_THREADS, 0, s>>>(ws, items * nsplit, KP, k, G, ldg,
                                                                                 gate);
   return cudaGetLastError();
 }

@@ -128,9 +128,13 @@ struct PairDispatch<NB, NB / 2> {
 // order, p = 0, 1, 2, ... (the order every earlier version used, so results
 // are bitwise unchanged).  The partials are loaded in batches of 32 before the
 // adds: the first version issued one load per add and was latency bound at
-// 30-50 us per call at k = 64 (profiles/r01_launches_config5.csv).
+// 30-50 us per call at k = 64 (profiles/r01_launches_config5.csv).  64-thread
+// blocks: the call is bound by each SM's L2 load throughput, so the k^2
+// elements are spread over as many SMs as possible (256-thread blocks put
+// k = 64 on 16 SMs: 14.4 us per call, 3 of them in config 1's 0.54 ms).
 constexpr int PR_BATCH = 32;
-static __global__ void __launch_bounds__(256) gram_partials_reduce(const double* __restrict__ ws, int nparts, int KP,
+constexpr int PR_THREADS = 64;
+static __global__ void __launch_bounds__(PR_THREADS) gram_partials_reduce(const double* __restrict__ ws, int nparts, int KP,
                                                                    int k, double* G, int ldg, const int* gate) {
   if (gate != nullptr && *gate != 0) return;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -148,10 +152,19 @@ static __global__ void __launch_bounds__(256) gram_partials_reduce(const double*
 #pragma unroll
     for (int j = 0; j < PR_BATCH; ++j) s += v[j];
   }
-  for (; p < nparts; ++p) s += src[p * ps];
+  if (p < nparts) {
+    // the remainder as one masked batch (a scalar loop here was one L2 round
+    // trip per partial: ~7 us of the call at 148 partials)
+    double v[PR_BATCH];
+#pragma unroll
+    for (int j = 0; j < PR_BATCH; ++j) v[j] = (p + j < nparts) ? src[(p + j) * ps] : 0.0;
+#pragma unroll
+    for (int j = 0; j < PR_BATCH; ++j)
+      if (p + j < nparts) s += v[j];
+  }
   G[(int64_t)c * ldg + r] = s;
   G[(int64_t)r * ldg + c] = s;
 }
-inline int gram_partials_reduce_blocks(int k) { return (int)(((int64_t)k * k + 255) / 256); }
+inline int gram_partials_reduce_blocks(int k) { return (int)(((int64_t)k * k + PR_THREADS - 1) / PR_THREADS); }
 
 }  // namespace cqr
