@@ -1623,13 +1623,13 @@ __global__ void __launch_bounds__(FK_THREADS, 1) factor_kernel(FactorArgs a) {
   double* rowbuf = fsm + 32;
   double* vec = rowbuf + kpad;
   double* wv = vec + kpad;
-  // k <= 128: X itself lives in shared memory (k^2 doubles) before the work area
-  const bool xs = (k <= FK_SMEM_K);
-  double* Xs = wv + kpad;                // X in shared memory (k <= 128)
-  const double* Xg = a.X;                // X in global memory (k > 128, formed by factor_prep_kernel)
-  double* Wsm = xs ? Xs + (int64_t)k * k : wv + kpad;   // shared work area
   // band-cluster path: a group of C CTAs (one cluster) per attempt chain
   const int C = a.ncl > 1 ? a.ncl : 1;
+  // k <= 128 on one CTA: X itself lives in shared memory (k^2 doubles) before the work area
+  const bool xs = (k <= FK_SMEM_K) && C == 1;
+  double* Xs = wv + kpad;                // X in shared memory (xs)
+  const double* Xg = a.X;                // X in global memory (formed by factor_prep_kernel)
+  double* Wsm = xs ? Xs + (int64_t)k * k : wv + kpad;   // shared work area
   const int group = (int)blockIdx.x / C, crank = (int)blockIdx.x - group * C;
   const int wdoubles = C > 1 ? (int)cluster_work_doubles(k) : (int)work_doubles(k);
   __shared__ double crec[2 * 8 * 4];
@@ -2314,10 +2314,10 @@ __global__ void __launch_bounds__(FW_WARPS * 32) factor_finish_wide_kernel(Facto
     for (int i = c + 1 + lane; i < KP; i += 32) out[(i / CT_K) * CT_TILE + i % CT_K] = 0.0;
 }
 
-static int g_cluster_mode = 1;   // host: band-cluster path for 128 < k <= 256 (cqr_debug_factor_cluster)
+static int g_cluster_mode = 1;   // host: band-cluster path for 96 < k <= 256 (cqr_debug_factor_cluster)
 
 int factor_set_cluster(int on) {
-  g_cluster_mode = on ? 1 : 0;
+  g_cluster_mode = (on >= 0 && on <= 2) ? on : 1;
   return 0;
 }
 
@@ -2369,12 +2369,19 @@ cudaError_t factor_launch(FactorArgs& a, cudaStream_t stream) {
   }
   static unsigned epoch = 0;
   a.epoch = ++epoch;   // tags the speculative handshake of this launch (no reset launch needed)
-  if (a.k > FK_SMEM_K) {
+  // band-cluster path: one cluster of ceil(k / 32) CTAs per attempt chain (band r on
+  // CTA r) for 96 < k <= 256 (mode 1, the default: at least 4 bands; with 2-3 bands
+  // the hand-overs cost what the cluster distributes -- measured k = 72: 60.5 -> 65.2
+  // us, k = 96: equal, k = 128: plain 87.9 -> 85.6, shifted 121 -> 105 us per call)
+  // or 64 < k <= 256 (mode 2, diagnostics).  The update policy's deflation at
+  // k <= 128 stays on the single CTA (Bt staged in shared memory)
+  const bool small_ok = !(a.policy == CQR_POLICY_UPDATE && a.q > 0);
+  const int kmin = !small_ok ? FK_SMEM_K : (g_cluster_mode == 2 ? 64 : 96);
+  a.ncl = (g_cluster_mode && a.k > kmin && a.k <= FK_BIG_K) ? (a.k + 31) / 32 : 1;
+  if (a.k > FK_SMEM_K || a.ncl > 1) {
     const int nt = (a.k + 31) / 32;
     factor_prep_kernel<<<nt * (nt + 1) / 2, FP_THREADS, 0, stream>>>(a);
   }
-  // 128 < k <= 256: one cluster of ceil(k / 32) CTAs per attempt chain (band r on CTA r)
-  a.ncl = (g_cluster_mode && a.k > FK_SMEM_K && a.k <= FK_BIG_K) ? (a.k + 31) / 32 : 1;
   if (a.ncl > 1) {
     smem = (32 + 3 * (size_t)kpad + (size_t)cluster_work_doubles(a.k)) * sizeof(double);
   }

@@ -1,4 +1,4 @@
-"""The band-cluster k x k stage (128 < k <= 256: one CTA per 32-row band in a
+"""The band-cluster k x k stage (96 < k <= 256: one CTA per 32-row band in a
 thread-block cluster, DSMEM hand-over, cluster-distributed power iteration,
 speculative RECOMPUTE merged by the finish kernel) against the single-CTA
 path on the same Gramians (cqr_debug_factor_cluster).  Both implement
@@ -58,7 +58,7 @@ def _run(k, policy, g, cluster, fixed_shift=0.0):
         cx.lib.cqr_debug_factor_cluster(1)
 
 
-@pytest.mark.parametrize("k", [129, 160, 200, 255, 256])
+@pytest.mark.parametrize("k", [100, 128, 129, 160, 200, 255, 256])
 @pytest.mark.parametrize("policy", ["plain", "recompute", "shift_once"])
 def test_cluster_matches_single_cta_on_spd(k, policy):
     g = _gram(k, "spd", seed=k)
@@ -74,7 +74,10 @@ def test_cluster_matches_single_cta_on_spd(k, policy):
     np.testing.assert_allclose(a[2], b[2], rtol=0, atol=1e-12 * np.abs(b[2]).max())
     if policy == "shift_once":
         np.testing.assert_allclose(a[0].shifts, b[0].shifts, rtol=1e-12)
-        assert a[0].norm_est == b[0].norm_est       # the distributed power iteration: the same bits
+        if k > 128:   # the same per-row and reduction order as the single CTA's X-in-L2 estimate: the same bits
+            assert a[0].norm_est == b[0].norm_est
+        else:         # the single CTA runs its warp-only iteration on X in shared memory (another order)
+            assert abs(a[0].norm_est / b[0].norm_est - 1) < 1e-12
 
 
 @pytest.mark.parametrize("k", [136, 256])

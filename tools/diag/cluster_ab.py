@@ -44,9 +44,12 @@ def gramian(k, kind, seed):
     return 0.5 * (g + g.T)
 
 
+CLUSTER_ON = int(os.environ.get("CQR_CLUSTER_MODE", "1"))
+
+
 def one(k, policy, kind, seed, cluster, q=0):
     cx = ctx()
-    cx.lib.cqr_debug_factor_cluster(cluster)
+    cx.lib.cqr_debug_factor_cluster(CLUSTER_ON if cluster else 0)
     eng = Engine(k, cq.AlgoConfig(), q=q)
     g = torch.from_numpy(gramian(k, kind, seed)).to(cx.device)
     eng.G.copy_(g)
@@ -87,7 +90,7 @@ def timing(k, policy, kind, n=20):
     out = {"k": k, "policy": policy, "kind": kind}
     for cluster in (0, 1):
         cx = ctx()
-        cx.lib.cqr_debug_factor_cluster(cluster)
+        cx.lib.cqr_debug_factor_cluster(CLUSTER_ON if cluster else 0)
         eng = Engine(k, cq.AlgoConfig())
         g = torch.from_numpy(gramian(k, kind, 1)).to(cx.device)
         for _ in range(3):
@@ -125,17 +128,21 @@ def timing(k, policy, kind, n=20):
 
 if __name__ == "__main__":
     bad = 0
-    for k in (129, 136, 160, 200, 224, 255, 256):
+    KS = (72, 96, 100, 128) if CLUSTER_ON == 2 else (129, 136, 160, 200, 224, 255, 256)
+    for k in KS:
         for policy, kind in (("plain", "spd"), ("plain", "illcond"), ("plain", "zerocol"), ("recompute", "spd"),
                              ("recompute", "illcond"), ("recompute", "indef"), ("shift_once", "illcond"),
                              ("fixed", "illcond"), ("estimate", "spd")):
             for seed in (1, 2):
                 bad += not compare(k, policy, kind, seed)
-    for k in (160, 256):
+    for k in ((96, 128) if CLUSTER_ON == 2 else (160, 256)):
         bad += not compare(k, "update", "illcond", 3, q=24)
         bad += not compare(k, "update", "spd", 3, q=24)
-    for k, policy, kind in ((256, "plain", "spd"), (256, "recompute", "spd"), (256, "recompute", "illcond"),
-                            (256, "shift_once", "illcond"), (192, "plain", "spd"), (160, "recompute", "illcond")):
+    TIMING = (((128, "plain", "spd"), (128, "recompute", "illcond"), (96, "plain", "spd"), (128, "shift_once", "illcond"),
+               (72, "plain", "spd")) if CLUSTER_ON == 2 else
+              ((256, "plain", "spd"), (256, "recompute", "spd"), (256, "recompute", "illcond"),
+               (256, "shift_once", "illcond"), (192, "plain", "spd"), (160, "recompute", "illcond")))
+    for k, policy, kind in TIMING:
         timing(k, policy, kind)
     ctx().lib.cqr_debug_factor_cluster(1)
     print(json.dumps({"mismatches": bad}))
