@@ -225,9 +225,9 @@ void cqr_debug_update_tma(int on);
 /* Diagnostics: 1 (default) = the blocked Cholesky in bands of 32 pivots with a
  * rank-32 update between bands; 0 = one lookahead chain over all block steps. */
 int cqr_debug_factor_banded(int on);
-/* 1 (default): 96 < k <= 256 factors on a thread-block cluster of ceil(k/32)
-   CTAs, one 32-row band each (the update policy with a basis: 128 < k);
-   2: from 64 < k; 0: the single-CTA path (for A/B comparisons). */
+/* 1 (default): 128 < k <= 256 (96 < k for the estimating policies) factors on
+   a thread-block cluster of ceil(k/32) CTAs, one 32-row band each; 2: from
+   64 < k (but the update policy with a basis); 0: the single-CTA path (A/B). */
 int cqr_debug_factor_cluster(int on);
 /* Diagnostics: globaltimer stamps (ns) of the band-cluster path's last attempt,
  * [band][event] (HOST array of 64; synchronous). */

@@ -35,6 +35,8 @@ class DeviceContext:
             raise RuntimeError(
                 "paper_2507_07788_b200 needs a CUDA device (B200, sm_100a); there is no CPU fallback")
         self.lib = _lib.load()
+        if "CQR_FACTOR_CLUSTER" in os.environ:   # diagnostics: k x k stage schedule (cqr_debug_factor_cluster)
+            self.lib.cqr_debug_factor_cluster(int(os.environ["CQR_FACTOR_CLUSTER"]))
         if torch.distributed.is_available() and torch.distributed.is_initialized():
             self.rank = torch.distributed.get_rank()
             self.world = torch.distributed.get_world_size()

@@ -2370,13 +2370,16 @@ cudaError_t factor_launch(FactorArgs& a, cudaStream_t stream) {
   static unsigned epoch = 0;
   a.epoch = ++epoch;   // tags the speculative handshake of this launch (no reset launch needed)
   // band-cluster path: one cluster of ceil(k / 32) CTAs per attempt chain (band r on
-  // CTA r) for 96 < k <= 256 (mode 1, the default: at least 4 bands; with 2-3 bands
-  // the hand-overs cost what the cluster distributes -- measured k = 72: 60.5 -> 65.2
-  // us, k = 96: equal, k = 128: plain 87.9 -> 85.6, shifted 121 -> 105 us per call)
-  // or 64 < k <= 256 (mode 2, diagnostics).  The update policy's deflation at
-  // k <= 128 stays on the single CTA (Bt staged in shared memory)
+  // CTA r) for 128 < k <= 256, and from 96 < k for the policies that run a norm
+  // estimate (its distributed power iteration is where 4 bands gain: k = 128
+  // shifted calls 121 -> 105 us; a plain k = 128 call measured 0.095 -> 0.103 ms
+  // in config 2, and with 2-3 bands the hand-overs cost what the cluster
+  // distributes).  Mode 2 (diagnostics): from 64 < k for every policy but the
+  // update policy's deflation, which stays on the single CTA at k <= 128.
+  const bool est_policy = a.policy == CQR_POLICY_SHIFT_ONCE || a.policy == CQR_POLICY_RECOMPUTE ||
+                          a.policy == CQR_POLICY_ESTIMATE;
   const bool small_ok = !(a.policy == CQR_POLICY_UPDATE && a.q > 0);
-  const int kmin = !small_ok ? FK_SMEM_K : (g_cluster_mode == 2 ? 64 : 96);
+  const int kmin = !small_ok ? FK_SMEM_K : (g_cluster_mode == 2 ? 64 : (est_policy ? 96 : FK_SMEM_K));
   a.ncl = (g_cluster_mode && a.k > kmin && a.k <= FK_BIG_K) ? (a.k + 31) / 32 : 1;
   if (a.k > FK_SMEM_K || a.ncl > 1) {
     const int nt = (a.k + 31) / 32;

@@ -34,6 +34,7 @@ def _gram(k, kind, seed):
 
 
 def _run(k, policy, g, cluster, fixed_shift=0.0):
+    """cluster: 1 -> mode 2 (the band-cluster path from k > 64, every policy); 0 -> single CTA."""
     import torch
 
     import paper_2507_07788_b200 as cq
@@ -42,7 +43,7 @@ def _run(k, policy, g, cluster, fixed_shift=0.0):
     from paper_2507_07788_b200._engine import Engine
 
     cx = ctx()
-    cx.lib.cqr_debug_factor_cluster(cluster)
+    cx.lib.cqr_debug_factor_cluster(2 if cluster else 0)
     try:
         eng = Engine(k, cq.AlgoConfig())
         eng.G.copy_(torch.from_numpy(g).to(cx.device))
