@@ -110,6 +110,7 @@ class Engine:
         self._next_slot = 0
         self._stat_ev = [None] * self.nslots   # event after each slot's status write
         self._r_pending = None
+        self._br_pending = None
         self._key = (k, q, self.cap)
         # Buffers come from the context's pool when an earlier run of the same
         # shape released them: a call then starts with one reset copy instead of
@@ -174,6 +175,11 @@ class Engine:
             if self._r_pending is not None:
                 self._r_pending[2].synchronize()
                 self.cx.release_pinned(self._r_pending[0])
+            if self._br_pending is not None:
+                if self._br_pending[2] is not None:
+                    self._br_pending[2].synchronize()
+                self.cx.release_pinned(self._br_pending[0])
+                self.cx.release_pinned(self._br_pending[1])
             ev = torch.cuda.Event()
             ev.record(self._stream)
             free = self.cx.engine_pool.setdefault(self._key, [])
@@ -354,6 +360,34 @@ class Engine:
             self.cx.release_pinned(buf)
             return out
         return self._to_host(self.Racc[:, : self.k])
+
+    def br_prefetch(self):
+        """Enqueue the downloads of B and R (whole Racc buffer) into one pair of
+        pinned buffers, reused on every call: the update loop enqueues them
+        behind every newly enqueued pass (passes after convergence are gated
+        no-ops, so the last downloads hold the final B and R), and br_host() then
+        waits once instead of two synchronous round trips after the loop."""
+        if self._br_pending is None:
+            bb = self.cx.acquire_pinned((self.B.numel() * 8,))
+            rb = self.cx.acquire_pinned((self.Racc.numel() * 8,))
+            self._br_pending = [bb, rb, None]
+        bb, rb, _ = self._br_pending
+        self._store_host(self.B, bb)
+        self._store_host(self.Racc, rb)
+        ev = torch.cuda.Event()
+        ev.record(self._stream)
+        self._br_pending[2] = ev
+
+    def br_host(self):
+        """(B, R) as row-major numpy arrays, from the last br_prefetch."""
+        bb, rb, ev = self._br_pending
+        self._br_pending = None
+        ev.synchronize()
+        b = bb.view(torch.float64)[: self.B.numel()].view(self.B.shape).numpy().T.copy()
+        r = rb.view(torch.float64)[: self.Racc.numel()].view(self.Racc.shape).numpy()[:, : self.k].T.copy()
+        self.cx.release_pinned(bb)
+        self.cx.release_pinned(rb)
+        return b, r
 
     def b_host(self):
         return self._to_host(self.B)

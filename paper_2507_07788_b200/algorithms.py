@@ -605,6 +605,7 @@ def _update_pipelined(eng, q_in, r_in, a_new, m, k, p, width, tol, cfg, ledger):
     while True:
         if its + 1 <= cfg.max_iter:
             enqueue(its + 1)
+        eng.br_prefetch()   # B and R as of the last enqueued pass (later passes are gated no-ops)
         (st,) = eng.collect([handles[its]])
         errs.append(st.err)
         _charge(ledger, "fro_norm", _flops.frobenius_flops(p))
@@ -636,7 +637,8 @@ def _update_pipelined(eng, q_in, r_in, a_new, m, k, p, width, tol, cfg, ledger):
         q_out = q_in._claim_tail(p)           # already written in place
     else:
         q_out = q_in.extended(outs[its - 1])
-    r_out = np.block([[r_in, eng.b_host()], [np.zeros((p, k)), eng.r_host()]])
+    b_host, r_host = eng.br_host()
+    r_out = np.block([[r_in, b_host], [np.zeros((p, k)), r_host]])
     return QRResult(q_out, r_out, its, shifts, attempts, success=success, orth_error=st.err,
                     pivot_margins=margins, decision_margins=dms, err_history=errs)
 

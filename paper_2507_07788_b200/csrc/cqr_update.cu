@@ -553,7 +553,14 @@ __global__ void update_reduce_kernel(const double* __restrict__ ws, int nparts, 
 #pragma unroll
       for (int j = 0; j < 32; ++j) s += v[j];
     }
-    for (; i < nparts; ++i) s += ws[i * ps + off];
+    if (i < nparts) {   // the remainder as one masked batch (one L2 round trip, not one per partial)
+      double v[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = (i + j < nparts) ? ws[(i + j) * ps + off] : 0.0;
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (i + j < nparts) s += v[j];
+    }
     if (e < nbt) Bt[(int64_t)c * ldbt + r] = s;
     else { G[(int64_t)c * ldg + r] = s; G[(int64_t)r * ldg + c] = s; }
   }
