@@ -777,27 +777,33 @@ __device__ __forceinline__ void fmark(int slot) {
 }
 
 // ---------------------------------------------------------------------------
-// Band-cluster Cholesky (128 < k <= 256).  One attempt runs on a thread-block
-// cluster of C = ceil(k / 32) CTAs; CTA r owns band r -- rows [32r, 32r + 32)
-// x columns [32r, k) of the upper triangle -- in its shared memory:
+// Band-cluster Cholesky (96 < k <= 256, see factor_launch).  One attempt runs
+// on a thread-block cluster of C = ceil(k / 32) CTAs; CTA r owns band r --
+// rows [32r, 32r + 32) x columns [32r, k) of the upper triangle -- in its
+// shared memory:
 //   1. load its band of X + sigma I (every load of the band in flight at once);
-//   2. for b = 0 .. r-1, as band b is published: stage R(band b, cols >= 32r)
-//      from Rk (L2, ld.global.cg) and apply the rank-32 update C -= R_b^T R_b
-//      to the band with DMMA (per element: P ascending, k4 0 then 4 -- the
-//      chain of the single-CTA banded path);
-//   3. factor its band with the in-band blocked steps (chol_banded);
-//   4. write its rows of R to Rk and publish the band (st.release.gpu of an
-//      epoch / attempt tagged flag; a breakdown or an abort is published too,
-//      so later bands stop instead of waiting);
+//   2. for b = 0 .. r-1: apply the rows of band b, block row by block row, as
+//      rank-8 DMMA updates of its band (per element: b, then P ascending, k4 0
+//      then 4 -- the chain of the single-CTA banded path).  The rows are read
+//      straight from band b's shared memory (DSMEM, ld.shared::cluster) once
+//      band b has counted them into this CTA's row counter for b (a cluster-
+//      scope release store): the next band takes every block row as it
+//      finishes, the later bands take a band once it is complete;
+//   3. factor its band with the in-band blocked steps (chol_banded); the hook
+//      counts each finished block row into the later bands' counters, from a
+//      worker thread (warp 0 runs the pivot chain).  A breakdown or an abort
+//      is counted too (+15), so later bands stop instead of waiting;
+//   4. write its rows of R to Rk;
 //   5. agree on the outcome: every CTA stores its record into every CTA's
 //      shared memory (DSMEM), one cluster barrier, the lowest band that did
 //      not hold decides (its pivot is the reference's first breakdown).
 // The single-CTA path runs the Schur complement of band 0 and seven rank-32
 // band updates (~60 us of DMMA at k = 256) on one SM between the bands; here
-// they run on C SMs while the bands factor, and the serial part is the
-// hand-over (stage + one rank-32 update) plus the in-band steps.
+// they run on C SMs while the bands factor, and the serial part is the last
+// block row's hand-over plus the in-band steps.  Counters carry the attempt
+// number (seq * 16 + rows), so a retry never reads an earlier attempt's count.
 // A cluster guarantees the C CTAs are co-resident, so waiting on a lower
-// band's flag always terminates (a band never waits on a higher one).
+// band always terminates (a band never waits on a higher one).
 constexpr int FC_LD = 36;   // staged band: column stride (conflict-free DMMA fragment loads)
 constexpr int FC_LD8 = 12;  // one staged block row (8 rows): column stride, conflict-free fragment loads
 
