@@ -222,6 +222,9 @@ int cqr_debug_factor_profile(unsigned long long* out16);
 /* Diagnostics: 1 (default) = the update pass stages narrow sub-panels with one
  * TMA tensor copy each; 0 = per-row-quad bulk copies only (comparisons). */
 void cqr_debug_update_tma(int on);
+/* Diagnostics: 1 (default) = update passes with bases up to 64 columns run two
+ * alternating 4-warp projection teams; 0 = one 8-warp projection group. */
+int cqr_debug_update_narrow_teams(int on);
 /* Diagnostics: 1 (default) = the blocked Cholesky in bands of 32 pivots with a
  * rank-32 update between bands; 0 = one lookahead chain over all block steps. */
 int cqr_debug_factor_banded(int on);

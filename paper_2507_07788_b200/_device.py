@@ -37,6 +37,8 @@ class DeviceContext:
         self.lib = _lib.load()
         if "CQR_FACTOR_CLUSTER" in os.environ:   # diagnostics: k x k stage schedule (cqr_debug_factor_cluster)
             self.lib.cqr_debug_factor_cluster(int(os.environ["CQR_FACTOR_CLUSTER"]))
+        if "CQR_UPDATE_NARROW_TEAMS" in os.environ:   # diagnostics: narrow update pass schedule
+            self.lib.cqr_debug_update_narrow_teams(int(os.environ["CQR_UPDATE_NARROW_TEAMS"]))
         if torch.distributed.is_available() and torch.distributed.is_initialized():
             self.rank = torch.distributed.get_rank()
             self.world = torch.distributed.get_world_size()

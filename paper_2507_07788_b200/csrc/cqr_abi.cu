@@ -270,6 +270,8 @@ int cqr_update_pass(const double* Qin, int64_t ldqin, int q, double* Q, int64_t 
 
 int cqr_debug_factor_profile(unsigned long long* out16) { return cqr::factor_profile(out16); }
 void cqr_debug_update_tma(int on) { cqr::set_update_tma(on); }
+
+int cqr_debug_update_narrow_teams(int on) { return cqr::update_set_narrow_teams(on); }
 int cqr_debug_factor_banded(int on) { return cqr::factor_set_banded(on); }
 
 int cqr_debug_factor_cluster(int on) { return cqr::factor_set_cluster(on); }

@@ -93,8 +93,10 @@ static int up_stages_with(int q, int sr, bool teams) {
 }
 // Two projection teams where they fit with four stages (65 <= q <= 144 at 32-row
 // sub-panels): with two stages the teams starve (q = 160: 3.63 -> 4.58 ms).
+static int g_narrow_teams = 1;   // cqr_debug_update_narrow_teams
 static bool up_teams_q(int q, int sr) {
   const int nq = (q + 63) / 64;
+  if (sr == 64 && nq == 1) return g_narrow_teams && up_stages_with(q, sr, true) >= 4;   // the narrow path
   return sr == 32 && (nq == 2 || nq == 3) && up_stages_with(q, sr, true) >= 4;
 }
 static int up_stages(int q, int sr) { return up_stages_with(q, sr, up_teams_q(q, sr)); }
@@ -192,6 +194,17 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(const __grid
           const int kk = kcolt(c, h) + t, n = 8 * nb + g;
           btt[c][h][nb] = (!init && kk < q && n < p) ? a.Bt[(int64_t)n * a.ldbt + kk] : 0.0;
         }
+    // narrow (q <= 64): warp wt owns the output blocks (row block (wt >> 1) + 2u,
+    // column block wt & 1) of proj over the full width, Bt in registers -- the
+    // 8-warp narrow mapping given to a 4-warp team, the same per-element chains
+    double btn[NARROW ? 16 : 1];
+    if constexpr (NARROW) {
+#pragma unroll
+      for (int ks = 0; ks < 16; ++ks) {
+        const int kk = 4 * ks + t, n = 8 * (wt & 1) + g;
+        btn[ks] = (!init && kk < q && n < p) ? a.Bt[(int64_t)n * a.ldbt + kk] : 0.0;
+      }
+    }
     double* tqt = tq + team * TE;
     const int bar = 2 + team;
     for (int64_t j = team; j < mine; j += 2) {
@@ -208,6 +221,35 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(const __grid
         for (int e = tt; e < (SR - nrows) * qs; e += 128) Qz[e] = 0.0;
       }
       if (!init) {
+       if constexpr (NARROW) {
+        constexpr int NU2 = NARROW ? RB / 2 : 1;
+        const int nbw = wt & 1;
+        double acc[NU2][4][2] = {};   // k4 steps round-robin over four accumulator chains per block
+#pragma unroll
+        for (int ks = 0; ks < 16; ++ks) {
+          if (4 * ks < q) {   // warp-uniform
+#pragma unroll
+            for (int u = 0; u < NU2; ++u) {
+              const int rbw = (wt >> 1) + 2 * u;
+              const double* xa = Qs + (2 * rbw + (g >> 2)) * 4 * qs + (g & 3) + 4 * t;
+              const double av = (4 * ks + t < q) ? xa[16 * ks] : 0.0;
+              dmma(acc[u][ks & 3], av, btn[ks]);
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < NU2; ++u) {
+          const int row = 8 * ((wt >> 1) + 2 * u) + g;
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int col = 8 * nbw + 2 * t + e;
+            const int off = (row >> 2) * 4 * UP_PB + 4 * col + (row & 3);
+            tqt[off] = (col < p && row < nrows)
+                           ? Ys[off] - ((acc[u][0][e] + acc[u][1][e]) + (acc[u][2][e] + acc[u][3][e])) : 0.0;
+          }
+        }
+        asm volatile("bar.sync %0, 128;" ::"r"(bar) : "memory");
+       } else {
         double pr[RB][2][2];
 #pragma unroll
         for (int rb = 0; rb < RB; ++rb)
@@ -246,6 +288,7 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(const __grid
           tqt[e] = (col < p && row < nrows) ? Ys[e] - sum : 0.0;
         }
         asm volatile("bar.sync %0, 128;" ::"r"(bar) : "memory");
+       }
         if (j >= UP_YS) mbar_wait(&yempty[ysj], yphj ^ 1);
         for (int qb = wt; qb < 2 * RB; qb += 4) {
           const int rb = qb >> 1, nb = qb & 1;
@@ -635,10 +678,15 @@ static cudaError_t launch_up_t(const UpdateArgs& a, int ctas, size_t smem, cudaS
 
 template <int NQ, int SR>
 static cudaError_t launch_up(const UpdateArgs& a, int ctas, size_t smem, cudaStream_t s) {
-  if constexpr (SR == 32 && (NQ == 2 || NQ == 3)) {
+  if constexpr ((SR == 32 && (NQ == 2 || NQ == 3)) || (SR == 64 && NQ == 1)) {
     if (up_teams_q(a.q, SR)) return launch_up_t<NQ, SR, true>(a, ctas, smem, s);
   }
   return launch_up_t<NQ, SR, false>(a, ctas, smem, s);
+}
+
+int update_set_narrow_teams(int on) {
+  g_narrow_teams = on ? 1 : 0;
+  return 0;
 }
 
 cudaError_t update_pass_launch(const double* Qin, int64_t ldqin, int q, const double* Qb, int64_t ldqb, double* Qo,
