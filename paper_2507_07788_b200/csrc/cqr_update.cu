@@ -512,7 +512,9 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(const __grid
           // a warp whose Bt' rows all lie past q (q < 64: NQ = 1 covers 64 columns)
           // skips its chain, warp-uniformly: at q = 16 six of the eight warps
           // issued DMMAs on zero operands in a pass throttled by the FP64 pipe
-          if (!PART && 64 * c + 8 * wb >= q) continue;
+          if constexpr (NQ == 1) {
+            if (8 * wb >= q) continue;
+          }
           const bool v = PART || 64 * c + 8 * wb + g < q;
           const double av = v ? xa[ks * 4 * qs + 256 * c] : 0.0;
           dmma(ct[c][0], av, b0);
