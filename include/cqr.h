@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define CQR_ABI_VERSION 8
+#define CQR_ABI_VERSION 9
 
 #define CQR_OK 0
 #define CQR_EINVAL (-1)
@@ -285,6 +285,50 @@ int cqr_resid_gram_supported(int k);
 size_t cqr_resid_gram_workspace_bytes(int64_t m, int k);
 int cqr_resid_gram(const double* Q, int64_t ldq, const double* A, int64_t lda, int64_t m, int k, const double* R_tiles,
                    double* DtD, int ldd, double* asq, void* ws, size_t ws_bytes, void* stream);
+
+/* Fixed-schedule runs (chol_qr, chol_qr2, s_chol_qr3), enqueued natively.
+ * The reference's fixed schedules (algorithms.py:201-244) take no host
+ * decision between passes: every pass is Gram -> factor -> TRMM, and the
+ * statuses are inspected only after the last one.  cqr_fixed_schedule
+ * enqueues the whole run with ONE host call, in the order the per-call API
+ * would (bitwise the same kernels and arguments):
+ *     Racc <- Racc0;  G = X^T X;
+ *     for i < passes:  cqr_factor(fcfg[i], status[i]);
+ *                      dst[i] = src_i R_i^-1 (+ G = dst[i]^T dst[i] unless i is the last pass)
+ *     R_host <- Racc (k * ldr doubles, mapped stores), when R_host != NULL
+ * with src_0 = X and src_i = dst[i-1] (dst[i] may equal src_i where the
+ * in-place rules of cqr_apply_gram / cqr_lincomb allow it).
+ * use_graph != 0: the run is captured once as a CUDA graph, keyed on every
+ * field of the plan and of the three factor configs, and replayed on later
+ * calls with the same key (one graph launch instead of ~10 kernel launches).
+ * Local rows only: no cross-rank reduction happens inside (world size 1). */
+#define CQR_FIXED_MAX_PASSES 3
+typedef struct cqr_fixed_plan {
+  int32_t passes;            /* 1 (chol_qr), 2 (chol_qr2), 3 (s_chol_qr3)   */
+  int32_t k;
+  int64_t m;                 /* local rows                                  */
+  const double* X;
+  int64_t ldx;
+  double* dst[CQR_FIXED_MAX_PASSES];
+  int64_t lddst[CQR_FIXED_MAX_PASSES];
+  double* G;                 /* k x k, ldg = k                              */
+  double* Rk;
+  double* Rinv;
+  double* Racc;
+  const double* Racc0;       /* reset source of Racc (k x ldr doubles)      */
+  double* R_host;            /* pinned host copy of Racc, or NULL           */
+  int32_t ldr;
+  int32_t use_graph;
+  const cqr_factor_config* fcfg[CQR_FIXED_MAX_PASSES];
+  void* status[CQR_FIXED_MAX_PASSES];  /* device slot: status record, then shifts at +96 bytes */
+  void* fws;
+  size_t fws_bytes;
+  void* ws;                  /* Gram / apply_gram workspace                 */
+  size_t ws_bytes;
+} cqr_fixed_plan;
+int cqr_fixed_schedule(const cqr_fixed_plan* plan, void* stream);
+/* number of CUDA graphs cached by cqr_fixed_schedule (this process) */
+int cqr_fixed_graphs(void);
 
 #ifdef __cplusplus
 }

@@ -12,6 +12,7 @@ Per run the engine owns, on the device:
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 import torch
@@ -20,6 +21,12 @@ from . import _lib
 from ._device import ctx, round_up
 
 STATUS_BYTES = 96   # sizeof(cqr_factor_status) rounded to 16
+
+# Fixed schedules (chol_qr, chol_qr2, s_chol_qr3) enqueue natively through
+# cqr_fixed_schedule, replayed as a CUDA graph: CQR_NATIVE_SCHEDULE=0 keeps the
+# per-kernel Python launches, =1 the native enqueue without a graph, =2 (default)
+# the native enqueue captured as a graph.
+NATIVE_SCHEDULE = int(os.environ.get("CQR_NATIVE_SCHEDULE", "2"))
 
 
 def _gram_ws(m_local, ka, kb, self_):
@@ -97,7 +104,7 @@ class PassStatus:
 class Engine:
     """Buffers and launches for one algorithm run on width-k blocks."""
 
-    def __init__(self, k, cfg, q=0):
+    def __init__(self, k, cfg, q=0, defer_reset=False):
         cx = ctx()
         self.cx = cx
         self.k = k
@@ -127,7 +134,8 @@ class Engine:
             self._stream.wait_event(ev)   # released on another stream
             (self.G, self.Rk, self.Rinv, self.Racc, self._racc0, self.stat_all, self.stat_host_all, self.fws,
              self.B, self.Bt, self._xch, self._fcfg, self._slot_ev) = bufs
-            self.Racc.copy_(self._racc0)
+            if not defer_reset:   # else the caller resets (reset_racc, or the native schedule)
+                self.Racc.copy_(self._racc0)
             if q:
                 self.B.zero_()
                 self.Bt.zero_()
@@ -257,6 +265,75 @@ class Engine:
         ev.record(self._stream)
         self._stat_ev[slot] = ev
         return slot
+
+    def reset_racc(self):
+        self.Racc.copy_(self._racc0)
+
+    def fixed_ok(self):
+        """The native fixed-schedule enqueue applies: one rank (no cross-rank
+        sum between a Gram and its factor call) and no per-launch timer or
+        decision trace attached."""
+        cx = self.cx
+        return NATIVE_SCHEDULE > 0 and cx.world == 1 and cx.trace is None and cx.timer is None
+
+    def run_fixed(self, policies, m_global, width, src, dsts):
+        """Enqueue a whole fixed schedule with one libcqr call
+        (cqr_fixed_schedule): Racc reset, Gram(src), then per pass i the k x k
+        stage (policies[i], status slot i) and dsts[i] = src_i R_i^-1 with the
+        next Gram (plain TRMM on the last pass), then R's download.  Returns
+        the status handles (slots 0..len-1) for collect()."""
+        cx = self.cx
+        k = self.k
+        n = len(policies)
+        assert 1 <= n <= 3 and len(dsts) == n and self._next_slot == 0
+        plan = _lib.FixedPlan()
+        plan.passes = n
+        plan.k = k
+        plan.m = src.m_local
+        plan.X = src.ptr()
+        plan.ldx = src.ld
+        for i, d in enumerate(dsts):
+            plan.dst[i] = d.ptr()
+            plan.lddst[i] = d.ld
+            fc = self._fcfg[i]
+            fc.policy = policies[i]
+            fc.shift_width = width
+            fc.m_global = m_global
+            fc.check_tol = 0
+            fc.tol = 0.0
+            fc.stop = 0
+            fc.update_b = 0
+            fc.est_max_iter = 100
+            fc.est_tol = 1e-2
+            fc.fixed_shift = 0.0
+            fc.gate = None
+            plan.fcfg[i] = ctypes.pointer(fc)
+            plan.status[i] = self.stat_all[i].data_ptr()
+        plan.G = self.G.data_ptr()
+        plan.Rk = self.Rk.data_ptr()
+        plan.Rinv = self.Rinv.data_ptr()
+        plan.Racc = self.Racc.data_ptr()
+        plan.Racc0 = self._racc0.data_ptr()
+        plan.ldr = self.ldr
+        buf = cx.acquire_pinned((self.Racc.numel() * 8,))
+        plan.R_host = buf.data_ptr()
+        plan.use_graph = 1 if NATIVE_SCHEDULE >= 2 else 0
+        plan.fws = self.fws.data_ptr()
+        plan.fws_bytes = self.fws.numel()
+        ws = cx.workspace(max(cx.lib.cqr_gram_workspace_bytes(src.m_local, k, k, 1),
+                              cx.lib.cqr_apply_gram_workspace_bytes(src.m_local, k)))
+        plan.ws = ws.data_ptr()
+        plan.ws_bytes = ws.numel()
+        _lib.check(cx.lib.cqr_fixed_schedule(ctypes.byref(plan), cx.stream), "fixed_schedule")
+        cx.launches += 2 + 2 * n + cx.lib.cqr_apply_gram_launches(k) * (n - 1) + 1 + 1
+        ev = self._slot_ev[0]
+        ev.record(self._stream)
+        for i in range(n):
+            self._stat_ev[i] = ev
+        self._next_slot = n % self.nslots
+        view = buf.view(torch.float64)[: self.Racc.numel()].view(self.Racc.shape)[:, :k]
+        self._r_pending = (buf, view, ev)
+        return list(range(n))
 
     # ------------------------------------------------------------ tall passes
     def gram(self, arr):

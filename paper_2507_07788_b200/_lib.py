@@ -70,6 +70,34 @@ class FactorStatus(ctypes.Structure):
     ]
 
 
+class FixedPlan(ctypes.Structure):
+    """cqr_fixed_plan (include/cqr.h)."""
+
+    _fields_ = [
+        ("passes", ctypes.c_int32),
+        ("k", ctypes.c_int32),
+        ("m", ctypes.c_int64),
+        ("X", ctypes.c_void_p),
+        ("ldx", ctypes.c_int64),
+        ("dst", ctypes.c_void_p * 3),
+        ("lddst", ctypes.c_int64 * 3),
+        ("G", ctypes.c_void_p),
+        ("Rk", ctypes.c_void_p),
+        ("Rinv", ctypes.c_void_p),
+        ("Racc", ctypes.c_void_p),
+        ("Racc0", ctypes.c_void_p),
+        ("R_host", ctypes.c_void_p),
+        ("ldr", ctypes.c_int32),
+        ("use_graph", ctypes.c_int32),
+        ("fcfg", ctypes.POINTER(FactorConfig) * 3),
+        ("status", ctypes.c_void_p * 3),
+        ("fws", ctypes.c_void_p),
+        ("fws_bytes", ctypes.c_size_t),
+        ("ws", ctypes.c_void_p),
+        ("ws_bytes", ctypes.c_size_t),
+    ]
+
+
 # name -> (restype, argtypes); mirrors include/cqr.h one to one
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
@@ -117,6 +145,8 @@ SIGNATURES = {
     "cqr_resid_gram_supported": (_I, [_I]),
     "cqr_resid_gram_workspace_bytes": (_SZ, [_I64, _I]),
     "cqr_resid_gram": (_I, [_P, _I64, _P, _I64, _I64, _I, _P, _P, _I, _P, _P, _SZ, _P]),
+    "cqr_fixed_schedule": (_I, [ctypes.POINTER(FixedPlan), _P]),
+    "cqr_fixed_graphs": (_I, []),
     "cqr_factor": (_I, [ctypes.POINTER(FactorConfig), _I, _P, _I, _P, _I, _I, _P, _P, _I, _P, _P, _I, _P, _P,
                         _P, _SZ, _P]),
 }

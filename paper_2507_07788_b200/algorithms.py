@@ -191,13 +191,7 @@ def chol_qr(a, cfg=None, ledger=None):
     if a.ncols < 1:
         raise ValueError("need at least one column")
     m, n = a.space.dim, a.ncols
-    eng = Engine(n, cfg)
-    eng.gram(a)
-    h = eng.factor_async(_lib.POLICY_PLAIN, m, n)
-    q = _fresh_like(a, n)
-    eng.apply(a, q, with_gram=False)
-    eng.r_prefetch()
-    (st,) = eng.collect([h])
+    eng, q, (st,) = _run_fixed(a, cfg, [_lib.POLICY_PLAIN])
     _charge(ledger, "gemm", _flops.gemm_flops(m, n, n))
     _charge_plain_attempt(ledger, n)
     _raise_for(st)
@@ -222,15 +216,7 @@ def chol_qr2(a, cfg=None, ledger=None):
     if a.ncols < 1:
         raise ValueError("need at least one column")
     m, n = a.space.dim, a.ncols
-    eng = Engine(n, cfg)
-    eng.gram(a)
-    h1 = eng.factor_async(_lib.POLICY_PLAIN, m, n)
-    q = _fresh_like(a, n)
-    eng.apply(a, q, with_gram=True)
-    h2 = eng.factor_async(_lib.POLICY_PLAIN, m, n)
-    _apply_last(eng, q)
-    eng.r_prefetch()
-    st1, st2 = eng.collect([h1, h2])
+    eng, q, (st1, st2) = _run_fixed(a, cfg, [_lib.POLICY_PLAIN, _lib.POLICY_PLAIN])
     margins = []
     for i, st in enumerate((st1, st2)):
         if i == 1:
@@ -266,6 +252,48 @@ def _apply_gram_into(eng, src, fresh_ok):
     return dst
 
 
+def _run_fixed(a, cfg, policies):
+    """Enqueue a fixed schedule -- Gram(A), then per pass the k x k stage
+    (policies[i]) and Q_i = Q_{i-1} R_i^-1 with the next pass's Gram (plain
+    TRMM on the last) -- and read the statuses once at the end.  Returns
+    (engine, Q, statuses).  On one rank the whole schedule is one libcqr call
+    (cqr_fixed_schedule, replayed as a CUDA graph); otherwise, or with a
+    timer / decision trace attached, the same launches go one by one."""
+    m, n = a.space.dim, a.ncols
+    eng = Engine(n, cfg, defer_reset=True)
+    npass = len(policies)
+    if eng.fixed_ok():
+        q = _fresh_like(a, n)
+        dsts = [q]
+        spare = None
+        for i in range(1, npass):
+            last = i == npass - 1
+            if eng.in_place_ok() if last else eng.in_place_gram_ok():
+                dsts.append(dsts[-1])
+                continue
+            if spare is None:
+                spare = _fresh_like(a, n)
+            dsts.append(spare if dsts[-1] is q else q)   # ping-pong: never the pass's own source
+        hs = eng.run_fixed(policies, m, n, a, dsts)
+        return eng, dsts[-1], eng.collect(hs)
+    eng.reset_racc()
+    eng.gram(a)
+    hs = []
+    q = a
+    for i, pol in enumerate(policies):
+        hs.append(eng.factor_async(pol, m, n))
+        if i < npass - 1:
+            q = _apply_gram_into(eng, q, fresh_ok=(i == 0))   # the first pass never writes A
+        elif i == 0:
+            dst = _fresh_like(a, n)
+            eng.apply(a, dst, with_gram=False)
+            q = dst
+        else:
+            _apply_last(eng, q)
+    eng.r_prefetch()
+    return eng, q, eng.collect(hs)
+
+
 def s_chol_qr3(a, cfg=None, ledger=None):
     """Shifted first pass (sigma from the first Gram's norm estimate), then two
     plain passes; a breakdown in any pass propagates (algorithms.py:223-244).
@@ -278,17 +306,7 @@ def s_chol_qr3(a, cfg=None, ledger=None):
     if a.ncols < 1:
         raise ValueError("need at least one column")
     m, n = a.space.dim, a.ncols
-    eng = Engine(n, cfg)
-    eng.gram(a)
-    hs = [eng.factor_async(_lib.POLICY_SHIFT_ONCE, m, n)]
-    q = _fresh_like(a, n)
-    eng.apply(a, q, with_gram=True)
-    hs.append(eng.factor_async(_lib.POLICY_PLAIN, m, n))
-    q = _apply_gram_into(eng, q, fresh_ok=False)
-    hs.append(eng.factor_async(_lib.POLICY_PLAIN, m, n))
-    _apply_last(eng, q)
-    eng.r_prefetch()
-    sts = eng.collect(hs)
+    eng, q, sts = _run_fixed(a, cfg, [_lib.POLICY_SHIFT_ONCE, _lib.POLICY_PLAIN, _lib.POLICY_PLAIN])
 
     st = sts[0]
     _charge(ledger, "gemm", _flops.gemm_flops(m, n, n))

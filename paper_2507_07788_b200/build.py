@@ -19,7 +19,8 @@ INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 LIB = os.path.join(HERE, "libcqr.so")
 OBJ = os.path.join(HERE, "build_obj")
 SOURCES = ["cqr_abi.cu", "cqr_gram.cu", "cqr_gram_pairs.cu", "cqr_gemm.cu", "cqr_layout.cu", "cqr_fused.cu",
-           "cqr_update.cu", "cqr_factor.cu", "cqr_small.cu", "cqr_device.cu", "cqr_metrics.cu"]
+           "cqr_update.cu", "cqr_factor.cu", "cqr_small.cu", "cqr_device.cu", "cqr_metrics.cu",
+           "cqr_schedule.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = [

@@ -35,6 +35,10 @@ int check_tall(const double* X, int64_t ldk, int64_t m, int k, const char* who) 
 
 }  // namespace
 
+namespace cqr {
+int set_error(int code, const std::string& msg) { return fail(code, msg); }
+}  // namespace cqr
+
 extern "C" {
 
 int cqr_abi_version(void) { return CQR_ABI_VERSION; }

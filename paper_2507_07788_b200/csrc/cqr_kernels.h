@@ -6,7 +6,12 @@
 
 #include "../../include/cqr.h"
 
+#include <string>
+
 namespace cqr {
+
+// record `msg` as cqr_last_error() of this thread and return `code` (cqr_abi.cu)
+int set_error(int code, const std::string& msg);
 
 int num_sms();   // of the current device (cqr_device.cu)
 // opt the kernel `fn` into `bytes` of dynamic shared memory on the current

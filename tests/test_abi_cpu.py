@@ -44,7 +44,7 @@ def test_python_binding_covers_the_header():
 
 
 def test_abi_version(lib):
-    assert lib.cqr_abi_version() == 8
+    assert lib.cqr_abi_version() == 9
 
 
 def test_struct_layouts_match_header(tmp_path):
@@ -55,7 +55,8 @@ def test_struct_layouts_match_header(tmp_path):
     from paper_2507_07788_b200 import _lib
 
     lines = []
-    for cname, cls in (("cqr_factor_status", _lib.FactorStatus), ("cqr_factor_config", _lib.FactorConfig)):
+    for cname, cls in (("cqr_factor_status", _lib.FactorStatus), ("cqr_factor_config", _lib.FactorConfig),
+                      ("cqr_fixed_plan", _lib.FixedPlan)):
         lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
         for f, _ in cls._fields_:
             lines.append(f'printf("{cname} {f} %zu\\n", offsetof({cname}, {f}));')
@@ -70,7 +71,8 @@ def test_struct_layouts_match_header(tmp_path):
         if line:
             name, field, val = line.split()
             table[(name, field)] = int(val)
-    for cname, cls in (("cqr_factor_status", _lib.FactorStatus), ("cqr_factor_config", _lib.FactorConfig)):
+    for cname, cls in (("cqr_factor_status", _lib.FactorStatus), ("cqr_factor_config", _lib.FactorConfig),
+                      ("cqr_fixed_plan", _lib.FixedPlan)):
         assert table[(cname, "size")] == ctypes.sizeof(cls)
         for f, _ in cls._fields_:
             assert table[(cname, f)] == getattr(cls, f).offset, (cname, f)

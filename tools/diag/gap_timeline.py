@@ -37,6 +37,10 @@ with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
 ev = sorted([e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA],
             key=lambda e: e.time_range.start)
 busy = sum(e.time_range.end - e.time_range.start for e in ev)
+durs = {}
+for i, e in enumerate(ev):
+    nm = e.name.split("(")[0].replace("void ", "")[:36]
+    durs.setdefault((i % max(1, len(ev) // args.calls), nm), []).append(e.time_range.end - e.time_range.start)
 gaps = {}
 prev = None
 for e in ev:
@@ -50,5 +54,7 @@ print(json.dumps({"m": m, "k": k, "wall_us_per_call": round(wall, 1),
                   "gpu_busy_us_per_call": round(busy / args.calls, 1),
                   "gpu_span_us_per_call": round(span / args.calls, 1),
                   "kernels_per_call": len(ev) / args.calls,
+                  "kernel_us_in_call_order": [[nm, round(sum(v) / len(v), 1)] for (i, nm), v in
+                                              sorted(durs.items())],
                   "idle_before_us_per_call": {n: round(sum(v) / args.calls, 1) for n, v in
                                               sorted(gaps.items(), key=lambda x: -sum(x[1]))}}, indent=1))
