@@ -50,6 +50,7 @@ class DeviceContext:
         self._ws = torch.empty(0, dtype=torch.uint8, device=self.device)
         self._ws2 = torch.empty(0, dtype=torch.uint8, device=self.device)
         self._pinned = {}   # shape -> free pinned host buffers (status slots; cudaHostAlloc is slow)
+        self._streams = {}   # raw cudaStream_t -> torch Stream (torch_stream)
         self.engine_pool = {}   # (k, q, status capacity) -> [(Engine buffers, release event)]
         self.launches = 0   # libcqr kernel launches issued (bench bookkeeping)
         self.timer = None   # optional KernelTimer (bench): CUDA events per libcqr call
@@ -59,6 +60,15 @@ class DeviceContext:
         self.trace = None
 
     # ---------------------------------------------------------------- plumbing
+    def torch_stream(self):
+        """torch's current stream as a Stream object, cached by raw handle
+        (torch.cuda.current_stream() builds a new object per query, ~8 us)."""
+        raw = _raw_stream(self.device.index)
+        s = self._streams.get(raw)
+        if s is None:
+            s = self._streams[raw] = torch.cuda.current_stream(self.device)
+        return s
+
     @property
     def stream(self):
         """Handle of torch's current stream on this device (the raw query: building

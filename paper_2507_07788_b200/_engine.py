@@ -87,6 +87,19 @@ _STATUS_DTYPE = np.dtype({
     "itemsize": ctypes.sizeof(_lib.FactorStatus)})
 
 
+_LAUNCHES = {}
+
+
+def _fixed_launches(lib, k, n):
+    """Kernels one cqr_fixed_schedule run launches: Gram (2), per pass the
+    k x k stage (2) and the TRMM (+ Gram), R's download (1)."""
+    key = (k, n)
+    v = _LAUNCHES.get(key)
+    if v is None:
+        v = _LAUNCHES[key] = 2 + 2 * n + lib.cqr_apply_gram_launches(k) * (n - 1) + 1 + 1
+    return v
+
+
 class PassStatus:
     """Host copy of one cqr_factor_status plus the shifts it appended."""
 
@@ -126,14 +139,14 @@ class Engine:
         # Rk / Rinv, so only Racc (and the update blocks) need resetting.
         # the stream this run enqueues on (a call runs on one stream; torch's
         # current_stream() costs ~8 us of host time per query)
-        self._stream = torch.cuda.current_stream(cx.device)
+        self._stream = cx.torch_stream()
         free = cx.engine_pool.get(self._key)
         reused = bool(free)
         if reused:
             bufs, ev = free.pop()
             self._stream.wait_event(ev)   # released on another stream
             (self.G, self.Rk, self.Rinv, self.Racc, self._racc0, self.stat_all, self.stat_host_all, self.fws,
-             self.B, self.Bt, self._xch, self._fcfg, self._slot_ev) = bufs
+             self.B, self.Bt, self._xch, self._fcfg, self._slot_ev, self._fx) = bufs
             if not defer_reset:   # else the caller resets (reset_racc, or the native schedule)
                 self.Racc.copy_(self._racc0)
             if q:
@@ -173,6 +186,7 @@ class Engine:
                 hp = self.stat_host_all[slot].data_ptr()
                 self._fcfg.append(_lib.FactorConfig(accumulate=1, status_mirror=hp, shifts_mirror=hp + STATUS_BYTES))
             self._slot_ev = [torch.cuda.Event() for _ in range(self.nslots)]
+            self._fx = None   # native fixed-schedule state (run_fixed), built on first use
         for fc in self._fcfg:
             fc.unit_roundoff = cfg.unit_roundoff
             fc.shift_escalation = cfg.shift_escalation
@@ -182,7 +196,8 @@ class Engine:
         try:
             if self._r_pending is not None:
                 self._r_pending[2].synchronize()
-                self.cx.release_pinned(self._r_pending[0])
+                if self._r_pending[0] is not None:
+                    self.cx.release_pinned(self._r_pending[0])
             if self._br_pending is not None:
                 if self._br_pending[2] is not None:
                     self._br_pending[2].synchronize()
@@ -193,9 +208,11 @@ class Engine:
             free = self.cx.engine_pool.setdefault(self._key, [])
             if len(free) < 2:
                 free.append(((self.G, self.Rk, self.Rinv, self.Racc, self._racc0, self.stat_all, self.stat_host_all,
-                              self.fws, self.B, self.Bt, self._xch, self._fcfg, self._slot_ev), ev))
+                              self.fws, self.B, self.Bt, self._xch, self._fcfg, self._slot_ev, self._fx), ev))
             else:
                 self.cx.release_pinned(self.stat_host_all)
+                if self._fx is not None:
+                    self.cx.release_pinned(self._fx[3])
         except Exception:   # interpreter shutdown
             pass
 
@@ -276,6 +293,32 @@ class Engine:
         cx = self.cx
         return NATIVE_SCHEDULE > 0 and cx.world == 1 and cx.trace is None and cx.timer is None
 
+    def _fixed_state(self):
+        """The cqr_fixed_plan of this engine's buffers with every static field
+        set, its dst / lddst arrays, the pinned R buffer it downloads into and
+        a NumPy view of R there (kept with the pooled buffers: per call only
+        the shape, the tall operands and the workspace are written)."""
+        if self._fx is None:
+            k = self.k
+            plan = _lib.FixedPlan()
+            plan.k = k
+            plan.G = self.G.data_ptr()
+            plan.Rk = self.Rk.data_ptr()
+            plan.Rinv = self.Rinv.data_ptr()
+            plan.Racc = self.Racc.data_ptr()
+            plan.Racc0 = self._racc0.data_ptr()
+            plan.ldr = self.ldr
+            plan.fws = self.fws.data_ptr()
+            plan.fws_bytes = self.fws.numel()
+            for i in range(3):
+                plan.fcfg[i] = ctypes.pointer(self._fcfg[i])
+                plan.status[i] = self.stat_all[i].data_ptr()
+            rbuf = self.cx.acquire_pinned((self.Racc.numel() * 8,))
+            plan.R_host = rbuf.data_ptr()
+            rview = rbuf.numpy().view(np.float64).reshape(self.Racc.shape)[:, :k]
+            self._fx = (plan, plan.dst, plan.lddst, rbuf, rview, {})
+        return self._fx
+
     def run_fixed(self, policies, m_global, width, src, dsts):
         """Enqueue a whole fixed schedule with one libcqr call
         (cqr_fixed_schedule): Racc reset, Gram(src), then per pass i the k x k
@@ -286,15 +329,15 @@ class Engine:
         k = self.k
         n = len(policies)
         assert 1 <= n <= 3 and len(dsts) == n and self._next_slot == 0
-        plan = _lib.FixedPlan()
+        plan, dst, lddst, _rbuf, rview, wsz = self._fixed_state()
+        m = src.m_local
         plan.passes = n
-        plan.k = k
-        plan.m = src.m_local
+        plan.m = m
         plan.X = src.ptr()
         plan.ldx = src.ld
         for i, d in enumerate(dsts):
-            plan.dst[i] = d.ptr()
-            plan.lddst[i] = d.ld
+            dst[i] = d.ptr()
+            lddst[i] = d.ld
             fc = self._fcfg[i]
             fc.policy = policies[i]
             fc.shift_width = width
@@ -307,32 +350,21 @@ class Engine:
             fc.est_tol = 1e-2
             fc.fixed_shift = 0.0
             fc.gate = None
-            plan.fcfg[i] = ctypes.pointer(fc)
-            plan.status[i] = self.stat_all[i].data_ptr()
-        plan.G = self.G.data_ptr()
-        plan.Rk = self.Rk.data_ptr()
-        plan.Rinv = self.Rinv.data_ptr()
-        plan.Racc = self.Racc.data_ptr()
-        plan.Racc0 = self._racc0.data_ptr()
-        plan.ldr = self.ldr
-        buf = cx.acquire_pinned((self.Racc.numel() * 8,))
-        plan.R_host = buf.data_ptr()
-        plan.use_graph = 1 if NATIVE_SCHEDULE >= 2 else 0
-        plan.fws = self.fws.data_ptr()
-        plan.fws_bytes = self.fws.numel()
-        ws = cx.workspace(max(cx.lib.cqr_gram_workspace_bytes(src.m_local, k, k, 1),
-                              cx.lib.cqr_apply_gram_workspace_bytes(src.m_local, k)))
+        need = wsz.get(m)
+        if need is None:
+            need = wsz[m] = max(cx.lib.cqr_gram_workspace_bytes(m, k, k, 1), cx.lib.cqr_apply_gram_workspace_bytes(m, k))
+        ws = cx.workspace(need)
         plan.ws = ws.data_ptr()
         plan.ws_bytes = ws.numel()
+        plan.use_graph = 1 if NATIVE_SCHEDULE >= 2 else 0
         _lib.check(cx.lib.cqr_fixed_schedule(ctypes.byref(plan), cx.stream), "fixed_schedule")
-        cx.launches += 2 + 2 * n + cx.lib.cqr_apply_gram_launches(k) * (n - 1) + 1 + 1
         ev = self._slot_ev[0]
         ev.record(self._stream)
+        cx.launches += _fixed_launches(cx.lib, k, n)
         for i in range(n):
             self._stat_ev[i] = ev
         self._next_slot = n % self.nslots
-        view = buf.view(torch.float64)[: self.Racc.numel()].view(self.Racc.shape)[:, :k]
-        self._r_pending = (buf, view, ev)
+        self._r_pending = (None, rview, ev)   # R lands in the engine's own pinned buffer
         return list(range(n))
 
     # ------------------------------------------------------------ tall passes
@@ -433,6 +465,8 @@ class Engine:
             buf, view, ev = self._r_pending
             self._r_pending = None
             ev.synchronize()
+            if buf is None:   # run_fixed: a NumPy view of the engine's own buffer
+                return view.T.copy()
             out = view.numpy().T.copy()
             self.cx.release_pinned(buf)
             return out

@@ -12,7 +12,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcqr.so")
+# CQR_LIB (diagnostics only): a variant library built by build.build(defines=..., out=...)
+LIB_PATH = os.environ.get("CQR_LIB") or os.path.join(HERE, "libcqr.so")
 
 CQR_OK = 0
 CQR_EINVAL = -1

@@ -40,20 +40,24 @@ def _stale():
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def _compile(src):
-    obj = os.path.join(OBJ, os.path.splitext(src)[0] + ".o")
-    cmd = [NVCC, *FLAGS, "-I", INCLUDE, "-c", "-o", obj, os.path.join(CSRC, src)]
+def _compile(src, defines=(), objdir=OBJ):
+    obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
+    cmd = [NVCC, *FLAGS, *["-D" + d for d in defines], "-I", INCLUDE, "-c", "-o", obj, os.path.join(CSRC, src)]
     res = subprocess.run(cmd, capture_output=True, text=True)
     return src, obj, res
 
 
-def build(force=False, verbose=False):
-    """Compile every .cu of csrc/ (in parallel) and link one shared library."""
-    if not force and not _stale():
+def build(force=False, verbose=False, defines=(), out=None):
+    """Compile every .cu of csrc/ (in parallel) and link one shared library.
+    `defines` / `out`: a diagnostic variant (e.g. CQR_L2_HINTS=0) written to
+    another path (the product library is always built without them)."""
+    lib = out or LIB
+    if not force and not defines and out is None and not _stale():
         return LIB
-    os.makedirs(OBJ, exist_ok=True)
+    objdir = OBJ if not defines else OBJ + "_" + "_".join(d.replace("=", "") for d in defines)
+    os.makedirs(objdir, exist_ok=True)
     with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as pool:
-        results = list(pool.map(_compile, SOURCES))
+        results = list(pool.map(lambda src: _compile(src, defines, objdir), SOURCES))
     report = []
     failed = False
     for src, _obj, res in results:
@@ -65,14 +69,15 @@ def build(force=False, verbose=False):
         sys.stderr.write("".join(report))
     if failed:
         raise RuntimeError("nvcc failed building libcqr.so")
-    link = [NVCC, *ARCH, "-shared", "-o", LIB] + [obj for _src, obj, _res in results]
+    link = [NVCC, *ARCH, "-shared", "-o", lib] + [obj for _src, obj, _res in results]
     res = subprocess.run(link, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc failed linking libcqr.so")
-    with open(os.path.join(HERE, "ptxas_report.txt"), "w") as fh:
-        fh.write("".join(report))
-    return LIB
+    if lib == LIB:
+        with open(os.path.join(HERE, "ptxas_report.txt"), "w") as fh:
+            fh.write("".join(report))
+    return lib
 
 
 if __name__ == "__main__":

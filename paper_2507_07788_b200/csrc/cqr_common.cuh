@@ -78,6 +78,15 @@ __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t by
                "r"(bytes)
                : "memory");
 }
+__device__ __forceinline__ void bulk_s2g_stream(void* dst, const void* src, uint32_t bytes) {
+#if CQR_L2_HINTS
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes), "l"(l2_evict_first())
+               : "memory");
+#else
+  bulk_s2g(dst, src, bytes);
+#endif
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
@@ -87,6 +96,50 @@ template <int N>
 __device__ __forceinline__ void bulk_wait() {
   asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
 }
+// Streaming tall operands (X, Q panels: read or written once per pass) carry
+// an L2 evict-first hint, so a pass that streams gigabytes through the 126 MB
+// L2 does not evict what the next kernels reuse: the k x k stage's code (the
+// factor kernel is ~1 MB of SASS; fetched cold from HBM it ran 16-37 us
+// slower per call after a tall pass, tools/diag/factor_cold.py), its Gram and
+// the coefficient tiles.  CQR_L2_HINTS=0 at build time turns the hints off.
+#ifndef CQR_L2_HINTS
+#define CQR_L2_HINTS 1
+#endif
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void bulk_g2s_stream(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+#if CQR_L2_HINTS
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(l2_evict_first())
+      : "memory");
+#else
+  bulk_g2s(dst, src, bytes, bar);
+#endif
+}
+__device__ __forceinline__ void tma_load_3d_stream(void* dst, const void* tmap, int c0, int c1, int c2, uint64_t* bar) {
+#if CQR_L2_HINTS
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;"
+      ::"r"(smem_u32(dst)), "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(l2_evict_first())
+      : "memory");
+#else
+  tma_load_3d(dst, tmap, c0, c1, c2, bar);
+#endif
+}
+// one streamed fp64 store (st.global.cs: evict-first in L2)
+__device__ __forceinline__ void st_stream(double* p, double v) {
+#if CQR_L2_HINTS
+  __stcs(p, v);
+#else
+  *p = v;
+#endif
+}
+
 // make generic-proxy shared-memory writes visible to the async (bulk) proxy
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

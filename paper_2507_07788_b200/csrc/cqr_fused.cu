@@ -152,9 +152,9 @@ __global__ void __launch_bounds__(FuCfg<KP>::THREADS, 1)
     const double* src = X + (r0 >> 2) * 4 * ldx;
     mbar_arrive_expect_tx(&xfull[st], (uint32_t)nq * k * 32);
     if (ldx == KP && kfull) {
-      bulk_g2s(dst, src, (uint32_t)nq * KP * 32, &xfull[st]);
+      bulk_g2s_stream(dst, src, (uint32_t)nq * KP * 32, &xfull[st]);
     } else {
-      for (int q = 0; q < nq; ++q) bulk_g2s(dst + q * 4 * KP, src + q * 4 * ldx, (uint32_t)k * 32, &xfull[st]);
+      for (int q = 0; q < nq; ++q) bulk_g2s_stream(dst + q * 4 * KP, src + q * 4 * ldx, (uint32_t)k * 32, &xfull[st]);
     }
   };
   if (tid == 0) {
@@ -194,9 +194,9 @@ __global__ void __launch_bounds__(FuCfg<KP>::THREADS, 1)
           const double* src = qbuf + qs * C::STAGE;
           double* dst = Q + (r0 >> 2) * 4 * ldq;
           if (ldq == KP && KFULL) {
-            bulk_s2g(dst, src, (uint32_t)nq * KP * 32);
+            bulk_s2g_stream(dst, src, (uint32_t)nq * KP * 32);
           } else {
-            for (int q = 0; q < nq; ++q) bulk_s2g(dst + q * 4 * ldq, src + q * 4 * KP, (uint32_t)k * 32);
+            for (int q = 0; q < nq; ++q) bulk_s2g_stream(dst + q * 4 * ldq, src + q * 4 * KP, (uint32_t)k * 32);
           }
           bulk_commit();
           if (prev >= 0) {
@@ -290,9 +290,9 @@ __global__ void __launch_bounds__(FuCfg<KP>::THREADS, 1)
         const double* src = qbuf + qs * C::STAGE;
         double* dst = Q + (r0 >> 2) * 4 * ldq;
         if (ldq == KP && KFULL) {
-          bulk_s2g(dst, src, (uint32_t)nq * KP * 32);
+          bulk_s2g_stream(dst, src, (uint32_t)nq * KP * 32);
         } else {
-          for (int q = 0; q < nq; ++q) bulk_s2g(dst + q * 4 * ldq, src + q * 4 * KP, (uint32_t)k * 32);
+          for (int q = 0; q < nq; ++q) bulk_s2g_stream(dst + q * 4 * ldq, src + q * 4 * KP, (uint32_t)k * 32);
         }
         bulk_commit();
       }
@@ -359,7 +359,11 @@ __host__ __device__ constexpr size_t rt_smem_doubles() {
 }
 
 __device__ __forceinline__ void st_global_v2(double* p, double a, double b) {
+#if CQR_L2_HINTS
+  asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
+#else
   asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
+#endif
 }
 
 // TRMM = false: the same sweep as a plain self Gram of X (k <= 64): the
@@ -404,9 +408,9 @@ __global__ void __launch_bounds__(RtCfg<KP>::THREADS, 1)
     const double* src = X + (r0 >> 2) * 4 * ldx;
     mbar_arrive_expect_tx(&full[st], (uint32_t)nq * k * 32);
     if (ldx == KP && KFULL) {
-      bulk_g2s(dst, src, (uint32_t)nq * KP * 32, &full[st]);
+      bulk_g2s_stream(dst, src, (uint32_t)nq * KP * 32, &full[st]);
     } else {
-      for (int q = 0; q < nq; ++q) bulk_g2s(dst + q * 4 * KP, src + q * 4 * ldx, (uint32_t)k * 32, &full[st]);
+      for (int q = 0; q < nq; ++q) bulk_g2s_stream(dst + q * 4 * KP, src + q * 4 * ldx, (uint32_t)k * 32, &full[st]);
     }
   };
   if (tid == 0) {

@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(GM_THREADS, 2) gemm_kernel(GemmArgs args) {
           __syncwarp();
           const double* xb = args.X + (r0 >> 2) * 4 * args.ldx + 4 * (int64_t)kc;
           for (int q = lane; q < nq; q += 32)
-            bulk_g2s(Xs + q * (GM_KC * 4), xb + q * 4 * args.ldx, (uint32_t)nxc * 32, &full[s]);
+            bulk_g2s_stream(Xs + q * (GM_KC * 4), xb + q * 4 * args.ldx, (uint32_t)nxc * 32, &full[s]);
           if (lane == 0)
             bulk_g2s(Cs, args.C + ((int64_t)nt * nkt + ch) * CT_TILE, CT_TILE * 8, &full[s]);
         }
@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(GM_THREADS, 2) gemm_kernel(GemmArgs args) {
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int col = n0 + 8 * col_block(j, wj) + 2 * t + e;
-            if (col < args.n) yq[4 * (int64_t)col] = acc[i][j][e];
+            if (col < args.n) st_stream(yq + 4 * (int64_t)col, acc[i][j][e]);
           }
       }
     }

@@ -109,9 +109,9 @@ __device__ __forceinline__ void stage_block(double* dst, const double* src, int6
   const int nq = nrows >> 2;
   const double* base = src + (r0 >> 2) * 4 * ldk + 4 * (int64_t)c0;
   if (ncol == GR_CT && ldk == GR_CT) {
-    if (lane == 0) bulk_g2s(dst, base, (uint32_t)nq * GR_QD * 8, bar);
+    if (lane == 0) bulk_g2s_stream(dst, base, (uint32_t)nq * GR_QD * 8, bar);
   } else {
-    for (int q = lane; q < nq; q += 32) bulk_g2s(dst + q * GR_QD, base + q * 4 * ldk, (uint32_t)ncol * 32, bar);
+    for (int q = lane; q < nq; q += 32) bulk_g2s_stream(dst + q * GR_QD, base + q * 4 * ldk, (uint32_t)ncol * 32, bar);
   }
 }
 

@@ -77,9 +77,9 @@ __global__ void __launch_bounds__(GPCfg<KP>::THREADS, 1) gram_pairs_kernel(const
     const double* src = X + (r0 >> 2) * 4 * ldx;
     mbar_arrive_expect_tx(&full[st], (uint32_t)nq * k * 32);
     if (ldx == KP && k == KP) {
-      bulk_g2s(dst, src, (uint32_t)nq * KP * 32, &full[st]);
+      bulk_g2s_stream(dst, src, (uint32_t)nq * KP * 32, &full[st]);
     } else {
-      for (int q = 0; q < nq; ++q) bulk_g2s(dst + q * 4 * KP, src + q * 4 * ldx, (uint32_t)k * 32, &full[st]);
+      for (int q = 0; q < nq; ++q) bulk_g2s_stream(dst + q * 4 * KP, src + q * 4 * ldx, (uint32_t)k * 32, &full[st]);
     }
   };
   if constexpr (C::PRODUCER) {

@@ -82,9 +82,9 @@ __global__ void __launch_bounds__(RsCfg<KP>::THREADS, 1)
     const double* src = Q + (r0 >> 2) * 4 * ldq;
     mbar_arrive_expect_tx(&full[st], (uint32_t)nq * k * 32);
     if (ldq == KP && KFULL) {
-      bulk_g2s(dst, src, (uint32_t)nq * KP * 32, &full[st]);
+      bulk_g2s_stream(dst, src, (uint32_t)nq * KP * 32, &full[st]);
     } else {
-      for (int q = 0; q < nq; ++q) bulk_g2s(dst + q * 4 * KP, src + q * 4 * ldq, (uint32_t)k * 32, &full[st]);
+      for (int q = 0; q < nq; ++q) bulk_g2s_stream(dst + q * 4 * KP, src + q * 4 * ldq, (uint32_t)k * 32, &full[st]);
     }
   };
   if (tid == 0) {

@@ -158,16 +158,16 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(const __grid
     const double* sq = a.Qin + (r0 >> 2) * 4 * a.ldqin;
     const double* sb = a.Qb + (r0 >> 2) * 4 * a.ldqb;
     if (a.use_tm_qin) {
-      tma_load_3d(dq, &a.tm_qin, 0, 0, (int)(r0 >> 2), &full[st]);
+      tma_load_3d_stream(dq, &a.tm_qin, 0, 0, (int)(r0 >> 2), &full[st]);
     } else {
-      for (int qq = 0; qq < nq; ++qq) bulk_g2s(dq + qq * 4 * qs, sq + qq * 4 * a.ldqin, (uint32_t)q * 32, &full[st]);
+      for (int qq = 0; qq < nq; ++qq) bulk_g2s_stream(dq + qq * 4 * qs, sq + qq * 4 * a.ldqin, (uint32_t)q * 32, &full[st]);
     }
     if (a.use_tm_qb) {
-      tma_load_3d(db, &a.tm_qb, 0, 0, (int)(r0 >> 2), &full[st]);
+      tma_load_3d_stream(db, &a.tm_qb, 0, 0, (int)(r0 >> 2), &full[st]);
     } else if (a.ldqb == UP_PB && p == UP_PB) {
-      bulk_g2s(db, sb, (uint32_t)nq * UP_PB * 32, &full[st]);
+      bulk_g2s_stream(db, sb, (uint32_t)nq * UP_PB * 32, &full[st]);
     } else {
-      for (int qq = 0; qq < nq; ++qq) bulk_g2s(db + qq * 4 * UP_PB, sb + qq * 4 * a.ldqb, (uint32_t)p * 32, &full[st]);
+      for (int qq = 0; qq < nq; ++qq) bulk_g2s_stream(db + qq * 4 * UP_PB, sb + qq * 4 * a.ldqb, (uint32_t)p * 32, &full[st]);
     }
   };
   if (tid == 0)
@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(const __grid
             const int cc = 8 * nb + 2 * t + e;
             const bool v = cc < p;
             yd[(r >> 2) * 4 * UP_PB + 4 * cc + (r & 3)] = v ? c2[e] : 0.0;
-            if (v && r < nrows) a.Qo[((r0 + r) >> 2) * 4 * a.ldqo + 4 * cc + (r & 3)] = c2[e];
+            if (v && r < nrows) st_stream(a.Qo + ((r0 + r) >> 2) * 4 * a.ldqo + 4 * cc + (r & 3), c2[e]);
           }
         }
       } else {
@@ -468,7 +468,7 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(const __grid
             const int cc = 8 * nb + 2 * t + e;
             const bool v = cc < p;
             yd[(r >> 2) * 4 * UP_PB + 4 * cc + (r & 3)] = v ? c2[e] : 0.0;
-            if (v && r < nrows) a.Qo[((r0 + r) >> 2) * 4 * a.ldqo + 4 * cc + (r & 3)] = c2[e];
+            if (v && r < nrows) st_stream(a.Qo + ((r0 + r) >> 2) * 4 * a.ldqo + 4 * cc + (r & 3), c2[e]);
           }
         }
       } else {
