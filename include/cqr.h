@@ -225,6 +225,15 @@ void cqr_debug_update_tma(int on);
 /* Diagnostics: 1 (default) = update passes with bases up to 64 columns run two
  * alternating 4-warp projection teams; 0 = one 8-warp projection group. */
 int cqr_debug_update_narrow_teams(int on);
+/* Diagnostics: in iteration-mode update passes with one projection group the
+ * cross-Gram warps may start sub-panel j only once the projection DMMAs of
+ * j + 1 are issued (their DMMAs then fill the projection group's serial tail).
+ * 0 = never, 1 = always, 2 (default) = where measured to pay (16-row sub-panels
+ * with a 4- or 5-stage ring).  Results are bitwise the same. */
+int cqr_debug_update_lag(int mode);
+/* Diagnostics: bases of at least q columns (145 <= q <= 193) stage 16-row
+ * sub-panels in the update pass, narrower ones 32-row (64-row up to 64 columns). */
+int cqr_debug_update_sr16_from(int q);
 /* Diagnostics: 1 (default) = the blocked Cholesky in bands of 32 pivots with a
  * rank-32 update between bands; 0 = one lookahead chain over all block steps. */
 int cqr_debug_factor_banded(int on);

@@ -39,6 +39,10 @@ class DeviceContext:
             self.lib.cqr_debug_factor_cluster(int(os.environ["CQR_FACTOR_CLUSTER"]))
         if "CQR_UPDATE_NARROW_TEAMS" in os.environ:   # diagnostics: narrow update pass schedule
             self.lib.cqr_debug_update_narrow_teams(int(os.environ["CQR_UPDATE_NARROW_TEAMS"]))
+        if "CQR_UPDATE_SR16_FROM" in os.environ:   # diagnostics: sub-panel height switch of the update pass
+            self.lib.cqr_debug_update_sr16_from(int(os.environ["CQR_UPDATE_SR16_FROM"]))
+        if "CQR_UPDATE_LAG" in os.environ:   # diagnostics: cross-Gram lag of the update pass
+            self.lib.cqr_debug_update_lag(int(os.environ["CQR_UPDATE_LAG"]))
         if torch.distributed.is_available() and torch.distributed.is_initialized():
             self.rank = torch.distributed.get_rank()
             self.world = torch.distributed.get_world_size()

@@ -21,7 +21,7 @@
 //     they release the stage, and the last one's lane 0 refills it.
 // Both groups issue q/8 DMMA per warp per 16 rows; the width enters as the
 // template parameter NQ = ceil(q/64) so no DMMA is predicated off.  Bases up to
-// 192 columns use 32-row sub-panels (half the per-row synchronisation).  Groups hand
+// 144 columns use 32-row sub-panels (half the per-row synchronisation).  Groups hand
 // over through mbarriers; the projection group syncs on a named barrier.
 // Per-CTA partials [Bt'(q_pad x 16) | G'(16 x 16)] are written once per CTA
 // and summed by a fixed-order reduce kernel.
@@ -71,13 +71,15 @@ struct alignas(64) UpdateArgs {
   int qs;                                 // staged column stride (= 4 mod 8)
   int ns;                                 // ring stages
   const int* gate;                        // no-op unless *gate == CQR_FACTORED
+  int lag;                                // cross-Gram group one sub-panel behind the projection DMMAs (see kernel)
 };
 
 static int up_qs(int q) { return (int)round_up(q, 8) + 4; }
 // 64-row sub-panels for bases up to 64 columns: the narrow pass is bound by the
 // per-sub-panel chain (projection -> t -> R^-1 -> hand-over), so twice the rows
 // per chain halve its cost per row (q = 16 at 8M rows: 1.45 -> see DESIGN)
-static int up_sr(int q) { return q <= 64 ? 64 : (q <= 192 ? 32 : 16); }
+static int g_sr16_from = 145;   // cqr_debug_update_sr16_from: bases from this width use 16-row sub-panels
+static int up_sr(int q) { return q <= 64 ? 64 : (q < g_sr16_from ? 32 : 16); }
 static bool up_narrow(int q) { return q <= 64; }
 static int up_stage(int q, int sr) { return sr * up_qs(q) + sr * UP_PB; }
 static int up_stages_with(int q, int sr, bool teams) {
@@ -117,7 +119,7 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(const __grid
   const int q = a.q, p = a.p, qs = a.qs, ns = a.ns;
   const int STG = SR * qs + SR * UP_PB;
   constexpr bool NARROW = NQ == 1 && SR >= 32;   // bases up to 64 columns
-  // 65 <= q <= 192: two independent projection teams of 4 warps take alternate
+  // 65 <= q <= 144: two independent projection teams of 4 warps take alternate
   // sub-panels, so one team's reduction / R^-1 / hand-over overlaps the other
   // team's DMMAs (one team of 8 left the cross-Gram warps waiting on Q')
   double* ris = smem;                      // R^-1 as [n][k] (ld 36)
@@ -125,7 +127,14 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(const __grid
   double* tq = red + (NARROW ? 0 : 8 * TE);   // t = Q - proj (QI, SR x 16), one per team
   double* yring = tq + (TEAMS ? 2 : 1) * TE;  // UP_YS x Q' (QI, SR x 16)
   double* stg = yring + UP_YS * TE;        // ns x [Q_in sub-panel (Q4 quads x qs x 4) | block (Q4 quads x 16 x 4)]
-  __shared__ __align__(8) uint64_t full[UP_MAXNS], empty[UP_MAXNS], yfull[UP_YS], yempty[UP_YS];
+  __shared__ __align__(8) uint64_t full[UP_MAXNS], empty[UP_MAXNS], yfull[UP_YS], yempty[UP_YS], pdone[UP_YS];
+  // Lag (single projection group, iteration mode): the cross-Gram group starts
+  // sub-panel j only once the projection DMMAs of j+1 are issued (pdone), so
+  // its DMMAs run during the projection group's serial tail (partials ->
+  // fixed-order sum -> R^-1 -> hand-over), when the FP64 pipe is otherwise
+  // idle (ncu at q = 320: the cross-Gram warps waited on Q' for 23% of their
+  // samples).  Timing only: the same operations in the same order per element.
+  const bool lag = a.lag != 0 && !TEAMS && a.initial == 0;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
@@ -135,7 +144,9 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(const __grid
 
   if (tid == 0) {
     for (int s = 0; s < ns; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 8); }
-    for (int s = 0; s < UP_YS; ++s) { mbar_init(&yfull[s], TEAMS ? 128 : 256); mbar_init(&yempty[s], 8); }
+    for (int s = 0; s < UP_YS; ++s) {
+      mbar_init(&yfull[s], TEAMS ? 128 : 256); mbar_init(&yempty[s], 8); mbar_init(&pdone[s], 8);
+    }
     fence_mbar_init();
   }
   if (!init) {
@@ -428,6 +439,10 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(const __grid
               dmma(pr[rb][1], av[rb], btr[c][h][1]);
             }
           }
+        if (lag) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&pdone[ys]);   // this warp's projection DMMAs of sub-panel j are issued
+        }
         // partials in the QI layout of the sub-panel (as tq, yd and the stage)
 #pragma unroll
         for (int rb = 0; rb < RB; ++rb)
@@ -500,6 +515,10 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(const __grid
     // over the sub-partitions and the blocks past q are skipped whole.
     const int cl0 = 64 * (NQ - 1);
     for (int64_t j = 0; j < mine; ++j) {
+      if (lag && j + 1 < mine) {
+        const int yn = (ys + 1 == UP_YS) ? 0 : ys + 1;
+        mbar_wait(&pdone[yn], (ys + 1 == UP_YS) ? (yph ^ 1) : yph);
+      }
       mbar_wait(&yfull[ys], yph);
       const double* Qs = stg + s * STG;
       const double* yd = yring + ys * TE;
@@ -690,6 +709,18 @@ int update_set_narrow_teams(int on) {
   g_narrow_teams = on ? 1 : 0;
   return 0;
 }
+int update_set_sr16_from(int q) {
+  if (q < 145 || q > 193) return -1;   // 65..144 run the two-team schedule on 32-row sub-panels
+  g_sr16_from = q;
+  return 0;
+}
+// 0 = never, 1 = always (wide single-group passes), 2 (default) = where it was
+// measured to pay: 16-row sub-panels with a 4- or 5-stage ring (q = 256..368)
+static int g_update_lag = 2;   // cqr_debug_update_lag
+int update_set_lag(int mode) {
+  g_update_lag = mode;
+  return 0;
+}
 
 cudaError_t update_pass_launch(const double* Qin, int64_t ldqin, int q, const double* Qb, int64_t ldqb, double* Qo,
                                int64_t ldqo, int p, int64_t rows, const double* Bt, int ldbt, const double* Rinv_tiles,
@@ -707,6 +738,10 @@ cudaError_t update_pass_launch(const double* Qin, int64_t ldqin, int q, const do
   a.gate = gate;
   a.qs = up_qs(q);
   const int sr = up_sr(q);
+  {
+    const int nst = up_stages(q, sr);
+    a.lag = g_update_lag == 1 || (g_update_lag == 2 && sr == 16 && (nst == 4 || nst == 5));
+  }
   // one tensor copy per sub-panel where the per-quad runs would be small
   a.use_tm_qin = (q * 32 < 8192) && encode_qi_map(&a.tm_qin, Qin, ldqin, q, rows, a.qs, sr) ? 1 : 0;
   a.use_tm_qb = !(ldqb == UP_PB && p == UP_PB) && encode_qi_map(&a.tm_qb, Qb, ldqb, p, rows, UP_PB, sr) ? 1 : 0;

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--q", type=int, default=256, help="basis width for --only update")
     ap.add_argument("--fk", default="64,128,256", help="widths for --only factor")
     ap.add_argument("--tma", type=int, default=1, help="update: TMA tensor staging of narrow sub-panels (0/1)")
+    ap.add_argument("--initial", action="store_true", help="update: time the initial pass (Bt = Q_in^T Q, G = Q^T Q)")
     ap.add_argument("--cap", type=int, default=0, help="update: column capacity of the basis (config 4's chain: 512)")
     a = ap.parse_args()
     import paper_2507_07788_b200 as cq
@@ -51,7 +52,7 @@ def main():
         eng.Bt.copy_(1e-3 * torch.randn_like(eng.Bt))
 
         def run():
-            eng.update_pass(q_in, qb, initial=False)
+            eng.update_pass(q_in, qb, initial=a.initial)
 
         run()
         torch.cuda.synchronize()
@@ -63,7 +64,9 @@ def main():
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / a.reps
         flops = 4.0 * m * a.q * k + 2.0 * m * k * (k + 1)
-        print(json.dumps({"m": m, "q": a.q, "p": k, "update_ms": ms, "update_tfs": flops / ms / 1e9,
+        if a.initial:
+            flops = 2.0 * m * a.q * k + 1.0 * m * k * (k + 1)
+        print(json.dumps({"m": m, "q": a.q, "p": k, "initial": a.initial, "cap": a.cap, "update_ms": ms, "update_tfs": flops / ms / 1e9,
                           "qin_gbs": m * a.q * 8 / ms / 1e6}))
         return
 
