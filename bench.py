@@ -41,6 +41,16 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 FP64_PEAK_TFS = 37.2          # measured DMMA peak, profiles/r01_fp64_peak.json
 FP64_PEAK_SRC = "measured DMMA.8x8x4 microbenchmark (profiles/r01_fp64_peak.json)"
+
+
+def _hbm_peak_gbs():
+    """The driver-measured copy bandwidth (MEASURED_PEAKS.json), else the
+    profiling recipe's fallback for B200."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except Exception:
+        return 6550.0
 # DRAM traffic of one dominant-kernel launch from `ncu --set full` captures at
 # the bench's exact per-launch shape (tools/profile_round.sh); per config: the
 # captures summed, and the (rows, cols) they were taken at.
@@ -596,6 +606,19 @@ def run_update_chain(cq, cx, cfg, m, world, rank, local):
     for rows_, qq, pp, init in up["work"]:
         fl += (2.0 * rows_ * qq * pp + rows_ * pp * (pp + 1)) * (1 if init else 2)
     tfs = fl / (sum(up["ms"]) * 1e-3) / 1e12
+    # per-pass bound: the slower of HBM bytes and FP64 flops for every launch (the
+    # initial pass of an append has half an iteration's flops on the same bytes and
+    # is HBM-bound), summed over the chain, against the kernels' measured time
+    hbm = _hbm_peak_gbs()
+    bound_ms = 0.0
+    for rows_, qq, pp, init in up["work"]:
+        f_ = (2.0 * rows_ * qq * pp + rows_ * pp * (pp + 1)) * (1 if init else 2)
+        b_ = 8.0 * rows_ * (qq + pp * (1 if init else 2))
+        bound_ms += max(f_ / (FP64_PEAK_TFS * 1e12), b_ / (hbm * 1e9)) * 1e3
+    per_pass = {"bound_ms_per_step": bound_ms / ARGS.steps, "kernel_ms_per_step": sum(up["ms"]) / ARGS.steps,
+                "frac": bound_ms / sum(up["ms"]), "hbm_peak_gbs": hbm,
+                "note": "sum over update-pass launches of max(flops / FP64 peak, bytes / HBM peak): initial passes "
+                        "(Bt = Q_in^T A, G = A^T A) are HBM-bound, iteration passes FP64-bound"}
     cpu = None
     if rank == 0 and world == 1 and not ARGS.no_cpu:
         rows = cfg["cpu_rows"]
@@ -614,7 +637,8 @@ def run_update_chain(cq, cx, cfg, m, world, rank, local):
             "roofline": {"bound": "tensor", "pipe": "FP64 DMMA.8x8x4 (tensor pipe)", "kernel": "update_pass", "achieved": tfs, "peak": FP64_PEAK_TFS,
                          "unit": "TFLOP/s", "frac": tfs / FP64_PEAK_TFS, "traffic": None,
                          "peak_source": FP64_PEAK_SRC,
-                         "flops_model": "2 m q p (projection) + 2 m q p (cross Gram) + 2 m p (p+1) per pass"},
+                         "flops_model": "2 m q p (projection) + 2 m q p (cross Gram) + 2 m p (p+1) per pass",
+                         "per_pass_bound": per_pass},
             "kernels": {n: {"launches_per_step": len(v["ms"]) / ARGS.steps, "mean_ms": float(np.mean(v["ms"]))}
                         for n, v in ktimes.items()},
             "gpu_launches": launches, "clocks": clocks.summary(), "e2e": None, "cpu_baseline": cpu}), flush=True)

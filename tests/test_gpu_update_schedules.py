@@ -102,3 +102,4 @@ def test_sub_panel_height_switch(q, initial):
     np.testing.assert_array_equal(a[0], b[0])
     for x, y in zip(a[1:], b[1:]):
         np.testing.assert_allclose(x, y, rtol=0, atol=1e-12 * max(1.0, float(np.abs(x).max())))
+

@@ -19,7 +19,7 @@ from paper_2507_07788_b200.workloads import device_gaussian  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--m", type=int, default=8_000_000)
 ap.add_argument("--qs", default=",".join(str(16 * j) for j in range(1, 32)))
-ap.add_argument("--settings", default="0:193,1:193,1:145", help="lag:sr16_from pairs")
+ap.add_argument("--settings", default="0:193,0:145,2:145", help="lag:sr16_from pairs")
 ap.add_argument("--reps", type=int, default=4)
 a = ap.parse_args()
 m, p = a.m, 16
