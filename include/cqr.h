@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define CQR_ABI_VERSION 9
+#define CQR_ABI_VERSION 10
 
 #define CQR_OK 0
 #define CQR_EINVAL (-1)
@@ -144,6 +144,13 @@ int cqr_cross_gram(const double* A, int64_t lda, int ka, const double* B, int64_
  * algorithms.py:168-174). */
 int cqr_lincomb(const double* X, int64_t ldx, int64_t m, int k, const double* C, int n, int upper, double* Y,
                 int64_t ldy, void* stream);
+
+/* Y = Yin - X C (m x n; general C in coefficient tiles, k x n): the projection of
+ * the update iteration and its subtraction in one pass, `proj = q_in.lincomb(bt);
+ * q.axpy(-1.0, proj)` (algorithms.py:442-444; varray.py:157-171), with the same two
+ * roundings per element.  Y may alias Yin (not X). */
+int cqr_lincomb_sub(const double* X, int64_t ldx, int64_t m, int k, const double* C, int n, const double* Yin,
+                    int64_t ldyin, double* Y, int64_t ldy, void* stream);
 
 /* Y += alpha X, in place.  Replaces DenseVectorArray.axpy (varray.py:165-171). */
 int cqr_axpy(double* Y, int64_t ldy, double alpha, const double* X, int64_t ldx, int64_t m, int n, void* stream);

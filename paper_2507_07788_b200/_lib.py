@@ -112,6 +112,7 @@ SIGNATURES = {
     "cqr_set_gram_pairs": (None, [_I]),
     "cqr_cross_gram": (_I, [_P, _I64, _I, _P, _I64, _I, _I64, _P, _I, _P, _SZ, _P]),
     "cqr_lincomb": (_I, [_P, _I64, _I64, _I, _P, _I, _I, _P, _I64, _P]),
+    "cqr_lincomb_sub": (_I, [_P, _I64, _I64, _I, _P, _I, _P, _I64, _P, _I64, _P]),
     "cqr_axpy": (_I, [_P, _I64, ctypes.c_double, _P, _I64, _I64, _I, _P]),
     "cqr_pack_tall": (_I, [_P, _I64, _I64, _I, _P, _I64, _P]),
     "cqr_unpack_tall": (_I, [_P, _I64, _I64, _I, _P, _I64, _P]),

@@ -567,11 +567,10 @@ def chol_qr_update(q_in, r_in, a_new, cfg=None, ledger=None):
             _charge(ledger, "gemm", _flops.gemm_flops(m, p, p))
             _charge(ledger, "gemm", _flops.gemm_flops(p, k, p) + p * p)
         else:
-            proj = _lincomb_device(q_in, eng.Bt, k, p)
+            # Q <- Q - Q_in Bt in one pass (the reference's lincomb + axpy), into a
+            # fresh array: the caller's block is never written
+            q = _lincomb_device(q_in, eng.Bt, k, p, minus_from=src)
             _charge(ledger, "gemm", _flops.gemm_flops(m, k, p))
-            if q is None:
-                q = a_new.copy()
-            q.axpy(-1.0, proj)
             _charge(ledger, "gemm", m * p)
             _charge(ledger, "trtri", _flops.tri_inverse_flops(p))
             tmp = _fresh_like(q, p)
@@ -661,17 +660,24 @@ def _update_pipelined(eng, q_in, r_in, a_new, m, k, p, width, tol, cfg, ledger):
                     pivot_margins=margins, decision_margins=dms, err_history=errs)
 
 
-def _lincomb_device(arr, coeff_dev, k, p):
+def _lincomb_device(arr, coeff_dev, k, p, minus_from=None):
     """arr (m x k) @ C with C = Bt already on the device as column-major k x p
-    (torch (p, k)), packed into coefficient tiles for libcqr."""
+    (torch (p, k)), packed into coefficient tiles for libcqr.  With
+    `minus_from` (m x p) the result is minus_from - arr @ C in one pass
+    (cqr_lincomb_sub: the projection and its axpy, algorithms.py:442-444, with
+    the same roundings), written to a fresh array."""
     from ._device import ctx
     from .varray import coeff_tiles
 
     cx = ctx()
     c = coeff_tiles(coeff_dev, k, p, k)
     out = _fresh_like(arr, p)
-    _lib.check(cx.lib.cqr_lincomb(arr.ptr(), arr.ld, arr.m_local, k, c.data_ptr(), p, 0, out.ptr(), out.ld,
-                                  cx.stream), "projection")
+    if minus_from is None:
+        _lib.check(cx.lib.cqr_lincomb(arr.ptr(), arr.ld, arr.m_local, k, c.data_ptr(), p, 0, out.ptr(), out.ld,
+                                      cx.stream), "projection")
+    else:
+        _lib.check(cx.lib.cqr_lincomb_sub(arr.ptr(), arr.ld, arr.m_local, k, c.data_ptr(), p, minus_from.ptr(),
+                                          minus_from.ld, out.ptr(), out.ld, cx.stream), "projection")
     cx.launches += 1
     return out
 

@@ -134,6 +134,28 @@ int cqr_lincomb(const double* X, int64_t ldx, int64_t m, int k, const double* C,
   return lincomb_impl(X, ldx, m, k, C, n, upper, Y, ldy, stream, nullptr);
 }
 
+int cqr_lincomb_sub(const double* X, int64_t ldx, int64_t m, int k, const double* C, int n, const double* Yin,
+                    int64_t ldyin, double* Y, int64_t ldy, void* stream) {
+  int rc = check_tall(X, ldx, m, k, "cqr_lincomb_sub(X)");
+  if (rc) return rc;
+  rc = check_tall(Y, ldy, m, n, "cqr_lincomb_sub(Y)");
+  if (rc) return rc;
+  rc = check_tall(Yin, ldyin, m, n, "cqr_lincomb_sub(Yin)");
+  if (rc) return rc;
+  if (n == 0 || m == 0) return CQR_OK;
+  if (k == 0) return fail(CQR_EINVAL, "cqr_lincomb_sub: k == 0 with n > 0 (copy Yin instead)");
+  if (C == nullptr || !aligned16(C)) return fail(CQR_EINVAL, "cqr_lincomb_sub: C (coefficient tiles) null / unaligned");
+  if (X == Y) return fail(CQR_EINVAL, "cqr_lincomb_sub: Y must not alias X");
+  cqr::GemmArgs a{};
+  a.X = X; a.ldx = ldx; a.kx = k;
+  a.C = C;
+  a.Y = Y; a.ldy = ldy; a.n = n;
+  a.Yin = Yin; a.ldyin = ldyin;
+  a.rows = cqr::round_up(m, 16);
+  a.upper = 0;
+  return cuda_check(cqr::gemm_launch(a, static_cast<cudaStream_t>(stream)), "cqr_lincomb_sub");
+}
+
 int cqr_axpy(double* Y, int64_t ldy, double alpha, const double* X, int64_t ldx, int64_t m, int n, void* stream) {
   int rc = check_tall(Y, ldy, m, n, "cqr_axpy(Y)");
   if (rc) return rc;

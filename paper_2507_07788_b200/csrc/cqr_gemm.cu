@@ -69,6 +69,13 @@ __device__ __forceinline__ void diag_chunk(double (&acc)[4][4][2], const double*
   }
 }
 
+// JL = live 8-column blocks per warp column: 4 for tiles wider than 32 output
+// columns, 2 for 17..32 (blocks 0..3 of the tile: j < 2 of both warp columns),
+// 1 for <= 16 -- a skinny general C (the projection Q_in Bt of the update path)
+// does not issue DMMAs for zero column blocks.  SUB: Y = Yin - X C (the
+// projection and its subtraction, algorithms.py:442-444, in one pass; the same
+// two roundings as lincomb + axpy).  The TRMM / full-width instance is <4, false>.
+template <int JL, bool SUB>
 __global__ void __launch_bounds__(GM_THREADS, 2) gemm_kernel(GemmArgs args) {
   if (args.gate != nullptr && *args.gate != 0) return;   // gated off
   extern __shared__ __align__(128) double smem[];
@@ -148,7 +155,7 @@ __global__ void __launch_bounds__(GM_THREADS, 2) gemm_kernel(GemmArgs args) {
 #pragma unroll
           for (int i = 0; i < 4; ++i) a[0][i] = xp[2 * i * (GM_KC * 4)];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) b[0][j] = cp[8 * col_block(j, wj) * CT_LD];
+          for (int j = 0; j < JL; ++j) b[0][j] = cp[8 * col_block(j, wj) * CT_LD];
 #pragma unroll
           for (int ks = 0; ks < GM_KC / 4; ++ks) {
             const int cur = ks & 1;
@@ -156,10 +163,10 @@ __global__ void __launch_bounds__(GM_THREADS, 2) gemm_kernel(GemmArgs args) {
 #pragma unroll
               for (int i = 0; i < 4; ++i) a[cur ^ 1][i] = xp[2 * i * (GM_KC * 4) + 16 * (ks + 1)];
 #pragma unroll
-              for (int j = 0; j < 4; ++j) b[cur ^ 1][j] = cp[8 * col_block(j, wj) * CT_LD + 4 * (ks + 1)];
+              for (int j = 0; j < JL; ++j) b[cur ^ 1][j] = cp[8 * col_block(j, wj) * CT_LD + 4 * (ks + 1)];
             }
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
+            for (int j = 0; j < JL; ++j)
 #pragma unroll
               for (int i = 0; i < 4; ++i) dmma(acc[i][j], a[cur][i], b[cur][j]);
           }
@@ -185,9 +192,9 @@ __global__ void __launch_bounds__(GM_THREADS, 2) gemm_kernel(GemmArgs args) {
 #pragma unroll
           for (int i = 0; i < 4; ++i) a[i] = kval ? xp[2 * i * (GM_KC * 4) + 16 * ks] : 0.0;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) b[j] = cp[8 * col_block(j, wj) * CT_LD + 4 * ks];
+          for (int j = 0; j < JL; ++j) b[j] = cp[8 * col_block(j, wj) * CT_LD + 4 * ks];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
+          for (int j = 0; j < JL; ++j) {
             if (args.upper && k4 > n0 + 8 * col_block(j, wj) + 7) continue;  // block of zeros
 #pragma unroll
             for (int i = 0; i < 4; ++i) dmma(acc[i][j], a[i], b[j]);
@@ -197,13 +204,37 @@ __global__ void __launch_bounds__(GM_THREADS, 2) gemm_kernel(GemmArgs args) {
         if (lane == 0) mbar_arrive(&empty[s]);
       }
       // ---- store this tile (rows < nrows, cols < n) in the QI layout
+      if constexpr (SUB) {
+        // Y = Yin - X C: all of the lane's Yin values are requested before the
+        // first store (the stores are volatile asm: interleaved, every load's
+        // latency would be exposed)
+        double yv[4][JL][2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int row = 32 * wi + 8 * i + g;
+          const double* yi = args.Yin + ((r0 + row) >> 2) * 4 * args.ldyin + (row & 3);
+#pragma unroll
+          for (int j = 0; j < JL; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int col = n0 + 8 * col_block(j, wj) + 2 * t + e;
+              yv[i][j][e] = (row < nrows && col < args.n) ? yi[4 * (int64_t)col] : 0.0;
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < JL; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) acc[i][j][e] = __dsub_rn(yv[i][j][e], acc[i][j][e]);
+      }
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int row = 32 * wi + 8 * i + g;
         if (row >= nrows) continue;
         double* yq = args.Y + ((r0 + row) >> 2) * 4 * args.ldy + (row & 3);
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < JL; ++j)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int col = n0 + 8 * col_block(j, wj) + 2 * t + e;
@@ -214,12 +245,16 @@ __global__ void __launch_bounds__(GM_THREADS, 2) gemm_kernel(GemmArgs args) {
   }
 }
 
+template <int JL, bool SUB>
+static cudaError_t gemm_launch_t(const GemmArgs& a, dim3 grid, size_t smem, cudaStream_t stream) {
+  cudaError_t e = smem_attr((const void*)gemm_kernel<JL, SUB>, smem);
+  if (e != cudaSuccess) return e;
+  gemm_kernel<JL, SUB><<<grid, GM_THREADS, smem, stream>>>(a);
+  return cudaGetLastError();
+}
+
 cudaError_t gemm_launch(GemmArgs& a, cudaStream_t stream) {
   const size_t smem = gemm_smem_bytes();
-  {
-    cudaError_t e = smem_attr((const void*)gemm_kernel, smem);
-    if (e != cudaSuccess) return e;
-  }
   a.ntile_n = (int)ceil_div(a.n, GM_BN);
   a.nrow_tiles = ceil_div(a.rows, GM_BR);
   if (a.nrow_tiles == 0 || a.n == 0) return cudaSuccess;
@@ -230,8 +265,18 @@ cudaError_t gemm_launch(GemmArgs& a, cudaStream_t stream) {
   if (gy > a.nrow_tiles) gy = a.nrow_tiles;
   if (gy > 65535) gy = 65535;
   dim3 grid(ngroups, (unsigned)gy);
-  gemm_kernel<<<grid, GM_THREADS, smem, stream>>>(a);
-  return cudaGetLastError();
+  // skinny general C: only the live column blocks (the triangular path keeps
+  // its compile-time block skips over the full tile)
+  const int jl = (a.upper || a.n > 32) ? 4 : (a.n > 16 ? 2 : 1);
+  if (a.Yin != nullptr) {
+    if (a.upper) return cudaErrorInvalidValue;
+    if (jl == 4) return gemm_launch_t<4, true>(a, grid, smem, stream);
+    if (jl == 2) return gemm_launch_t<2, true>(a, grid, smem, stream);
+    return gemm_launch_t<1, true>(a, grid, smem, stream);
+  }
+  if (jl == 4) return gemm_launch_t<4, false>(a, grid, smem, stream);
+  if (jl == 2) return gemm_launch_t<2, false>(a, grid, smem, stream);
+  return gemm_launch_t<1, false>(a, grid, smem, stream);
 }
 
 }  // namespace cqr

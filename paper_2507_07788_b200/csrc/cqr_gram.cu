@@ -130,6 +130,7 @@ __global__ void __launch_bounds__(GR_THREADS, 2) gram_kernel(GramArgs args) {
   const int ia0 = ba * GR_CT, jb0 = bb * GR_CT;
   const int ncolA = min(GR_CT, args.ka - ia0);
   const int ncolB = (kind == 2) ? 0 : min(GR_CT, args.kb - jb0);
+  const bool narrowB = !self && ncolB <= 32;
 
   const int64_t npan = args.npanels;
   const int64_t p_begin = npan * split / args.nsplit;
@@ -178,7 +179,13 @@ __global__ void __launch_bounds__(GR_THREADS, 2) gram_kernel(GramArgs args) {
     const int nk4 = (int)imin64(GR_BR, args.rows - r0) >> 2;
     const double* As = stage_base + s * GR_STAGE_DOUBLES + fo;
     const double* Bs = As + GR_BLK;
-    if (kind == 0) {
+    if (kind == 0 && narrowB) {
+      // B has at most 32 columns (a skinny cross Gram: Q_in^T Q of the update
+      // path): instead of two warps multiplying the tile's empty right half, the
+      // k4 steps are split over warp pairs -- warps 0/1 take the even steps of
+      // A sub-tiles 0/1, warps 2/3 the odd ones, summed below in a fixed order
+      subtile<false>(acc0, As + 128 * (warp & 1), Bs, warp >> 1, nk4, 2);
+    } else if (kind == 0) {
       const int wi = warp >> 1, wj = warp & 1;
       subtile<false>(acc0, As + 128 * wi, Bs + 128 * wj, 0, nk4, 1);
     } else if (kind == 1) {
@@ -200,7 +207,23 @@ __global__ void __launch_bounds__(GR_THREADS, 2) gram_kernel(GramArgs args) {
 
   // ---------------- partials -> workspace: item slots of 64x64 (tile-local column-major)
   double* out = args.ws + ((int64_t)split * args.nitems + item) * (2 * GR_CT * GR_CT);
-  if (kind == 0) {
+  if (kind == 0 && narrowB) {
+    const int r0 = 32 * (warp & 1);
+    if (warp >= 2) store_acc(acc0, out + GR_CT * GR_CT, r0, 0, g, t);   // odd steps parked in the second slot
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (warp < 2) {
+      const double* o3 = out + GR_CT * GR_CT;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int idx = (8 * j + 2 * t + e) * GR_CT + r0 + 8 * i + g;
+            out[idx] = acc0[i][j][e] + o3[idx];
+          }
+    }
+  } else if (kind == 0) {
     store_acc(acc0, out, 32 * (warp >> 1), 32 * (warp & 1), g, t);
   } else if (kind == 1) {
     double* o = out + ((warp < 2) ? 0 : GR_CT * GR_CT);

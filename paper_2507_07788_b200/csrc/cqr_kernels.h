@@ -50,6 +50,7 @@ struct GemmArgs {
   int ntile_n;
   int64_t nrow_tiles;
   const int* gate = nullptr;   // launch is a no-op unless *gate == CQR_FACTORED (0)
+  const double* Yin = nullptr; int64_t ldyin = 0;   // non-null: Y = Yin - X C (general C only; may alias Y)
 };
 cudaError_t gemm_launch(GemmArgs& a, cudaStream_t stream);
 

@@ -44,7 +44,7 @@ def test_python_binding_covers_the_header():
 
 
 def test_abi_version(lib):
-    assert lib.cqr_abi_version() == 9
+    assert lib.cqr_abi_version() == 10
 
 
 def test_struct_layouts_match_header(tmp_path):

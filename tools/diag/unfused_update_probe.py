@@ -41,6 +41,7 @@ def t(fn, reps=5):
 
 out = {"m": m, "q": q, "p": p}
 out["lincomb_proj_ms"] = t(lambda: alg._lincomb_device(q_in, bt, q, p))
+out["lincomb_sub_ms"] = t(lambda: alg._lincomb_device(q_in, bt, q, p, minus_from=blk))
 proj = alg._lincomb_device(q_in, bt, q, p)
 out["axpy_ms"] = t(lambda: blk.axpy(-1.0, proj))
 out["trmm_ms"] = t(lambda: eng.apply(blk, tmp, with_gram=False))
