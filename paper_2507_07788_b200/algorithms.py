@@ -573,13 +573,16 @@ def chol_qr_update(q_in, r_in, a_new, cfg=None, ledger=None):
             _charge(ledger, "gemm", _flops.gemm_flops(m, k, p))
             _charge(ledger, "gemm", m * p)
             _charge(ledger, "trtri", _flops.tri_inverse_flops(p))
-            tmp = _fresh_like(q, p)
-            eng.apply(q, tmp, with_gram=False)
-            q = tmp
+            # Q <- Q R^-1 with G = Q^T Q from the same kernel where the block has
+            # at most 64 columns (in place: q is this call's own array)
+            q = _apply_gram_into(eng, q, fresh_ok=False)
             _charge(ledger, "gemm", _flops.gemm_flops(m, p, p))
             _charge(ledger, "gemm", _flops.gemm_flops(k, p, p) + k * p)
             _charge(ledger, "trmm", _flops.trmm_flops(p))
-            deflated_gram(q)
+            cross_gram_device(q_in, q, out=eng.Bt)
+            _charge(ledger, "gemm", _flops.gemm_flops(m, k, p))
+            _charge(ledger, "gemm", _flops.gemm_flops(m, p, p))
+            _charge(ledger, "gemm", _flops.gemm_flops(p, k, p) + p * p)
         its += 1
     if q is None:
         q = a_new.copy()
