@@ -82,3 +82,24 @@ def test_lincomb_sub_in_place_alias():
     _lib.check(cx.lib.cqr_lincomb_sub(xa.ptr(), xa.ld, xa.m_local, k, tiles.data_ptr(), n, ya.ptr(), ya.ld, ya.ptr(),
                                       ya.ld, cx.stream), "lincomb_sub")
     np.testing.assert_array_equal(ya.to_numpy(), want)
+
+
+@pytest.mark.parametrize("ka,kb", [(8, 32), (64, 32), (100, 24), (224, 32), (130, 1), (64, 16), (96, 33), (40, 64)])
+def test_skinny_cross_gram_matches_numpy(ka, kb):
+    """A^T B with a right operand of at most 32 columns takes the warp-pair k
+    split of the cross-Gram kernel (wider ones the 2 x 2 sub-tile map): both
+    against NumPy, and deterministic run to run."""
+    import paper_2507_07788_b200 as cq
+    from paper_2507_07788_b200._engine import cross_gram_host
+
+    m = 7001                      # ragged: not a multiple of the 32-row stage
+    rng = np.random.default_rng(ka * 100 + kb)
+    a = rng.standard_normal((m, ka))
+    b = rng.standard_normal((m, kb))
+    aa, bb = cq.CudaVectorArray.from_numpy(a), cq.CudaVectorArray.from_numpy(b)
+    g1 = cross_gram_host(aa, bb)
+    g2 = cross_gram_host(aa, bb)
+    np.testing.assert_array_equal(g1, g2)
+    ref = a.T @ b
+    assert g1.shape == ref.shape
+    assert np.max(np.abs(g1 - ref)) <= 1e-13 * m
