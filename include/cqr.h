@@ -238,6 +238,11 @@ int cqr_debug_update_narrow_teams(int on);
  * 0 = never, 1 = always, 2 (default) = where measured to pay (16-row sub-panels
  * with a 4- or 5-stage ring).  Results are bitwise the same. */
 int cqr_debug_update_lag(int mode);
+/* Diagnostics: 1 (default) = in the initial pass of an append (full 16-column
+ * block, rows a multiple of the sub-panel height) the cross-Gram warps read the
+ * staged block in place; 0 = the projection warps copy it into the Q' ring first
+ * (the path of ragged / narrower blocks).  Bitwise the same results. */
+int cqr_debug_update_direct(int on);
 /* Diagnostics: bases of at least q columns (145 <= q <= 193) stage 16-row
  * sub-panels in the update pass, narrower ones 32-row (64-row up to 64 columns). */
 int cqr_debug_update_sr16_from(int q);

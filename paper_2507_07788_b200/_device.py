@@ -41,6 +41,8 @@ class DeviceContext:
             self.lib.cqr_debug_update_narrow_teams(int(os.environ["CQR_UPDATE_NARROW_TEAMS"]))
         if "CQR_UPDATE_SR16_FROM" in os.environ:   # diagnostics: sub-panel height switch of the update pass
             self.lib.cqr_debug_update_sr16_from(int(os.environ["CQR_UPDATE_SR16_FROM"]))
+        if "CQR_UPDATE_DIRECT" in os.environ:   # diagnostics: initial passes read the staged block in place
+            self.lib.cqr_debug_update_direct(int(os.environ["CQR_UPDATE_DIRECT"]))
         if "CQR_UPDATE_LAG" in os.environ:   # diagnostics: cross-Gram lag of the update pass
             self.lib.cqr_debug_update_lag(int(os.environ["CQR_UPDATE_LAG"]))
         if torch.distributed.is_available() and torch.distributed.is_initialized():

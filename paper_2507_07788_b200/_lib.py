@@ -137,6 +137,7 @@ SIGNATURES = {
     "cqr_debug_factor_banded": (_I, [_I]),
     "cqr_debug_update_narrow_teams": (_I, [_I]),
     "cqr_debug_update_lag": (_I, [_I]),
+    "cqr_debug_update_direct": (_I, [_I]),
     "cqr_debug_update_sr16_from": (_I, [_I]),
     "cqr_debug_factor_cluster": (_I, [_I]),
     "cqr_debug_factor_cluster_profile": (_I, [ctypes.POINTER(ctypes.c_ulonglong)]),

@@ -299,6 +299,7 @@ void cqr_debug_update_tma(int on) { cqr::set_update_tma(on); }
 
 int cqr_debug_update_narrow_teams(int on) { return cqr::update_set_narrow_teams(on); }
 int cqr_debug_update_lag(int on) { return cqr::update_set_lag(on); }
+int cqr_debug_update_direct(int on) { return cqr::update_set_direct(on); }
 int cqr_debug_update_sr16_from(int q) { return cqr::update_set_sr16_from(q); }
 int cqr_debug_factor_banded(int on) { return cqr::factor_set_banded(on); }
 

@@ -81,6 +81,7 @@ cudaError_t gram_rt_launch(const double* X, int64_t ldx, int k, int64_t rows, do
 void set_update_tma(int on);
 int update_set_narrow_teams(int on);
 int update_set_lag(int on);
+int update_set_direct(int on);
 int update_set_sr16_from(int q);
 bool update_pass_supported(int q, int p);
 size_t update_pass_ws_bytes(int64_t rows, int q);

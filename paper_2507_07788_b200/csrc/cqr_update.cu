@@ -72,6 +72,7 @@ struct alignas(64) UpdateArgs {
   int ns;                                 // ring stages
   const int* gate;                        // no-op unless *gate == CQR_FACTORED
   int lag;                                // cross-Gram group one sub-panel behind the projection DMMAs (see kernel)
+  int direct;                             // initial mode: the cross-Gram warps read the block from the stage (see kernel)
 };
 
 static int up_qs(int q) { return (int)round_up(q, 8) + 4; }
@@ -135,6 +136,11 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(const __grid
   // idle (ncu at q = 320: the cross-Gram warps waited on Q' for 23% of their
   // samples).  Timing only: the same operations in the same order per element.
   const bool lag = a.lag != 0 && !TEAMS && a.initial == 0;
+  // Direct (initial mode, full 16-column blocks, rows a multiple of SR): Q' is the
+  // staged block itself, so the cross-Gram warps wait for the stage and read it in
+  // place; the projection group's copy into the Q' ring and its hand-over (a
+  // latency chain per sub-panel that bounds the narrow initial passes) are skipped.
+  const bool direct = a.direct != 0 && a.initial != 0;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
@@ -218,7 +224,7 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(const __grid
     }
     double* tqt = tq + team * TE;
     const int bar = 2 + team;
-    for (int64_t j = team; j < mine; j += 2) {
+    for (int64_t j = team; j < (direct ? 0 : mine); j += 2) {
       const int sj = (int)(j % ns), ysj = (int)(j % UP_YS);
       const uint32_t phj = (uint32_t)((j / ns) & 1), yphj = (uint32_t)((j / UP_YS) & 1);
       const int64_t r0 = (blockIdx.x + j * gridDim.x) * SR;
@@ -372,7 +378,7 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(const __grid
           btr[c][h][nb] = (!init && kk < q && n < p) ? a.Bt[(int64_t)n * a.ldbt + kk] : 0.0;
         }
     }
-    for (int64_t j = 0; j < mine; ++j) {
+    for (int64_t j = 0; j < (direct ? 0 : mine); ++j) {
       const int64_t r0 = (blockIdx.x + j * gridDim.x) * SR;
       const int nrows = (int)imin64(SR, a.rows - r0);
       mbar_wait(&full[s], ph);
@@ -519,9 +525,15 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(const __grid
         const int yn = (ys + 1 == UP_YS) ? 0 : ys + 1;
         mbar_wait(&pdone[yn], (ys + 1 == UP_YS) ? (yph ^ 1) : yph);
       }
-      mbar_wait(&yfull[ys], yph);
       const double* Qs = stg + s * STG;
-      const double* yd = yring + ys * TE;
+      const double* yd;
+      if (direct) {
+        mbar_wait(&full[s], ph);
+        yd = Qs + SR * qs;
+      } else {
+        mbar_wait(&yfull[ys], yph);
+        yd = yring + ys * TE;
+      }
       const double* xa = Qs + 4 * (8 * wb + g) + t;   // Q_in(row t, column 8wb + g)
 #pragma unroll
       for (int ks = 0; ks < Q4; ++ks) {
@@ -557,7 +569,7 @@ __global__ void __launch_bounds__(UP_THREADS, 1) update_pass_kernel(const __grid
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&empty[s]);
-        mbar_arrive(&yempty[ys]);
+        if (!direct) mbar_arrive(&yempty[ys]);
         if (wb == 7 && j + ns < mine) {
           mbar_wait(&empty[s], ph);   // all 8 cross-Gram warps are done with the stage
           issue(j + ns, s);
@@ -716,6 +728,11 @@ int update_set_sr16_from(int q) {
 }
 // 0 = never, 1 = always (wide single-group passes), 2 (default) = where it was
 // measured to pay: 16-row sub-panels with a 4- or 5-stage ring (q = 256..368)
+static int g_update_direct = 1;   // cqr_debug_update_direct
+int update_set_direct(int on) {
+  g_update_direct = on ? 1 : 0;
+  return 0;
+}
 static int g_update_lag = 2;   // cqr_debug_update_lag
 int update_set_lag(int mode) {
   g_update_lag = mode;
@@ -738,6 +755,7 @@ cudaError_t update_pass_launch(const double* Qin, int64_t ldqin, int q, const do
   a.gate = gate;
   a.qs = up_qs(q);
   const int sr = up_sr(q);
+  a.direct = (g_update_direct && initial && p == UP_PB && rows % sr == 0) ? 1 : 0;
   {
     const int nst = up_stages(q, sr);
     a.lag = g_update_lag == 1 || (g_update_lag == 2 && sr == 16 && (nst == 4 || nst == 5));

@@ -19,7 +19,7 @@ DEFAULT_MODE = 2
 DEFAULT_SR16_FROM = 145
 
 
-def _pass(m, q, p, initial, teams, seed, mode=None, sr16_from=None):
+def _pass(m, q, p, initial, teams, seed, mode=None, sr16_from=None, direct=None):
     import torch
 
     import paper_2507_07788_b200 as cq
@@ -33,6 +33,8 @@ def _pass(m, q, p, initial, teams, seed, mode=None, sr16_from=None):
         cx.lib.cqr_debug_update_lag(mode)
     if sr16_from is not None:
         assert cx.lib.cqr_debug_update_sr16_from(sr16_from) == 0
+    if direct is not None:
+        cx.lib.cqr_debug_update_direct(direct)
     try:
         rng = np.random.default_rng(seed)
         qin = cq.CudaVectorArray.from_numpy(np.linalg.qr(rng.standard_normal((m, q)))[0])
@@ -49,6 +51,7 @@ def _pass(m, q, p, initial, teams, seed, mode=None, sr16_from=None):
         cx.lib.cqr_debug_update_narrow_teams(1)
         cx.lib.cqr_debug_update_lag(DEFAULT_MODE)
         cx.lib.cqr_debug_update_sr16_from(DEFAULT_SR16_FROM)
+        cx.lib.cqr_debug_update_direct(1)
 
 
 @pytest.mark.parametrize("q", [1, 7, 16, 33, 48, 64])
@@ -103,3 +106,15 @@ def test_sub_panel_height_switch(q, initial):
     for x, y in zip(a[1:], b[1:]):
         np.testing.assert_allclose(x, y, rtol=0, atol=1e-12 * max(1.0, float(np.abs(x).max())))
 
+
+
+@pytest.mark.parametrize("q", [1, 16, 40, 64, 100, 144, 160, 256, 333, 496])
+@pytest.mark.parametrize("m", [64 * 500, 64 * 500 + 16])
+def test_initial_pass_direct_matches_copy_bitwise(q, m):
+    """Initial pass (Bt = Q_in^T A, G = A^T A): the cross-Gram warps reading the
+    staged block in place (cqr_debug_update_direct(1), full sub-panels only) against
+    the copy through the Q' ring; with ragged rows both runs take the copy path."""
+    a = _pass(m, q, 16, True, 1, seed=q, direct=0)
+    b = _pass(m, q, 16, True, 1, seed=q, direct=1)
+    for x, y in zip(a, b):
+        np.testing.assert_array_equal(x, y)
