@@ -251,9 +251,14 @@ def replay_iterated(trace, mine, cfg, kind="rs"):
         e = trace[i]
         g, bt = _device_x(e)
         k = g.shape[0]
+        # width of the rounding noise in the factored matrix: its own k, plus, for a
+        # deflated Gramian G - Bt^T Bt, the q-term dot products of the deflation (the
+        # device's factor kernel and the oracle order them differently)
+        kn = k
         if kind == "update" and bt is not None and bt.size:
             x = co._deflated_from(g, bt)
             top = float(np.max(np.diag(g))) if g.size else None
+            kn = k + bt.shape[0]
         else:
             x = g
             top = None
@@ -295,7 +300,7 @@ def replay_iterated(trace, mine, cfg, kind="rs"):
         out.passes += 1
         structural = exc is not None and x[exc.pivot_index, exc.pivot_index] == 0.0   # a zero column
         if a_o is None or (a_o > 0) != (a_m > 0) or a_o != a_m:
-            if (a_o is not None and (a_o > 0) != (a_m > 0)) and fragile_margin(dm, k) and not structural:
+            if (a_o is not None and (a_o > 0) != (a_m > 0)) and fragile_margin(dm, kn) and not structural:
                 out.fragile += 1
                 pm += a_m
                 continue
