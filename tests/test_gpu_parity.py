@@ -211,8 +211,9 @@ def test_update_golden(case):
     assert res.success == ref.success == case["success"]
     p = a_new.ncols
     tol = algo_cfg(case).effective_tol(p)
-    cmp = P.compare_iterated(res, ref, p, tol)
-    gcmp = P.compare_iterated(res, P.Record(case), p, tol)
+    kn = p + q_in.ncols          # deflated Gramian: rounding noise of width p + q (parity.py)
+    cmp = P.compare_iterated(res, ref, kn, tol)
+    gcmp = P.compare_iterated(res, P.Record(case), kn, tol)
     rep = P.replay_iterated(trace, res, oracle_cfg(case), "update")
     assert rep.passes == res.iterations, rep
     if case["name"] in UPDATE_ROUNDING:

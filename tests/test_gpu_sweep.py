@@ -88,7 +88,7 @@ def test_sweep_single(case):
     mine, ref, my_exc, ref_exc = _run_both(algo, x, cq, co)
     if my_exc is not None or ref_exc is not None:
         # both raise, or the deciding pivot sits at the rounding level
-        if P.compare_single(mine, my_exc, ref, ref_exc, k):
+        if P.compare_single(mine, my_exc, ref, ref_exc, k, m=m):
             STATS["both_raised"] += 1
         else:
             STATS["parted_rounding"] += 1
@@ -157,7 +157,7 @@ def _update_case(i, m, k, cond):
     np.testing.assert_array_equal(mine.r[:k, :k], r_in)
     np.testing.assert_array_equal(mine.r[k:, :k], 0.0)
     tol = cq.AlgoConfig().effective_tol(p)
-    cmp = P.compare_iterated(mine, ref, p, tol)
+    cmp = P.compare_iterated(mine, ref, p + k, tol)    # deflated Gramian: noise width k + q (parity.py)
     STATS["decisions"] += cmp.decisions
     STATS["shifted"] += cmp.shifted
     STATS["parted_rounding"] += 0 if cmp.full else 1
@@ -165,7 +165,14 @@ def _update_case(i, m, k, cond):
     if mine.success and ref.success:
         qd = mine.q.to_numpy()
         loo = float(np.linalg.norm(np.eye(k + p) - qd.T @ qd))
-        assert P.within10(loo, co.loo_fro(ref.q), k + p, diverged), (loo, co.loo_fro(ref.q))
+        # the deflation G - Bt^T Bt cancels ratio-fold (ratio = max diag G / max diag X, from
+        # the oracle), so X -- and with it the norms of the new columns -- carries a relative
+        # rounding error of ~u ratio in any implementation (the floor of the shift comparison,
+        # parity.py); a block that converges in one pass keeps it (case 11509: 1200 x (1 + 1),
+        # ratio ~ 600, device 7.1e-14 against 4.5e-15, both below tol = 1e-13)
+        ratio = max(getattr(ref, "deflation_ratios", None) or [1.0])
+        floor = max(diverged or 0.0, P.U * ratio)
+        assert P.within10(loo, co.loo_fro(ref.q), k + p, floor), (loo, co.loo_fro(ref.q), ratio)
 
 
 # Wide widths (the k x k paths for 128 < k <= 256 and the banded L2 path for
